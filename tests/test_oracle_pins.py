@@ -1,0 +1,505 @@
+"""Pins of the C++ oracle against what the paper and mathematics fix
+(SURVEY.md §8(c) "Pins" P1-P14).  CPU only; no GPU, no CUDA library.
+
+Each test names the pin and the passage it follows.  None of them retypes
+the oracle's own formula: they use closed forms, the EWA Jacobian,
+brute-force search, ray marching, naive counting, the paper's printed tile
+counts (tests/golden/) and invariants.
+"""
+from __future__ import annotations
+
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import scenegen as sg
+from helpers import C0, identity_camera, lowres_compose, quat_to_R, rot_to_quat, scene_from, tiny_set
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# --------------------------------------------------------------------- activation (SPEC examples)
+
+def test_activation_spec_examples(oracle_mod):
+    """build_covariance (Eq.1) and sh_to_color DC examples."""
+    ex = json.load(open(os.path.join(GOLDEN, "spec_examples.json")))
+    for c in ex["covariance"]:
+        sc = scene_from([[0, 0, 5]], c["scale"], quats=c["quat_wxyz"])
+        a = oracle_mod.Oracle(sc).activated()
+        np.testing.assert_allclose(a["cov"][0], c["cov_xx_xy_xz_yy_yz_zz"], atol=1e-6)
+        inv = np.linalg.inv(np.array(c["cov_xx_xy_xz_yy_yz_zz"])[[0, 1, 2, 1, 3, 4, 2, 4, 5]].reshape(3, 3))
+        np.testing.assert_allclose(a["icov"][0], inv[[0, 0, 0, 1, 1, 2], [0, 1, 2, 1, 2, 2]], atol=1e-6)
+    for c in ex["sh_dc"]:
+        sc = scene_from([[0, 0, 5]], 0.05, opacities=0.5, dc=c["dc"])
+        o = oracle_mod.Oracle(sc).prepare([identity_camera(32, 32, 16)])
+        rgb = o.splats(0)[0, 34:37]
+        np.testing.assert_allclose(rgb, c["rgb"], atol=1e-6)
+
+
+def test_activation_rejects_nonfinite(oracle_mod):
+    """non-finite records are dropped (not clamped) and counted."""
+    sc = scene_from([[0, 0, 5], [0, 0, 6], [1, 1, 7]], 0.1)
+    sc.means[1, 0] = np.nan
+    sc.log_scales[2, 1] = np.inf
+    o = oracle_mod.Oracle(sc)
+    assert o.n_rejected == 2 and o.n == 1
+
+
+def test_qcut_is_the_1_over_255_threshold(oracle_mod):
+    """alpha = sigma*exp(-q/2) >= 1/255  <=>  q <= q_cut."""
+    ops = np.array([0.0039, 0.004, 0.05, 0.5, 0.99])
+    sc = scene_from(np.tile([[0, 0, 5]], (5, 1)), 0.1, opacities=ops)
+    a = oracle_mod.Oracle(sc).activated()
+    for s, q in zip(a["sigma"], a["qcut"]):
+        if q >= 0:
+            assert abs(s * math.exp(-q / 2) - 1 / 255) < 1e-7
+        else:
+            assert s < 1 / 255
+
+
+# --------------------------------------------------------------------- P1 / P2 closed forms
+
+@pytest.mark.parametrize("f,s,z,sigma,dc", [(64.0, 0.1, 4.0, 0.9, 0.3), (100.0, 0.05, 2.5, 0.6, -0.4),
+                                            (40.0, 0.3, 7.0, 0.99, 1.2)])
+def test_P1_onaxis_isotropic_closed_form(oracle_mod, f, s, z, sigma, dc):
+    """P1: one isotropic Gaussian on the optical axis: q = |D|^2/(f^2 s^2/z^2 + 0.3),
+    alpha = min(.99, sigma e^{-q/2}), RGB = alpha*max(0,.5+C0*dc), A = alpha,
+    Depth = alpha*z/|d| (Eq.2 single term; OP on axis)."""
+    W = H = 64
+    sc = scene_from([[0, 0, z]], s, opacities=sigma, dc=[dc] * 3)
+    o = oracle_mod.Oracle(sc).prepare([identity_camera(W, H, f)], assign_tile=16)
+    (img, dep), = o.render()
+    jj, ii = np.mgrid[0:H, 0:W]
+    dx, dy = ii + 0.5 - W / 2, jj + 0.5 - H / 2
+    q = (dx ** 2 + dy ** 2) / (f * f * s * s / (z * z) + 0.3)
+    a = np.minimum(0.99, sigma * np.exp(-q / 2))
+    qcut = 2 * math.log(255 * np.float32(sigma))
+    inside = q <= qcut * (1 - 1e-5)
+    outside = q > qcut * (1 + 1e-5)
+    col = max(0.0, 0.5 + C0 * dc)
+    dn = np.sqrt((dx / f) ** 2 + (dy / f) ** 2 + 1)
+    np.testing.assert_allclose(img[..., 3][inside], a[inside], rtol=2e-5, atol=1e-7)
+    np.testing.assert_allclose(img[..., 0][inside], (a * col)[inside], rtol=2e-5, atol=1e-7)
+    np.testing.assert_allclose(dep[inside], (a * z / dn)[inside], rtol=2e-5, atol=1e-6)
+    assert np.all(img[..., 3][outside] == 0) and np.all(dep[outside] == 0)
+    assert inside.sum() > 20
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_P2_op_equals_ewa_on_axis(oracle_mod, seed):
+    """P2: a Gaussian on the optical axis with ANY covariance: Optimal
+    Projection equals the EWA local-affine projection (Eq.3) at every
+    pixel, Sigma_pix = J Sigma_c J^T + 0.3 I with J = (f/z)[I 0]."""
+    rs = np.random.default_rng(seed)
+    W = H = 64
+    f, z = 48.0, 3.0 + seed
+    q4 = rs.normal(size=4)
+    q4 /= np.linalg.norm(q4)
+    scales = np.exp(rs.uniform(np.log(0.03), np.log(0.4), 3))
+    sc = scene_from([[0, 0, z]], scales, quats=q4, opacities=0.95, dc=[1.0] * 3)
+    o = oracle_mod.Oracle(sc).prepare([identity_camera(W, H, f)], assign_tile=16)
+    (img, _), = o.render()
+    act = o.activated()
+    cov = act["cov"][0].astype(np.float64)[[0, 1, 2, 1, 3, 4, 2, 4, 5]].reshape(3, 3)
+    Sp = (f / z) ** 2 * cov[:2, :2] + 0.3 * np.eye(2)
+    Si = np.linalg.inv(Sp)
+    jj, ii = np.mgrid[0:H, 0:W]
+    D = np.stack([ii + 0.5 - W / 2, jj + 0.5 - H / 2], -1)
+    q = np.einsum("...i,ij,...j->...", D, Si, D)
+    a = np.minimum(0.99, act["sigma"][0] * np.exp(-q / 2))
+    qcut = float(act["qcut"][0])
+    inside = q <= qcut * (1 - 1e-4)
+    np.testing.assert_allclose(img[..., 3][inside], a[inside], rtol=5e-5, atol=1e-7)
+    assert np.all(img[..., 3][q > qcut * (1 + 1e-4)] == 0)
+
+
+# --------------------------------------------------------------------- P3 / P4 tile culling
+
+def test_P3_eq4_edge_optimal_vs_grid(oracle_mod):
+    """P3: Eq.4 with t clamped to the segment is <= every point of a
+    2000-point grid along the edge; isotropic C reduces to the clamped
+    orthogonal projection."""
+    rs = np.random.default_rng(7)
+    ts = np.linspace(0, 1, 2000)
+    for _ in range(500):
+        L = rs.normal(size=(2, 2))
+        Cm = L @ L.T + 0.05 * np.eye(2)
+        Cc = np.array([Cm[0, 0], Cm[0, 1], Cm[1, 1]], np.float32)
+        p = rs.normal(size=2).astype(np.float32) * 3
+        d = rs.normal(size=2).astype(np.float32) * 2
+        q, xh = oracle_mod.eq4_edge(Cc, p, d)
+        Cd = Cc.astype(np.float64)[[0, 1, 1, 2]].reshape(2, 2)
+        X = p[None, :].astype(np.float64) + ts[:, None] * d[None, :].astype(np.float64)
+        qg = np.einsum("ni,ij,nj->n", X, Cd, X)
+        assert q <= qg.min() * (1 + 1e-5) + 1e-6
+    # isotropic: clamped orthogonal projection of the mean (origin) onto the segment
+    q, xh = oracle_mod.eq4_edge(np.array([1, 0, 1], np.float32), np.array([-2, -3], np.float32),
+                                np.array([1, 0], np.float32))
+    np.testing.assert_allclose(xh, [-1, -3])
+    q, xh = oracle_mod.eq4_edge(np.array([1, 0, 1], np.float32), np.array([-0.5, -3], np.float32),
+                                np.array([1, 0], np.float32))
+    np.testing.assert_allclose(xh, [0, -3], atol=1e-7)
+
+
+def _sample_q(sp, x, y):
+    """q at rays (x, y, 1) in double: intersect the ray with the optimal plane
+    u.p = 1, take tangent-plane coordinates, evaluate the 2D conic
+    (dense-sampling oracle, independent of the float evaluation order)."""
+    u, e1, e2 = (sp[a:a + 3].astype(np.float64) for a in (4, 7, 10))
+    C = sp[16:19].astype(np.float64)
+    s = u[0] * x + u[1] * y + u[2]
+    with np.errstate(divide="ignore", invalid="ignore"):
+        y1 = (e1[0] * x + e1[1] * y + e1[2]) / s
+        y2 = (e2[0] * x + e2[1] * y + e2[2]) / s
+        q = C[0] * y1 * y1 + 2 * C[1] * y1 * y2 + C[2] * y2 * y2
+    return np.where(s > 0, q, np.inf)
+
+
+@pytest.mark.parametrize("seed", [0, 1])
+def test_P4_culling_sound_and_qmin_optimal(oracle_mod, seed):
+    """P4: dense 64x64 per-tile ray sampling never finds q <= q_cut
+    in a culled tile; for kept tiles the Eq.4 quad minimum is <= every dense
+    sample (it is the minimum of q over the tile)."""
+    sc = sg.random_scene(seed, n=300)
+    cam = identity_camera(128, 128, 64.0)
+    o = oracle_mod.Oracle(sc).prepare([cam], assign_tile=16)
+    sps = o.splats(0)
+    n_cull = n_keep = 0
+    lin = np.linspace(0, 1, 64)
+    for g in range(0, 300, 3):
+        sp = sps[g]
+        if sp[0] == 0:
+            continue
+        for ty in range(8):
+            for tx in range(8):
+                x0, y0 = tx * 16, ty * 16
+                r = o.tile_test(0, g, x0, y0, x0 + 16, y0 + 16)
+                X = ((x0 + 16 * lin)[None, :] - cam.cx) / cam.fx
+                Y = ((y0 + 16 * lin)[:, None] - cam.cy) / cam.fy
+                qd = _sample_q(sp, X, Y)
+                qcut = float(sp[38])
+                if r["keep"] == 0:
+                    n_cull += 1
+                    assert qd.min() > qcut, (g, tx, ty)
+                else:
+                    n_keep += 1
+                    assert r["qmin"] <= qd.min() * (1 + 1e-4) + 1e-6, (g, tx, ty, r["qmin"], qd.min())
+    assert n_cull > 100 and n_keep > 50
+
+
+def test_pair_counts_equal_bruteforce_enumeration(oracle_mod):
+    """total pair count = for every tile, every splat passing the
+    same culling test (quadratic brute force), i.e. the footprint rect, cone
+    cull and SAT early-out never drop a pair; invisible tiles never get one."""
+    sc = sg.random_scene(3, n=200)
+    cam = identity_camera(96, 80, 50.0, mask_slot=0)
+    mask = np.ones((80, 96), np.uint8)
+    mask[:20, :40] = 0
+    mask[60:, 70:] = 0
+    o = oracle_mod.Oracle(sc)
+    o.set_mask(0, mask)
+    o.prepare([cam], assign_tile=16)
+    counts = o.counts()
+    sps = o.splats(0)
+    _, vis = o.tile_info(0)
+    for g in range(200):
+        c = 0
+        if sps[g, 0] != 0:
+            for ty in range(5):
+                for tx in range(6):
+                    if vis[ty, tx] and o.tile_test(0, g, tx * 16, ty * 16, min(tx * 16 + 16, 96), ty * 16 + 16)["keep"] == 1:
+                        c += 1
+        else:
+            # culled splats: never contribute anywhere (dense check on the full image)
+            X = (np.arange(96)[None, :] + 0.5 - cam.cx) / cam.fx
+            Y = (np.arange(80)[:, None] + 0.5 - cam.cy) / cam.fy
+        assert counts[g] == c, g
+    k, v = o.pairs()
+    tiles = (k >> np.uint64(32)).astype(np.int64)
+    assert np.all(vis.reshape(-1)[tiles] == 1)
+
+
+# --------------------------------------------------------------------- P5 / P6 depth
+
+def test_P5_depth_isotropic_and_raymarch(oracle_mod):
+    """P5: isotropic Sigma -> t = (mu-o).d_hat (orthogonal
+    foot); a ray through mu gives |mu-o|; anisotropic -> the 1D ray-march argmax
+    of the 3D density along the ray."""
+    cam = identity_camera(64, 64, 32.0)
+    sc = scene_from([[0.3, -0.2, 4.0]], 0.2)
+    o = oracle_mod.Oracle(sc).prepare([cam])
+    mu = np.array([0.3, -0.2, 4.0])
+    for (xs, ys) in [(32.0, 32.0), (40.5, 20.25), (10.0, 50.0)]:
+        d = np.array([(xs - 32) / 32, (ys - 32) / 32, 1.0])
+        tau = o.sample_depth(0, 0, xs, ys)
+        np.testing.assert_allclose(tau * np.linalg.norm(d), mu @ d / np.linalg.norm(d), rtol=1e-5)
+    # ray through mu
+    xs, ys = 32 + 32 * 0.3 / 4.0, 32 - 32 * 0.2 / 4.0
+    d = np.array([(xs - 32) / 32, (ys - 32) / 32, 1.0])
+    np.testing.assert_allclose(o.sample_depth(0, 0, xs, ys) * np.linalg.norm(d), np.linalg.norm(mu), rtol=1e-5)
+    # anisotropic: ray march
+    rs = np.random.default_rng(3)
+    for trial in range(5):
+        q4 = rs.normal(size=4)
+        sc = scene_from([[rs.uniform(-1, 1), rs.uniform(-1, 1), rs.uniform(3, 6)]],
+                        np.exp(rs.uniform(np.log(0.02), np.log(0.5), 3)), quats=q4 / np.linalg.norm(q4))
+        o = oracle_mod.Oracle(sc).prepare([cam])
+        icov = o.activated()["icov"][0].astype(np.float64)[[0, 1, 2, 1, 3, 4, 2, 4, 5]].reshape(3, 3)
+        mu = sc.means[0].astype(np.float64)
+        xs, ys = rs.uniform(0, 64), rs.uniform(0, 64)
+        d = np.array([(xs - 32) / 32, (ys - 32) / 32, 1.0])
+        dh = d / np.linalg.norm(d)
+        ts = np.linspace(0.0, 20.0, 100001)
+        P = ts[:, None] * dh[None, :] - mu[None, :]
+        dens = -np.einsum("ni,ij,nj->n", P, icov, P)
+        tm = ts[np.argmax(dens)]
+        got = o.sample_depth(0, 0, np.float32(xs), np.float32(ys)) * np.linalg.norm(d)
+        assert abs(got - tm) <= 2 * (ts[1] - ts[0]) + 1e-5 * tm
+
+
+def test_P6_depth_rotation_invariant(oracle_mod):
+    """P6 (P:270-275 popping): the per-ray depth depends only on
+    the world ray, not on the camera rotation (view-space z does change)."""
+    rs = np.random.default_rng(11)
+    q4 = rs.normal(size=4)
+    sc = scene_from([[0.4, 0.1, 5.0]], [0.3, 0.05, 0.12], quats=q4 / np.linalg.norm(q4))
+    mu = sc.means[0].astype(np.float64)
+    w = mu / np.linalg.norm(mu) + np.array([0.01, -0.02, 0.0])
+    w /= np.linalg.norm(w)
+    dists, zs = [], []
+    for yaw in (0.0, 0.2, -0.3, 0.35):
+        R_cw = np.array([[math.cos(yaw), 0, math.sin(yaw)], [0, 1, 0], [-math.sin(yaw), 0, math.cos(yaw)]])
+        cam = sg.Camera(np.ascontiguousarray(R_cw.T, np.float32), np.zeros(3, np.float32), 200.0, 200.0, 256.0, 256.0,
+                        512, 512, -1)
+        o = oracle_mod.Oracle(sc).prepare([cam])
+        wc = cam.R_wc.astype(np.float64) @ w
+        xs, ys = 256 + 200 * wc[0] / wc[2], 256 + 200 * wc[1] / wc[2]
+        d = np.array([(np.float32(xs) - 256) / 200, (np.float32(ys) - 256) / 200, 1.0])
+        dists.append(o.sample_depth(0, 0, np.float32(xs), np.float32(ys)) * np.linalg.norm(d))
+        zs.append((cam.R_wc.astype(np.float64) @ mu)[2])
+    assert np.ptp(dists) / np.mean(dists) < 2e-5
+    assert np.ptp(zs) / np.mean(zs) > 1e-2
+
+
+# --------------------------------------------------------------------- P7 / P8 SAT and tile grid
+
+def test_P7_sat_matches_naive_counting(oracle_mod):
+    """P7: rectangle counts from the summed-area table
+    equal naive counting."""
+    rs = np.random.default_rng(5)
+    for _ in range(100):
+        th, tw = rs.integers(1, 40), rs.integers(1, 40)
+        bits = (rs.random((th, tw)) < rs.random()).astype(np.uint8)
+        S = oracle_mod.sat(bits)
+        assert S[-1, -1] == bits.sum()
+        for _ in range(30):
+            x0, x1 = sorted(rs.integers(0, tw, 2))
+            y0, y1 = sorted(rs.integers(0, th, 2))
+            assert oracle_mod.sat_count(S, x0, y0, x1, y1) == bits[y0:y1 + 1, x0:x1 + 1].sum()
+
+
+def test_P8_paper_tile_counts(oracle_mod):
+    """P8: at 2064x2272 with 32x32 tiles there are 4615 coarse tiles and, with
+    the fovea = half the image size, 1085 high-resolution tiles (P:657,
+    tests/golden/paper_tile_counts.json)."""
+    gold = json.load(open(os.path.join(GOLDEN, "paper_tile_counts.json")))
+    W, H = gold["width"], gold["height"]
+    o = oracle_mod.Oracle(scene_from(np.zeros((0, 3)), 0.1))
+    cam = identity_camera(W, H, 722.6)
+    fov = sg.Fovea((W / 2, H / 2), (W / 4, H / 4), 0.10)
+    o.prepare([cam], [fov], assign_tile=gold["tile"])
+    cls, vis = o.tile_info(0)
+    assert cls.size == gold["total"]
+    assert int((cls == 0).sum()) == gold["high_res"]
+    st = o.stats()
+    assert st["tiles_high"] + st["tiles_low"] + st["tiles_hybrid"] + st["tiles_invisible"] == gold["total"]
+
+
+# --------------------------------------------------------------------- P9 / P10 brute force and invariants
+
+@pytest.mark.parametrize("seed", list(range(100, 120)))
+def test_P9_windowed_equals_bruteforce_full_sort(oracle_mod, seed):
+    """P9: with a window that never overflows, the tiled,
+    windowed StopThePop blend equals a tile-free per-pixel full sort of every
+    Gaussian with alpha >= 1/255 at that pixel -- bit for bit."""
+    sc, cam = tiny_set(seed)
+    for K in (64, 16):
+        o = oracle_mod.Oracle(sc).prepare([cam], assign_tile=16, window_k=K)
+        (img, dep), = o.render()
+        st = o.stats()
+        bf, bd = o.bruteforce(0)
+        if st["overflow_samples"] == 0:
+            assert np.array_equal(img, bf) and np.array_equal(dep, bd)
+        else:
+            assert K == 16
+
+
+def test_P9_window_overflow_differs_and_is_counted(oracle_mod):
+    """A depth complexity above K makes the window an approximation:
+    overflow samples are counted; with K >= list length it is exact again."""
+    rs = np.random.default_rng(1)
+    n = 40
+    means = np.stack([rs.uniform(-0.05, 0.05, n), rs.uniform(-0.05, 0.05, n), rs.uniform(3, 3.5, n)], 1)
+    # reversed emission depth vs ray depth is likely with big, overlapping, anisotropic splats
+    sc = scene_from(means, [0.5, 0.5, 0.02], opacities=0.08)
+    sc.quats[:] = np.stack([np.ones(n), rs.normal(0, 0.5, n), rs.normal(0, 0.5, n), np.zeros(n)], 1)
+    cam = identity_camera(32, 32, 16.0)
+    o = oracle_mod.Oracle(sc).prepare([cam], window_k=4)
+    (img, _), = o.render()
+    assert o.stats()["overflow_samples"] > 0
+    o2 = oracle_mod.Oracle(sc).prepare([cam], window_k=64)
+    (img2, _), = o2.render()
+    bf, _ = o2.bruteforce(0)
+    assert np.array_equal(img2, bf)
+
+
+def test_P10_invariants(oracle_mod):
+    """P10 (Eq.2): A = 1-T in [0,1], RGB >= 0, alpha <= 0.99
+    (a single opaque splat gives A <= 0.99), empty scene -> background,
+    terminated samples have A > 1-1e-4 (T < 1e-4 stops, L11)."""
+    cam = identity_camera(64, 64, 32.0)
+    # empty scene
+    o = oracle_mod.Oracle(scene_from(np.zeros((0, 3)), 0.1)).prepare([cam], background=(0.2, 0.3, 0.4))
+    (img, dep), = o.render()
+    assert np.all(img[..., :3] == np.array([0.2, 0.3, 0.4], np.float32)) and np.all(img[..., 3] == 0)
+    assert np.all(dep == 0)
+    # single opaque splat: alpha clamp
+    o = oracle_mod.Oracle(scene_from([[0, 0, 3]], 3.0, opacities=0.999999, dc=[1, 1, 1])).prepare([cam])
+    (img, dep), = o.render()
+    assert img[..., 3].max() == np.float32(0.99) and (img[..., 3] == np.float32(0.99)).sum() > 20
+    # random scene
+    o = oracle_mod.Oracle(sg.random_scene(2)).prepare([identity_camera(128, 128, 64.0)])
+    (img, dep), = o.render()
+    assert np.all(img[..., :3] >= 0) and np.all((img[..., 3] >= 0) & (img[..., 3] <= 1)) and np.all(dep >= 0)
+    # many opaque layers: termination
+    n = 30
+    sc = scene_from(np.stack([np.zeros(n), np.zeros(n), np.linspace(2, 4, n)], 1), 1.0, opacities=0.9)
+    o = oracle_mod.Oracle(sc).prepare([cam])
+    (img, _), = o.render()
+    st = o.stats()
+    assert st["terminated_samples"] > 0
+    assert img[32, 32, 3] > 1 - 1e-4
+
+
+# --------------------------------------------------------------------- P11 fovea and compose
+
+def test_P11_fovea_covering_image_equals_full_rate(oracle_mod):
+    """P11: a fovea covering the whole image equals non-foveated
+    rendering with 32x32 assignment and 16x16 items (bit-identical)."""
+    sc = sg.random_scene(4, n=500)
+    cam = identity_camera(96, 64, 48.0)
+    big = sg.Fovea((48, 32), (1000, 1000), 0.1)
+    (a, ad), = oracle_mod.Oracle(sc).prepare([cam], [big], assign_tile=32).render()
+    (b, bd), = oracle_mod.Oracle(sc).prepare([cam], None, assign_tile=32).render()
+    assert np.array_equal(a, b) and np.array_equal(ad, bd)
+
+
+def test_P11_compose_matches_independent_reconstruction(oracle_mod):
+    """P11/O12: HighRes pixels equal the full-rate
+    render; LowRes pixels equal the nearest-neighbour + renormalised 3x3 blur of
+    the 2x2-group-centre samples (obtained independently from a half-pixel
+    shifted full-rate render with an exact window); Hybrid pixels equal
+    w*P + (1-w)*avg2x2(P)."""
+    sc = sg.random_scene(5, n=400, xy_frac=1.3)
+    W, H, T = 256, 192, 32
+    cam = identity_camera(W, H, 100.0)
+    gxc, gyc, rx, ry, rho = 128.0, 96.0, 40.0, 40.0, 0.25
+    fov = sg.Fovea((gxc, gyc), (rx, ry), rho)
+    o = oracle_mod.Oracle(sc).prepare([cam], [fov], assign_tile=T, window_k=4096)
+    (img, dep), = o.render()
+    cls, _ = o.tile_info(0)
+    (full, fulld), = oracle_mod.Oracle(sc).prepare([cam], None, assign_tile=T, window_k=4096).render()
+    shifted = identity_camera(W, H, 100.0, cx=cam.cx - 0.5, cy=cam.cy - 0.5)
+    (sh, shd), = oracle_mod.Oracle(sc).prepare([shifted], None, assign_tile=16, window_k=4096).render()
+    # group (gx, gy) sample = shifted render at pixel (2gx, 2gy)
+    low_s = np.concatenate([sh, shd[..., None]], -1)[0::2, 0::2].astype(np.float64)
+    out = np.concatenate([img, dep[..., None]], -1).astype(np.float64)
+    ref_full = np.concatenate([full, fulld[..., None]], -1).astype(np.float64)
+    jj, ii = np.mgrid[0:H, 0:W]
+    pcls = cls[jj // T, ii // T]
+    hi = pcls == 0
+    assert hi.any() and (pcls == 1).any() and (pcls == 2).any()
+    np.testing.assert_allclose(out[hi], ref_full[hi], rtol=1e-6, atol=1e-6)
+    lowref, low = lowres_compose(low_s, cls, T, W, H)
+    np.testing.assert_allclose(out[low], lowref[low], rtol=1e-5, atol=2e-6)
+    # hybrid
+    px, py = ii + 0.5, jj + 0.5
+    ax = np.maximum(np.abs(px - gxc) - rx, 0) / (rho * 2 * rx)
+    ay = np.maximum(np.abs(py - gyc) - ry, 0) / (rho * 2 * ry)
+    w = np.clip(1 - np.maximum(ax, ay), 0, 1)
+    g = ref_full.reshape(H // 2, 2, W // 2, 2, 5)
+    avg = ((g[:, 0, :, 0] + g[:, 0, :, 1]) + (g[:, 1, :, 0] + g[:, 1, :, 1])) * 0.25
+    avg_px = avg[jj // 2, ii // 2]
+    hyb = pcls == 2
+    ref_h = w[..., None] * ref_full + (1 - w[..., None]) * avg_px
+    np.testing.assert_allclose(out[hyb], ref_h[hyb], rtol=1e-5, atol=2e-6)
+
+
+def test_blur_of_constant_and_impulse():
+    """P11: the reconstruction filter of P:438 keeps a constant and
+    stamps an impulse as 1/16, 2/16, 4/16 (independent check of the helper the
+    compose test above relies on)."""
+    T, W, H = 32, 64, 64
+    cls = np.ones((2, 2), np.int32)
+    s = np.full((32, 32, 5), 0.7)
+    out, low = lowres_compose(s, cls, T, W, H)
+    assert np.allclose(out, 0.7)
+    s = np.zeros((32, 32, 5))
+    s[8, 8] = 1.0  # pixels (16..17, 16..17)
+    out, _ = lowres_compose(s, cls, T, W, H)
+    assert np.isclose(out[15, 15, 0], 1 / 16) and np.isclose(out[16, 16, 0], 9 / 16)
+
+
+# --------------------------------------------------------------------- P13 / P14
+
+@pytest.mark.parametrize("seed", [0, 6])
+def test_P13_large_fov_identity(oracle_mod, seed):
+    """P13 (App. D): crop [W,2W)x[H,2H) of a 3W x 3H render with
+    the principal point shifted by (W, H) is bit-identical to the W x H render:
+    Optimal Projection has no projection error."""
+    sc = sg.random_scene(seed, n=600, z_range=(1.5, 6.0), xy_frac=2.0)
+    W, H = 64, 48
+    small = identity_camera(W, H, 40.0)
+    large = identity_camera(3 * W, 3 * H, 40.0, cx=small.cx + W, cy=small.cy + H)
+    (a, ad), = oracle_mod.Oracle(sc).prepare([small], assign_tile=16).render()
+    (b, bd), = oracle_mod.Oracle(sc).prepare([large], assign_tile=16).render()
+    assert np.array_equal(a, b[H:2 * H, W:2 * W]) and np.array_equal(ad, bd[H:2 * H, W:2 * W])
+
+
+def test_P14_determinism_across_threads(oracle_mod):
+    """P14: byte-identical outputs across runs and thread counts."""
+    sc = sg.random_scene(8, n=800)
+    cams = [identity_camera(128, 96, 60.0), identity_camera(128, 96, 60.0, position=(0.06, 0, 0))]
+    fov = [sg.Fovea((64, 48), (32, 24), 0.1)] * 2
+    outs = []
+    for th in (1, 3, 8):
+        o = oracle_mod.Oracle(sc).prepare(cams, fov, assign_tile=32, threads=th)
+        outs.append((o.render(), o.pairs(), o.counts()))
+    for r in outs[1:]:
+        for (a, ad), (b, bd) in zip(outs[0][0], r[0]):
+            assert np.array_equal(a, b) and np.array_equal(ad, bd)
+        assert np.array_equal(outs[0][1][0], r[1][0]) and np.array_equal(outs[0][1][1], r[1][1])
+        assert np.array_equal(outs[0][2], r[2])
+
+
+def test_keys_sorted_stable_and_ranges(oracle_mod):
+    """O8: the sorted list is the stable sort of the emitted list
+    (ties keep (view, g, tile) emission order); ranges delimit each tile."""
+    sc = sg.random_scene(9, n=500)
+    cams = [identity_camera(128, 96, 60.0), identity_camera(128, 96, 60.0, position=(0.06, 0, 0))]
+    o = oracle_mod.Oracle(sc).prepare(cams, assign_tile=16)
+    ku, vu = o.pairs(False)
+    ks, vs_ = o.pairs(True)
+    order = np.argsort(ku, kind="stable")
+    assert np.array_equal(ks, ku[order]) and np.array_equal(vs_, vu[order])
+    R = o.ranges()
+    tiles = (ks >> np.uint64(32)).astype(np.int64)
+    for t in range(R.shape[0]):
+        assert np.all(tiles[R[t, 0]:R[t, 1]] == t)
+        assert R[t, 1] - R[t, 0] == (tiles == t).sum()
+    # emission order: view-major, then g ascending
+    view_of = (ku >> np.uint64(32)).astype(np.int64) // (8 * 6)
+    assert np.all(np.diff(view_of) >= 0)
