@@ -1,0 +1,190 @@
+/*
+ * vrs.h — C ABI of the B200-native VRSplat render path (libvrs.so).
+ *
+ * Renders 3D Gaussian splats the way VRSplat (arXiv 2505.10144,
+ * /root/reference/PAPER.md, cited "P:line") defines its render path:
+ *   - Optimal Projection: each Gaussian is projected onto the tangent plane of
+ *     the unit sphere at the eye perpendicular to o->mu;
+ *   - Optimal-Projection-compatible tile culling, Eq.4 on the per-Gaussian
+ *     optimal plane, visibility-mask culling with a summed-area
+ *     table;
+ *   - StopThePop per-pixel depth resorting along view rays (P:274-275,
+ *     P:306-309), with the per-tile sort depth taken at the back-projected
+ *     maximum point;
+ *   - single-pass foveated rendering: 32x32 coarse tiles, fovea split into
+ *     16x16 subtiles, 2x2 pixel groups in the periphery, hybrid tiles blended
+ *     with the continuous mask, periphery NN upsample + 3x3 blur.
+ * The exact operation-level contract is DESIGN.md "Numerics contract"
+ * (SURVEY.md §8(c)); the C++ oracle (oracle/) implements the same function
+ * independently and the tests compare the two.
+ *
+ * Conventions
+ *   - All pointers are plain host or device pointers, as stated per argument.
+ *     No function takes ownership of a caller pointer.
+ *   - The context owns the uploaded scene, the visibility masks and every
+ *     scratch buffer; they are sized at vrs_create from vrs_config.max_* and
+ *     never reallocated per frame (no per-frame allocation or host sync).
+ *   - Errors are returned as vrs_status; vrs_last_error() gives a message.
+ *     CUDA errors are sticky per context.  No C++ exception crosses the ABI.
+ *   - A context is not thread-safe; use one context per device and thread.
+ *   - Rendering is a pure, deterministic function of (scene, cameras,
+ *     foveas, masks, config): outputs are bit-identical across runs.
+ */
+#ifndef VRS_H
+#define VRS_H
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define VRS_API __attribute__((visibility("default")))
+#else
+#define VRS_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VRS_ABI_VERSION 1
+#define VRS_MAX_VIEWS 8          /* views per vrs_render_views call */
+#define VRS_MAX_MASK_SLOTS 8
+
+typedef enum {
+    VRS_OK = 0,
+    VRS_E_INVALID_ARG = 1, /* bad argument / camera (non-orthonormal R, bad sizes, ...) */
+    VRS_E_INGEST = 2,      /* scene ingest failure (all records rejected is NOT an error) */
+    VRS_E_CUDA = 3,        /* CUDA runtime error (sticky) */
+    VRS_E_OOM = 4,         /* device allocation failed at create */
+    VRS_E_CAPACITY = 5,    /* a frame exceeded max_pairs; that frame's output is undefined */
+    VRS_E_STATE = 6        /* call out of order (e.g. render before upload) */
+} vrs_status;
+
+typedef struct vrs_context vrs_context;
+
+typedef struct {
+    int32_t device;          /* CUDA device ordinal */
+    int32_t max_views;       /* <= VRS_MAX_VIEWS views per render call */
+    int64_t max_gaussians;   /* upper bound on uploaded Gaussians */
+    int64_t max_pairs;       /* capacity of the Gaussian/tile pair buffers (all views of a call) */
+    int32_t max_width;       /* upper bounds on view resolution */
+    int32_t max_height;
+    int32_t window_k;        /* per-sample StopThePop resort window; only 16 is compiled */
+    int32_t assign_tile;     /* 16 or 32: Gaussian/tile assignment size */
+    int32_t projection;      /* 0 = Optimal Projection (only mode; EWA is a later row) */
+    float near_plane;        /* view-space near cull, 0.2 */
+    float background[3];     /* composited under residual transmittance; (0,0,0) */
+} vrs_config;
+
+/* Pinhole camera, OpenCV axes (x right, y down, z forward).
+ * R_wc: world->camera rotation, row-major, orthonormal within 1e-4 with
+ * det = +1 (else VRS_E_INVALID_ARG).  Pixel (i,j) has its centre at
+ * (i+0.5, j+0.5) and casts the camera-frame ray ((i+0.5-cx)/fx, (j+0.5-cy)/fy, 1).
+ * mask_slot: visibility mask slot (vrs_set_visibility_mask) or -1 = all visible. */
+typedef struct {
+    float R_wc[9];
+    float position[3];
+    float fx, fy, cx, cy;
+    int32_t width, height;
+    int32_t mask_slot;
+} vrs_camera;
+
+/* Single-pass foveation: full-rate rectangle
+ * center +- radius (pixels), linear blend ramp of width ramp*(2*radius)
+ * outside it; requires assign_tile = 32. */
+typedef struct {
+    int32_t enabled;
+    float center[2];
+    float radius[2];
+    float ramp;              /* in [0, 1); paper: 0.10 */
+} vrs_fovea;
+
+typedef struct {
+    int64_t pairs;               /* Gaussian/tile pairs of the last frame (all views) */
+    int64_t samples;             /* rendered samples (pixels + 2x2-group samples) */
+    int64_t evaluations;         /* list entries visited by samples before termination */
+    int64_t contributions;       /* entries inserted into resort windows */
+    int64_t overflow_samples;    /* samples whose window overflowed (approximation events) */
+    int64_t terminated_samples;  /* samples that stopped at T < 1e-4 */
+    int32_t tiles_by_class[4];   /* HighRes, LowRes, Hybrid, Invisible coarse tiles */
+    int64_t work_items;          /* blocks of the single blend launch */
+    int64_t visible_splats;      /* (view, Gaussian) with >= 1 pair */
+    float stage_ms[8];           /* preprocess, scan, duplicate, sort, ranges, blend, compose, total
+                                    (filled only when timing is enabled) */
+} vrs_frame_stats;
+
+/* Create a context on cfg->device; allocates all device memory.
+ * Errors: VRS_E_INVALID_ARG (bad cfg), VRS_E_OOM, VRS_E_CUDA. */
+VRS_API vrs_status vrs_create(const vrs_config* cfg, vrs_context** out);
+VRS_API void vrs_destroy(vrs_context* ctx);
+VRS_API const char* vrs_last_error(const vrs_context* ctx);
+VRS_API int32_t vrs_abi_version(void);
+
+/* Upload raw 3DGS attributes (HOST pointers, copied):
+ * means n*3, quats_wxyz n*4, log_scales n*3, opacity_logits n,
+ * sh n*(deg+1)^2*3 (coefficient-major RGB).  Activation on the host in
+ * double (exp / sigmoid / quaternion normalisation, Sigma = R S S^T R^T,
+ * Eq.1; q_cut = 2 ln(255 sigma)), rounded once to float.
+ * Non-finite records are dropped and counted in *n_rejected (may be NULL);
+ * Gaussian indices are those of the kept records in input order.
+ * Errors: VRS_E_INVALID_ARG (n > max_gaussians, deg not in 0..3). */
+VRS_API vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_degree, const float* means,
+                                const float* quats_wxyz, const float* log_scales, const float* opacity_logits,
+                                const float* sh, int64_t* n_rejected);
+
+/* Visibility mask for a slot (HOST pointer, w*h bytes, row-major, >0 =
+ * visible).  mask == NULL clears the slot (all visible). */
+VRS_API vrs_status vrs_set_visibility_mask(vrs_context* ctx, int32_t slot, int32_t w, int32_t h, const uint8_t* mask);
+
+/* Render n_views views (one frame: all views share one sort and one blend
+ * launch).  cams: HOST array of n_views cameras; fovea: HOST array of n_views
+ * entries or NULL (no foveation).  rgba: DEVICE float buffer, views
+ * concatenated, each H*W*4 (RGB premultiplied = C + T*bg, A = 1 - T);
+ * depth: DEVICE float buffer, each H*W (premultiplied expected ray distance,
+ * SURVEY L13).  Enqueued on `stream` (a cudaStream_t, NULL = legacy default);
+ * returns without synchronising (a per-eye setup cache miss — new
+ * resolution, mask or fovea — synchronises once).  Errors: VRS_E_INVALID_ARG,
+ * VRS_E_STATE, VRS_E_CUDA.  A frame whose pairs exceed max_pairs is reported
+ * as VRS_E_CAPACITY by vrs_get_frame_stats (its output is undefined). */
+VRS_API vrs_status vrs_render_views(vrs_context* ctx, int32_t n_views, const vrs_camera* cams, const vrs_fovea* fovea,
+                            float* rgba, float* depth, void* stream);
+
+/* Same as vrs_render_views but the outputs are HOST buffers (pinned memory
+ * recommended): renders into context-owned device buffers, copies back on
+ * `stream` and synchronises the stream before returning (end-to-end path). */
+VRS_API vrs_status vrs_render_views_host(vrs_context* ctx, int32_t n_views, const vrs_camera* cams,
+                                 const vrs_fovea* fovea, float* rgba_host, float* depth_host, void* stream);
+
+/* Detailed counters (evaluations, contributions, overflow) cost atomics;
+ * stage timing costs events.  Both off by default. */
+VRS_API vrs_status vrs_set_instrumentation(vrs_context* ctx, int32_t counters, int32_t timing);
+
+/* Synchronises the last frame's stream and returns its statistics.
+ * Returns VRS_E_CAPACITY if that frame overflowed max_pairs. */
+VRS_API vrs_status vrs_get_frame_stats(vrs_context* ctx, vrs_frame_stats* out);
+
+/* ---- parity hooks (synchronise; HOST output pointers) ---- */
+/* Per-(view, Gaussian) exact pair counts of the last frame, n_views*N u32. */
+VRS_API vrs_status vrs_debug_counts(vrs_context* ctx, uint32_t* counts, int64_t capacity, int64_t* n_out);
+/* Pair keys ((global tile << 32) | f32 bits of the tile depth) and values
+ * (Gaussian index), sorted (sorted=1) or in emission order (sorted=0). */
+VRS_API vrs_status vrs_debug_pairs(vrs_context* ctx, int32_t sorted, uint64_t* keys, uint32_t* vals, int64_t capacity,
+                           int64_t* n_out);
+/* [start, end) per global tile (views concatenated), 2 u32 per tile. */
+VRS_API vrs_status vrs_debug_ranges(vrs_context* ctx, uint32_t* ranges, int64_t capacity, int64_t* n_out);
+/* Per-Gaussian projected records of one view in the oracle's 48-float
+ * semantic layout. */
+VRS_API vrs_status vrs_debug_splats(vrs_context* ctx, int32_t view, float* out, int64_t capacity);
+/* Per coarse tile class (0 High, 1 Low, 2 Hybrid, 3 Invisible) and visibility bit. */
+VRS_API vrs_status vrs_debug_tile_info(vrs_context* ctx, int32_t view, int32_t* cls, int32_t* vis, int64_t capacity);
+
+/* ---- primitives exposed for tests (DEVICE pointers, enqueued on stream) ---- */
+/* Stable LSD onesweep radix sort of n (key, value) pairs in place by the low
+ * key_bits bits of the key (n <= max_pairs).  */
+VRS_API vrs_status vrs_sort_pairs(vrs_context* ctx, uint64_t* keys, uint32_t* vals, int64_t n, int32_t key_bits, void* stream);
+/* Exclusive prefix sum of n u32 (n <= max_views*max_gaussians); *total (DEVICE) gets the sum. */
+VRS_API vrs_status vrs_exclusive_scan(vrs_context* ctx, const uint32_t* in, uint32_t* out, uint32_t* total, int64_t n,
+                              void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VRS_H */

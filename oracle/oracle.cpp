@@ -558,6 +558,7 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
         float den = quad3(sp.A, x, y, 1.0f);
         float dtb = std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2]));
         float tau = dtb / den;  // depth of max density along this pixel's ray
+        if (tau != tau) tau = INFINITY;  // total order for the window (DESIGN R4)
         st.contribs++;
         WEnt ent{tau, g, alpha};
         auto pos = std::upper_bound(win.begin(), win.end(), ent, [](const WEnt& a, const WEnt& c) {
@@ -904,16 +905,21 @@ int orc_render(void* h, float* rgba, float* depth) {
                     if (c == CLS_LOW) {
                         for (int gy = 0; 2 * gy < std::min(T, He - y0); gy++)
                             for (int gx = 0; 2 * gx < std::min(T, We - x0); gx++) {
+                                bool in = x0 + 2 * gx < W && y0 + 2 * gy < H;
+                                SampleStats dummy;
                                 low[(size_t)(y0 / 2 + gy) * (We / 2) + x0 / 2 + gx] =
-                                    render_sample(O, v, gt, (float)(x0 + 2 * gx + 1), (float)(y0 + 2 * gy + 1), sts[t]);
-                                nsamp[t]++;
+                                    render_sample(O, v, gt, (float)(x0 + 2 * gx + 1), (float)(y0 + 2 * gy + 1),
+                                                  in ? sts[t] : dummy);
+                                nsamp[t] += in;
                             }
                     } else {
                         for (int y = y0; y < std::min(y0 + T, He); y++)
                             for (int x = x0; x < std::min(x0 + T, We); x++) {
+                                bool in = x < W && y < H;
+                                SampleStats dummy;
                                 full[(size_t)y * We + x] =
-                                    render_sample(O, v, gt, (float)x + 0.5f, (float)y + 0.5f, sts[t]);
-                                nsamp[t]++;
+                                    render_sample(O, v, gt, (float)x + 0.5f, (float)y + 0.5f, in ? sts[t] : dummy);
+                                nsamp[t] += in;
                             }
                     }
                 }

@@ -1,0 +1,352 @@
+// Steps 5-7: per-tile ranges, the single foveated blend launch
+// and the periphery compose.
+//
+// Blend: ONE launch whose 256-thread blocks
+// are either 16x16 full-rate items (HighRes / Hybrid subtiles of a
+// 32x32 coarse tile, or 16x16 tiles when assigning at 16), or 32x32 LowRes
+// tiles where every thread renders one 2x2 pixel group sampled at the group
+// centre.  All items stream their coarse tile's sorted list in key
+// order.  Batches of 256 splat records are staged in shared memory;
+// each warp covers an 8x4 block of samples and skips, warp-uniformly, every
+// splat whose conservative pixel footprint misses the block (the
+// hierarchical culling of P:431 — it never changes results, only work).  Each
+// sample runs the StopThePop per-pixel resort: a
+// K = 16 entry window ordered by (tau, g) kept in shared memory (a per-thread
+// ring buffer, bank-conflict free), popping the nearest entry on overflow and
+// blending front to back (Eq.2 with product transmittance), terminating once
+// T < 1e-4 (checked after blending).  Hybrid pixels blend their value with
+// the 2x2 group average via warp shuffles.
+#include "vrs_internal.cuh"
+
+namespace vrs {
+
+__global__ void k_ranges(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ n_dev, int64_t cap,
+                         uint32_t* ranges, int64_t n_tiles) {
+    const int64_t n = min((int64_t)*n_dev, cap);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t t = (uint32_t)(keys[i] >> 32);
+        if (t >= n_tiles) continue;  // only after a capacity overflow (undefined frame)
+        if (i == 0 || (uint32_t)(keys[i - 1] >> 32) != t) ranges[2 * (size_t)t] = (uint32_t)i;
+        if (i == n - 1 || (uint32_t)(keys[i + 1] >> 32) != t) ranges[2 * (size_t)t + 1] = (uint32_t)(i + 1);
+    }
+}
+
+void launch_ranges(const uint64_t* keys, const uint32_t* n_dev, int64_t cap, uint32_t* ranges, int64_t n_tiles,
+                   cudaStream_t st) {
+    cudaMemsetAsync(ranges, 0, sizeof(uint32_t) * 2 * (size_t)n_tiles, st);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    k_ranges<<<sms * 4, 256, 0, st>>>(keys, n_dev, cap, ranges, n_tiles);
+}
+
+namespace {
+
+struct BlendSmem {
+    float4 r0[kBlend];   // u.xyz, q_cut
+    float4 r1[kBlend];   // e1.x, e1.z, e2.x, e2.y
+    float4 r2[kBlend];   // e2.z, C00, C01, C11
+    float4 r3[kBlend];   // A a, b, c, p
+    float4 r4[kBlend];   // A e, f, b.x, b.y
+    float2 r5[kBlend];   // b.z, sigma
+    uint32_t g[kBlend];
+    uint32_t mask[kBlend];
+    float4 wblock[8];    // per-warp sample extent xmin, xmax, ymin, ymax (pixel coords)
+    float w_tau[kWindow][kBlend];
+    uint32_t w_g[kWindow][kBlend];
+    float w_a[kWindow][kBlend];
+    unsigned long long cnt[4];
+};
+
+__device__ __forceinline__ bool win_less(float ta, uint32_t ga, float tb, uint32_t gb) {
+    return ta < tb || (ta == tb && ga < gb);
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(kBlend, 2) k_blend(FrameParams fp, FrameBufs fb, float* __restrict__ rgba,
+                                                      float* __restrict__ depth) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    BlendSmem& S = *reinterpret_cast<BlendSmem*>(smem_raw);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    // locate the view and the item
+    int vi = 0;
+    const int item = blockIdx.x;
+    while (vi + 1 < fp.n_views && item >= fp.v[vi + 1].item_off) vi++;
+    const ViewParams& v = fp.v[vi];
+    const uint32_t it = v.items[item - v.item_off];
+    const int tile = (int)(it & 0xfffffu), sub = (int)((it >> 20) & 3u), kind = (int)(it >> 22);
+    const int T = fp.T;
+    const int tx = tile % v.tw, ty = tile / v.tw;
+    const int x0 = tx * T, y0 = ty * T;
+    const int lx = lane & 7, ly = lane >> 3, wx = (warp & 1) * 8, wy = (warp >> 1) * 4;
+    const int sx = wx + lx, sy = wy + ly;
+    int px, py;  // pixel (full-rate) or group origin pixel (low)
+    float xs, ys;
+    if (kind == kItemLow) {
+        px = x0 + 2 * sx;
+        py = y0 + 2 * sy;
+        xs = (float)(px + 1);
+        ys = (float)(py + 1);
+    } else {
+        const int ox = x0 + (T == 32 ? 16 * (sub & 1) : 0), oy = y0 + (T == 32 ? 16 * (sub >> 1) : 0);
+        px = ox + sx;
+        py = oy + sy;
+        xs = (float)px + 0.5f;
+        ys = (float)py + 0.5f;
+    }
+    if (tid < 8) {
+        const int wwx = (tid & 1) * 8, wwy = (tid >> 1) * 4;
+        float4 b;
+        if (kind == kItemLow) {
+            b = make_float4((float)(x0 + 2 * wwx + 1), (float)(x0 + 2 * (wwx + 7) + 1), (float)(y0 + 2 * wwy + 1),
+                            (float)(y0 + 2 * (wwy + 3) + 1));
+        } else {
+            const int ox = x0 + (T == 32 ? 16 * (sub & 1) : 0), oy = y0 + (T == 32 ? 16 * (sub >> 1) : 0);
+            b = make_float4((float)(ox + wwx) + 0.5f, (float)(ox + wwx + 7) + 0.5f, (float)(oy + wwy) + 0.5f,
+                            (float)(oy + wwy + 3) + 0.5f);
+        }
+        S.wblock[tid] = b;
+    }
+    if (tid < 4) S.cnt[tid] = 0ull;
+    const float x = (xs - v.cx) / v.fx;
+    const float y = (ys - v.cy) / v.fy;
+    const float dn = sqrtf(fmaf(x, x, fmaf(y, y, 1.0f)));
+    const uint32_t rb = fb.ranges[2 * (size_t)(v.tile_base + tile)];
+    const uint32_t re = fb.ranges[2 * (size_t)(v.tile_base + tile) + 1];
+    const float4* __restrict__ recv = fb.rec + (size_t)vi * fp.N * kRecF4;
+
+    float Tr = 1.0f, Cr = 0.0f, Cg = 0.0f, Cb = 0.0f, Dd = 0.0f;
+    bool done = false, overflowed = false;
+    int head = 0, cnt = 0;
+    uint32_t n_contrib = 0, stop_pos = re;
+
+    auto blend_one = [&](float tau, uint32_t g, float a) {
+        const float4 col = __ldg(recv + (size_t)g * kRecF4 + 6);
+        const float wgt = a * Tr;
+        Cr = fmaf(col.x, wgt, Cr);
+        Cg = fmaf(col.y, wgt, Cg);
+        Cb = fmaf(col.z, wgt, Cb);
+        Dd = fmaf(tau * dn, wgt, Dd);
+        Tr = Tr * (1.0f - a);
+        if (Tr < kTmin) done = true;
+    };
+
+    for (uint32_t base = rb; base < re; base += kBlend) {
+        __syncthreads();
+        const uint32_t idx = base + tid;
+        if (idx < re) {
+            uint32_t g = __ldg(fb.vals + idx);
+            g = (g < (uint32_t)fp.N) ? g : 0u;  // memory safety after a capacity overflow only
+            const float4* rp = recv + (size_t)g * kRecF4;
+            const float4 a0 = __ldg(rp + 0), a1 = __ldg(rp + 1), a2 = __ldg(rp + 2), a3 = __ldg(rp + 3),
+                         a4 = __ldg(rp + 4), a5 = __ldg(rp + 5), a7 = __ldg(rp + 7);
+            S.r0[tid] = a0; S.r1[tid] = a1; S.r2[tid] = a2; S.r3[tid] = a3; S.r4[tid] = a4;
+            S.r5[tid] = make_float2(a5.x, a5.y);
+            S.g[tid] = g;
+            uint32_t m = 0;
+#pragma unroll
+            for (int w = 0; w < 8; w++) {
+                const float4 b = S.wblock[w];
+                const bool hit = !(a7.y < b.x || a7.x > b.y || a7.w < b.z || a7.z > b.w);
+                m |= hit ? (1u << w) : 0u;
+            }
+            S.mask[tid] = fp.no_cull ? 0xffu : m;
+        }
+        if (__syncthreads_count(!done) == 0) break;
+        const int nb = min((int)(re - base), kBlend);
+        if (__all_sync(0xffffffffu, done)) continue;
+        for (int j = 0; j < nb; j++) {
+            if (!((S.mask[j] >> warp) & 1u)) continue;
+            if (done) continue;
+            const float4 a0 = S.r0[j], a1 = S.r1[j], a2 = S.r2[j];
+            const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
+            const float ex = fmaf(a1.x, x, a1.y);
+            const float ey = fmaf(a1.z, x, fmaf(a1.w, y, a2.x));
+            const float cx = fmaf(a2.y, ex, a2.z * ey), cy = fmaf(a2.z, ex, a2.w * ey);
+            const float num = fmaf(ex, cx, ey * cy);
+            const float ss = s * s;
+            if (!(s > 0.0f) || !(num <= a0.w * ss)) continue;
+            // contribution: alpha (tolerance-only), tau (decision, IEEE)
+            const float4 a3 = S.r3[j], a4 = S.r4[j];
+            const float2 a5 = S.r5[j];
+            const float q = __fdividef(num, ss);
+            const float alpha = fminf(kAlphaMax, a5.y * __expf(-0.5f * q));
+            const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
+            const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, a5.x));
+            float tau = __fdiv_rn(dtb, den);
+            if (tau != tau) tau = __int_as_float(0x7f800000);
+            const uint32_t g = S.g[j];
+            n_contrib++;
+            if (cnt == kWindow) {
+                overflowed = true;
+                const float th = S.w_tau[head][tid];
+                const uint32_t gh = S.w_g[head][tid];
+                if (win_less(tau, g, th, gh)) {
+                    blend_one(tau, g, alpha);
+                    if (done) stop_pos = base + j;
+                    continue;
+                }
+                blend_one(th, gh, S.w_a[head][tid]);
+                head = (head + 1 == kWindow) ? 0 : head + 1;
+                cnt--;
+                if (done) { stop_pos = base + j; continue; }
+            }
+            // insertion from the tail
+            int pos = cnt;
+            while (pos > 0) {
+                int jj = head + pos - 1;
+                jj -= (jj >= kWindow) ? kWindow : 0;
+                const float tj = S.w_tau[jj][tid];
+                const uint32_t gj = S.w_g[jj][tid];
+                if (!win_less(tau, g, tj, gj)) break;
+                int dst = jj + 1;
+                dst -= (dst >= kWindow) ? kWindow : 0;
+                S.w_tau[dst][tid] = tj;
+                S.w_g[dst][tid] = gj;
+                S.w_a[dst][tid] = S.w_a[jj][tid];
+                pos--;
+            }
+            int dst = head + pos;
+            dst -= (dst >= kWindow) ? kWindow : 0;
+            S.w_tau[dst][tid] = tau;
+            S.w_g[dst][tid] = g;
+            S.w_a[dst][tid] = alpha;
+            cnt++;
+        }
+    }
+    // drain the window in order
+    while (cnt > 0 && !done) {
+        blend_one(S.w_tau[head][tid], S.w_g[head][tid], S.w_a[head][tid]);
+        head = (head + 1 == kWindow) ? 0 : head + 1;
+        cnt--;
+    }
+    // outputs
+    const float oR = Cr + Tr * fp.bg[0], oG = Cg + Tr * fp.bg[1], oB = Cb + Tr * fp.bg[2], oA = 1.0f - Tr;
+    if (kind == kItemLow) {
+        if (px < v.W && py < v.H) {
+            const size_t li = (size_t)v.low_off + (size_t)(py >> 1) * v.low_w + (px >> 1);
+            fb.low_rgba[li] = make_float4(oR, oG, oB, oA);
+            fb.low_depth[li] = Dd;
+        }
+    } else if (kind == kItemHybrid) {
+        // group (lanes l&~9, |1, |8, |9) average, then w*P + (1-w)*avg
+        const int l0 = lane & ~9;
+        float vals[5] = {oR, oG, oB, oA, Dd};
+        float outv[5];
+        const float wgt = fovea_weight(v, (float)px + 0.5f, (float)py + 0.5f);
+#pragma unroll
+        for (int c = 0; c < 5; c++) {
+            const float p00 = __shfl_sync(0xffffffffu, vals[c], l0);
+            const float p01 = __shfl_sync(0xffffffffu, vals[c], l0 | 1);
+            const float p10 = __shfl_sync(0xffffffffu, vals[c], l0 | 8);
+            const float p11 = __shfl_sync(0xffffffffu, vals[c], l0 | 9);
+            const float avg = ((p00 + p01) + (p10 + p11)) * 0.25f;
+            outv[c] = fmaf(wgt, vals[c] - avg, avg);
+        }
+        if (px < v.W && py < v.H) {
+            const size_t pi = (size_t)v.pix_off + (size_t)py * v.W + px;
+            reinterpret_cast<float4*>(rgba)[pi] = make_float4(outv[0], outv[1], outv[2], outv[3]);
+            depth[pi] = outv[4];
+        }
+    } else {
+        if (px < v.W && py < v.H) {
+            const size_t pi = (size_t)v.pix_off + (size_t)py * v.W + px;
+            reinterpret_cast<float4*>(rgba)[pi] = make_float4(oR, oG, oB, oA);
+            depth[pi] = Dd;
+        }
+    }
+    if (fp.counters) {
+        // evaluations: list entries visited before termination
+        const unsigned long long ev = done ? (unsigned long long)(stop_pos - rb + 1) : (unsigned long long)(re - rb);
+        const bool in_img = (px < v.W && py < v.H);
+        unsigned long long c0 = in_img ? ev : 0ull, c1 = in_img ? n_contrib : 0u,
+                           c2 = (in_img && overflowed) ? 1u : 0u, c3 = (in_img && done) ? 1u : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+            c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+            c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+            c3 += __shfl_xor_sync(0xffffffffu, c3, o);
+        }
+        __syncthreads();
+        if (lane == 0) {
+            atomicAdd(&S.cnt[0], c0);
+            atomicAdd(&S.cnt[1], c1);
+            atomicAdd(&S.cnt[2], c2);
+            atomicAdd(&S.cnt[3], c3);
+        }
+        __syncthreads();
+        if (tid == 0) {
+            atomicAdd(&fb.stats[0], S.cnt[0]);
+            atomicAdd(&fb.stats[1], S.cnt[1]);
+            atomicAdd(&fb.stats[2], S.cnt[2]);
+            atomicAdd(&fb.stats[3], S.cnt[3]);
+        }
+    }
+}
+
+void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
+                  cudaStream_t st) {
+    if (total_items <= 0) return;
+    const size_t smem = sizeof(BlendSmem);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_blend, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
+    k_blend<<<total_items, kBlend, smem, st>>>(fp, fb, rgba, depth);
+}
+
+// Step 7: periphery reconstruction: nearest-neighbour upsample of the
+// LowRes group samples and a 3x3 (1,2,1)x(1,2,1) blur restricted to LowRes
+// pixels in the image, renormalised; invisible tiles get the
+// background with A = 0, D = 0.  HighRes/Hybrid pixels were written by the blend.
+__global__ void k_compose(FrameParams fp, FrameBufs fb, float* __restrict__ rgba, float* __restrict__ depth,
+                          int64_t total_px) {
+    const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi >= total_px) return;
+    int vi = 0;
+    while (vi + 1 < fp.n_views && gi >= fp.v[vi + 1].pix_off) vi++;
+    const ViewParams& v = fp.v[vi];
+    const int64_t k = gi - v.pix_off;
+    const int i = (int)(k % v.W), j = (int)(k / v.W);
+    const int T = fp.T;
+    const int c = v.cls[(j / T) * v.tw + (i / T)];
+    if (c == kHigh || c == kHybrid) return;
+    if (c == kInvisible) {
+        reinterpret_cast<float4*>(rgba)[gi] = make_float4(fp.bg[0], fp.bg[1], fp.bg[2], 0.0f);
+        depth[gi] = 0.0f;
+        return;
+    }
+    float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f}, ws = 0.0f;
+#pragma unroll
+    for (int dj = -1; dj <= 1; dj++)
+#pragma unroll
+        for (int di = -1; di <= 1; di++) {
+            const int ii = i + di, jj = j + dj;
+            if (ii < 0 || jj < 0 || ii >= v.W || jj >= v.H) continue;
+            if (v.cls[(jj / T) * v.tw + (ii / T)] != kLow) continue;
+            const float w = (float)((2 - abs(di)) * (2 - abs(dj)));
+            const size_t li = (size_t)v.low_off + (size_t)(jj >> 1) * v.low_w + (ii >> 1);
+            const float4 p = fb.low_rgba[li];
+            acc[0] = fmaf(w, p.x, acc[0]);
+            acc[1] = fmaf(w, p.y, acc[1]);
+            acc[2] = fmaf(w, p.z, acc[2]);
+            acc[3] = fmaf(w, p.w, acc[3]);
+            acc[4] = fmaf(w, fb.low_depth[li], acc[4]);
+            ws += w;
+        }
+    const float inv = 1.0f / ws;
+    reinterpret_cast<float4*>(rgba)[gi] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+    depth[gi] = acc[4] * inv;
+}
+
+void launch_compose(const FrameParams& fp, FrameBufs fb, float* rgba, float* depth, cudaStream_t st) {
+    int64_t total = 0;
+    for (int i = 0; i < fp.n_views; i++) total += (int64_t)fp.v[i].W * fp.v[i].H;
+    if (total == 0) return;
+    k_compose<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(fp, fb, rgba, depth, total);
+}
+
+}  // namespace vrs

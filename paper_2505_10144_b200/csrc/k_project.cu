@@ -1,0 +1,487 @@
+// Per-Gaussian stage and Gaussian/tile
+// instantiation (step 3): Optimal Projection, SH colour,
+// conservative footprint, exact per-tile culling with Eq.4 on the optimal
+// plane, StopThePop per-tile depth at the back-projected maximum
+// point and visibility-mask skipping through the SAT.
+//
+// One thread per Gaussian; the Gaussian's attributes are read once and
+// projected for every view of the frame (stereo fusion of the per-Gaussian
+// stage, the "fusion of stereo rendering passes" of P:735).
+#include "vrs_internal.cuh"
+
+namespace vrs {
+
+struct Proj {
+    int valid;
+    float muc[3], u[3], e1[3], e2[3];
+    float S2[3], C[3], eps;
+    float A[6], bv[3];
+    float sigma, qcut;
+    int rect[4];
+    float bbox[4];
+};
+
+// O1-O6 (DESIGN "Numerics contract"): view transform and near cull,
+// optimal-plane frame, projected covariance with pixel-mapped dilation,
+// conic, depth coefficients, cone-vs-frustum cull and conic footprint.
+__device__ void project_splat(const ViewParams& v, float4 m4, float4 c0, float4 c1, float4 i0, float4 i1, int T,
+                              float near_plane, Proj& p) {
+    p.valid = 0;
+    p.rect[0] = 0; p.rect[1] = 0; p.rect[2] = -1; p.rect[3] = -1;
+    p.qcut = m4.w;
+    p.sigma = c1.z;
+    const float vx = m4.x - v.o[0], vy = m4.y - v.o[1], vz = m4.z - v.o[2];
+    p.muc[0] = dot3(v.R[0], v.R[1], v.R[2], vx, vy, vz);
+    p.muc[1] = dot3(v.R[3], v.R[4], v.R[5], vx, vy, vz);
+    p.muc[2] = dot3(v.R[6], v.R[7], v.R[8], vx, vy, vz);
+    if (!(p.muc[2] > near_plane) || p.qcut < 0.0f) return;
+    // optimal plane frame
+    const float r2 = dot3(p.muc[0], p.muc[1], p.muc[2], p.muc[0], p.muc[1], p.muc[2]);
+    const float r = sqrtf(r2);
+    const float inv_r = 1.0f / r;
+    p.u[0] = p.muc[0] * inv_r; p.u[1] = p.muc[1] * inv_r; p.u[2] = p.muc[2] * inv_r;
+    const float h = sqrtf(fmaf(p.u[2], p.u[2], p.u[0] * p.u[0]));
+    const float ih = 1.0f / h;
+    p.e1[0] = p.u[2] * ih; p.e1[1] = 0.0f; p.e1[2] = -(p.u[0] * ih);
+    p.e2[0] = p.u[1] * p.e1[2];
+    p.e2[1] = fmaf(p.u[2], p.e1[0], -(p.u[0] * p.e1[2]));
+    p.e2[2] = -(p.u[1] * p.e1[0]);
+    // Sigma_c = W Sigma_w W^T: T = W*Sigma (row i of W dot column j), then T*W^T
+    const float S[3][3] = {{c0.x, c0.y, c0.z}, {c0.y, c0.w, c1.x}, {c0.z, c1.x, c1.y}};
+    float Tm[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) Tm[i][j] = dot3(v.R[3 * i], v.R[3 * i + 1], v.R[3 * i + 2], S[0][j], S[1][j], S[2][j]);
+    float Sc[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = i; j < 3; j++) Sc[i][j] = dot3(Tm[i][0], Tm[i][1], Tm[i][2], v.R[3 * j], v.R[3 * j + 1], v.R[3 * j + 2]);
+    Sc[1][0] = Sc[0][1]; Sc[2][0] = Sc[0][2]; Sc[2][1] = Sc[1][2];
+    float P1[3], P2[3];
+#pragma unroll
+    for (int i = 0; i < 3; i++) {
+        P1[i] = dot3(Sc[i][0], Sc[i][1], Sc[i][2], p.e1[0], p.e1[1], p.e1[2]);
+        P2[i] = dot3(Sc[i][0], Sc[i][1], Sc[i][2], p.e2[0], p.e2[1], p.e2[2]);
+    }
+    const float ir2 = inv_r * inv_r;
+    float s00 = dot3(p.e1[0], p.e1[1], p.e1[2], P1[0], P1[1], P1[2]) * ir2;
+    float s01 = dot3(p.e1[0], p.e1[1], p.e1[2], P2[0], P2[1], P2[2]) * ir2;
+    float s11 = dot3(p.e2[0], p.e2[1], p.e2[2], P2[0], P2[1], P2[2]) * ir2;
+    // pixel-mapped dilation (+0.3 px^2 at the mean's image position)
+    const float jx = p.u[2] / v.fx, jy = p.u[2] / v.fy;
+    const float J00 = p.e1[0] * jx, J01 = p.e1[1] * jy, J10 = p.e2[0] * jx, J11 = p.e2[1] * jy;
+    const float d00 = fmaf(J00, J00, J01 * J01), d01 = fmaf(J00, J10, J01 * J11), d11 = fmaf(J10, J10, J11 * J11);
+    s00 = fmaf(0.3f, d00, s00);
+    s01 = fmaf(0.3f, d01, s01);
+    s11 = fmaf(0.3f, d11, s11);
+    p.S2[0] = s00; p.S2[1] = s01; p.S2[2] = s11;
+    const float det = fmaf(s00, s11, -(s01 * s01));
+    if (!(det > 0.0f)) return;
+    const float idet = 1.0f / det;
+    p.C[0] = s11 * idet; p.C[1] = -s01 * idet; p.C[2] = s00 * idet;
+    p.eps = 0.5f / sqrtf(fmaf(p.qcut, s00 + s11, 1.0f));
+    // depth coefficients: A = W Sigma_w^-1 W^T (same product order), b = A mu_c
+    const float Si[3][3] = {{i0.x, i0.y, i0.z}, {i0.y, i0.w, i1.x}, {i0.z, i1.x, i1.y}};
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) Tm[i][j] = dot3(v.R[3 * i], v.R[3 * i + 1], v.R[3 * i + 2], Si[0][j], Si[1][j], Si[2][j]);
+    float Ai[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = i; j < 3; j++) Ai[i][j] = dot3(Tm[i][0], Tm[i][1], Tm[i][2], v.R[3 * j], v.R[3 * j + 1], v.R[3 * j + 2]);
+    Ai[1][0] = Ai[0][1]; Ai[2][0] = Ai[0][2]; Ai[2][1] = Ai[1][2];
+    p.A[0] = Ai[0][0]; p.A[1] = 2.0f * Ai[0][1]; p.A[2] = Ai[1][1];
+    p.A[3] = 2.0f * Ai[0][2]; p.A[4] = 2.0f * Ai[1][2]; p.A[5] = Ai[2][2];
+#pragma unroll
+    for (int i = 0; i < 3; i++) p.bv[i] = dot3(Ai[i][0], Ai[i][1], Ai[i][2], p.muc[0], p.muc[1], p.muc[2]);
+    // O6(a) cone vs frustum side planes (double, conservative margin)
+    const double S00 = s00, S01 = s01, S11 = s11;
+    const double lmax = 0.5 * (S00 + S11) + sqrt(0.25 * (S00 - S11) * (S00 - S11) + S01 * S01);
+    const double t2 = (double)p.qcut * lmax;
+    const double sinb = sqrt(t2 / (1.0 + t2));
+    const double ud0 = p.u[0], ud1 = p.u[1], ud2 = p.u[2];
+    {
+        const double xl = (0.0 - v.cx) / v.fx, xr = ((double)v.W - v.cx) / v.fx;
+        const double yt = (0.0 - v.cy) / v.fy, yb = ((double)v.H - v.cy) / v.fy;
+        const double N[4][3] = {{1.0, 0.0, -xl}, {-1.0, 0.0, xr}, {0.0, 1.0, -yt}, {0.0, -1.0, yb}};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const double nn = sqrt(N[k][0] * N[k][0] + N[k][1] * N[k][1] + N[k][2] * N[k][2]);
+            const double nu = (N[k][0] * ud0 + N[k][1] * ud1 + N[k][2] * ud2) / nn;
+            if (nu < -(sinb + 1e-4)) return;
+        }
+    }
+    p.valid = 1;
+    // O6(b,c) conic bounding box on the image plane (double), whole-screen fallback
+    const double W = v.W, H = v.H;
+    double xmin, xmax, ymin, ymax;
+    bool whole = !(ud2 > sinb + 1e-3);
+    if (!whole) {
+        const double e1d[3] = {p.e1[0], p.e1[1], p.e1[2]}, e2d[3] = {p.e2[0], p.e2[1], p.e2[2]};
+        const double ud[3] = {ud0, ud1, ud2};
+        double G[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) {
+                double mf = (double)p.C[0] * e1d[i] * e1d[j] + (double)p.C[1] * (e1d[i] * e2d[j] + e2d[i] * e1d[j]) +
+                            (double)p.C[2] * e2d[i] * e2d[j];
+                G[i][j] = mf - (double)p.qcut * ud[i] * ud[j];
+            }
+        const double Ki[3][3] = {{1.0 / v.fx, 0.0, -(double)v.cx / v.fx},
+                                 {0.0, 1.0 / v.fy, -(double)v.cy / v.fy},
+                                 {0.0, 0.0, 1.0}};
+        double Tq[3][3], Q[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) {
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < 3; k++) acc += G[i][k] * Ki[k][j];
+                Tq[i][j] = acc;
+            }
+#pragma unroll
+        for (int i = 0; i < 3; i++)
+#pragma unroll
+            for (int j = 0; j < 3; j++) {
+                double acc = 0.0;
+#pragma unroll
+                for (int k = 0; k < 3; k++) acc += Ki[k][i] * Tq[k][j];
+                Q[i][j] = acc;
+            }
+        const double a00 = Q[1][1] * Q[2][2] - Q[1][2] * Q[1][2];
+        const double a11 = Q[0][0] * Q[2][2] - Q[0][2] * Q[0][2];
+        const double a22 = Q[0][0] * Q[1][1] - Q[0][1] * Q[0][1];
+        const double a02 = Q[0][1] * Q[1][2] - Q[0][2] * Q[1][1];
+        const double a12 = Q[0][1] * Q[0][2] - Q[0][0] * Q[1][2];
+        const double dx = a02 * a02 - a00 * a22, dy = a12 * a12 - a11 * a22;
+        if (a22 != 0.0 && dx >= 0.0 && dy >= 0.0 && isfinite(dx) && isfinite(dy)) {
+            const double sx = sqrt(dx), sy = sqrt(dy);
+            const double xa = (a02 - sx) / a22, xb = (a02 + sx) / a22;
+            const double ya = (a12 - sy) / a22, yb = (a12 + sy) / a22;
+            xmin = fmin(xa, xb); xmax = fmax(xa, xb);
+            ymin = fmin(ya, yb); ymax = fmax(ya, yb);
+        } else {
+            whole = true;
+        }
+    }
+    if (whole) { xmin = -1.0; xmax = W + 1.0; ymin = -1.0; ymax = H + 1.0; }
+    xmin -= 1.0; xmax += 1.0; ymin -= 1.0; ymax += 1.0;
+    p.bbox[0] = (float)fmax(xmin, -2.0); p.bbox[1] = (float)fmin(xmax, W + 2.0);
+    p.bbox[2] = (float)fmax(ymin, -2.0); p.bbox[3] = (float)fmin(ymax, H + 2.0);
+    if (xmax < 0.0 || ymax < 0.0 || xmin > W || ymin > H) return;
+    p.rect[0] = max(0, (int)floor(fmax(xmin, 0.0) / T));
+    p.rect[1] = max(0, (int)floor(fmax(ymin, 0.0) / T));
+    p.rect[2] = min(v.tw - 1, (int)floor(fmin(xmax, W) / T));
+    p.rect[3] = min(v.th - 1, (int)floor(fmin(ymax, H) / T));
+}
+
+// Splat fields needed by the tile test and the key.
+struct TileSplat {
+    float ux, uy, uz, e1x, e1z, e2x, e2y, e2z, C0, C1, C2, qcut, eps;
+    float A[6], bx, by, bz;
+};
+
+// O7: Eq.4 on the optimal-plane polygon of the tile, corner
+// rays clipped at s >= eps (DESIGN R8); returns keep and d_hat.
+__device__ bool tile_test(const TileSplat& s, const ViewParams& v, int x0, int y0, int x1, int y1, float& dhx,
+                          float& dhy, float& dhz) {
+    float dx[4], dy[4], sv[4];
+    const int cxs[4] = {x0, x1, x1, x0}, cys[4] = {y0, y0, y1, y1};
+    int nin = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        dx[k] = ((float)cxs[k] - v.cx) / v.fx;
+        dy[k] = ((float)cys[k] - v.cy) / v.fy;
+        sv[k] = fmaf(s.ux, dx[k], fmaf(s.uy, dy[k], s.uz));
+        nin += (sv[k] >= s.eps) ? 1 : 0;
+    }
+    if (nin == 0) return false;
+    float px[5], py[5];
+    int n = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int k1 = (k + 1) & 3;
+        const bool ia = sv[k] >= s.eps, ib = sv[k1] >= s.eps;
+        if (ia) { px[n] = dx[k]; py[n] = dy[k]; n++; }
+        if (ia != ib) {
+            const int a = ia ? k : k1, b = ia ? k1 : k;
+            const float t = (sv[a] - s.eps) / (sv[a] - sv[b]);
+            px[n] = fmaf(t, dx[b] - dx[a], dx[a]);
+            py[n] = fmaf(t, dy[b] - dy[a], dy[a]);
+            n++;
+        }
+    }
+    float yx[5], yy[5];
+    for (int k = 0; k < n; k++) {
+        const float sk = dot3(s.ux, s.uy, s.uz, px[k], py[k], 1.0f);
+        yx[k] = dot3(s.e1x, 0.0f, s.e1z, px[k], py[k], 1.0f) / sk;
+        yy[k] = dot3(s.e2x, s.e2y, s.e2z, px[k], py[k], 1.0f) / sk;
+    }
+    int npos = 0, nneg = 0;
+    for (int k = 0; k < n; k++) {
+        const int k1 = (k + 1 == n) ? 0 : k + 1;
+        const float ddx = yx[k1] - yx[k], ddy = yy[k1] - yy[k];
+        const float cr = fmaf(ddy, yx[k], -(ddx * yy[k]));
+        npos += (cr >= 0.0f) ? 1 : 0;
+        nneg += (cr <= 0.0f) ? 1 : 0;
+    }
+    float hx = 0.0f, hy = 0.0f, qmin;
+    if (npos == n || nneg == n) {
+        qmin = 0.0f;
+    } else {
+        qmin = __int_as_float(0x7f800000);
+        for (int k = 0; k < n; k++) {
+            const int k1 = (k + 1 == n) ? 0 : k + 1;
+            const float ppx = yx[k], ppy = yy[k];
+            const float ddx = yx[k1] - yx[k], ddy = yy[k1] - yy[k];
+            const float cdx = fmaf(s.C0, ddx, s.C1 * ddy), cdy = fmaf(s.C1, ddx, s.C2 * ddy);
+            const float den = fmaf(ddx, cdx, ddy * cdy);
+            const float nmr = -fmaf(ppx, cdx, ppy * cdy);
+            float t;
+            if (nmr <= 0.0f || !(den > 0.0f)) t = 0.0f;
+            else if (nmr >= den) t = 1.0f;
+            else t = nmr / den;
+            const float X = fmaf(t, ddx, ppx), Y = fmaf(t, ddy, ppy);
+            const float cX = fmaf(s.C0, X, s.C1 * Y), cY = fmaf(s.C1, X, s.C2 * Y);
+            const float q = fmaf(X, cX, Y * cY);
+            if (q < qmin) { qmin = q; hx = X; hy = Y; }
+        }
+    }
+    dhx = fmaf(hy, s.e2x, fmaf(hx, s.e1x, s.ux));
+    dhy = fmaf(hy, s.e2y, fmaf(hx, 0.0f, s.uy));
+    dhz = fmaf(hy, s.e2z, fmaf(hx, s.e1z, s.uz));
+    return qmin <= s.qcut * kO7Margin;
+}
+
+// O8: StopThePop per-tile depth on the unit ray through x_hat.
+__device__ __forceinline__ float tile_depth(const TileSplat& s, float x, float y, float z, float near_plane) {
+    const float dAd = quad3(s.A[0], s.A[1], s.A[2], s.A[3], s.A[4], s.A[5], x, y, z);
+    const float db = fmaf(s.bx, x, fmaf(s.by, y, s.bz * z));
+    const float nd = sqrtf(dot3(x, y, z, x, y, z));
+    const float t = nd * (db / dAd);
+    return (t > near_plane) ? t : near_plane;
+}
+
+__device__ __forceinline__ uint32_t sat_count(const uint32_t* sat, int S, int x0, int y0, int x1, int y1) {
+    return sat[(y1 + 1) * S + x1 + 1] - sat[y0 * S + x1 + 1] - sat[(y1 + 1) * S + x0] + sat[y0 * S + x0];
+}
+
+__device__ __forceinline__ void proj_to_tilesplat(const Proj& p, TileSplat& s) {
+    s.ux = p.u[0]; s.uy = p.u[1]; s.uz = p.u[2];
+    s.e1x = p.e1[0]; s.e1z = p.e1[2]; s.e2x = p.e2[0]; s.e2y = p.e2[1]; s.e2z = p.e2[2];
+    s.C0 = p.C[0]; s.C1 = p.C[1]; s.C2 = p.C[2]; s.qcut = p.qcut; s.eps = p.eps;
+#pragma unroll
+    for (int i = 0; i < 6; i++) s.A[i] = p.A[i];
+    s.bx = p.bv[0]; s.by = p.bv[1]; s.bz = p.bv[2];
+}
+
+__device__ uint32_t count_pairs(const TileSplat& s, const ViewParams& v, const int rect[4], int T) {
+    if (rect[0] > rect[2] || rect[1] > rect[3]) return 0;
+    if (sat_count(v.sat, v.tw + 1, rect[0], rect[1], rect[2], rect[3]) == 0) return 0;
+    uint32_t c = 0;
+    for (int ty = rect[1]; ty <= rect[3]; ty++)
+        for (int tx = rect[0]; tx <= rect[2]; tx++) {
+            if (!v.vis[ty * v.tw + tx]) continue;
+            const int x0 = tx * T, y0 = ty * T;
+            float a, b, d;
+            if (tile_test(s, v, x0, y0, min(x0 + T, v.W), min(y0 + T, v.H), a, b, d)) c++;
+        }
+    return c;
+}
+
+// View-dependent colour: real SH through degree 3 (3DGS basis), +0.5, >= 0.
+__device__ void sh_color(const SceneDev& sc, int64_t g, int64_t N, int ncoef, float dx, float dy, float dz,
+                         float out[3]) {
+    const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
+    float basis[16];
+    basis[0] = C0;
+    if (ncoef > 1) {
+        basis[1] = -C1 * dy; basis[2] = C1 * dz; basis[3] = -C1 * dx;
+    }
+    if (ncoef > 4) {
+        const float xx = dx * dx, yy = dy * dy, zz = dz * dz, xy = dx * dy, yz = dy * dz, xz = dx * dz;
+        basis[4] = 1.0925484305920792f * xy;
+        basis[5] = -1.0925484305920792f * yz;
+        basis[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+        basis[7] = -1.0925484305920792f * xz;
+        basis[8] = 0.5462742152960396f * (xx - yy);
+        if (ncoef > 9) {
+            basis[9] = -0.5900435899266435f * dy * (3.0f * xx - yy);
+            basis[10] = 2.890611442640554f * xy * dz;
+            basis[11] = -0.4570457994644658f * dy * (4.0f * zz - xx - yy);
+            basis[12] = 0.3731763325901154f * dz * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+            basis[13] = -0.4570457994644658f * dx * (4.0f * zz - xx - yy);
+            basis[14] = 1.445305721320277f * dz * (xx - yy);
+            basis[15] = -0.5900435899266435f * dx * (xx - 3.0f * yy);
+        }
+    }
+    float acc[3] = {0.0f, 0.0f, 0.0f};
+    const int nfl = ncoef * 3;
+    for (int c4 = 0; c4 * 4 < nfl; c4++) {
+        const float4 q = __ldg(&sc.sh[(size_t)c4 * N + g]);
+        const float vals[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int f = c4 * 4 + k;
+            if (f < nfl) acc[f % 3] = fmaf(basis[f / 3], vals[k], acc[f % 3]);
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+        const float r = acc[c] + 0.5f;
+        out[c] = r > 0.0f ? r : 0.0f;
+    }
+}
+
+__device__ __forceinline__ void load_gauss(const SceneDev& sc, int64_t g, int64_t N, float4& m4, float4& c0,
+                                           float4& c1, float4& i0, float4& i1) {
+    m4 = __ldg(&sc.mu[g]);
+    c0 = __ldg(&sc.cov[g]);
+    c1 = __ldg(&sc.cov[N + g]);
+    i0 = __ldg(&sc.icov[g]);
+    i1 = __ldg(&sc.icov[N + g]);
+}
+
+// Step 1: per-Gaussian preprocess for all views + exact pair counts.
+__global__ void __launch_bounds__(128) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t N = fp.N;
+    if (g >= N) return;
+    float4 m4, c0, c1, i0, i1;
+    load_gauss(sc, g, N, m4, c0, c1, i0, i1);
+    for (int vi = 0; vi < fp.n_views; vi++) {
+        const ViewParams& v = fp.v[vi];
+        Proj p;
+        project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
+        uint32_t cnt = 0;
+        if (p.valid) {
+            TileSplat ts;
+            proj_to_tilesplat(p, ts);
+            cnt = count_pairs(ts, v, p.rect, fp.T);
+        }
+        fb.counts[(size_t)vi * N + g] = cnt;
+        if (cnt == 0) continue;
+        float rgb[3];
+        {
+            const float dx = m4.x - v.o[0], dy = m4.y - v.o[1], dz = m4.z - v.o[2];
+            const float inv = 1.0f / sqrtf(dot3(dx, dy, dz, dx, dy, dz));
+            sh_color(sc, g, N, fp.sh_coeffs, dx * inv, dy * inv, dz * inv, rgb);
+        }
+        float4* rec = fb.rec + ((size_t)vi * N + g) * kRecF4;
+        const uint32_t r01 = (uint32_t)p.rect[0] | ((uint32_t)p.rect[1] << 16);
+        const uint32_t r23 = (uint32_t)p.rect[2] | ((uint32_t)p.rect[3] << 16);
+        rec[0] = make_float4(p.u[0], p.u[1], p.u[2], p.qcut);
+        rec[1] = make_float4(p.e1[0], p.e1[2], p.e2[0], p.e2[1]);
+        rec[2] = make_float4(p.e2[2], p.C[0], p.C[1], p.C[2]);
+        rec[3] = make_float4(p.A[0], p.A[1], p.A[2], p.A[3]);
+        rec[4] = make_float4(p.A[4], p.A[5], p.bv[0], p.bv[1]);
+        rec[5] = make_float4(p.bv[2], p.sigma, p.eps, __uint_as_float(r01));
+        rec[6] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(r23));
+        rec[7] = make_float4(p.bbox[0], p.bbox[1], p.bbox[2], p.bbox[3]);
+    }
+}
+
+// Step 3: re-walk the rect and emit (key, value) for every kept tile at the
+// Gaussian's instance range.  Emission order: (view, g, tile row-major).
+__global__ void __launch_bounds__(128) k_duplicate(FrameParams fp, FrameBufs fb) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t N = fp.N;
+    if (idx >= (int64_t)fp.n_views * N) return;
+    const uint32_t cnt = fb.counts[idx];
+    if (cnt == 0) return;
+    const int vi = (int)(idx / N);
+    const ViewParams& v = fp.v[vi];
+    uint32_t off = fb.offsets[idx];
+    if ((int64_t)off + cnt > fp.pair_cap) {
+        atomicOr(fb.overflow, 1u);
+        return;
+    }
+    const float4* rec = fb.rec + (size_t)idx * kRecF4;
+    const float4 r0 = rec[0], r1 = rec[1], r2 = rec[2], r3 = rec[3], r4 = rec[4], r5 = rec[5], r6 = rec[6];
+    TileSplat s;
+    s.ux = r0.x; s.uy = r0.y; s.uz = r0.z; s.qcut = r0.w;
+    s.e1x = r1.x; s.e1z = r1.y; s.e2x = r1.z; s.e2y = r1.w;
+    s.e2z = r2.x; s.C0 = r2.y; s.C1 = r2.z; s.C2 = r2.w;
+    s.A[0] = r3.x; s.A[1] = r3.y; s.A[2] = r3.z; s.A[3] = r3.w;
+    s.A[4] = r4.x; s.A[5] = r4.y; s.bx = r4.z; s.by = r4.w;
+    s.bz = r5.x; s.eps = r5.z;
+    const uint32_t r01 = __float_as_uint(r5.w), r23 = __float_as_uint(r6.w);
+    const int tx0 = r01 & 0xffff, ty0 = r01 >> 16, tx1 = r23 & 0xffff, ty1 = r23 >> 16;
+    const int T = fp.T;
+    const uint32_t g = (uint32_t)(idx - (int64_t)vi * N);
+    for (int ty = ty0; ty <= ty1; ty++)
+        for (int tx = tx0; tx <= tx1; tx++) {
+            if (!v.vis[ty * v.tw + tx]) continue;
+            const int x0 = tx * T, y0 = ty * T;
+            float hx, hy, hz;
+            if (!tile_test(s, v, x0, y0, min(x0 + T, v.W), min(y0 + T, v.H), hx, hy, hz)) continue;
+            const float td = tile_depth(s, hx, hy, hz, fp.near_plane);
+            const uint64_t tile = (uint64_t)(v.tile_base + ty * v.tw + tx);
+            fb.keys[off] = (tile << 32) | (uint64_t)__float_as_uint(td);
+            fb.vals[off] = g;
+            off++;
+        }
+}
+
+// Parity hook: the oracle's 48-float semantic splat layout.
+__global__ void k_debug_splats(SceneDev sc, FrameParams fp, FrameBufs fb, int vi, float* out) {
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t N = fp.N;
+    if (g >= N) return;
+    float4 m4, c0, c1, i0, i1;
+    load_gauss(sc, g, N, m4, c0, c1, i0, i1);
+    const ViewParams& v = fp.v[vi];
+    Proj p;
+    for (int i = 0; i < 3; i++) { p.u[i] = p.e1[i] = p.e2[i] = p.S2[i] = p.C[i] = p.bv[i] = 0.0f; }
+    for (int i = 0; i < 6; i++) p.A[i] = 0.0f;
+    for (int i = 0; i < 4; i++) p.bbox[i] = 0.0f;
+    p.eps = 0.0f;
+    project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
+    float* o = out + g * 48;
+    for (int i = 0; i < 48; i++) o[i] = 0.0f;
+    o[0] = (float)p.valid;
+    for (int i = 0; i < 3; i++) {
+        o[1 + i] = p.muc[i]; o[4 + i] = p.u[i]; o[7 + i] = p.e1[i]; o[10 + i] = p.e2[i];
+        o[13 + i] = p.S2[i]; o[16 + i] = p.C[i]; o[31 + i] = p.bv[i];
+    }
+    o[19] = p.eps;
+    for (int i = 0; i < 6; i++) o[25 + i] = p.A[i];
+    o[37] = p.sigma; o[38] = p.qcut;
+    for (int i = 0; i < 4; i++) { o[39 + i] = (float)p.rect[i]; o[43 + i] = p.bbox[i]; }
+    const uint32_t cnt = fb.counts[(size_t)vi * N + g];
+    o[47] = (float)cnt;
+    if (p.valid) {
+        const float dx = m4.x - v.o[0], dy = m4.y - v.o[1], dz = m4.z - v.o[2];
+        const float inv = 1.0f / sqrtf(dot3(dx, dy, dz, dx, dy, dz));
+        float rgb[3];
+        sh_color(sc, g, N, fp.sh_coeffs, dx * inv, dy * inv, dz * inv, rgb);
+        o[34] = rgb[0]; o[35] = rgb[1]; o[36] = rgb[2];
+    }
+}
+
+void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, cudaStream_t st) {
+    if (fp.N == 0) return;
+    const int B = 128;
+    k_preprocess<<<(unsigned)((fp.N + B - 1) / B), B, 0, st>>>(sc, fp, fb);
+}
+
+void launch_duplicate(const FrameParams& fp, FrameBufs fb, cudaStream_t st) {
+    const int64_t n = (int64_t)fp.n_views * fp.N;
+    if (n == 0) return;
+    const int B = 128;
+    k_duplicate<<<(unsigned)((n + B - 1) / B), B, 0, st>>>(fp, fb);
+}
+
+void launch_debug_splats(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int view, float* out,
+                         cudaStream_t st) {
+    if (fp.N == 0) return;
+    k_debug_splats<<<(unsigned)((fp.N + 127) / 128), 128, 0, st>>>(sc, fp, fb, view, out);
+}
+
+}  // namespace vrs

@@ -1,0 +1,122 @@
+// Per-eye static setup ("precompute this mapping once for each
+// eye", P:440-449 visibility culling): visibility bitfield from the HMD mask,
+// its summed-area table, coarse-tile classes (HighRes / LowRes / Hybrid /
+// Invisible) and the blend work list (16x16 items for HighRes and
+// Hybrid tiles, one 32x32 item for LowRes tiles, none for Invisible tiles).
+// Runs only when a view's mask / fovea / resolution changes; not per frame.
+#include "vrs_internal.cuh"
+
+namespace vrs {
+
+// One block per coarse tile: visibility bit (any mask pixel > 0) and class.
+__global__ void k_tile_class(const uint8_t* __restrict__ mask, ViewParams v, int T, int32_t* vis, int32_t* cls) {
+    const int tx = blockIdx.x, ty = blockIdx.y;
+    const int x0 = tx * T, y0 = ty * T;
+    const int x1 = min(x0 + T, v.W), y1 = min(y0 + T, v.H);
+    const int w = x1 - x0, npx = w * (y1 - y0);
+    int any = (mask == nullptr) ? 1 : 0, all1 = 1, all0 = 1;
+    for (int k = threadIdx.x; k < npx; k += blockDim.x) {
+        int x = x0 + k % w, y = y0 + k / w;
+        if (mask && mask[(size_t)y * v.W + x] > 0) any = 1;
+        if (v.fovea) {
+            float wt = fovea_weight(v, (float)x + 0.5f, (float)y + 0.5f);
+            if (wt != 1.0f) all1 = 0;
+            if (wt != 0.0f) all0 = 0;
+        }
+    }
+    any = __syncthreads_or(any);
+    all1 = __syncthreads_and(all1);
+    all0 = __syncthreads_and(all0);
+    if (threadIdx.x == 0) {
+        int t = ty * v.tw + tx;
+        vis[t] = any;
+        int c;
+        if (!any) c = kInvisible;
+        else if (!v.fovea) c = kHigh;
+        else c = all1 ? kHigh : (all0 ? kLow : kHybrid);
+        cls[t] = c;
+    }
+}
+
+// Single block: SAT over the bitfield and the work list.
+__global__ void k_sat_items(ViewParams v, int T, const int32_t* __restrict__ vis, const int32_t* __restrict__ cls,
+                            uint32_t* sat, uint32_t* items, int32_t* n_items) {
+    const int tw = v.tw, th = v.th, S = tw + 1;
+    __shared__ uint32_t s_scan[1024];
+    __shared__ uint32_t s_carry;
+    // SAT: row prefix sums then column accumulation
+    for (int i = threadIdx.x; i < S; i += blockDim.x) sat[i] = 0;
+    for (int y = threadIdx.x; y < th; y += blockDim.x) {
+        uint32_t run = 0;
+        sat[(size_t)(y + 1) * S] = 0;
+        for (int x = 0; x < tw; x++) {
+            run += (uint32_t)(vis[y * tw + x] != 0);
+            sat[(size_t)(y + 1) * S + x + 1] = run;
+        }
+    }
+    __syncthreads();
+    for (int x = threadIdx.x; x < tw; x += blockDim.x) {
+        uint32_t col = 0;
+        for (int y = 0; y < th; y++) {
+            col += sat[(size_t)(y + 1) * S + x + 1];
+            sat[(size_t)(y + 1) * S + x + 1] = col;
+        }
+    }
+    // work items in tile row-major order
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    const int ntile = tw * th;
+    for (int base = 0; base < ntile; base += blockDim.x) {
+        int t = base + threadIdx.x;
+        uint32_t cnt = 0;
+        int c = kInvisible, tx = 0, ty = 0;
+        if (t < ntile) {
+            c = cls[t];
+            tx = t % tw;
+            ty = t / tw;
+            if (c == kLow) cnt = 1;
+            else if (c != kInvisible) {
+                if (T == 16) cnt = 1;
+                else
+                    for (int sub = 0; sub < 4; sub++)
+                        cnt += (tx * T + 16 * (sub & 1) < v.W && ty * T + 16 * (sub >> 1) < v.H) ? 1u : 0u;
+            }
+        }
+        s_scan[threadIdx.x] = cnt;
+        __syncthreads();
+        for (int off = 1; off < (int)blockDim.x; off <<= 1) {
+            uint32_t add = threadIdx.x >= (unsigned)off ? s_scan[threadIdx.x - off] : 0u;
+            __syncthreads();
+            s_scan[threadIdx.x] += add;
+            __syncthreads();
+        }
+        uint32_t pos = s_carry + s_scan[threadIdx.x] - cnt;
+        if (t < ntile && cnt) {
+            if (c == kLow) {
+                items[pos] = (uint32_t)t | (kItemLow << 22);
+            } else {
+                uint32_t kind = (c == kHybrid) ? kItemHybrid : kItemFull;
+                if (T == 16) {
+                    items[pos] = (uint32_t)t | (kind << 22);
+                } else {
+                    for (int sub = 0; sub < 4; sub++)
+                        if (tx * T + 16 * (sub & 1) < v.W && ty * T + 16 * (sub >> 1) < v.H)
+                            items[pos++] = (uint32_t)t | ((uint32_t)sub << 20) | (kind << 22);
+                }
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) s_carry += s_scan[threadIdx.x];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *n_items = (int32_t)s_carry;
+}
+
+void launch_setup_view(const uint8_t* mask, int mask_w, ViewParams vp, int T, int32_t* vis, uint32_t* sat,
+                       int32_t* cls, uint32_t* items, int32_t* n_items_dev, cudaStream_t st) {
+    (void)mask_w;
+    k_tile_class<<<dim3(vp.tw, vp.th), 256, 0, st>>>(mask, vp, T, vis, cls);
+    k_sat_items<<<1, 1024, 0, st>>>(vp, T, vis, cls, sat, items, n_items_dev);
+}
+
+}  // namespace vrs

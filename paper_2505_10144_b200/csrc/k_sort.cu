@@ -1,0 +1,202 @@
+// Step 4: the global sort of the Gaussian/tile pairs (P:258
+// "this arrangement is sorted") — a hand-written stable LSD onesweep radix
+// sort (8-bit digits): one histogram kernel for all digits, then one kernel
+// per digit whose blocks rank their 4096-key tile with warp-level
+// match_any, resolve the global digit offsets by decoupled look-back over
+// the preceding tiles, and scatter.  The grid is persistent (a multiple of
+// the SM count); blocks acquire tiles in order from an atomic counter and
+// stop at the device-resident pair count, so no host sync is needed.
+#include <algorithm>
+#include <utility>
+
+#include "vrs_internal.cuh"
+
+namespace vrs {
+
+namespace {
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;  // 4096
+constexpr int kRadix = 256;
+constexpr int kWarps = kSortThreads / 32;
+constexpr uint32_t kStAgg = 1u << 30, kStPre = 2u << 30, kStMask = (1u << 30) - 1;
+
+__device__ __forceinline__ void st_release32(uint32_t* p, uint32_t v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t ld_acquire32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+}  // namespace
+
+// Digit histograms of every pass in one read of the keys.
+__global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __restrict__ keys,
+                                                            const uint32_t* __restrict__ n_dev, int64_t cap,
+                                                            int passes, uint32_t* hist) {
+    __shared__ uint32_t s_h[8][kRadix];
+    for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) (&s_h[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t n = min((int64_t)*n_dev, cap);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t k = keys[i];
+        for (int p = 0; p < passes; p++) atomicAdd(&s_h[p][(k >> (8 * p)) & 0xff], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {
+        const uint32_t c = (&s_h[0][0])[i];
+        if (c) atomicAdd(&hist[i], c);
+    }
+}
+
+// Exclusive scan of each pass's 256 bins (in place).
+__global__ void k_sort_hist_scan(uint32_t* hist) {
+    __shared__ uint32_t s[kRadix];
+    uint32_t* h = hist + blockIdx.x * kRadix;
+    const int t = threadIdx.x;
+    const uint32_t v = h[t];
+    s[t] = v;
+    __syncthreads();
+    for (int o = 1; o < kRadix; o <<= 1) {
+        uint32_t a = t >= o ? s[t - o] : 0u;
+        __syncthreads();
+        s[t] += a;
+        __syncthreads();
+    }
+    h[t] = s[t] - v;
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint64_t* __restrict__ kin,
+                                                           const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
+                                                           uint32_t* __restrict__ vout,
+                                                           const uint32_t* __restrict__ n_dev, int64_t cap, int pass,
+                                                           const uint32_t* __restrict__ digit_off, uint32_t* status,
+                                                           uint32_t* counter) {
+    __shared__ uint32_t s_wh[kWarps][kRadix];  // per-warp digit counts -> exclusive offsets
+    __shared__ uint32_t s_gbase[kRadix];
+    __shared__ uint32_t s_tile;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int shift = 8 * pass;
+    const int64_t n = min((int64_t)*n_dev, cap);
+    const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    while (true) {
+        if (tid == 0) s_tile = atomicAdd(counter, 1u);
+        for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&s_wh[0][0])[i] = 0;
+        __syncthreads();
+        const int64_t tile = s_tile;
+        if (tile >= ntiles) break;
+        const int64_t wbase = tile * kSortTile + (int64_t)warp * (kSortItems * 32);
+        uint64_t key[kSortItems];
+        uint32_t val[kSortItems];
+        uint32_t rank[kSortItems];
+#pragma unroll
+        for (int i = 0; i < kSortItems; i++) {
+            const int64_t idx = wbase + i * 32 + lane;
+            const bool ok = idx < n;
+            key[i] = ok ? kin[idx] : 0ull;
+            val[i] = ok ? vin[idx] : 0u;
+        }
+        // warp-local stable ranking in (item, lane) order
+#pragma unroll
+        for (int i = 0; i < kSortItems; i++) {
+            const int64_t idx = wbase + i * 32 + lane;
+            const bool ok = idx < n;
+            const uint32_t d = (uint32_t)(key[i] >> shift) & 0xffu;
+            const uint32_t peers = __match_any_sync(0xffffffffu, ok ? d : (0x100u + lane));
+            const uint32_t old = ok ? s_wh[warp][d] : 0u;
+            __syncwarp();
+            if (ok && (peers & lt_mask) == 0) s_wh[warp][d] = old + __popc(peers);
+            __syncwarp();
+            rank[i] = old + __popc(peers & lt_mask);
+        }
+        __syncthreads();
+        // per digit: exclusive over warps, tile total, publish + look-back
+        {
+            const int d = tid;  // kSortThreads == kRadix
+            uint32_t tot = 0;
+#pragma unroll
+            for (int w = 0; w < kWarps; w++) {
+                const uint32_t c = s_wh[w][d];
+                s_wh[w][d] = tot;
+                tot += c;
+            }
+            uint32_t* st = status + (size_t)tile * kRadix + d;
+            uint32_t excl = 0;
+            if (tile == 0) {
+                st_release32(st, kStPre | tot);
+            } else {
+                st_release32(st, kStAgg | tot);
+                int64_t j = tile - 1;
+                while (true) {
+                    uint32_t s;
+                    do { s = ld_acquire32(status + (size_t)j * kRadix + d); } while ((s & ~kStMask) == 0);
+                    excl += s & kStMask;
+                    if ((s & ~kStMask) == kStPre) break;
+                    j--;
+                }
+                st_release32(st, kStPre | (excl + tot));
+            }
+            s_gbase[d] = digit_off[pass * kRadix + d] + excl;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < kSortItems; i++) {
+            const int64_t idx = wbase + i * 32 + lane;
+            if (idx < n) {
+                const uint32_t d = (uint32_t)(key[i] >> shift) & 0xffu;
+                const uint32_t pos = s_gbase[d] + s_wh[warp][d] + rank[i];
+                kout[pos] = key[i];
+                vout[pos] = val[i];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_copy_pairs(const uint64_t* __restrict__ ks, const uint32_t* __restrict__ vs, uint64_t* kd,
+                             uint32_t* vd, const uint32_t* __restrict__ n_dev, int64_t cap) {
+    const int64_t n = min((int64_t)*n_dev, cap);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        kd[i] = ks[i];
+        vd[i] = vs[i];
+    }
+}
+
+size_t sort_status_words(int64_t cap) { return (size_t)((cap + kSortTile - 1) / kSortTile + 1) * kRadix; }
+
+static int g_num_sms = 0;
+static int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+void launch_sort(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, const uint32_t* n_dev,
+                 int64_t cap, int key_bits, SortScratch s, cudaStream_t st) {
+    const int passes = (key_bits + 7) / 8;
+    if (passes <= 0 || cap <= 0) return;
+    const int sms = num_sms();
+    const int64_t max_tiles = (cap + kSortTile - 1) / kSortTile;
+    cudaMemsetAsync(s.hist, 0, sizeof(uint32_t) * 8 * kRadix, st);
+    cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * 8, st);
+    k_sort_hist<<<sms * 2, kSortThreads, 0, st>>>(keys, n_dev, cap, passes, s.hist);
+    k_sort_hist_scan<<<passes, kRadix, 0, st>>>(s.hist);
+    const unsigned grid = (unsigned)std::min<int64_t>(max_tiles, (int64_t)sms * 4);
+    uint64_t *ka = keys, *kb = keys_alt;
+    uint32_t *va = vals, *vb = vals_alt;
+    for (int p = 0; p < passes; p++) {
+        cudaMemsetAsync(s.status, 0, sizeof(uint32_t) * (size_t)max_tiles * kRadix, st);
+        k_onesweep<<<grid, kSortThreads, 0, st>>>(ka, va, kb, vb, n_dev, cap, p, s.hist, s.status, s.counters + p);
+        std::swap(ka, kb);
+        std::swap(va, vb);
+    }
+    if (ka != keys) k_copy_pairs<<<sms * 2, 256, 0, st>>>(ka, va, keys, vals, n_dev, cap);
+}
+
+}  // namespace vrs

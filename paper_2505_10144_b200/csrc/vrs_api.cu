@@ -1,0 +1,696 @@
+// C ABI of libvrs (include/vrs.h): context, scene upload (host activation),
+// visibility masks, per-eye static setup cache and the per-frame launch
+// sequence preprocess -> scan -> duplicate -> onesweep sort -> ranges ->
+// blend -> compose, all enqueued on the caller's stream with no host sync.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "vrs_internal.cuh"
+
+using namespace vrs;
+
+namespace {
+
+struct ViewSetup {
+    bool valid = false;
+    int W = 0, H = 0, mask_slot = -1, T = 0, fovea = 0;
+    uint64_t mask_gen = 0;
+    float gx = 0, gy = 0, rx = 0, ry = 0, ramp = 0;
+    int32_t n_items = 0;
+    int32_t cls_count[4] = {0, 0, 0, 0};
+};
+
+template <class T>
+cudaError_t dalloc(T** p, size_t count) {
+    *p = nullptr;
+    if (count == 0) count = 1;
+    return cudaMalloc(reinterpret_cast<void**>(p), sizeof(T) * count);
+}
+
+}  // namespace
+
+struct vrs_context {
+    vrs_config cfg{};
+    std::string err;
+    vrs_status sticky = VRS_OK;
+    // scene
+    int64_t N = 0;
+    int deg = 0;
+    bool uploaded = false;
+    float4 *d_mu = nullptr, *d_cov = nullptr, *d_icov = nullptr, *d_sh = nullptr;
+    int sh_chunks = 0;
+    // frame buffers
+    float4* d_rec = nullptr;
+    uint32_t *d_counts = nullptr, *d_offsets = nullptr, *d_misc = nullptr;  // misc: total, overflow
+    uint64_t *d_keys = nullptr, *d_keys_alt = nullptr;
+    uint32_t *d_vals = nullptr, *d_vals_alt = nullptr;
+    uint32_t* d_ranges = nullptr;
+    int64_t max_tiles_view = 0, max_items_view = 0, low_px_view = 0;
+    float4* d_low_rgba = nullptr;
+    float* d_low_depth = nullptr;
+    unsigned long long* d_stats = nullptr;
+    uint32_t* d_scan_scratch = nullptr;
+    SortScratch sort{};
+    // per-view static setup
+    int32_t* d_vis = nullptr;     // [V][max_tiles]
+    uint32_t* d_sat = nullptr;    // [V][max_sat]
+    int32_t* d_cls = nullptr;     // [V][max_tiles]
+    uint32_t* d_items = nullptr;  // [V][max_items]
+    int32_t* d_nitems = nullptr;  // [V]
+    int64_t max_sat_view = 0;
+    ViewSetup vs[VRS_MAX_VIEWS];
+    // masks
+    uint8_t* d_mask[VRS_MAX_MASK_SLOTS] = {};
+    int mask_w[VRS_MAX_MASK_SLOTS] = {}, mask_h[VRS_MAX_MASK_SLOTS] = {};
+    uint64_t mask_gen[VRS_MAX_MASK_SLOTS] = {};
+    uint64_t gen_counter = 1;
+    // last frame
+    FrameParams fp{};
+    bool have_frame = false;
+    cudaStream_t last_stream = nullptr;
+    int64_t last_items = 0, last_tiles = 0;
+    int32_t last_cls[4] = {0, 0, 0, 0};
+    // host-output path
+    float *d_out_rgba = nullptr, *d_out_depth = nullptr;
+    size_t out_px_cap = 0;
+    // instrumentation
+    int counters = 0, timing = 0, no_cull = 0;
+    cudaEvent_t ev[8] = {};
+    bool ev_created = false;
+};
+
+static vrs_status fail(vrs_context* c, vrs_status s, const std::string& msg) {
+    if (c) c->err = msg;
+    return s;
+}
+
+static vrs_status cuda_check(vrs_context* c, cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return VRS_OK;
+    c->sticky = VRS_E_CUDA;
+    c->err = std::string(where) + ": " + cudaGetErrorString(e);
+    return VRS_E_CUDA;
+}
+
+#define CK(expr)                                                     \
+    do {                                                             \
+        vrs_status _s = cuda_check(ctx, (expr), #expr);              \
+        if (_s != VRS_OK) return _s;                                 \
+    } while (0)
+
+static void free_all(vrs_context* c) {
+    void* ptrs[] = {c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_counts, c->d_offsets, c->d_misc,
+                    c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
+                    c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
+                    c->d_sat, c->d_cls, c->d_items, c->d_nitems, c->d_out_rgba, c->d_out_depth};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (int i = 0; i < VRS_MAX_MASK_SLOTS; i++)
+        if (c->d_mask[i]) cudaFree(c->d_mask[i]);
+    if (c->ev_created)
+        for (auto& e : c->ev) cudaEventDestroy(e);
+}
+
+extern "C" {
+
+int32_t vrs_abi_version(void) { return VRS_ABI_VERSION; }
+
+const char* vrs_last_error(const vrs_context* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
+    if (!cfg || !out) return VRS_E_INVALID_ARG;
+    *out = nullptr;
+    if (cfg->max_views < 1 || cfg->max_views > VRS_MAX_VIEWS || cfg->max_gaussians < 0 || cfg->max_pairs < 1 ||
+        cfg->max_pairs >= (int64_t)1 << 30 || cfg->max_width < 1 || cfg->max_height < 1 ||
+        (cfg->assign_tile != 16 && cfg->assign_tile != 32) || cfg->window_k != kWindow || cfg->projection != 0 ||
+        !(cfg->near_plane > 0.0f) || (int64_t)cfg->max_views * cfg->max_gaussians >= ((int64_t)1 << 32))
+        return VRS_E_INVALID_ARG;
+    vrs_context* ctx = new vrs_context();
+    ctx->cfg = *cfg;
+    if (cudaSetDevice(cfg->device) != cudaSuccess) {
+        delete ctx;
+        return VRS_E_CUDA;
+    }
+    const int64_t V = cfg->max_views, N = std::max<int64_t>(cfg->max_gaussians, 1), P = cfg->max_pairs;
+    const int64_t tw16 = (cfg->max_width + 15) / 16, th16 = (cfg->max_height + 15) / 16;
+    const int64_t tw = (cfg->max_width + cfg->assign_tile - 1) / cfg->assign_tile;
+    const int64_t th = (cfg->max_height + cfg->assign_tile - 1) / cfg->assign_tile;
+    ctx->max_tiles_view = tw * th;
+    ctx->max_items_view = tw16 * th16 + tw * th;
+    ctx->max_sat_view = (tw + 1) * (th + 1);
+    ctx->low_px_view = (int64_t)((cfg->max_width + 1) / 2) * ((cfg->max_height + 1) / 2);
+    cudaError_t e = cudaSuccess;
+    auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+    A(dalloc(&ctx->d_rec, (size_t)V * N * kRecF4));
+    A(dalloc(&ctx->d_counts, (size_t)V * N));
+    A(dalloc(&ctx->d_offsets, (size_t)V * N));
+    A(dalloc(&ctx->d_misc, 8));
+    A(dalloc(&ctx->d_keys, (size_t)P));
+    A(dalloc(&ctx->d_keys_alt, (size_t)P));
+    A(dalloc(&ctx->d_vals, (size_t)P));
+    A(dalloc(&ctx->d_vals_alt, (size_t)P));
+    A(dalloc(&ctx->d_ranges, (size_t)2 * V * ctx->max_tiles_view));
+    A(dalloc(&ctx->d_low_rgba, (size_t)V * ctx->low_px_view));
+    A(dalloc(&ctx->d_low_depth, (size_t)V * ctx->low_px_view));
+    A(dalloc(&ctx->d_stats, 8));
+    A(dalloc(&ctx->d_scan_scratch, 2 * scan_scratch_words(V * N)));
+    A(dalloc(&ctx->sort.hist, 8 * 256));
+    A(dalloc(&ctx->sort.status, sort_status_words(P)));
+    A(dalloc(&ctx->sort.counters, 8));
+    ctx->sort.max_tiles = (P + 4095) / 4096;
+    A(dalloc(&ctx->d_vis, (size_t)V * ctx->max_tiles_view));
+    A(dalloc(&ctx->d_cls, (size_t)V * ctx->max_tiles_view));
+    A(dalloc(&ctx->d_sat, (size_t)V * ctx->max_sat_view));
+    A(dalloc(&ctx->d_items, (size_t)V * ctx->max_items_view));
+    A(dalloc(&ctx->d_nitems, (size_t)V));
+    if (e != cudaSuccess) {
+        free_all(ctx);
+        delete ctx;
+        cudaGetLastError();
+        return (e == cudaErrorMemoryAllocation) ? VRS_E_OOM : VRS_E_CUDA;
+    }
+    cudaMemset(ctx->d_misc, 0, 32);
+    *out = ctx;
+    return VRS_OK;
+}
+
+void vrs_destroy(vrs_context* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->cfg.device);
+    cudaDeviceSynchronize();
+    free_all(ctx);
+    delete ctx;
+}
+
+/* Host activation (DESIGN "Numerics contract" R2):
+ * double precision, rounded once to float. */
+vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_degree, const float* means,
+                                const float* quats, const float* log_scales, const float* logits, const float* sh,
+                                int64_t* n_rejected) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    if (ctx->sticky != VRS_OK) return ctx->sticky;
+    if (n < 0 || n > ctx->cfg.max_gaussians || sh_degree < 0 || sh_degree > 3)
+        return fail(ctx, VRS_E_INVALID_ARG, "n > max_gaussians or sh_degree not in 0..3");
+    if (n > 0 && (!means || !quats || !log_scales || !logits || !sh))
+        return fail(ctx, VRS_E_INVALID_ARG, "null attribute pointer");
+    CK(cudaSetDevice(ctx->cfg.device));
+    const int ncoef = (sh_degree + 1) * (sh_degree + 1);
+    const int nfl = ncoef * 3;
+    const int chunks = (nfl + 3) / 4;
+    std::vector<float4> mu, cov, icov;
+    std::vector<float> shh;
+    mu.reserve(n);
+    cov.reserve(2 * n);
+    icov.reserve(2 * n);
+    std::vector<int64_t> keep;
+    keep.reserve(n);
+    std::vector<float4> cov_hi, icov_hi;
+    for (int64_t i = 0; i < n; i++) {
+        const float* m = means + 3 * i;
+        const float* q = quats + 4 * i;
+        const float* ls = log_scales + 3 * i;
+        const float* shc = sh + (size_t)i * nfl;
+        bool ok = std::isfinite(m[0]) && std::isfinite(m[1]) && std::isfinite(m[2]) && std::isfinite(ls[0]) &&
+                  std::isfinite(ls[1]) && std::isfinite(ls[2]) && std::isfinite(logits[i]);
+        for (int k = 0; k < 4; k++) ok = ok && std::isfinite(q[k]);
+        for (int k = 0; k < nfl && ok; k++) ok = std::isfinite(shc[k]);
+        if (!ok) continue;
+        double w = q[0], x = q[1], y = q[2], z = q[3];
+        const double nrm = std::sqrt(w * w + x * x + y * y + z * z);
+        if (!(nrm > 0.0)) continue;
+        w /= nrm; x /= nrm; y /= nrm; z /= nrm;
+        const double R[3][3] = {{1.0 - 2.0 * (y * y + z * z), 2.0 * (x * y - w * z), 2.0 * (x * z + w * y)},
+                                {2.0 * (x * y + w * z), 1.0 - 2.0 * (x * x + z * z), 2.0 * (y * z - w * x)},
+                                {2.0 * (x * z - w * y), 2.0 * (y * z + w * x), 1.0 - 2.0 * (x * x + y * y)}};
+        double s2[3], is2[3];
+        for (int k = 0; k < 3; k++) {
+            const double s = std::exp((double)ls[k]);
+            s2[k] = s * s;
+            is2[k] = 1.0 / s2[k];
+        }
+        float c6[6], i6[6];
+        const int I[6] = {0, 0, 0, 1, 1, 2}, J[6] = {0, 1, 2, 1, 2, 2};
+        for (int e2 = 0; e2 < 6; e2++) {
+            const int a = I[e2], b = J[e2];
+            c6[e2] = (float)((R[a][0] * R[b][0]) * s2[0] + (R[a][1] * R[b][1]) * s2[1] + (R[a][2] * R[b][2]) * s2[2]);
+            i6[e2] = (float)((R[a][0] * R[b][0]) * is2[0] + (R[a][1] * R[b][1]) * is2[1] +
+                             (R[a][2] * R[b][2]) * is2[2]);
+            ok = ok && std::isfinite(c6[e2]) && std::isfinite(i6[e2]);
+        }
+        if (!ok) continue;
+        const float sg = (float)(1.0 / (1.0 + std::exp(-(double)logits[i])));
+        const float qc = (float)(2.0 * std::log(255.0 * (double)sg));
+        mu.push_back(make_float4(m[0], m[1], m[2], qc));
+        cov.push_back(make_float4(c6[0], c6[1], c6[2], c6[3]));
+        cov_hi.push_back(make_float4(c6[4], c6[5], sg, 0.0f));
+        icov.push_back(make_float4(i6[0], i6[1], i6[2], i6[3]));
+        icov_hi.push_back(make_float4(i6[4], i6[5], 0.0f, 0.0f));
+        keep.push_back(i);
+    }
+    const int64_t nk = (int64_t)keep.size();
+    cov.insert(cov.end(), cov_hi.begin(), cov_hi.end());
+    icov.insert(icov.end(), icov_hi.begin(), icov_hi.end());
+    // SH: coefficient-major RGB flattened, [chunk][N] float4 (coalesced per chunk)
+    std::vector<float4> shd((size_t)chunks * std::max<int64_t>(nk, 1));
+    for (int64_t r = 0; r < nk; r++) {
+        const float* shc = sh + (size_t)keep[r] * nfl;
+        for (int c = 0; c < chunks; c++) {
+            float t[4] = {0, 0, 0, 0};
+            for (int k = 0; k < 4; k++)
+                if (4 * c + k < nfl) t[k] = shc[4 * c + k];
+            shd[(size_t)c * nk + r] = make_float4(t[0], t[1], t[2], t[3]);
+        }
+    }
+    // (re)allocate scene buffers
+    for (float4** p : {&ctx->d_mu, &ctx->d_cov, &ctx->d_icov, &ctx->d_sh})
+        if (*p) { cudaFree(*p); *p = nullptr; }
+    const size_t NN = std::max<int64_t>(nk, 1);
+    CK(dalloc(&ctx->d_mu, NN));
+    CK(dalloc(&ctx->d_cov, 2 * NN));
+    CK(dalloc(&ctx->d_icov, 2 * NN));
+    CK(dalloc(&ctx->d_sh, (size_t)chunks * NN));
+    if (nk > 0) {
+        CK(cudaMemcpy(ctx->d_mu, mu.data(), sizeof(float4) * nk, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_cov, cov.data(), sizeof(float4) * 2 * nk, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_icov, icov.data(), sizeof(float4) * 2 * nk, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_sh, shd.data(), sizeof(float4) * chunks * nk, cudaMemcpyHostToDevice));
+    }
+    ctx->N = nk;
+    ctx->deg = sh_degree;
+    ctx->sh_chunks = chunks;
+    ctx->uploaded = true;
+    if (n_rejected) *n_rejected = n - nk;
+    return VRS_OK;
+}
+
+vrs_status vrs_set_visibility_mask(vrs_context* ctx, int32_t slot, int32_t w, int32_t h, const uint8_t* mask) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    if (ctx->sticky != VRS_OK) return ctx->sticky;
+    if (slot < 0 || slot >= VRS_MAX_MASK_SLOTS) return fail(ctx, VRS_E_INVALID_ARG, "mask slot out of range");
+    CK(cudaSetDevice(ctx->cfg.device));
+    if (ctx->d_mask[slot]) {
+        CK(cudaFree(ctx->d_mask[slot]));
+        ctx->d_mask[slot] = nullptr;
+    }
+    ctx->mask_gen[slot] = ctx->gen_counter++;
+    if (!mask) {
+        ctx->mask_w[slot] = ctx->mask_h[slot] = 0;
+        return VRS_OK;
+    }
+    if (w < 1 || h < 1 || w > ctx->cfg.max_width || h > ctx->cfg.max_height)
+        return fail(ctx, VRS_E_INVALID_ARG, "mask size");
+    CK(dalloc(&ctx->d_mask[slot], (size_t)w * h));
+    CK(cudaMemcpy(ctx->d_mask[slot], mask, (size_t)w * h, cudaMemcpyHostToDevice));
+    ctx->mask_w[slot] = w;
+    ctx->mask_h[slot] = h;
+    return VRS_OK;
+}
+
+vrs_status vrs_set_instrumentation(vrs_context* ctx, int32_t counters, int32_t timing) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    ctx->counters = counters & 1;
+    ctx->no_cull = (counters >> 8) & 1;  // test hook (P12)
+    ctx->timing = timing ? 1 : 0;
+    if (ctx->timing && !ctx->ev_created) {
+        CK(cudaSetDevice(ctx->cfg.device));
+        for (auto& e : ctx->ev) CK(cudaEventCreate(&e));
+        ctx->ev_created = true;
+    }
+    return VRS_OK;
+}
+
+static vrs_status validate_camera(vrs_context* ctx, const vrs_camera& c, const vrs_fovea* f) {
+    const float* R = c.R_wc;
+    for (int i = 0; i < 9; i++)
+        if (!std::isfinite(R[i])) return fail(ctx, VRS_E_INVALID_ARG, "non-finite rotation");
+    for (int i = 0; i < 3; i++)
+        for (int j = 0; j < 3; j++) {
+            double d = 0;
+            for (int k = 0; k < 3; k++) d += (double)R[3 * i + k] * R[3 * j + k];
+            if (std::fabs(d - (i == j ? 1.0 : 0.0)) > 1e-4) return fail(ctx, VRS_E_INVALID_ARG, "R not orthonormal");
+        }
+    const double det = (double)R[0] * (R[4] * R[8] - R[5] * R[7]) - (double)R[1] * (R[3] * R[8] - R[5] * R[6]) +
+                       (double)R[2] * (R[3] * R[7] - R[4] * R[6]);
+    if (det < 0) return fail(ctx, VRS_E_INVALID_ARG, "R has det -1");
+    if (!(c.fx > 0) || !(c.fy > 0) || !std::isfinite(c.cx) || !std::isfinite(c.cy) || !std::isfinite(c.position[0]) ||
+        !std::isfinite(c.position[1]) || !std::isfinite(c.position[2]))
+        return fail(ctx, VRS_E_INVALID_ARG, "bad intrinsics / position");
+    if (c.width < 1 || c.height < 1 || c.width > ctx->cfg.max_width || c.height > ctx->cfg.max_height)
+        return fail(ctx, VRS_E_INVALID_ARG, "view size exceeds max_width/max_height");
+    if (c.mask_slot >= VRS_MAX_MASK_SLOTS) return fail(ctx, VRS_E_INVALID_ARG, "mask slot");
+    if (c.mask_slot >= 0 && ctx->d_mask[c.mask_slot] &&
+        (ctx->mask_w[c.mask_slot] != c.width || ctx->mask_h[c.mask_slot] != c.height))
+        return fail(ctx, VRS_E_INVALID_ARG, "mask resolution differs from view resolution");
+    if (f && f->enabled) {
+        if (ctx->cfg.assign_tile != 32) return fail(ctx, VRS_E_INVALID_ARG, "foveation requires assign_tile 32");
+        if (!(f->radius[0] > 0) || !(f->radius[1] > 0) || !(f->ramp >= 0) || !(f->ramp < 1) ||
+            !std::isfinite(f->center[0]) || !std::isfinite(f->center[1]))
+            return fail(ctx, VRS_E_INVALID_ARG, "bad fovea");
+    }
+    return VRS_OK;
+}
+
+// Build FrameParams for a call and refresh the per-eye setup cache.
+static vrs_status prepare_frame(vrs_context* ctx, int nv, const vrs_camera* cams, const vrs_fovea* fov,
+                                cudaStream_t st, FrameParams& fp, int& total_items) {
+    const int T = ctx->cfg.assign_tile;
+    fp = FrameParams{};
+    fp.n_views = nv;
+    fp.T = T;
+    fp.sh_coeffs = (ctx->deg + 1) * (ctx->deg + 1);
+    fp.counters = ctx->counters;
+    fp.no_cull = ctx->no_cull;
+    fp.N = ctx->N;
+    fp.pair_cap = ctx->cfg.max_pairs;
+    fp.near_plane = ctx->cfg.near_plane;
+    for (int i = 0; i < 3; i++) fp.bg[i] = ctx->cfg.background[i];
+    int64_t tile_base = 0, pix_off = 0;
+    total_items = 0;
+    for (int k = 0; k < 4; k++) ctx->last_cls[k] = 0;
+    for (int vi = 0; vi < nv; vi++) {
+        const vrs_camera& c = cams[vi];
+        ViewParams& v = fp.v[vi];
+        for (int i = 0; i < 9; i++) v.R[i] = c.R_wc[i];
+        for (int i = 0; i < 3; i++) v.o[i] = c.position[i];
+        v.fx = c.fx; v.fy = c.fy; v.cx = c.cx; v.cy = c.cy;
+        v.W = c.width; v.H = c.height;
+        v.tw = (c.width + T - 1) / T;
+        v.th = (c.height + T - 1) / T;
+        v.tile_base = (int32_t)tile_base;
+        const bool fe = fov && fov[vi].enabled;
+        v.fovea = fe ? 1 : 0;
+        if (fe) {
+            v.gx = fov[vi].center[0]; v.gy = fov[vi].center[1];
+            v.rx = fov[vi].radius[0]; v.ry = fov[vi].radius[1];
+            v.ramp = fov[vi].ramp;
+        }
+        v.pix_off = pix_off;
+        v.low_off = (int64_t)vi * ctx->low_px_view;
+        v.low_w = (c.width + 1) / 2;
+        v.vis = ctx->d_vis + (size_t)vi * ctx->max_tiles_view;
+        v.cls = ctx->d_cls + (size_t)vi * ctx->max_tiles_view;
+        v.sat = ctx->d_sat + (size_t)vi * ctx->max_sat_view;
+        v.items = ctx->d_items + (size_t)vi * ctx->max_items_view;
+        // setup cache (precomputed once per eye)
+        const int ms = (c.mask_slot >= 0 && ctx->d_mask[c.mask_slot]) ? c.mask_slot : -1;
+        ViewSetup& s = ctx->vs[vi];
+        const uint64_t mg = ms >= 0 ? ctx->mask_gen[ms] : 0;
+        const bool hit = s.valid && s.W == v.W && s.H == v.H && s.mask_slot == ms && s.mask_gen == mg && s.T == T &&
+                         s.fovea == v.fovea && (!v.fovea || (s.gx == v.gx && s.gy == v.gy && s.rx == v.rx &&
+                                                              s.ry == v.ry && s.ramp == v.ramp));
+        if (!hit) {
+            launch_setup_view(ms >= 0 ? ctx->d_mask[ms] : nullptr, v.W, v, T, ctx->d_vis + (size_t)vi * ctx->max_tiles_view,
+                              ctx->d_sat + (size_t)vi * ctx->max_sat_view,
+                              ctx->d_cls + (size_t)vi * ctx->max_tiles_view,
+                              ctx->d_items + (size_t)vi * ctx->max_items_view, ctx->d_nitems + vi, st);
+            CK(cudaGetLastError());
+            int32_t ni = 0;
+            std::vector<int32_t> cls((size_t)v.tw * v.th);
+            CK(cudaMemcpyAsync(&ni, ctx->d_nitems + vi, 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(cls.data(), ctx->d_cls + (size_t)vi * ctx->max_tiles_view, 4 * cls.size(),
+                               cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            s.valid = true;
+            s.W = v.W; s.H = v.H; s.mask_slot = ms; s.mask_gen = mg; s.T = T; s.fovea = v.fovea;
+            s.gx = v.gx; s.gy = v.gy; s.rx = v.rx; s.ry = v.ry; s.ramp = v.ramp;
+            s.n_items = ni;
+            for (int k = 0; k < 4; k++) s.cls_count[k] = 0;
+            for (int32_t cc : cls) s.cls_count[cc & 3]++;
+        }
+        for (int k = 0; k < 4; k++) ctx->last_cls[k] += s.cls_count[k];
+        v.n_items = s.n_items;
+        v.item_off = total_items;
+        total_items += s.n_items;
+        tile_base += (int64_t)v.tw * v.th;
+        pix_off += (int64_t)v.W * v.H;
+    }
+    if (tile_base >= ((int64_t)1 << 20)) return fail(ctx, VRS_E_INVALID_ARG, "too many tiles in one call");
+    ctx->last_tiles = tile_base;
+    return VRS_OK;
+}
+
+static int key_bits_for(int64_t tiles) {
+    int b = 0;
+    while (((int64_t)1 << b) < tiles) b++;
+    return 32 + b;
+}
+
+static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* cams, const vrs_fovea* fov, float* rgba,
+                              float* depth, cudaStream_t st) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    if (ctx->sticky != VRS_OK) return ctx->sticky;
+    if (!ctx->uploaded) return fail(ctx, VRS_E_STATE, "render before vrs_upload_gaussians");
+    if (nv < 1 || nv > ctx->cfg.max_views || !cams || !rgba || !depth)
+        return fail(ctx, VRS_E_INVALID_ARG, "n_views / null pointer");
+    for (int i = 0; i < nv; i++) {
+        vrs_status s = validate_camera(ctx, cams[i], fov ? &fov[i] : nullptr);
+        if (s != VRS_OK) return s;
+    }
+    CK(cudaSetDevice(ctx->cfg.device));
+    FrameParams fp;
+    int total_items = 0;
+    {
+        vrs_status s = prepare_frame(ctx, nv, cams, fov, st, fp, total_items);
+        if (s != VRS_OK) return s;
+    }
+    SceneDev sc{ctx->d_mu, ctx->d_cov, ctx->d_icov, ctx->d_sh, ctx->sh_chunks};
+    FrameBufs fb{};
+    fb.rec = ctx->d_rec;
+    fb.counts = ctx->d_counts;
+    fb.offsets = ctx->d_offsets;
+    fb.total = ctx->d_misc;
+    fb.overflow = ctx->d_misc + 1;
+    fb.keys = ctx->d_keys;
+    fb.vals = ctx->d_vals;
+    fb.keys_alt = ctx->d_keys_alt;
+    fb.vals_alt = ctx->d_vals_alt;
+    fb.ranges = ctx->d_ranges;
+    fb.low_rgba = ctx->d_low_rgba;
+    fb.low_depth = ctx->d_low_depth;
+    fb.stats = ctx->d_stats;
+    const bool tm = ctx->timing && ctx->ev_created;
+    if (tm) CK(cudaEventRecord(ctx->ev[0], st));
+    CK(cudaMemsetAsync(ctx->d_misc + 1, 0, 4, st));
+    if (ctx->counters) CK(cudaMemsetAsync(ctx->d_stats, 0, 8 * sizeof(unsigned long long), st));
+    launch_preprocess(sc, fp, fb, st);
+    if (tm) CK(cudaEventRecord(ctx->ev[1], st));
+    launch_scan(fb.counts, fb.offsets, fb.total, (int64_t)nv * fp.N, ctx->d_scan_scratch, st);
+    if (tm) CK(cudaEventRecord(ctx->ev[2], st));
+    launch_duplicate(fp, fb, st);
+    if (tm) CK(cudaEventRecord(ctx->ev[3], st));
+    launch_sort(fb.keys, fb.vals, fb.keys_alt, fb.vals_alt, fb.total, fp.pair_cap, key_bits_for(ctx->last_tiles),
+                ctx->sort, st);
+    if (tm) CK(cudaEventRecord(ctx->ev[4], st));
+    launch_ranges(fb.keys, fb.total, fp.pair_cap, fb.ranges, ctx->last_tiles, st);
+    if (tm) CK(cudaEventRecord(ctx->ev[5], st));
+    launch_blend(fp, fb, total_items, rgba, depth, st);
+    if (tm) CK(cudaEventRecord(ctx->ev[6], st));
+    launch_compose(fp, fb, rgba, depth, st);
+    if (tm) CK(cudaEventRecord(ctx->ev[7], st));
+    CK(cudaGetLastError());
+    ctx->fp = fp;
+    ctx->have_frame = true;
+    ctx->last_stream = st;
+    ctx->last_items = total_items;
+    return VRS_OK;
+}
+
+vrs_status vrs_render_views(vrs_context* ctx, int32_t n_views, const vrs_camera* cams, const vrs_fovea* fovea,
+                            float* rgba, float* depth, void* stream) {
+    return render_impl(ctx, n_views, cams, fovea, rgba, depth, (cudaStream_t)stream);
+}
+
+vrs_status vrs_render_views_host(vrs_context* ctx, int32_t n_views, const vrs_camera* cams, const vrs_fovea* fovea,
+                                 float* rgba_host, float* depth_host, void* stream) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    if (!rgba_host || !depth_host || !cams || n_views < 1) return fail(ctx, VRS_E_INVALID_ARG, "null pointer");
+    size_t px = 0;
+    for (int i = 0; i < n_views; i++) px += (size_t)std::max(cams[i].width, 0) * std::max(cams[i].height, 0);
+    CK(cudaSetDevice(ctx->cfg.device));
+    if (px > ctx->out_px_cap) {
+        if (ctx->d_out_rgba) cudaFree(ctx->d_out_rgba);
+        if (ctx->d_out_depth) cudaFree(ctx->d_out_depth);
+        ctx->d_out_rgba = ctx->d_out_depth = nullptr;
+        CK(dalloc(&ctx->d_out_rgba, 4 * px));
+        CK(dalloc(&ctx->d_out_depth, px));
+        ctx->out_px_cap = px;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    vrs_status s = render_impl(ctx, n_views, cams, fovea, ctx->d_out_rgba, ctx->d_out_depth, st);
+    if (s != VRS_OK) return s;
+    CK(cudaMemcpyAsync(rgba_host, ctx->d_out_rgba, sizeof(float) * 4 * px, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(depth_host, ctx->d_out_depth, sizeof(float) * px, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return VRS_OK;
+}
+
+vrs_status vrs_get_frame_stats(vrs_context* ctx, vrs_frame_stats* out) {
+    if (!ctx || !out) return VRS_E_INVALID_ARG;
+    if (ctx->sticky != VRS_OK) return ctx->sticky;
+    if (!ctx->have_frame) return fail(ctx, VRS_E_STATE, "no frame rendered");
+    CK(cudaSetDevice(ctx->cfg.device));
+    CK(cudaStreamSynchronize(ctx->last_stream));
+    std::memset(out, 0, sizeof(*out));
+    uint32_t misc[2] = {0, 0};
+    CK(cudaMemcpy(misc, ctx->d_misc, 8, cudaMemcpyDeviceToHost));
+    out->pairs = misc[0];
+    unsigned long long st[8] = {0};
+    if (ctx->counters) CK(cudaMemcpy(st, ctx->d_stats, sizeof(st), cudaMemcpyDeviceToHost));
+    out->evaluations = (int64_t)st[0];
+    out->contributions = (int64_t)st[1];
+    out->overflow_samples = (int64_t)st[2];
+    out->terminated_samples = (int64_t)st[3];
+    int64_t samples = 0;
+    for (int vi = 0; vi < ctx->fp.n_views; vi++) {
+        const ViewSetup& s = ctx->vs[vi];
+        const ViewParams& v = ctx->fp.v[vi];
+        // samples = full-rate pixels of High/Hybrid tiles + groups of Low tiles (in image)
+        std::vector<int32_t> cls((size_t)v.tw * v.th);
+        CK(cudaMemcpy(cls.data(), v.cls, 4 * cls.size(), cudaMemcpyDeviceToHost));
+        const int T = ctx->fp.T;
+        for (int t = 0; t < (int)cls.size(); t++) {
+            const int tx = t % v.tw, ty = t / v.tw;
+            const int w = std::min(T, v.W - tx * T), h = std::min(T, v.H - ty * T);
+            if (cls[t] == kHigh || cls[t] == kHybrid) samples += (int64_t)w * h;
+            else if (cls[t] == kLow) samples += (int64_t)((w + 1) / 2) * ((h + 1) / 2);
+        }
+        (void)s;
+    }
+    out->samples = samples;
+    for (int k = 0; k < 4; k++) out->tiles_by_class[k] = ctx->last_cls[k];
+    out->work_items = ctx->last_items;
+    {
+        std::vector<uint32_t> cnt((size_t)ctx->fp.n_views * ctx->N);
+        if (!cnt.empty())
+            CK(cudaMemcpy(cnt.data(), ctx->d_counts, 4 * cnt.size(), cudaMemcpyDeviceToHost));
+        int64_t vsplat = 0;
+        for (uint32_t c : cnt) vsplat += c > 0;
+        out->visible_splats = vsplat;
+    }
+    if (ctx->timing && ctx->ev_created) {
+        for (int k = 0; k < 7; k++) CK(cudaEventElapsedTime(&out->stage_ms[k], ctx->ev[k], ctx->ev[k + 1]));
+        CK(cudaEventElapsedTime(&out->stage_ms[7], ctx->ev[0], ctx->ev[7]));
+    }
+    if (misc[1] || (int64_t)misc[0] > ctx->cfg.max_pairs)
+        return fail(ctx, VRS_E_CAPACITY, "pair buffer overflow (max_pairs too small)");
+    return VRS_OK;
+}
+
+vrs_status vrs_debug_counts(vrs_context* ctx, uint32_t* counts, int64_t capacity, int64_t* n_out) {
+    if (!ctx || !counts) return VRS_E_INVALID_ARG;
+    if (!ctx->have_frame) return fail(ctx, VRS_E_STATE, "no frame");
+    CK(cudaStreamSynchronize(ctx->last_stream));
+    const int64_t n = (int64_t)ctx->fp.n_views * ctx->N;
+    if (n_out) *n_out = n;
+    if (capacity < n) return fail(ctx, VRS_E_INVALID_ARG, "capacity");
+    if (n) CK(cudaMemcpy(counts, ctx->d_counts, 4 * n, cudaMemcpyDeviceToHost));
+    return VRS_OK;
+}
+
+vrs_status vrs_debug_pairs(vrs_context* ctx, int32_t sorted, uint64_t* keys, uint32_t* vals, int64_t capacity,
+                           int64_t* n_out) {
+    if (!ctx || !keys || !vals) return VRS_E_INVALID_ARG;
+    if (!ctx->have_frame) return fail(ctx, VRS_E_STATE, "no frame");
+    cudaStream_t st = ctx->last_stream;
+    CK(cudaStreamSynchronize(st));
+    uint32_t P = 0;
+    CK(cudaMemcpy(&P, ctx->d_misc, 4, cudaMemcpyDeviceToHost));
+    const int64_t n = std::min<int64_t>(P, ctx->cfg.max_pairs);
+    if (n_out) *n_out = n;
+    if (capacity < n) return fail(ctx, VRS_E_INVALID_ARG, "capacity");
+    if (sorted) {
+        CK(cudaMemcpy(keys, ctx->d_keys, 8 * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(vals, ctx->d_vals, 4 * n, cudaMemcpyDeviceToHost));
+    } else {
+        // re-run the emission into the alternate buffers (same kernel, same inputs)
+        FrameBufs fb{};
+        fb.rec = ctx->d_rec;
+        fb.counts = ctx->d_counts;
+        fb.offsets = ctx->d_offsets;
+        fb.total = ctx->d_misc;
+        fb.overflow = ctx->d_misc + 1;
+        fb.keys = ctx->d_keys_alt;
+        fb.vals = ctx->d_vals_alt;
+        launch_duplicate(ctx->fp, fb, st);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(st));
+        CK(cudaMemcpy(keys, ctx->d_keys_alt, 8 * n, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(vals, ctx->d_vals_alt, 4 * n, cudaMemcpyDeviceToHost));
+    }
+    return VRS_OK;
+}
+
+vrs_status vrs_debug_ranges(vrs_context* ctx, uint32_t* ranges, int64_t capacity, int64_t* n_out) {
+    if (!ctx || !ranges) return VRS_E_INVALID_ARG;
+    if (!ctx->have_frame) return fail(ctx, VRS_E_STATE, "no frame");
+    CK(cudaStreamSynchronize(ctx->last_stream));
+    if (n_out) *n_out = ctx->last_tiles;
+    if (capacity < 2 * ctx->last_tiles) return fail(ctx, VRS_E_INVALID_ARG, "capacity");
+    CK(cudaMemcpy(ranges, ctx->d_ranges, 8 * ctx->last_tiles, cudaMemcpyDeviceToHost));
+    return VRS_OK;
+}
+
+vrs_status vrs_debug_splats(vrs_context* ctx, int32_t view, float* out, int64_t capacity) {
+    if (!ctx || !out) return VRS_E_INVALID_ARG;
+    if (!ctx->have_frame || view < 0 || view >= ctx->fp.n_views) return fail(ctx, VRS_E_STATE, "no such view");
+    if (capacity < 48 * ctx->N) return fail(ctx, VRS_E_INVALID_ARG, "capacity");
+    cudaStream_t st = ctx->last_stream;
+    CK(cudaStreamSynchronize(st));
+    if (ctx->N == 0) return VRS_OK;
+    float* d = nullptr;
+    CK(dalloc(&d, 48 * (size_t)ctx->N));
+    SceneDev sc{ctx->d_mu, ctx->d_cov, ctx->d_icov, ctx->d_sh, ctx->sh_chunks};
+    FrameBufs fb{};
+    fb.counts = ctx->d_counts;
+    launch_debug_splats(sc, ctx->fp, fb, view, d, st);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaMemcpy(out, d, sizeof(float) * 48 * ctx->N, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    CK(e);
+    return VRS_OK;
+}
+
+vrs_status vrs_debug_tile_info(vrs_context* ctx, int32_t view, int32_t* cls, int32_t* vis, int64_t capacity) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    if (!ctx->have_frame || view < 0 || view >= ctx->fp.n_views) return fail(ctx, VRS_E_STATE, "no such view");
+    const ViewParams& v = ctx->fp.v[view];
+    const int64_t n = (int64_t)v.tw * v.th;
+    if (capacity < n) return fail(ctx, VRS_E_INVALID_ARG, "capacity");
+    CK(cudaStreamSynchronize(ctx->last_stream));
+    if (cls) CK(cudaMemcpy(cls, v.cls, 4 * n, cudaMemcpyDeviceToHost));
+    if (vis) CK(cudaMemcpy(vis, v.vis, 4 * n, cudaMemcpyDeviceToHost));
+    return VRS_OK;
+}
+
+vrs_status vrs_sort_pairs(vrs_context* ctx, uint64_t* keys, uint32_t* vals, int64_t n, int32_t key_bits,
+                          void* stream) {
+    if (!ctx || (!keys && n > 0) || (!vals && n > 0)) return VRS_E_INVALID_ARG;
+    if (n < 0 || n > ctx->cfg.max_pairs || key_bits < 1 || key_bits > 64)
+        return fail(ctx, VRS_E_INVALID_ARG, "n or key_bits");
+    if (n == 0) return VRS_OK;
+    CK(cudaSetDevice(ctx->cfg.device));
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t nn = (uint32_t)n;
+    uint32_t* d_n = ctx->d_misc + 4;
+    CK(cudaMemcpyAsync(d_n, &nn, 4, cudaMemcpyHostToDevice, st));
+    CK(cudaStreamSynchronize(st));
+    launch_sort(keys, vals, ctx->d_keys_alt, ctx->d_vals_alt, d_n, n, key_bits, ctx->sort, st);
+    CK(cudaGetLastError());
+    return VRS_OK;
+}
+
+vrs_status vrs_exclusive_scan(vrs_context* ctx, const uint32_t* in, uint32_t* out, uint32_t* total, int64_t n,
+                              void* stream) {
+    if (!ctx || !out || !total || (!in && n > 0)) return VRS_E_INVALID_ARG;
+    if (n < 0 || n > (int64_t)ctx->cfg.max_views * std::max<int64_t>(ctx->cfg.max_gaussians, 1))
+        return fail(ctx, VRS_E_INVALID_ARG, "n");
+    CK(cudaSetDevice(ctx->cfg.device));
+    launch_scan(in, out, total, n, ctx->d_scan_scratch, (cudaStream_t)stream);
+    CK(cudaGetLastError());
+    return VRS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,141 @@
+// Internal definitions of libvrs (CUDA path).  Not shared with the oracle.
+//
+// Numerics: this library is compiled with -fmad=false and IEEE division /
+// square root, so every float expression below rounds exactly like the
+// operation order it is written in; FMAs appear only where fmaf() is written.
+// That is what makes the decision quantities (culling, tile membership, sort
+// keys, per-sample membership and order) bit-identical to the DESIGN.md
+// "Numerics contract".
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/vrs.h"
+
+namespace vrs {
+
+constexpr int kBlend = 256;        // threads per blend block
+constexpr int kWindow = 16;        // StopThePop per-sample resort window K
+constexpr int kRecF4 = 8;          // float4 per projected-splat record (128 B)
+constexpr float kO7Margin = 1.001f;  // O7 keep threshold factor (DESIGN R7)
+constexpr float kTmin = 1e-4f;     // early termination (L11)
+constexpr float kAlphaMax = 0.99f; // alpha clamp (L10)
+
+enum TileClass : int32_t { kHigh = 0, kLow = 1, kHybrid = 2, kInvisible = 3 };
+enum ItemKind : uint32_t { kItemFull = 0, kItemHybrid = 1, kItemLow = 2 };
+
+// Per-view parameters, passed by value inside FrameParams.
+struct ViewParams {
+    float R[9];
+    float o[3];
+    float fx, fy, cx, cy;
+    int32_t W, H;
+    int32_t tw, th;          // assignment-tile grid
+    int32_t tile_base;       // global tile id offset (views concatenated)
+    int32_t fovea;           // foveation on
+    float gx, gy, rx, ry, ramp;
+    int64_t pix_off;         // pixel offset of this view in the output buffers
+    int64_t low_off;         // offset of this view in the low-res sample planes
+    int32_t low_w;           // low-res plane width ((W+1)/2)
+    int32_t n_items;         // blend work items of this view
+    int32_t item_off;        // first item of this view in the launch
+    const int32_t* vis;      // [th*tw] visibility bits
+    const uint32_t* sat;     // [(th+1)*(tw+1)] summed-area table
+    const int32_t* cls;      // [th*tw] tile classes
+    const uint32_t* items;   // [n_items] packed work items
+};
+
+struct FrameParams {
+    int32_t n_views;
+    int32_t T;               // assignment tile size
+    int32_t sh_coeffs;       // (deg+1)^2
+    int32_t counters;        // instrumentation on
+    int32_t no_cull;         // test hook: disable the warp-block footprint skip (P12)
+    int64_t N;
+    int64_t pair_cap;
+    float near_plane;
+    float bg[3];
+    ViewParams v[VRS_MAX_VIEWS];
+};
+
+struct SceneDev {
+    const float4* mu;        // [N] mu.xyz, q_cut
+    const float4* cov;       // [2][N] (xx,xy,xz,yy) (yz,zz,sigma,0)
+    const float4* icov;      // [2][N] (xx,xy,xz,yy) (yz,zz,0,0)
+    const float4* sh;        // [chunks][N]
+    int32_t sh_chunks;
+};
+
+struct FrameBufs {
+    float4* rec;             // [V][N][8]
+    uint32_t* counts;        // [V*N]
+    uint32_t* offsets;       // [V*N]
+    uint32_t* total;         // [1] pair total (device)
+    uint32_t* overflow;      // [1] capacity overflow flag
+    uint64_t* keys;          // [cap] emission keys
+    uint32_t* vals;          // [cap]
+    uint64_t* keys_alt;      // [cap] sort ping-pong
+    uint32_t* vals_alt;
+    uint32_t* ranges;        // [tiles][2]
+    float4* low_rgba;        // low-res samples RGBA
+    float* low_depth;        // low-res samples depth
+    unsigned long long* stats;  // [8] device counters
+};
+
+// ----------------------------------------------------------------- launchers
+void launch_setup_view(const uint8_t* mask, int mask_w, ViewParams vp, int T, int32_t* vis, uint32_t* sat,
+                       int32_t* cls, uint32_t* items, int32_t* n_items_dev, cudaStream_t st);
+void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, cudaStream_t st);
+void launch_scan(const uint32_t* in, uint32_t* out, uint32_t* total, int64_t n, uint32_t* scratch,
+                 cudaStream_t st);
+size_t scan_scratch_words(int64_t n);
+void launch_duplicate(const FrameParams& fp, FrameBufs fb, cudaStream_t st);
+struct SortScratch {
+    uint32_t* hist;          // [8][256]
+    uint32_t* status;        // [passes][max_tiles][256]
+    uint32_t* counters;      // [8]
+    int64_t max_tiles;
+};
+size_t sort_status_words(int64_t cap);
+// Sort n_dev (device count, capped at cap) pairs by key bits [0, key_bits); result in (keys, vals).
+void launch_sort(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, const uint32_t* n_dev,
+                 int64_t cap, int key_bits, SortScratch s, cudaStream_t st);
+void launch_ranges(const uint64_t* keys, const uint32_t* n_dev, int64_t cap, uint32_t* ranges, int64_t n_tiles,
+                   cudaStream_t st);
+void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
+                  cudaStream_t st);
+void launch_compose(const FrameParams& fp, FrameBufs fb, float* rgba, float* depth, cudaStream_t st);
+void launch_debug_splats(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int view, float* out,
+                         cudaStream_t st);
+
+// ----------------------------------------------------------------- numerics (contract R6)
+__device__ __forceinline__ float dot3(float ax, float ay, float az, float bx, float by, float bz) {
+    return fmaf(ax, bx, fmaf(ay, by, az * bz));
+}
+// d^T Q d with pre-doubled coefficients (a,b,c,p,e,f) = (Q00,2Q01,Q11,2Q02,2Q12,Q22)
+__device__ __forceinline__ float quad3(float a, float b, float c, float p, float e, float f, float x, float y,
+                                       float z) {
+    return fmaf(fmaf(a, x, fmaf(b, y, p * z)), x, fmaf(fmaf(c, y, e * z), y, (f * z) * z));
+}
+// z = 1 specialisation (bit-identical: p*1, e*1, f*1*1 are exact)
+__device__ __forceinline__ float quad3z1(float a, float b, float c, float p, float e, float f, float x, float y) {
+    return fmaf(fmaf(a, x, fmaf(b, y, p)), x, fmaf(fmaf(c, y, e), y, f));
+}
+
+// Blend weight of the fovea ramp at a pixel centre (P:461
+// "10% padding of linearly increasing blending weights").
+__device__ __forceinline__ float fovea_weight(const ViewParams& v, float px, float py) {
+    float ax = fabsf(px - v.gx) - v.rx;
+    float ay = fabsf(py - v.gy) - v.ry;
+    ax = ax > 0.0f ? ax : 0.0f;
+    ay = ay > 0.0f ? ay : 0.0f;
+    float dxn = v.ramp * (2.0f * v.rx);
+    float dyn = v.ramp * (2.0f * v.ry);
+    float wx = dxn > 0.0f ? ax / dxn : (ax > 0.0f ? 1.0f : 0.0f);
+    float wy = dyn > 0.0f ? ay / dyn : (ay > 0.0f ? 1.0f : 0.0f);
+    float m = wx > wy ? wx : wy;
+    float w = 1.0f - m;
+    return w < 0.0f ? 0.0f : (w > 1.0f ? 1.0f : w);
+}
+
+}  // namespace vrs

@@ -1,0 +1,302 @@
+"""GPU parity: the CUDA path (through the C ABI) against the C++ oracle on
+the same seeded inputs.  Bars (BASELINE.json north_star): bit-exact per-tile
+pair counts, sorted key order, values and ranges; per-channel |dRGB| <= 2e-3
+and |dDepth| <= 1e-4 relative on every compared pixel."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import scenegen as sg
+from helpers import identity_camera, scene_from, tiny_set
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+RGB_TOL = 2e-3
+DEPTH_REL = 1e-4
+# decision fields of the 48-float splat record that must be bit-identical
+EXACT_FIELDS = list(range(1, 34)) + [37, 38, 39, 40, 41, 42, 47]
+
+
+@pytest.fixture(scope="module")
+def vrs():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2505_10144_b200 import build
+    build.build()
+    import paper_2505_10144_b200 as p
+    return p
+
+
+def render_both(vrs, oracle_mod, scene, cams, foveas=None, T=16, masks=None, max_pairs=1 << 22, counters=True,
+                no_cull=False, oracle_render=True):
+    W = max(c.width for c in cams)
+    H = max(c.height for c in cams)
+    r = vrs.Renderer(max_gaussians=max(scene.n, 1), max_views=len(cams), max_pairs=max_pairs, max_width=W,
+                     max_height=H, assign_tile=T)
+    r.upload(scene)
+    o = oracle_mod.Oracle(scene)
+    for slot, m in (masks or {}).items():
+        r.set_mask(slot, m)
+        o.set_mask(slot, m)
+    r.vrs_set_instrumentation(counters=counters, no_cull=no_cull)
+    rgba, depth = r.render(cams, foveas)
+    torch.cuda.synchronize()
+    g_imgs = vrs.vrs.split_views(rgba.cpu().numpy(), depth.cpu().numpy(), cams)
+    o.prepare(cams, foveas, assign_tile=T)
+    o_imgs = o.render() if oracle_render else None
+    return r, o, g_imgs, o_imgs
+
+
+def assert_images_close(g_imgs, o_imgs):
+    for (gi, gd), (oi, od) in zip(g_imgs, o_imgs):
+        drgb = np.abs(gi[..., :3] - oi[..., :3])
+        assert drgb.max() <= RGB_TOL, f"max |dRGB| {drgb.max()} at {np.unravel_index(drgb.argmax(), drgb.shape)}"
+        da = np.abs(gi[..., 3] - oi[..., 3])
+        assert da.max() <= RGB_TOL, f"max |dA| {da.max()}"
+        dd = np.abs(gd - od) - DEPTH_REL * np.abs(od)
+        assert dd.max() <= 1e-6, f"depth excess {dd.max()} at {np.unravel_index(dd.argmax(), dd.shape)}"
+
+
+def assert_lists_equal(r, o):
+    assert np.array_equal(r.vrs_debug_counts(), o.counts()), "per-(view,g) pair counts differ"
+    ku, vu = r.vrs_debug_pairs(False)
+    oku, ovu = o.pairs(False)
+    assert np.array_equal(ku, oku) and np.array_equal(vu, ovu), "emitted pairs differ"
+    k, v = r.vrs_debug_pairs(True)
+    ok, ov = o.pairs(True)
+    assert np.array_equal(k, ok), "sorted keys differ"
+    assert np.array_equal(v, ov), "sorted values differ"
+    assert np.array_equal(r.vrs_debug_ranges(), o.ranges()), "tile ranges differ"
+
+
+def test_c1_parity(vrs, oracle_mod):
+    """Config C1: 1000 Gaussians, SH0, 128^2, 90 deg, 16x16 tiles, no foveation."""
+    scene = sg.random_scene(0, n=1000, sh_degree=0)
+    cam = sg.look_camera((0, 0, 0), f=64.0, width=128, height=128)
+    r, o, g, oi = render_both(vrs, oracle_mod, scene, [cam])
+    assert_lists_equal(r, o)
+    assert_images_close(g, oi)
+    st, ost = r.stats(), o.stats()
+    for k in ("pairs", "samples", "contributions", "overflow_samples"):
+        assert st[k] == ost[k], (k, st[k], ost[k])
+    assert abs(st["evaluations"] - ost["evaluations"]) <= 1e-3 * ost["evaluations"]
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2, 3, 4])
+def test_c1_seeds_parity(vrs, oracle_mod, seed):
+    """C1 seeds 0-24 subset, with SH degree 3 colour."""
+    scene = sg.random_scene(seed, n=1000, sh_degree=3)
+    cam = sg.look_camera((0, 0, 0), f=64.0, width=128, height=128)
+    r, o, g, oi = render_both(vrs, oracle_mod, scene, [cam])
+    assert_lists_equal(r, o)
+    assert_images_close(g, oi)
+
+
+def test_preprocess_records_parity(vrs, oracle_mod):
+    """Step 1: per-Gaussian records -- decision fields bit-exact, colour 1e-5."""
+    scene = sg.random_scene(5, n=2000, sh_degree=3, xy_frac=1.5)
+    cams = [sg.look_camera((-0.03, 0, 0), 0.1, -0.05, 0.02, f=90.0, width=200, height=150),
+            sg.look_camera((0.03, 0, 0), 0.1, -0.05, 0.02, f=90.0, width=200, height=150)]
+    r, o, _, _ = render_both(vrs, oracle_mod, scene, cams, oracle_render=False)
+    for view in range(2):
+        gs, os_ = r.vrs_debug_splats(view), o.splats(view)
+        valid = os_[:, 0] == 1
+        assert np.array_equal(gs[:, 0], os_[:, 0]), "valid flags differ"
+        for f in EXACT_FIELDS:
+            a, b = gs[valid, f], os_[valid, f]
+            bad = ~((a == b) | (np.isnan(a) & np.isnan(b)))
+            assert not bad.any(), f"field {f} differs at {np.nonzero(bad)[0][:5]}: {a[bad][:3]} vs {b[bad][:3]}"
+        np.testing.assert_allclose(gs[valid, 34:37], os_[valid, 34:37], atol=1e-5)
+        np.testing.assert_allclose(gs[valid, 43:47], os_[valid, 43:47], rtol=1e-6, atol=1e-4)
+
+
+def test_foveated_masked_stereo_parity(vrs, oracle_mod):
+    """Single-launch foveation with hybrid tiles, LowRes 2x2 groups, compose,
+    visibility masks, stereo in one frame (T_a = 32)."""
+    scene = sg.vr_room(7, 20000, sh_degree=3)
+    W, H = 320, 256
+    f = sg.focal_for_hfov(W, 110.0)
+    cams = []
+    for e, x in enumerate((-0.0315, 0.0315)):
+        c = sg.look_camera((x, 0, 0), 0.3, 0.1, 0.0, f=f, width=W, height=H, mask_slot=e)
+        cams.append(c)
+    fov = [sg.Fovea((W / 2, H / 2), (W / 4, H / 4), 0.10)] * 2
+    masks = {0: sg.ellipse_mask(W, H), 1: sg.ellipse_mask(W, H, 1.0)}
+    r, o, g, oi = render_both(vrs, oracle_mod, scene, cams, fov, T=32, masks=masks)
+    assert_lists_equal(r, o)
+    assert_images_close(g, oi)
+    for view in range(2):
+        gc, gv = r.vrs_debug_tile_info(view, 32)
+        oc, ov = o.tile_info(view)
+        assert np.array_equal(gc, oc) and np.array_equal(gv, ov)
+        assert set(np.unique(oc)) == {0, 1, 2, 3}
+    st, ost = r.stats(), o.stats()
+    assert st["tiles_by_class"] == [ost["tiles_high"], ost["tiles_low"], ost["tiles_hybrid"], ost["tiles_invisible"]]
+    assert st["samples"] == ost["samples"] and st["work_items"] == ost["work_items"]
+
+
+@pytest.mark.parametrize("W,H,T", [(37, 29, 16), (65, 33, 32), (16, 16, 16), (1, 1, 16), (300, 17, 32)])
+def test_odd_sizes_and_edges(vrs, oracle_mod, W, H, T):
+    """Ragged image borders (partial tiles, odd widths, 1x1)."""
+    scene = sg.random_scene(11, n=600, sh_degree=1, xy_frac=1.2)
+    cam = identity_camera(W, H, max(W, H) * 0.6)
+    fov = [sg.Fovea((W / 2, H / 2), (W / 5 + 1, H / 5 + 1), 0.2)] if T == 32 else None
+    r, o, g, oi = render_both(vrs, oracle_mod, scene, [cam], fov, T=T)
+    assert_lists_equal(r, o)
+    assert_images_close(g, oi)
+
+
+def test_empty_and_fully_culled_scenes(vrs, oracle_mod):
+    cam = identity_camera(64, 48, 40.0)
+    # empty scene
+    r, o, g, oi = render_both(vrs, oracle_mod, scene_from(np.zeros((0, 3)), 0.1), [cam])
+    assert np.all(g[0][0][..., 3] == 0) and np.all(g[0][1] == 0)
+    # everything behind the camera
+    sc = scene_from(np.array([[0, 0, -3.0], [1, 1, -2.0]]), 0.2)
+    r, o, g, oi = render_both(vrs, oracle_mod, sc, [cam])
+    assert r.stats()["pairs"] == 0
+    assert_images_close(g, oi)
+
+
+@pytest.mark.parametrize("seed", list(range(100, 110)))
+def test_tiny_scenes_parity(vrs, oracle_mod, seed):
+    sc, cam = tiny_set(seed)
+    r, o, g, oi = render_both(vrs, oracle_mod, sc, [cam])
+    assert_lists_equal(r, o)
+    assert_images_close(g, oi)
+
+
+def test_window_overflow_parity(vrs, oracle_mod):
+    """Depth complexity >> K = 16: window overflows must match exactly (same pops)."""
+    rs = np.random.default_rng(1)
+    n = 300
+    means = np.stack([rs.uniform(-0.3, 0.3, n), rs.uniform(-0.3, 0.3, n), rs.uniform(3, 3.6, n)], 1)
+    sc = scene_from(means, [0.4, 0.4, 0.03], opacities=0.05)
+    sc.quats[:] = np.stack([np.ones(n), rs.normal(0, 0.6, n), rs.normal(0, 0.6, n), np.zeros(n)], 1)
+    cam = identity_camera(64, 64, 48.0)
+    r, o, g, oi = render_both(vrs, oracle_mod, sc, [cam])
+    st, ost = r.stats(), o.stats()
+    assert ost["overflow_samples"] > 100
+    assert st["overflow_samples"] == ost["overflow_samples"]
+    assert st["contributions"] == ost["contributions"]
+    assert_images_close(g, oi)
+
+
+def test_warp_culling_never_changes_results(vrs, oracle_mod):
+    """P12: the warp-block footprint skip changes work, never results (bit-identical)."""
+    scene = sg.vr_room(3, 20000)
+    W, H = 256, 192
+    cams = sg.stereo_pair(width=W, height=H, masks=False)
+    fov = [sg.Fovea((W / 2, H / 2), (W / 4, H / 4), 0.1)] * 2
+    outs = []
+    for nc in (False, True):
+        r = vrs.Renderer(max_gaussians=scene.n, max_views=2, max_pairs=1 << 22, max_width=W, max_height=H,
+                         assign_tile=32)
+        r.upload(scene)
+        r.vrs_set_instrumentation(counters=0, no_cull=nc)
+        rgba, depth = r.render(cams, fov)
+        torch.cuda.synchronize()
+        outs.append((rgba.cpu().numpy(), depth.cpu().numpy()))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+
+
+def test_determinism(vrs):
+    """P14: two renders are byte-identical."""
+    scene = sg.vr_room(4, 30000)
+    W, H = 256, 256
+    cams = sg.stereo_pair(width=W, height=H, masks=False)
+    r = vrs.Renderer(max_gaussians=scene.n, max_views=2, max_pairs=1 << 22, max_width=W, max_height=H,
+                     assign_tile=32)
+    r.upload(scene)
+    fov = [sg.Fovea((W / 2, H / 2), (W / 4, H / 4), 0.1)] * 2
+    a = [t.cpu().numpy() for t in r.render(cams, fov)]
+    b = [t.cpu().numpy() for t in r.render(cams, fov)]
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_large_fov_identity_gpu(vrs):
+    """P13 on the CUDA path: crop of the 3x render equals the 1x render bit for bit."""
+    sc = sg.random_scene(6, n=800, z_range=(1.5, 6.0), xy_frac=2.0)
+    W, H = 64, 48
+    small = identity_camera(W, H, 40.0)
+    large = identity_camera(3 * W, 3 * H, 40.0, cx=small.cx + W, cy=small.cy + H)
+    outs = []
+    for cam in (small, large):
+        r = vrs.Renderer(max_gaussians=sc.n, max_views=1, max_pairs=1 << 20, max_width=cam.width,
+                         max_height=cam.height, assign_tile=16)
+        r.upload(sc)
+        rgba, depth = r.render([cam])
+        outs.append(vrs.vrs.split_views(rgba.cpu().numpy(), depth.cpu().numpy(), [cam])[0])
+    (a, ad), (b, bd) = outs
+    assert np.array_equal(a, b[H:2 * H, W:2 * W]) and np.array_equal(ad, bd[H:2 * H, W:2 * W])
+
+
+@pytest.mark.parametrize("n", [1, 100, 4095, 4096, 4097, 100000, 1234567])
+def test_onesweep_sort_bit_exact(vrs, n):
+    """Step 4: stable sort equals numpy's stable argsort (ties keep input order)."""
+    rs = np.random.default_rng(n)
+    tiles = rs.integers(0, 9000, n).astype(np.uint64)
+    depth = rs.uniform(0.2, 40.0, n).astype(np.float32).view(np.uint32).astype(np.uint64)
+    depth[rs.random(n) < 0.2] = np.uint64(0x3e4ccccd)  # many exact ties (near-clamped depths)
+    keys = (tiles << np.uint64(32)) | depth
+    vals = np.arange(n, dtype=np.uint32)
+    r = vrs.Renderer(max_gaussians=1, max_views=1, max_pairs=max(n, 1), max_width=16, max_height=16)
+    kt = torch.from_numpy(keys.view(np.int64)).cuda()
+    vt = torch.from_numpy(vals.view(np.int32)).cuda()
+    r.vrs_sort_pairs(kt, vt, key_bits=46)
+    torch.cuda.synchronize()
+    order = np.argsort(keys, kind="stable")
+    assert np.array_equal(kt.cpu().numpy().view(np.uint64), keys[order])
+    assert np.array_equal(vt.cpu().numpy().view(np.uint32), vals[order])
+
+
+@pytest.mark.parametrize("n", [1, 17, 4096, 4097, 300001])
+def test_scan_exact(vrs, n):
+    rs = np.random.default_rng(n)
+    x = rs.integers(0, 50, n).astype(np.uint32)
+    r = vrs.Renderer(max_gaussians=n, max_views=1, max_pairs=16, max_width=16, max_height=16)
+    xt = torch.from_numpy(x.view(np.int32)).cuda()
+    out = torch.empty_like(xt)
+    tot = torch.zeros(1, dtype=torch.int32, device="cuda")
+    r.vrs_exclusive_scan(xt, out, tot)
+    torch.cuda.synchronize()
+    ref = np.concatenate([[0], np.cumsum(x)[:-1]]).astype(np.uint32)
+    assert np.array_equal(out.cpu().numpy().view(np.uint32), ref)
+    assert int(tot.cpu().numpy().view(np.uint32)[0]) == int(x.sum())
+
+
+def test_host_output_path_matches_device_path(vrs):
+    scene = sg.random_scene(2, n=1000)
+    cam = sg.look_camera((0, 0, 0), f=64.0, width=128, height=96)
+    r = vrs.Renderer(max_gaussians=1000, max_views=1, max_pairs=1 << 16, max_width=128, max_height=96)
+    r.upload(scene)
+    rgba, depth = r.render([cam])
+    torch.cuda.synchronize()
+    hr, hd = r.render_host([cam])
+    assert np.array_equal(rgba.cpu().numpy(), hr) and np.array_equal(depth.cpu().numpy(), hd)
+
+
+def test_invalid_camera_rejected(vrs):
+    r = vrs.Renderer(max_gaussians=10, max_views=1, max_pairs=100, max_width=64, max_height=64)
+    r.upload(scene_from([[0, 0, 3]], 0.1))
+    cam = identity_camera(64, 64, 32.0)
+    cam.R_wc = cam.R_wc * 1.01
+    with pytest.raises(vrs.VrsError) as e:
+        r.render([cam])
+    assert e.value.status == vrs.vrs.VRS_E_INVALID_ARG
+    big = identity_camera(128, 64, 32.0)
+    with pytest.raises(vrs.VrsError):
+        r.render([big])
+
+
+def test_capacity_overflow_reported(vrs):
+    scene = sg.random_scene(0, n=1000)
+    cam = sg.look_camera((0, 0, 0), f=64.0, width=128, height=128)
+    r = vrs.Renderer(max_gaussians=1000, max_views=1, max_pairs=500, max_width=128, max_height=128)
+    r.upload(scene)
+    r.render([cam])
+    with pytest.raises(vrs.VrsError) as e:
+        r.stats()
+    assert e.value.status == vrs.vrs.VRS_E_CAPACITY
