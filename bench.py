@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""bench.py — stereo frames/s of the VRSplat render path on B200.
+
+Default workload (BASELINE.json metric, config C2): 500k-Gaussian "vr_room"
+scene (SH degree 3), stereo 2 x 2064 x 2208 at 110 deg FoV, single-pass
+foveated (fovea = half the image, 10% ramp), synthetic ellipse visibility
+masks, one sort and one blend launch per stereo frame.  One step = one full
+stereo frame through every stage (preprocess, scan, duplicate, onesweep
+sort, ranges, blend, compose).
+
+Timing: W untimed warm-up frames; then K frames, each bracketed by CUDA
+events on the render stream, with an L2 flush (a 256 MB write) between frames
+outside the events; barrier + synchronize around the timed region; the
+max over ranks is reported.  N > 1 (torchrun): rank 0 builds the scene and
+NCCL-broadcasts the raw arrays (the only data-path collective); every rank
+renders its own stereo frames (weak scaling over views).
+
+``--impl reference`` times the C++ oracle (the only reference this paper
+has: no code was published) on the box's host cores on a bounded sample of
+the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import scenegen as sg  # noqa: E402
+
+CONFIGS = {
+    # name: (n_gaussians, scale_mul, sh_degree, foveated, assign_tile, masks)
+    "c2": dict(n=500_000, scale_mul=1.0, sh=3, fovea=True, T=32, masks=True, seed=2,
+               desc="500k vr_room SH3, stereo 2x2064x2208, 110deg, single-pass foveated, ellipse masks"),
+    "c3": dict(n=3_000_000, scale_mul=(1 / 6) ** 0.5, sh=3, fovea=False, T=16, masks=False, seed=3,
+               desc="3M vr_room SH3 (scales x0.408), stereo 2x2064x2208, 110deg, no foveation"),
+    "c1": dict(n=1000, scale_mul=None, sh=0, fovea=False, T=16, masks=False, seed=0,
+               desc="1000 random Gaussians SH0, one 128x128 view, 90deg, 16x16 tiles"),
+}
+METRIC = "stereo frames/sec (2x2064x2208, foveated) at 500k Gaussians; ms/stage"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="vrs", choices=["vrs", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-flush", action="store_true")
+    ap.add_argument("--quiet", action="store_true")
+    return ap.parse_args()
+
+
+def make_workload(cfg_name):
+    c = CONFIGS[cfg_name]
+    if cfg_name == "c1":
+        scene = sg.random_scene(c["seed"], n=c["n"], sh_degree=0)
+        cams = [sg.look_camera((0, 0, 0), f=64.0, width=128, height=128)]
+        return scene, cams, None, {}
+    scene = sg.vr_room(c["seed"], c["n"], scale_mul=c["scale_mul"], sh_degree=c["sh"])
+    cams = sg.stereo_pair(masks=c["masks"])
+    fov = [sg.quest_fovea()] * 2 if c["fovea"] else None
+    masks = {0: sg.ellipse_mask(sg.QUEST_W, sg.QUEST_H), 1: sg.ellipse_mask(sg.QUEST_W, sg.QUEST_H)} if c["masks"] else {}
+    return scene, cams, fov, masks
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return json.load(open(p)), "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def cpu_baseline(scene, cams, fov, masks, T, budget_s=15.0):
+    """The oracle as it stands on the host cores, on a bounded sample:
+    full per-Gaussian stage + instantiation + sort + ranges for both eyes, then
+    a random sample of output pixels; frames/s extrapolated to the full frame."""
+    import oracle
+    ncores = os.cpu_count() or 1
+    o = oracle.Oracle(scene)
+    for k, m in masks.items():
+        o.set_mask(k, m)
+    t0 = time.perf_counter()
+    o.prepare(cams, fov, assign_tile=T, threads=ncores)
+    t_prep = time.perf_counter() - t0
+    total_px = sum(c.width * c.height for c in cams)
+    rs = np.random.default_rng(123)
+    n = 512
+    t_pix, done = 0.0, 0
+    while t_prep + t_pix < budget_s and done < total_px:
+        vxy = np.stack([rs.integers(0, len(cams), n), rs.integers(0, cams[0].width, n),
+                        rs.integers(0, cams[0].height, n)], 1)
+        t0 = time.perf_counter()
+        o.render_pixels(vxy)
+        t_pix += time.perf_counter() - t0
+        done += n
+        n = min(n * 2, 65536)
+    frame_s = t_prep + t_pix * (total_px / done)
+    return {"value": 1.0 / frame_s, "unit": "stereo frames/s" if len(cams) == 2 else "frames/s", "cores": ncores,
+            "kind": "oracle",
+            "sample": f"full preprocess+pairs+sort+ranges of the frame ({t_prep:.2f}s) + {done} random output "
+                      f"pixels ({t_pix:.2f}s) of {total_px}, extrapolated per pixel"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    scene, cams, fov, masks = make_workload(args.config)
+    budget = max(2.0, 150.0 / max(1, args.steps + args.warmup))
+    vals = []
+    for s in range(args.warmup + args.steps):
+        r = cpu_baseline(scene, cams, fov, masks, cfg["T"], budget_s=budget)
+        if s >= args.warmup:
+            vals.append(r)
+    v = statistics.median([r["value"] for r in vals])
+    line = {"metric": METRIC, "value": v, "unit": vals[0]["unit"], "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": args.config, "desc": cfg["desc"]},
+            "cpu_baseline": {"value": v, "unit": vals[0]["unit"], "cores": vals[0]["cores"], "kind": "oracle",
+                             "sample": vals[0]["sample"]},
+            "e2e": {"value": v, "unit": vals[0]["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    cfg = CONFIGS[args.config]
+
+    # ---- scene: rank 0 generates, NCCL broadcast of the raw arrays (only data-path collective)
+    if rank == 0:
+        scene, cams, fov, masks = make_workload(args.config)
+    else:
+        _, cams, fov, masks = None, None, None, None
+        scene = None
+    if world > 1:
+        n = cfg["n"]
+        k = (cfg["sh"] + 1) ** 2
+        bufs = {"means": (n, 3), "quats": (n, 4), "log_scales": (n, 3), "logits": (n,), "sh": (n, k, 3)}
+        tens = {}
+        for name, shape in bufs.items():
+            if rank == 0:
+                t = torch.from_numpy(np.ascontiguousarray(getattr(scene, name))).cuda()
+            else:
+                t = torch.empty(shape, dtype=torch.float32, device="cuda")
+            dist.broadcast(t, 0)
+            tens[name] = t.cpu().numpy()
+        if rank != 0:
+            scene = sg.RawScene(tens["means"], tens["quats"], tens["log_scales"], tens["logits"], tens["sh"], cfg["sh"])
+            _, cams, fov, masks = (None,) + make_cams_only(args.config)
+    from paper_2505_10144_b200 import Renderer
+
+    W = max(c.width for c in cams)
+    H = max(c.height for c in cams)
+    r = Renderer(max_gaussians=scene.n, max_views=len(cams), max_pairs=16 << 20 if cfg["n"] > 1e6 else 6 << 20,
+                 max_width=W, max_height=H, assign_tile=cfg["T"], device=local)
+    r.upload(scene)
+    for k, m in masks.items():
+        r.set_mask(k, m)
+    stream = torch.cuda.Stream(device=local)
+    rgba, depth = r.alloc_outputs(cams)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    # counters run (outside timing): workload counters for the roofline
+    r.vrs_set_instrumentation(counters=1, timing=0)
+    with torch.cuda.stream(stream):
+        r.render(cams, fov, rgba, depth, stream=stream)
+    counters = r.stats()
+    r.vrs_set_instrumentation(counters=0, timing=1)
+
+    for _ in range(args.warmup):
+        with torch.cuda.stream(stream):
+            r.render(cams, fov, rgba, depth, stream=stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms, stage = [], []
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            with torch.cuda.stream(stream):
+                if not args.no_flush:
+                    flush.fill_(s & 0xff)
+                ev0[s].record(stream)
+                r.render(cams, fov, rgba, depth, stream=stream)
+                ev1[s].record(stream)
+            st = r.stats()  # syncs the stream; outside the event pair
+            stage.append(st["stage_ms"])
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    step_ms = [ev0[s].elapsed_time(ev1[s]) for s in range(args.steps)]
+    ms = float(np.mean(step_ms))
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms_max = float(ms_t.item())
+    stage_ms = np.mean(np.array(stage), axis=0).tolist()
+    names = ["preprocess", "scan", "duplicate", "sort", "ranges", "blend", "compose"]
+
+    # ---- end to end through the C ABI with HOST buffers (pinned), copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        px = sum(c.width * c.height for c in cams)
+        hr = torch.empty((px, 4), dtype=torch.float32).pin_memory()
+        hd = torch.empty(px, dtype=torch.float32).pin_memory()
+        for _ in range(2):
+            r.render_host(cams, fov, hr, hd, stream=stream)
+        n_e2e = min(args.steps, 20)
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            r.render_host(cams, fov, hr, hd, stream=stream)
+        e2e_s = (time.perf_counter() - t0) / n_e2e
+        e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
+        cam_bytes = len(cams) * (72 + 24)
+        e2e = {"value": world / float(e_t.item()), "unit": "stereo frames/s" if len(cams) == 2 else "frames/s",
+               "h2d_bytes_per_step": cam_bytes, "d2h_bytes_per_step": int(px * 20),
+               "note": "vrs_render_views_host: render + D2H of RGBA f32 + depth f32 into pinned host memory; "
+                       "camera/fovea structs travel as kernel parameters"}
+
+    if rank == 0:
+        peaks, src = measured_peaks()
+        clocks = clk.summary()
+        sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+        # dominant kernel: blend, issue-bound: algorithmic
+        # lane-instructions = 11 per evaluation + 65 per contribution
+        blend_ms = stage_ms[5]
+        alg_ops = 11.0 * counters["evaluations"] + 65.0 * counters["contributions"]
+        peak_ops = 148 * 4 * 32 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        achieved = alg_ops / (blend_ms * 1e-3) if blend_ms > 0 else 0.0
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "blend_traffic.json")
+        if os.path.exists(tp):
+            try:
+                traffic = json.load(open(tp)).get(args.config)
+            except Exception:
+                traffic = None
+        n_views = len(cams)
+        key_bits = 32 + int(np.ceil(np.log2(max(2, sum(((c.width + cfg["T"] - 1) // cfg["T"]) *
+                                                        ((c.height + cfg["T"] - 1) // cfg["T"]) for c in cams)))))
+        launches_per_step = 7 + 2 + (key_bits + 7) // 8 + (1 if ((key_bits + 7) // 8) % 2 else 0)
+        line = {
+            "metric": METRIC if args.config == "c2" else METRIC + f" [{args.config}]",
+            "value": world * 1000.0 / ms_max,
+            "unit": "stereo frames/s" if n_views == 2 else "frames/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": args.config, "desc": cfg["desc"], "gaussians": scene.n, "views": n_views,
+                       "resolution": [cams[0].width, cams[0].height], "assign_tile": cfg["T"],
+                       "l2": "flushed between steps (256 MB write, outside the event pair)" if not args.no_flush
+                       else "not flushed", "parallelism": f"views x{world} (replicated scene, weak)"},
+            "stage_ms": dict(zip(names, stage_ms)),
+            "workload_counters": {k: counters[k] for k in ("pairs", "samples", "evaluations", "contributions",
+                                                           "overflow_samples", "terminated_samples", "work_items",
+                                                           "visible_splats")},
+            "tiles_by_class": dict(zip(["high", "low", "hybrid", "invisible"], counters["tiles_by_class"])),
+            "roofline": {"kernel": "k_blend", "bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
+                         "unit": "T lane-instr/s", "frac": achieved / peak_ops, "traffic": traffic,
+                         "peak_source": f"148 SM x 4 schedulers x 32 lanes x sm_max_mhz ({src} MEASURED_PEAKS)",
+                         "algorithmic_ops_per_launch": alg_ops},
+            "clocks": clocks,
+            "gpu_launches": launches_per_step * args.steps,
+            "e2e": e2e,
+            "context": {"paper_rtx4090_ms_per_stereo_frame_0.5M_scenes": [9.89, 12.19],
+                        "paper_headline": "72+ FPS on RTX 4090 at 2x2064x2272 (P:91, P:107)"},
+        }
+        if not args.no_cpu_baseline and world == 1:
+            line["cpu_baseline"] = cpu_baseline(scene, cams, fov, masks, cfg["T"])
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def make_cams_only(cfg_name):
+    c = CONFIGS[cfg_name]
+    if cfg_name == "c1":
+        return [sg.look_camera((0, 0, 0), f=64.0, width=128, height=128)], None, {}
+    cams = sg.stereo_pair(masks=c["masks"])
+    fov = [sg.quest_fovea()] * 2 if c["fovea"] else None
+    masks = {0: sg.ellipse_mask(sg.QUEST_W, sg.QUEST_H), 1: sg.ellipse_mask(sg.QUEST_W, sg.QUEST_H)} if c["masks"] else {}
+    return cams, fov, masks
+
+
+if __name__ == "__main__":
+    main()
