@@ -7,6 +7,8 @@
 // One thread per Gaussian; the Gaussian's attributes are read once and
 // projected for every view of the frame (stereo fusion of the per-Gaussian
 // stage, the "fusion of stereo rendering passes" of P:735).
+#include <algorithm>
+
 #include "vrs_internal.cuh"
 
 namespace vrs {
@@ -281,20 +283,6 @@ __device__ __forceinline__ void proj_to_tilesplat(const Proj& p, TileSplat& s) {
     s.bx = p.bv[0]; s.by = p.bv[1]; s.bz = p.bv[2];
 }
 
-__device__ uint32_t count_pairs(const TileSplat& s, const ViewParams& v, const int rect[4], int T) {
-    if (rect[0] > rect[2] || rect[1] > rect[3]) return 0;
-    if (sat_count(v.sat, v.tw + 1, rect[0], rect[1], rect[2], rect[3]) == 0) return 0;
-    uint32_t c = 0;
-    for (int ty = rect[1]; ty <= rect[3]; ty++)
-        for (int tx = rect[0]; tx <= rect[2]; tx++) {
-            if (!v.vis[ty * v.tw + tx]) continue;
-            const int x0 = tx * T, y0 = ty * T;
-            float a, b, d;
-            if (tile_test(s, v, x0, y0, min(x0 + T, v.W), min(y0 + T, v.H), a, b, d)) c++;
-        }
-    return c;
-}
-
 // View-dependent colour: real SH through degree 3 (3DGS basis), +0.5, >= 0.
 __device__ void sh_color(const SceneDev& sc, int64_t g, int64_t N, int ncoef, float dx, float dy, float dz,
                          float out[3]) {
@@ -348,7 +336,7 @@ __device__ __forceinline__ void load_gauss(const SceneDev& sc, int64_t g, int64_
     i1 = __ldg(&sc.icov[N + g]);
 }
 
-// Step 1: per-Gaussian preprocess for all views + exact pair counts.
+// Step 1: per-Gaussian preprocess for all views + candidate tile counts.
 __global__ void __launch_bounds__(128) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t N = fp.N;
@@ -359,13 +347,13 @@ __global__ void __launch_bounds__(128) k_preprocess(SceneDev sc, FrameParams fp,
         const ViewParams& v = fp.v[vi];
         Proj p;
         project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
+        // number of (Gaussian, tile) candidates = rect area, 0 if the rect holds no
+        // visible tile (SAT); the exact Eq.4 tests run load-balanced in k_tiletest
         uint32_t cnt = 0;
-        if (p.valid) {
-            TileSplat ts;
-            proj_to_tilesplat(p, ts);
-            cnt = count_pairs(ts, v, p.rect, fp.T);
-        }
-        fb.counts[(size_t)vi * N + g] = cnt;
+        if (p.valid && p.rect[0] <= p.rect[2] && p.rect[1] <= p.rect[3] &&
+            sat_count(v.sat, v.tw + 1, p.rect[0], p.rect[1], p.rect[2], p.rect[3]) > 0)
+            cnt = (uint32_t)((p.rect[2] - p.rect[0] + 1) * (p.rect[3] - p.rect[1] + 1));
+        fb.ntests[(size_t)vi * N + g] = cnt;
         if (cnt == 0) continue;
         float rgb[3];
         {
@@ -387,46 +375,103 @@ __global__ void __launch_bounds__(128) k_preprocess(SceneDev sc, FrameParams fp,
     }
 }
 
-// Step 3: re-walk the rect and emit (key, value) for every kept tile at the
-// Gaussian's instance range.  Emission order: (view, g, tile row-major).
-__global__ void __launch_bounds__(128) k_duplicate(FrameParams fp, FrameBufs fb) {
-    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const int64_t N = fp.N;
-    if (idx >= (int64_t)fp.n_views * N) return;
-    const uint32_t cnt = fb.counts[idx];
-    if (cnt == 0) return;
-    const int vi = (int)(idx / N);
-    const ViewParams& v = fp.v[vi];
-    uint32_t off = fb.offsets[idx];
-    if ((int64_t)off + cnt > fp.pair_cap) {
-        atomicOr(fb.overflow, 1u);
-        return;
+__device__ __forceinline__ int64_t upper_bound_u32(const uint32_t* __restrict__ a, int64_t lo, int64_t hi,
+                                                   uint32_t x) {
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (__ldg(a + mid) <= x) lo = mid + 1;
+        else hi = mid;
     }
-    const float4* rec = fb.rec + (size_t)idx * kRecF4;
-    const float4 r0 = rec[0], r1 = rec[1], r2 = rec[2], r3 = rec[3], r4 = rec[4], r5 = rec[5], r6 = rec[6];
-    TileSplat s;
-    s.ux = r0.x; s.uy = r0.y; s.uz = r0.z; s.qcut = r0.w;
-    s.e1x = r1.x; s.e1z = r1.y; s.e2x = r1.z; s.e2y = r1.w;
-    s.e2z = r2.x; s.C0 = r2.y; s.C1 = r2.z; s.C2 = r2.w;
-    s.A[0] = r3.x; s.A[1] = r3.y; s.A[2] = r3.z; s.A[3] = r3.w;
-    s.A[4] = r4.x; s.A[5] = r4.y; s.bx = r4.z; s.by = r4.w;
-    s.bz = r5.x; s.eps = r5.z;
-    const uint32_t r01 = __float_as_uint(r5.w), r23 = __float_as_uint(r6.w);
-    const int tx0 = r01 & 0xffff, ty0 = r01 >> 16, tx1 = r23 & 0xffff, ty1 = r23 >> 16;
+    return lo;
+}
+
+// Step 3a: one thread per (Gaussian, candidate tile): Eq.4 test (O7) and key
+// (O8).  Candidates are laid out (view, g, tile row-major) by the scan of the
+// per-splat rect areas, so every thread does one test (load-balanced: big
+// footprints no longer serialise a thread).  Writes keep flag, key, value.
+__global__ void __launch_bounds__(256) k_tiletest(FrameParams fp, FrameBufs fb, int64_t test_cap) {
+    const int64_t VN = (int64_t)fp.n_views * fp.N;
+    const int64_t total = min((int64_t)*fb.total_tests, test_cap);
+    const int lane = threadIdx.x & 31;
     const int T = fp.T;
-    const uint32_t g = (uint32_t)(idx - (int64_t)vi * N);
-    for (int ty = ty0; ty <= ty1; ty++)
-        for (int tx = tx0; tx <= tx1; tx++) {
-            if (!v.vis[ty * v.tw + tx]) continue;
+    for (int64_t tw0 = ((int64_t)blockIdx.x * blockDim.x) + (threadIdx.x & ~31); tw0 < total;
+         tw0 += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = tw0 + lane;
+        // warp-cooperative search: bracket the warp's splats, then search inside
+        const int64_t tw1 = min(tw0 + 31, total - 1);
+        int64_t b = 0;
+        if (lane < 2) b = upper_bound_u32(fb.toff, 0, VN, (uint32_t)(lane == 0 ? tw0 : tw1)) - 1;
+        const int64_t s_lo = __shfl_sync(0xffffffffu, b, 0), s_hi = __shfl_sync(0xffffffffu, b, 1);
+        if (t >= total) continue;
+        const int64_t sidx = upper_bound_u32(fb.toff, s_lo, s_hi + 1, (uint32_t)t) - 1;
+        const uint32_t l = (uint32_t)(t - fb.toff[sidx]);
+        const int vi = (int)(sidx / fp.N);
+        const ViewParams& v = fp.v[vi];
+        const float4* rec = fb.rec + (size_t)sidx * kRecF4;
+        const float4 r0 = __ldg(rec + 0), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2), r5 = __ldg(rec + 5),
+                     r6 = __ldg(rec + 6);
+        const uint32_t r01 = __float_as_uint(r5.w), r23 = __float_as_uint(r6.w);
+        const int tx0 = r01 & 0xffff, ty0 = r01 >> 16, tx1 = r23 & 0xffff;
+        const int rw = tx1 - tx0 + 1;
+        const int tx = tx0 + (int)(l % (uint32_t)rw), ty = ty0 + (int)(l / (uint32_t)rw);
+        uint32_t keep = 0;
+        uint64_t key = 0;
+        if (v.vis[ty * v.tw + tx]) {
+            TileSplat s;
+            s.ux = r0.x; s.uy = r0.y; s.uz = r0.z; s.qcut = r0.w;
+            s.e1x = r1.x; s.e1z = r1.y; s.e2x = r1.z; s.e2y = r1.w;
+            s.e2z = r2.x; s.C0 = r2.y; s.C1 = r2.z; s.C2 = r2.w;
+            s.eps = r5.z;
             const int x0 = tx * T, y0 = ty * T;
             float hx, hy, hz;
-            if (!tile_test(s, v, x0, y0, min(x0 + T, v.W), min(y0 + T, v.H), hx, hy, hz)) continue;
-            const float td = tile_depth(s, hx, hy, hz, fp.near_plane);
-            const uint64_t tile = (uint64_t)(v.tile_base + ty * v.tw + tx);
-            fb.keys[off] = (tile << 32) | (uint64_t)__float_as_uint(td);
-            fb.vals[off] = g;
-            off++;
+            if (tile_test(s, v, x0, y0, min(x0 + T, v.W), min(y0 + T, v.H), hx, hy, hz)) {
+                const float4 r3 = __ldg(rec + 3), r4 = __ldg(rec + 4);
+                s.A[0] = r3.x; s.A[1] = r3.y; s.A[2] = r3.z; s.A[3] = r3.w;
+                s.A[4] = r4.x; s.A[5] = r4.y; s.bx = r4.z; s.by = r4.w; s.bz = r5.x;
+                const float td = tile_depth(s, hx, hy, hz, fp.near_plane);
+                const uint64_t tile = (uint64_t)(v.tile_base + ty * v.tw + tx);
+                key = (tile << 32) | (uint64_t)__float_as_uint(td);
+                keep = 1;
+            }
         }
+        fb.tflag[t] = keep;
+        if (keep) {
+            fb.tkey[t] = key;
+            fb.tval[t] = (uint32_t)(sidx - (int64_t)vi * fp.N);
+        }
+    }
+}
+
+// Step 3b: compaction of the kept candidates at their scanned positions:
+// the pair list in (view, g, tile row-major) emission order.
+__global__ void k_compact(FrameBufs fb, int64_t test_cap, int64_t pair_cap, uint64_t* __restrict__ keys,
+                          uint32_t* __restrict__ vals) {
+    const int64_t total = min((int64_t)*fb.total_tests, test_cap);
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        if (!fb.tflag[t]) continue;
+        const uint32_t pos = fb.tpos[t];
+        if (pos < pair_cap) {
+            keys[pos] = fb.tkey[t];
+            vals[pos] = fb.tval[t];
+        }
+    }
+}
+
+// Exact per-(view, g) pair counts (parity hook / statistics only).
+__global__ void k_counts(FrameParams fp, FrameBufs fb, int64_t test_cap) {
+    const int64_t VN = (int64_t)fp.n_views * fp.N;
+    const int64_t total = min((int64_t)*fb.total_tests, test_cap);
+    const uint32_t pairs = *fb.total;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < VN; s += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t n = fb.ntests[s], a = fb.toff[s];
+        uint32_t c = 0;
+        if (n && (int64_t)a < total) {
+            const uint32_t pa = fb.tpos[a];
+            const uint32_t pb = ((int64_t)a + n < total) ? fb.tpos[a + n] : pairs;
+            c = pb - pa;
+        }
+        fb.counts[s] = c;
+    }
 }
 
 // Parity hook: the oracle's 48-float semantic splat layout.
@@ -471,11 +516,31 @@ void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, 
     k_preprocess<<<(unsigned)((fp.N + B - 1) / B), B, 0, st>>>(sc, fp, fb);
 }
 
-void launch_duplicate(const FrameParams& fp, FrameBufs fb, cudaStream_t st) {
+static int sm_count() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {
+    if ((int64_t)fp.n_views * fp.N == 0) return;
+    k_tiletest<<<sm_count() * 8, 256, 0, st>>>(fp, fb, test_cap);
+}
+
+void launch_compact(FrameBufs fb, int64_t test_cap, int64_t pair_cap, uint64_t* keys, uint32_t* vals,
+                    cudaStream_t st) {
+    k_compact<<<sm_count() * 8, 256, 0, st>>>(fb, test_cap, pair_cap, keys, vals);
+}
+
+void launch_counts(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {
     const int64_t n = (int64_t)fp.n_views * fp.N;
     if (n == 0) return;
-    const int B = 128;
-    k_duplicate<<<(unsigned)((n + B - 1) / B), B, 0, st>>>(fp, fb);
+    k_counts<<<(unsigned)std::min<int64_t>((n + 255) / 256, 65535), 256, 0, st>>>(fp, fb, test_cap);
 }
 
 void launch_debug_splats(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int view, float* out,

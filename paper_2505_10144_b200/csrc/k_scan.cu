@@ -3,6 +3,8 @@
 // "compute the range of each Gaussian's instances inside this buffer").
 // Single pass, decoupled look-back: each 4096-element tile publishes its
 // aggregate, then its inclusive prefix, in one 64-bit status word.
+#include <algorithm>
+
 #include "vrs_internal.cuh"
 
 namespace vrs {
@@ -24,110 +26,129 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 }  // namespace
 
 // scratch[0] low word: tile counter; scratch[1 + t]: status of tile t.
+// Persistent: blocks take tiles in order from the counter until n (read on the
+// device, so the scanned length need not be known on the host) is covered.
 __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
-                                                       uint32_t* total, int64_t n, unsigned long long* scratch) {
+                                                       uint32_t* total, const uint32_t* __restrict__ n_dev,
+                                                       int64_t cap, unsigned long long* scratch) {
     __shared__ uint32_t s_tile, s_excl;
     __shared__ uint32_t s_warp[kScanThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_tile = atomicAdd(reinterpret_cast<unsigned int*>(scratch), 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    const int64_t base = (int64_t)tile * kScanTile + (int64_t)tid * kScanItems;
-    uint32_t v[kScanItems];
-    if (base + kScanItems <= n && ((reinterpret_cast<uintptr_t>(in + base) & 15) == 0)) {
-        const uint4* p = reinterpret_cast<const uint4*>(in + base);
-#pragma unroll
-        for (int k = 0; k < kScanItems / 4; k++) {
-            uint4 q = __ldg(p + k);
-            v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
-        }
-    } else {
-#pragma unroll
-        for (int k = 0; k < kScanItems; k++) v[k] = (base + k < n) ? in[base + k] : 0u;
-    }
-    uint32_t tsum = 0;
-#pragma unroll
-    for (int k = 0; k < kScanItems; k++) tsum += v[k];
-    // warp inclusive scan of thread sums
-    uint32_t inc = tsum;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-        if (lane >= o) inc += y;
-    }
-    if (lane == 31) s_warp[warp] = inc;
-    __syncthreads();
-    uint32_t wpre = 0, agg = 0;
-#pragma unroll
-    for (int w = 0; w < kScanThreads / 32; w++) {
-        if (w < warp) wpre += s_warp[w];
-        agg += s_warp[w];
+    const int64_t n = n_dev ? min((int64_t)*n_dev, cap) : cap;
+    const int64_t ntiles = (n + kScanTile - 1) / kScanTile;
+    if (n == 0) {
+        if (blockIdx.x == 0 && tid == 0) *total = 0;
+        return;
     }
     unsigned long long* status = scratch + 1;
-    if (warp == 0) {
-        uint32_t excl = 0;
-        if (tile == 0) {
-            if (lane == 0) st_release(&status[0], kFlagPre | agg);
-        } else {
-            if (lane == 0) st_release(&status[tile], kFlagAgg | agg);
-            int64_t j = (int64_t)tile - 1;
-            while (true) {
-                const int64_t jj = j - lane;
-                unsigned long long s = 0;
-                if (jj >= 0) {
-                    do { s = ld_acquire(&status[jj]); } while ((s >> 32) == 0);
-                } else {
-                    s = kFlagPre;  // virtual prefix 0 before tile 0
-                }
-                const unsigned pre_mask = __ballot_sync(0xffffffffu, (s >> 32) == 2);
-                const int stop = pre_mask ? (__ffs(pre_mask) - 1) : 31;
-                uint32_t val = (lane <= stop) ? (uint32_t)s : 0u;
+    while (true) {
+        if (tid == 0) s_tile = atomicAdd(reinterpret_cast<unsigned int*>(scratch), 1u);
+        __syncthreads();
+        const uint32_t tile = s_tile;
+        if ((int64_t)tile >= ntiles) break;
+        const int64_t base = (int64_t)tile * kScanTile + (int64_t)tid * kScanItems;
+        uint32_t v[kScanItems];
+        if (base + kScanItems <= n && ((reinterpret_cast<uintptr_t>(in + base) & 15) == 0)) {
+            const uint4* p = reinterpret_cast<const uint4*>(in + base);
 #pragma unroll
-                for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-                excl += val;
-                if (pre_mask) break;
-                j -= 32;
+            for (int k = 0; k < kScanItems / 4; k++) {
+                uint4 q = __ldcs(p + k);
+                v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
             }
-            if (lane == 0) st_release(&status[tile], kFlagPre | (excl + agg));
-        }
-        if (lane == 0) s_excl = excl;
-    }
-    __syncthreads();
-    uint32_t run = s_excl + wpre + inc - tsum;
-    if (base + kScanItems <= n && ((reinterpret_cast<uintptr_t>(out + base) & 15) == 0)) {
-        uint4* p = reinterpret_cast<uint4*>(out + base);
+        } else {
 #pragma unroll
-        for (int k = 0; k < kScanItems / 4; k++) {
-            uint4 q;
-            q.x = run; run += v[4 * k];
-            q.y = run; run += v[4 * k + 1];
-            q.z = run; run += v[4 * k + 2];
-            q.w = run; run += v[4 * k + 3];
-            p[k] = q;
+            for (int k = 0; k < kScanItems; k++) v[k] = (base + k < n) ? in[base + k] : 0u;
         }
-    } else {
+        uint32_t tsum = 0;
 #pragma unroll
-        for (int k = 0; k < kScanItems; k++) {
-            if (base + k < n) out[base + k] = run;
-            run += v[k];
+        for (int k = 0; k < kScanItems; k++) tsum += v[k];
+        uint32_t inc = tsum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
         }
+        if (lane == 31) s_warp[warp] = inc;
+        __syncthreads();
+        uint32_t wpre = 0, agg = 0;
+#pragma unroll
+        for (int w = 0; w < kScanThreads / 32; w++) {
+            if (w < warp) wpre += s_warp[w];
+            agg += s_warp[w];
+        }
+        if (warp == 0) {
+            uint32_t excl = 0;
+            if (tile == 0) {
+                if (lane == 0) st_release(&status[0], kFlagPre | agg);
+            } else {
+                if (lane == 0) st_release(&status[tile], kFlagAgg | agg);
+                int64_t j = (int64_t)tile - 1;
+                while (true) {
+                    const int64_t jj = j - lane;
+                    unsigned long long st = 0;
+                    if (jj >= 0) {
+                        do { st = ld_acquire(&status[jj]); } while ((st >> 32) == 0);
+                    } else {
+                        st = kFlagPre;
+                    }
+                    const unsigned pre_mask = __ballot_sync(0xffffffffu, (st >> 32) == 2);
+                    const int stop = pre_mask ? (__ffs(pre_mask) - 1) : 31;
+                    uint32_t val = (lane <= stop) ? (uint32_t)st : 0u;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                    excl += val;
+                    if (pre_mask) break;
+                    j -= 32;
+                }
+                if (lane == 0) st_release(&status[tile], kFlagPre | (excl + agg));
+            }
+            if (lane == 0) s_excl = excl;
+        }
+        __syncthreads();
+        uint32_t run = s_excl + wpre + inc - tsum;
+        if (base + kScanItems <= n && ((reinterpret_cast<uintptr_t>(out + base) & 15) == 0)) {
+            uint4* p = reinterpret_cast<uint4*>(out + base);
+#pragma unroll
+            for (int k = 0; k < kScanItems / 4; k++) {
+                uint4 q;
+                q.x = run; run += v[4 * k];
+                q.y = run; run += v[4 * k + 1];
+                q.z = run; run += v[4 * k + 2];
+                q.w = run; run += v[4 * k + 3];
+                p[k] = q;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < kScanItems; k++) {
+                if (base + k < n) out[base + k] = run;
+                run += v[k];
+            }
+        }
+        if (tid == 0 && (int64_t)tile == ntiles - 1) *total = s_excl + agg;
+        __syncthreads();
     }
-    const int64_t tiles = (n + kScanTile - 1) / kScanTile;
-    if (tid == 0 && (int64_t)tile == tiles - 1) *total = s_excl + agg;
 }
 
 size_t scan_scratch_words(int64_t n) { return (size_t)((n + kScanTile - 1) / kScanTile) + 2; }
 
-void launch_scan(const uint32_t* in, uint32_t* out, uint32_t* total, int64_t n, uint32_t* scratch32,
-                 cudaStream_t st) {
+void launch_scan(const uint32_t* in, uint32_t* out, uint32_t* total, const uint32_t* n_dev, int64_t cap,
+                 uint32_t* scratch32, cudaStream_t st) {
     unsigned long long* scratch = reinterpret_cast<unsigned long long*>(scratch32);
-    if (n <= 0) {
+    if (cap <= 0) {
         cudaMemsetAsync(total, 0, 4, st);
         return;
     }
-    const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    const int64_t tiles = (cap + kScanTile - 1) / kScanTile;
     cudaMemsetAsync(scratch, 0, (size_t)(tiles + 1) * 8, st);
-    k_scan<<<(unsigned)tiles, kScanThreads, 0, st>>>(in, out, total, n, scratch);
+    const int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * 4);
+    k_scan<<<(unsigned)grid, kScanThreads, 0, st>>>(in, out, total, n_dev, cap, scratch);
 }
 
 }  // namespace vrs

@@ -44,7 +44,10 @@ struct vrs_context {
     int sh_chunks = 0;
     // frame buffers
     float4* d_rec = nullptr;
-    uint32_t *d_counts = nullptr, *d_offsets = nullptr, *d_misc = nullptr;  // misc: total, overflow
+    uint32_t *d_counts = nullptr, *d_ntests = nullptr, *d_toff = nullptr, *d_misc = nullptr;  // misc: pairs, overflow, tests
+    uint32_t *d_tflag = nullptr, *d_tpos = nullptr, *d_tval = nullptr;
+    uint64_t* d_tkey = nullptr;
+    int64_t test_cap = 0;
     uint64_t *d_keys = nullptr, *d_keys_alt = nullptr;
     uint32_t *d_vals = nullptr, *d_vals_alt = nullptr;
     uint32_t* d_ranges = nullptr;
@@ -101,7 +104,8 @@ static vrs_status cuda_check(vrs_context* c, cudaError_t e, const char* where) {
     } while (0)
 
 static void free_all(vrs_context* c) {
-    void* ptrs[] = {c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_counts, c->d_offsets, c->d_misc,
+    void* ptrs[] = {c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_counts, c->d_ntests, c->d_toff, c->d_misc,
+                    c->d_tflag, c->d_tpos, c->d_tval, c->d_tkey,
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
                     c->d_sat, c->d_cls, c->d_items, c->d_nitems, c->d_out_rgba, c->d_out_depth};
@@ -145,7 +149,13 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
     A(dalloc(&ctx->d_rec, (size_t)V * N * kRecF4));
     A(dalloc(&ctx->d_counts, (size_t)V * N));
-    A(dalloc(&ctx->d_offsets, (size_t)V * N));
+    A(dalloc(&ctx->d_ntests, (size_t)V * N));
+    A(dalloc(&ctx->d_toff, (size_t)V * N));
+    ctx->test_cap = 4 * P;
+    A(dalloc(&ctx->d_tflag, (size_t)ctx->test_cap));
+    A(dalloc(&ctx->d_tpos, (size_t)ctx->test_cap));
+    A(dalloc(&ctx->d_tval, (size_t)ctx->test_cap));
+    A(dalloc(&ctx->d_tkey, (size_t)ctx->test_cap));
     A(dalloc(&ctx->d_misc, 8));
     A(dalloc(&ctx->d_keys, (size_t)P));
     A(dalloc(&ctx->d_keys_alt, (size_t)P));
@@ -155,7 +165,7 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     A(dalloc(&ctx->d_low_rgba, (size_t)V * ctx->low_px_view));
     A(dalloc(&ctx->d_low_depth, (size_t)V * ctx->low_px_view));
     A(dalloc(&ctx->d_stats, 8));
-    A(dalloc(&ctx->d_scan_scratch, 2 * scan_scratch_words(V * N)));
+    A(dalloc(&ctx->d_scan_scratch, 2 * scan_scratch_words(std::max<int64_t>(V * N, ctx->test_cap))));
     A(dalloc(&ctx->sort.hist, 8 * 256));
     A(dalloc(&ctx->sort.status, sort_status_words(P)));
     A(dalloc(&ctx->sort.counters, 8));
@@ -437,6 +447,30 @@ static int key_bits_for(int64_t tiles) {
     return 32 + b;
 }
 
+static FrameBufs frame_bufs(vrs_context* ctx) {
+    FrameBufs fb{};
+    fb.rec = ctx->d_rec;
+    fb.ntests = ctx->d_ntests;
+    fb.toff = ctx->d_toff;
+    fb.total_tests = ctx->d_misc + 2;
+    fb.tflag = ctx->d_tflag;
+    fb.tpos = ctx->d_tpos;
+    fb.tkey = ctx->d_tkey;
+    fb.tval = ctx->d_tval;
+    fb.counts = ctx->d_counts;
+    fb.total = ctx->d_misc;
+    fb.overflow = ctx->d_misc + 1;
+    fb.keys = ctx->d_keys;
+    fb.vals = ctx->d_vals;
+    fb.keys_alt = ctx->d_keys_alt;
+    fb.vals_alt = ctx->d_vals_alt;
+    fb.ranges = ctx->d_ranges;
+    fb.low_rgba = ctx->d_low_rgba;
+    fb.low_depth = ctx->d_low_depth;
+    fb.stats = ctx->d_stats;
+    return fb;
+}
+
 static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* cams, const vrs_fovea* fov, float* rgba,
                               float* depth, cudaStream_t st) {
     if (!ctx) return VRS_E_INVALID_ARG;
@@ -456,29 +490,18 @@ static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* ca
         if (s != VRS_OK) return s;
     }
     SceneDev sc{ctx->d_mu, ctx->d_cov, ctx->d_icov, ctx->d_sh, ctx->sh_chunks};
-    FrameBufs fb{};
-    fb.rec = ctx->d_rec;
-    fb.counts = ctx->d_counts;
-    fb.offsets = ctx->d_offsets;
-    fb.total = ctx->d_misc;
-    fb.overflow = ctx->d_misc + 1;
-    fb.keys = ctx->d_keys;
-    fb.vals = ctx->d_vals;
-    fb.keys_alt = ctx->d_keys_alt;
-    fb.vals_alt = ctx->d_vals_alt;
-    fb.ranges = ctx->d_ranges;
-    fb.low_rgba = ctx->d_low_rgba;
-    fb.low_depth = ctx->d_low_depth;
-    fb.stats = ctx->d_stats;
+    FrameBufs fb = frame_bufs(ctx);
     const bool tm = ctx->timing && ctx->ev_created;
     if (tm) CK(cudaEventRecord(ctx->ev[0], st));
     CK(cudaMemsetAsync(ctx->d_misc + 1, 0, 4, st));
     if (ctx->counters) CK(cudaMemsetAsync(ctx->d_stats, 0, 8 * sizeof(unsigned long long), st));
     launch_preprocess(sc, fp, fb, st);
     if (tm) CK(cudaEventRecord(ctx->ev[1], st));
-    launch_scan(fb.counts, fb.offsets, fb.total, (int64_t)nv * fp.N, ctx->d_scan_scratch, st);
+    launch_scan(fb.ntests, fb.toff, fb.total_tests, nullptr, (int64_t)nv * fp.N, ctx->d_scan_scratch, st);
     if (tm) CK(cudaEventRecord(ctx->ev[2], st));
-    launch_duplicate(fp, fb, st);
+    launch_tiletest(fp, fb, ctx->test_cap, st);
+    launch_scan(fb.tflag, fb.tpos, fb.total, fb.total_tests, ctx->test_cap, ctx->d_scan_scratch, st);
+    launch_compact(fb, ctx->test_cap, fp.pair_cap, fb.keys, fb.vals, st);
     if (tm) CK(cudaEventRecord(ctx->ev[3], st));
     launch_sort(fb.keys, fb.vals, fb.keys_alt, fb.vals_alt, fb.total, fp.pair_cap, key_bits_for(ctx->last_tiles),
                 ctx->sort, st);
@@ -533,8 +556,8 @@ vrs_status vrs_get_frame_stats(vrs_context* ctx, vrs_frame_stats* out) {
     CK(cudaSetDevice(ctx->cfg.device));
     CK(cudaStreamSynchronize(ctx->last_stream));
     std::memset(out, 0, sizeof(*out));
-    uint32_t misc[2] = {0, 0};
-    CK(cudaMemcpy(misc, ctx->d_misc, 8, cudaMemcpyDeviceToHost));
+    uint32_t misc[3] = {0, 0, 0};
+    CK(cudaMemcpy(misc, ctx->d_misc, 12, cudaMemcpyDeviceToHost));
     out->pairs = misc[0];
     unsigned long long st[8] = {0};
     if (ctx->counters) CK(cudaMemcpy(st, ctx->d_stats, sizeof(st), cudaMemcpyDeviceToHost));
@@ -563,6 +586,8 @@ vrs_status vrs_get_frame_stats(vrs_context* ctx, vrs_frame_stats* out) {
     out->work_items = ctx->last_items;
     {
         std::vector<uint32_t> cnt((size_t)ctx->fp.n_views * ctx->N);
+        launch_counts(ctx->fp, frame_bufs(ctx), ctx->test_cap, ctx->last_stream);
+        CK(cudaStreamSynchronize(ctx->last_stream));
         if (!cnt.empty())
             CK(cudaMemcpy(cnt.data(), ctx->d_counts, 4 * cnt.size(), cudaMemcpyDeviceToHost));
         int64_t vsplat = 0;
@@ -573,7 +598,7 @@ vrs_status vrs_get_frame_stats(vrs_context* ctx, vrs_frame_stats* out) {
         for (int k = 0; k < 7; k++) CK(cudaEventElapsedTime(&out->stage_ms[k], ctx->ev[k], ctx->ev[k + 1]));
         CK(cudaEventElapsedTime(&out->stage_ms[7], ctx->ev[0], ctx->ev[7]));
     }
-    if (misc[1] || (int64_t)misc[0] > ctx->cfg.max_pairs)
+    if (misc[1] || (int64_t)misc[0] > ctx->cfg.max_pairs || (int64_t)misc[2] > ctx->test_cap)
         return fail(ctx, VRS_E_CAPACITY, "pair buffer overflow (max_pairs too small)");
     return VRS_OK;
 }
@@ -585,6 +610,8 @@ vrs_status vrs_debug_counts(vrs_context* ctx, uint32_t* counts, int64_t capacity
     const int64_t n = (int64_t)ctx->fp.n_views * ctx->N;
     if (n_out) *n_out = n;
     if (capacity < n) return fail(ctx, VRS_E_INVALID_ARG, "capacity");
+    launch_counts(ctx->fp, frame_bufs(ctx), ctx->test_cap, ctx->last_stream);
+    CK(cudaStreamSynchronize(ctx->last_stream));
     if (n) CK(cudaMemcpy(counts, ctx->d_counts, 4 * n, cudaMemcpyDeviceToHost));
     return VRS_OK;
 }
@@ -604,16 +631,8 @@ vrs_status vrs_debug_pairs(vrs_context* ctx, int32_t sorted, uint64_t* keys, uin
         CK(cudaMemcpy(keys, ctx->d_keys, 8 * n, cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(vals, ctx->d_vals, 4 * n, cudaMemcpyDeviceToHost));
     } else {
-        // re-run the emission into the alternate buffers (same kernel, same inputs)
-        FrameBufs fb{};
-        fb.rec = ctx->d_rec;
-        fb.counts = ctx->d_counts;
-        fb.offsets = ctx->d_offsets;
-        fb.total = ctx->d_misc;
-        fb.overflow = ctx->d_misc + 1;
-        fb.keys = ctx->d_keys_alt;
-        fb.vals = ctx->d_vals_alt;
-        launch_duplicate(ctx->fp, fb, st);
+        // re-run the compaction (emission order) into the alternate buffers
+        launch_compact(frame_bufs(ctx), ctx->test_cap, ctx->cfg.max_pairs, ctx->d_keys_alt, ctx->d_vals_alt, st);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(st));
         CK(cudaMemcpy(keys, ctx->d_keys_alt, 8 * n, cudaMemcpyDeviceToHost));
@@ -642,8 +661,8 @@ vrs_status vrs_debug_splats(vrs_context* ctx, int32_t view, float* out, int64_t 
     float* d = nullptr;
     CK(dalloc(&d, 48 * (size_t)ctx->N));
     SceneDev sc{ctx->d_mu, ctx->d_cov, ctx->d_icov, ctx->d_sh, ctx->sh_chunks};
-    FrameBufs fb{};
-    fb.counts = ctx->d_counts;
+    FrameBufs fb = frame_bufs(ctx);
+    launch_counts(ctx->fp, fb, ctx->test_cap, st);
     launch_debug_splats(sc, ctx->fp, fb, view, d, st);
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);
@@ -688,7 +707,7 @@ vrs_status vrs_exclusive_scan(vrs_context* ctx, const uint32_t* in, uint32_t* ou
     if (n < 0 || n > (int64_t)ctx->cfg.max_views * std::max<int64_t>(ctx->cfg.max_gaussians, 1))
         return fail(ctx, VRS_E_INVALID_ARG, "n");
     CK(cudaSetDevice(ctx->cfg.device));
-    launch_scan(in, out, total, n, ctx->d_scan_scratch, (cudaStream_t)stream);
+    launch_scan(in, out, total, nullptr, n, ctx->d_scan_scratch, (cudaStream_t)stream);
     CK(cudaGetLastError());
     return VRS_OK;
 }

@@ -68,8 +68,14 @@ struct SceneDev {
 
 struct FrameBufs {
     float4* rec;             // [V][N][8]
-    uint32_t* counts;        // [V*N]
-    uint32_t* offsets;       // [V*N]
+    uint32_t* ntests;        // [V*N] candidate (Gaussian, tile) tests = rect area
+    uint32_t* toff;          // [V*N] exclusive scan of ntests
+    uint32_t* total_tests;   // [1] (device)
+    uint32_t* tflag;         // [test_cap] keep flags
+    uint32_t* tpos;          // [test_cap] exclusive scan of tflag = pair position
+    uint64_t* tkey;          // [test_cap] key of kept candidates
+    uint32_t* tval;          // [test_cap] Gaussian index of kept candidates
+    uint32_t* counts;        // [V*N] exact pair counts (parity hook only)
     uint32_t* total;         // [1] pair total (device)
     uint32_t* overflow;      // [1] capacity overflow flag
     uint64_t* keys;          // [cap] emission keys
@@ -86,10 +92,14 @@ struct FrameBufs {
 void launch_setup_view(const uint8_t* mask, int mask_w, ViewParams vp, int T, int32_t* vis, uint32_t* sat,
                        int32_t* cls, uint32_t* items, int32_t* n_items_dev, cudaStream_t st);
 void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, cudaStream_t st);
-void launch_scan(const uint32_t* in, uint32_t* out, uint32_t* total, int64_t n, uint32_t* scratch,
-                 cudaStream_t st);
+// Exclusive scan of n = min(*n_dev, cap) u32 (n_dev may be null: n = cap); *total = sum.
+void launch_scan(const uint32_t* in, uint32_t* out, uint32_t* total, const uint32_t* n_dev, int64_t cap,
+                 uint32_t* scratch, cudaStream_t st);
 size_t scan_scratch_words(int64_t n);
-void launch_duplicate(const FrameParams& fp, FrameBufs fb, cudaStream_t st);
+void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st);
+void launch_compact(FrameBufs fb, int64_t test_cap, int64_t pair_cap, uint64_t* keys, uint32_t* vals,
+                    cudaStream_t st);
+void launch_counts(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st);
 struct SortScratch {
     uint32_t* hist;          // [8][256]
     uint32_t* status;        // [passes][max_tiles][256]
