@@ -558,7 +558,7 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
         float den = quad3(sp.A, x, y, 1.0f);
         float dtb = std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2]));
         float tau = dtb / den;  // depth of max density along this pixel's ray
-        if (tau != tau) tau = INFINITY;  // total order for the window (DESIGN R4)
+        tau = std::fmax(tau, -1e30f) + 0.0f;  // canonical: NaN/-inf -> -1e30, -0 -> +0 (DESIGN R4)
         st.contribs++;
         WEnt ent{tau, g, alpha};
         auto pos = std::upper_bound(win.begin(), win.end(), ent, [](const WEnt& a, const WEnt& c) {
@@ -1002,7 +1002,7 @@ int orc_render_bruteforce(void* h, int view, float* rgba, float* depth) {
                 double alpha = std::min(0.99, (double)sp.sigma * std::exp(-0.5 * q));
                 float den = quad3(sp.A, x, y, 1.0f);
                 float dtb = std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2]));
-                all.push_back(WEnt{dtb / den, (uint32_t)g, alpha});
+                all.push_back(WEnt{std::fmax(dtb / den, -1e30f) + 0.0f, (uint32_t)g, alpha});
             }
             std::stable_sort(all.begin(), all.end(), [](const WEnt& a, const WEnt& c) {
                 return a.tau < c.tau || (a.tau == c.tau && a.g < c.g);

@@ -48,22 +48,49 @@ struct BlendSmem {
     float4 r2[kBlend];   // e2.z, C00, C01, C11
     float4 r3[kBlend];   // A a, b, c, p
     float4 r4[kBlend];   // A e, f, b.x, b.y
-    float2 r5[kBlend];   // b.z, sigma
-    uint32_t g[kBlend];
+    float4 r5[kBlend];   // b.z, sigma, g (bits), -
     uint32_t mask[kBlend];
     float4 wblock[8];    // per-warp sample extent xmin, xmax, ymin, ymax (pixel coords)
-    float w_tau[kWindow][kBlend];
-    uint32_t w_g[kWindow][kBlend];
+    // per-thread resort window: ring of K slots, (tau, g) packed into one
+    // order-preserving 64-bit key, alpha alongside; [slot][thread] layout is
+    // bank-conflict free for any per-thread slot index
+    unsigned long long w_key[kWindow][kBlend];
     float w_a[kWindow][kBlend];
     unsigned long long cnt[4];
 };
 
-__device__ __forceinline__ bool win_less(float ta, uint32_t ga, float tb, uint32_t gb) {
-    return ta < tb || (ta == tb && ga < gb);
+constexpr uint32_t kSlotBytes = kBlend * 8;                   // one ring slot of keys
+constexpr uint32_t kRingMask = (kWindow - 1) * kSlotBytes;    // byte-offset ring mask
+static_assert((kWindow & (kWindow - 1)) == 0, "ring needs a power-of-two window");
+
+// Canonical tau (DESIGN R4: max(tau, -1e30) maps NaN/-inf to -1e30, +0.0 maps
+// -0 to +0), then (tau, g) -> u64 whose unsigned order is the (tau, g)
+// lexicographic order.
+__device__ __forceinline__ unsigned long long order_key(float tau, uint32_t g) {
+    const uint32_t b = __float_as_uint(fmaxf(tau, -1e30f) + 0.0f);
+    const uint32_t k = b ^ ((uint32_t)((int32_t)b >> 31) | 0x80000000u);
+    return ((unsigned long long)k << 32) | g;
+}
+// sentinel: tau = -2e30 (finite, below every canonical tau), g = 0, alpha = 0
+constexpr unsigned long long kSentinelKey = (unsigned long long)(~0xf1c9f2cau) << 32;
+__device__ __forceinline__ float fast_rcp(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float fast_ex2(float x) {
+    float r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ float key_tau(unsigned long long key) {
+    const uint32_t k = (uint32_t)(key >> 32);
+    return __uint_as_float(k ^ (((int32_t)k < 0) ? 0x80000000u : 0xffffffffu));
 }
 
 }  // namespace
 
+template <bool kCounters>
 __global__ void __launch_bounds__(kBlend, 2) k_blend(FrameParams fp, FrameBufs fb, float* __restrict__ rgba,
                                                       float* __restrict__ depth) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -83,13 +110,14 @@ __global__ void __launch_bounds__(kBlend, 2) k_blend(FrameParams fp, FrameBufs f
     const int sx = wx + lx, sy = wy + ly;
     int px, py;  // pixel (full-rate) or group origin pixel (low)
     float xs, ys;
+    const int ox = (kind == kItemLow) ? x0 : x0 + (T == 32 ? 16 * (sub & 1) : 0);
+    const int oy = (kind == kItemLow) ? y0 : y0 + (T == 32 ? 16 * (sub >> 1) : 0);
     if (kind == kItemLow) {
         px = x0 + 2 * sx;
         py = y0 + 2 * sy;
         xs = (float)(px + 1);
         ys = (float)(py + 1);
     } else {
-        const int ox = x0 + (T == 32 ? 16 * (sub & 1) : 0), oy = y0 + (T == 32 ? 16 * (sub >> 1) : 0);
         px = ox + sx;
         py = oy + sy;
         xs = (float)px + 0.5f;
@@ -98,38 +126,49 @@ __global__ void __launch_bounds__(kBlend, 2) k_blend(FrameParams fp, FrameBufs f
     if (tid < 8) {
         const int wwx = (tid & 1) * 8, wwy = (tid >> 1) * 4;
         float4 b;
-        if (kind == kItemLow) {
+        if (kind == kItemLow)
             b = make_float4((float)(x0 + 2 * wwx + 1), (float)(x0 + 2 * (wwx + 7) + 1), (float)(y0 + 2 * wwy + 1),
                             (float)(y0 + 2 * (wwy + 3) + 1));
-        } else {
-            const int ox = x0 + (T == 32 ? 16 * (sub & 1) : 0), oy = y0 + (T == 32 ? 16 * (sub >> 1) : 0);
+        else
             b = make_float4((float)(ox + wwx) + 0.5f, (float)(ox + wwx + 7) + 0.5f, (float)(oy + wwy) + 0.5f,
                             (float)(oy + wwy + 3) + 0.5f);
-        }
         S.wblock[tid] = b;
     }
-    if (tid < 4) S.cnt[tid] = 0ull;
+    if (kCounters && tid < 4) S.cnt[tid] = 0ull;
     const float x = (xs - v.cx) / v.fx;
     const float y = (ys - v.cy) / v.fy;
     const float dn = sqrtf(fmaf(x, x, fmaf(y, y, 1.0f)));
     const uint32_t rb = fb.ranges[2 * (size_t)(v.tile_base + tile)];
     const uint32_t re = fb.ranges[2 * (size_t)(v.tile_base + tile) + 1];
     const float4* __restrict__ recv = fb.rec + (size_t)vi * fp.N * kRecF4;
+    const float4* __restrict__ colv = fb.col + (size_t)vi * fp.N;
+    char* const wkb = reinterpret_cast<char*>(&S.w_key[0][tid]);
+    char* const wab = reinterpret_cast<char*>(&S.w_a[0][tid]);
+#define WK(off) (*reinterpret_cast<unsigned long long*>(wkb + (off)))
+#define WA(off) (*reinterpret_cast<float*>(wab + ((off) >> 1)))
+    // The window starts full of K sentinels (tau = -2e30 < every canonical
+    // depth, alpha = 0): popping a sentinel is an exact no-op, so every
+    // contribution runs the same straight-line "insert, pop min" code.
+#pragma unroll
+    for (int k = 0; k < kWindow; k++) {
+        WK(k * kSlotBytes) = kSentinelKey;
+        WA(k * kSlotBytes) = 0.0f;
+    }
 
     float Tr = 1.0f, Cr = 0.0f, Cg = 0.0f, Cb = 0.0f, Dd = 0.0f;
-    bool done = false, overflowed = false;
-    int head = 0, cnt = 0;
+    bool done = false;
+    uint32_t hk = 0;  // byte offset of the ring head
     uint32_t n_contrib = 0, stop_pos = re;
 
-    auto blend_one = [&](float tau, uint32_t g, float a) {
-        const float4 col = __ldg(recv + (size_t)g * kRecF4 + 6);
+    auto blend_one = [&](unsigned long long key, float a) {
+        const float4 col = __ldg(colv + (uint32_t)key);
         const float wgt = a * Tr;
         Cr = fmaf(col.x, wgt, Cr);
         Cg = fmaf(col.y, wgt, Cg);
         Cb = fmaf(col.z, wgt, Cb);
-        Dd = fmaf(tau * dn, wgt, Dd);
+        Dd = fmaf(key_tau(key) * dn, wgt, Dd);
         Tr = Tr * (1.0f - a);
-        if (Tr < kTmin) done = true;
+        done = Tr < kTmin;
     };
 
     for (uint32_t base = rb; base < re; base += kBlend) {
@@ -142,8 +181,7 @@ __global__ void __launch_bounds__(kBlend, 2) k_blend(FrameParams fp, FrameBufs f
             const float4 a0 = __ldg(rp + 0), a1 = __ldg(rp + 1), a2 = __ldg(rp + 2), a3 = __ldg(rp + 3),
                          a4 = __ldg(rp + 4), a5 = __ldg(rp + 5), a7 = __ldg(rp + 7);
             S.r0[tid] = a0; S.r1[tid] = a1; S.r2[tid] = a2; S.r3[tid] = a3; S.r4[tid] = a4;
-            S.r5[tid] = make_float2(a5.x, a5.y);
-            S.g[tid] = g;
+            S.r5[tid] = make_float4(a5.x, a5.y, __uint_as_float(g), 0.0f);
             uint32_t m = 0;
 #pragma unroll
             for (int w = 0; w < 8; w++) {
@@ -155,72 +193,63 @@ __global__ void __launch_bounds__(kBlend, 2) k_blend(FrameParams fp, FrameBufs f
         }
         if (__syncthreads_count(!done) == 0) break;
         const int nb = min((int)(re - base), kBlend);
-        if (__all_sync(0xffffffffu, done)) continue;
-        for (int j = 0; j < nb; j++) {
-            if (!((S.mask[j] >> warp) & 1u)) continue;
-            if (done) continue;
-            const float4 a0 = S.r0[j], a1 = S.r1[j], a2 = S.r2[j];
-            const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
-            const float ex = fmaf(a1.x, x, a1.y);
-            const float ey = fmaf(a1.z, x, fmaf(a1.w, y, a2.x));
-            const float cx = fmaf(a2.y, ex, a2.z * ey), cy = fmaf(a2.z, ex, a2.w * ey);
-            const float num = fmaf(ex, cx, ey * cy);
-            const float ss = s * s;
-            if (!(s > 0.0f) || !(num <= a0.w * ss)) continue;
-            // contribution: alpha (tolerance-only), tau (decision, IEEE)
-            const float4 a3 = S.r3[j], a4 = S.r4[j];
-            const float2 a5 = S.r5[j];
-            const float q = __fdividef(num, ss);
-            const float alpha = fminf(kAlphaMax, a5.y * __expf(-0.5f * q));
-            const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
-            const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, a5.x));
-            float tau = __fdiv_rn(dtb, den);
-            if (tau != tau) tau = __int_as_float(0x7f800000);
-            const uint32_t g = S.g[j];
-            n_contrib++;
-            if (cnt == kWindow) {
-                overflowed = true;
-                const float th = S.w_tau[head][tid];
-                const uint32_t gh = S.w_g[head][tid];
-                if (win_less(tau, g, th, gh)) {
-                    blend_one(tau, g, alpha);
-                    if (done) stop_pos = base + j;
-                    continue;
+        for (int c = 0; c < nb; c += 32) {
+            if (__all_sync(0xffffffffu, done)) break;
+            const bool rel = (c + lane < nb) && ((S.mask[c + lane] >> warp) & 1u);
+            unsigned bits = __ballot_sync(0xffffffffu, rel);
+            while (bits) {
+                const int j = c + __ffs(bits) - 1;
+                bits &= bits - 1;
+                if (done) continue;
+                const float4 a0 = S.r0[j], a1 = S.r1[j], a2 = S.r2[j];
+                const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
+                const float ex = fmaf(a1.x, x, a1.y);
+                const float ey = fmaf(a1.z, x, fmaf(a1.w, y, a2.x));
+                const float cx = fmaf(a2.y, ex, a2.z * ey), cy = fmaf(a2.z, ex, a2.w * ey);
+                const float num = fmaf(ex, cx, ey * cy);
+                const float ss = s * s;
+                if (!(s > 0.0f) || !(num <= a0.w * ss)) continue;
+                // contribution: alpha (tolerance-only), tau (decision, IEEE division)
+                const float4 a3 = S.r3[j], a4 = S.r4[j], a5 = S.r5[j];
+                const float q = num * fast_rcp(ss);
+                const float alpha = fminf(kAlphaMax, a5.y * fast_ex2(-0.72134752044448170368f * q));
+                const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
+                const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, a5.x));
+                const unsigned long long key = order_key(__fdiv_rn(dtb, den), __float_as_uint(a5.z));
+                if (kCounters) n_contrib++;
+                // insert, then pop the minimum of the K+1 entries
+                const unsigned long long kh = WK(hk);
+                const bool direct = key < kh;  // the new entry is the minimum
+                const float ah = WA(hk);
+                blend_one(direct ? key : kh, direct ? alpha : ah);
+                if (kCounters && done) stop_pos = base + j;
+                if (direct || done) continue;
+                hk = (hk + kSlotBytes) & kRingMask;
+                // insertion from the tail (entries arrive nearly sorted)
+                uint32_t jo = (hk + (kWindow - 2) * kSlotBytes) & kRingMask;
+#pragma unroll 1
+                for (int left = kWindow - 1; left > 0; left--) {
+                    const unsigned long long kj = WK(jo);
+                    if (kj <= key) break;
+                    const uint32_t dst = (jo + kSlotBytes) & kRingMask;
+                    WK(dst) = kj;
+                    WA(dst) = WA(jo);
+                    jo = (jo + kRingMask) & kRingMask;
                 }
-                blend_one(th, gh, S.w_a[head][tid]);
-                head = (head + 1 == kWindow) ? 0 : head + 1;
-                cnt--;
-                if (done) { stop_pos = base + j; continue; }
+                const uint32_t dst = (jo + kSlotBytes) & kRingMask;
+                WK(dst) = key;
+                WA(dst) = alpha;
             }
-            // insertion from the tail
-            int pos = cnt;
-            while (pos > 0) {
-                int jj = head + pos - 1;
-                jj -= (jj >= kWindow) ? kWindow : 0;
-                const float tj = S.w_tau[jj][tid];
-                const uint32_t gj = S.w_g[jj][tid];
-                if (!win_less(tau, g, tj, gj)) break;
-                int dst = jj + 1;
-                dst -= (dst >= kWindow) ? kWindow : 0;
-                S.w_tau[dst][tid] = tj;
-                S.w_g[dst][tid] = gj;
-                S.w_a[dst][tid] = S.w_a[jj][tid];
-                pos--;
-            }
-            int dst = head + pos;
-            dst -= (dst >= kWindow) ? kWindow : 0;
-            S.w_tau[dst][tid] = tau;
-            S.w_g[dst][tid] = g;
-            S.w_a[dst][tid] = alpha;
-            cnt++;
         }
     }
-    // drain the window in order
-    while (cnt > 0 && !done) {
-        blend_one(S.w_tau[head][tid], S.w_g[head][tid], S.w_a[head][tid]);
-        head = (head + 1 == kWindow) ? 0 : head + 1;
-        cnt--;
+    // drain the window in order (sentinels pop as no-ops)
+#pragma unroll 1
+    for (int k = 0; k < kWindow && !done; k++) {
+        blend_one(WK(hk), WA(hk));
+        hk = (hk + kSlotBytes) & kRingMask;
     }
+#undef WK
+#undef WA
     // outputs
     const float oR = Cr + Tr * fp.bg[0], oG = Cg + Tr * fp.bg[1], oB = Cb + Tr * fp.bg[2], oA = 1.0f - Tr;
     if (kind == kItemLow) {
@@ -256,10 +285,11 @@ __global__ void __launch_bounds__(kBlend, 2) k_blend(FrameParams fp, FrameBufs f
             depth[pi] = Dd;
         }
     }
-    if (fp.counters) {
+    if (kCounters) {
         // evaluations: list entries visited before termination
         const unsigned long long ev = done ? (unsigned long long)(stop_pos - rb + 1) : (unsigned long long)(re - rb);
         const bool in_img = (px < v.W && py < v.H);
+        const bool overflowed = n_contrib > (uint32_t)kWindow;
         unsigned long long c0 = in_img ? ev : 0ull, c1 = in_img ? n_contrib : 0u,
                            c2 = (in_img && overflowed) ? 1u : 0u, c3 = (in_img && done) ? 1u : 0u;
 #pragma unroll
@@ -292,10 +322,14 @@ void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* r
     const size_t smem = sizeof(BlendSmem);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_blend, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
-    k_blend<<<total_items, kBlend, smem, st>>>(fp, fb, rgba, depth);
+    if (fp.counters)
+        k_blend<true><<<total_items, kBlend, smem, st>>>(fp, fb, rgba, depth);
+    else
+        k_blend<false><<<total_items, kBlend, smem, st>>>(fp, fb, rgba, depth);
 }
 
 // Step 7: periphery reconstruction: nearest-neighbour upsample of the

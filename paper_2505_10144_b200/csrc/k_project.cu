@@ -372,6 +372,7 @@ __global__ void __launch_bounds__(128) k_preprocess(SceneDev sc, FrameParams fp,
         rec[5] = make_float4(p.bv[2], p.sigma, p.eps, __uint_as_float(r01));
         rec[6] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(r23));
         rec[7] = make_float4(p.bbox[0], p.bbox[1], p.bbox[2], p.bbox[3]);
+        fb.col[(size_t)vi * N + g] = make_float4(rgb[0], rgb[1], rgb[2], 0.0f);
     }
 }
 

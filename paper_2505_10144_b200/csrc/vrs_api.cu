@@ -44,6 +44,7 @@ struct vrs_context {
     int sh_chunks = 0;
     // frame buffers
     float4* d_rec = nullptr;
+    float4* d_col = nullptr;
     uint32_t *d_counts = nullptr, *d_ntests = nullptr, *d_toff = nullptr, *d_misc = nullptr;  // misc: pairs, overflow, tests
     uint32_t *d_tflag = nullptr, *d_tpos = nullptr, *d_tval = nullptr;
     uint64_t* d_tkey = nullptr;
@@ -104,7 +105,7 @@ static vrs_status cuda_check(vrs_context* c, cudaError_t e, const char* where) {
     } while (0)
 
 static void free_all(vrs_context* c) {
-    void* ptrs[] = {c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_counts, c->d_ntests, c->d_toff, c->d_misc,
+    void* ptrs[] = {c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_col, c->d_counts, c->d_ntests, c->d_toff, c->d_misc,
                     c->d_tflag, c->d_tpos, c->d_tval, c->d_tkey,
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
@@ -148,6 +149,7 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     cudaError_t e = cudaSuccess;
     auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
     A(dalloc(&ctx->d_rec, (size_t)V * N * kRecF4));
+    A(dalloc(&ctx->d_col, (size_t)V * N));
     A(dalloc(&ctx->d_counts, (size_t)V * N));
     A(dalloc(&ctx->d_ntests, (size_t)V * N));
     A(dalloc(&ctx->d_toff, (size_t)V * N));
@@ -450,6 +452,7 @@ static int key_bits_for(int64_t tiles) {
 static FrameBufs frame_bufs(vrs_context* ctx) {
     FrameBufs fb{};
     fb.rec = ctx->d_rec;
+    fb.col = ctx->d_col;
     fb.ntests = ctx->d_ntests;
     fb.toff = ctx->d_toff;
     fb.total_tests = ctx->d_misc + 2;

@@ -83,6 +83,7 @@ struct FrameBufs {
     uint64_t* keys_alt;      // [cap] sort ping-pong
     uint32_t* vals_alt;
     uint32_t* ranges;        // [tiles][2]
+    float4* col;             // [V][N] view-dependent colour (rgb, 0) of projected splats
     float4* low_rgba;        // low-res samples RGBA
     float* low_depth;        // low-res samples depth
     unsigned long long* stats;  // [8] device counters
