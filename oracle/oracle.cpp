@@ -373,9 +373,9 @@ static bool tile_test(const Splat& sp, const orc_view& v, int x0, int y0, int x1
     float yx[5], yy[5];
     for (int k = 0; k < n; k++) {
         float d[3] = {px[k], py[k], 1.0f};
-        float sk = dot3(sp.u, d);
-        yx[k] = dot3(sp.e1, d) / sk;
-        yy[k] = dot3(sp.e2, d) / sk;
+        float is = 1.0f / dot3(sp.u, d);  // chart point = (e1.d, e2.d) / (u.d)  (R6: one IEEE reciprocal)
+        yx[k] = dot3(sp.e1, d) * is;
+        yy[k] = dot3(sp.e2, d) * is;
     }
     // mean (chart origin) inside the convex polygon: all edge cross products share a sign
     int npos = 0, nneg = 0;

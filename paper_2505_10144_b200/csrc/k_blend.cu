@@ -335,51 +335,105 @@ void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* r
 // Step 7: periphery reconstruction: nearest-neighbour upsample of the
 // LowRes group samples and a 3x3 (1,2,1)x(1,2,1) blur restricted to LowRes
 // pixels in the image, renormalised; invisible tiles get the
-// background with A = 0, D = 0.  HighRes/Hybrid pixels were written by the blend.
+// background with A = 0, D = 0.  HighRes/Hybrid pixels were written by the
+// blend.  One thread per 2x2 pixel group: the 3x3 neighbourhood of group
+// samples covers the blur footprint of all four pixels.
 __global__ void k_compose(FrameParams fp, FrameBufs fb, float* __restrict__ rgba, float* __restrict__ depth,
-                          int64_t total_px) {
+                          int64_t total_groups) {
     const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gi >= total_px) return;
+    if (gi >= total_groups) return;
     int vi = 0;
-    while (vi + 1 < fp.n_views && gi >= fp.v[vi + 1].pix_off) vi++;
+    while (vi + 1 < fp.n_views && gi >= fp.v[vi + 1].low_off) vi++;
     const ViewParams& v = fp.v[vi];
-    const int64_t k = gi - v.pix_off;
-    const int i = (int)(k % v.W), j = (int)(k / v.W);
-    const int T = fp.T;
-    const int c = v.cls[(j / T) * v.tw + (i / T)];
+    const int64_t k = gi - v.low_off;
+    const int gx = (int)(k % v.low_w), gy = (int)(k / v.low_w);
+    if (2 * gy >= v.H) return;  // gap between views' low-res planes
+    const int T = fp.T, i0 = 2 * gx, j0 = 2 * gy;
+    const int c = v.cls[(j0 / T) * v.tw + (i0 / T)];
     if (c == kHigh || c == kHybrid) return;
+    float4 outc[2][2];
+    float outd[2][2];
     if (c == kInvisible) {
-        reinterpret_cast<float4*>(rgba)[gi] = make_float4(fp.bg[0], fp.bg[1], fp.bg[2], 0.0f);
-        depth[gi] = 0.0f;
-        return;
+#pragma unroll
+        for (int b = 0; b < 2; b++)
+#pragma unroll
+            for (int a = 0; a < 2; a++) {
+                outc[b][a] = make_float4(fp.bg[0], fp.bg[1], fp.bg[2], 0.0f);
+                outd[b][a] = 0.0f;
+            }
+    } else {
+        // gather the 3x3 neighbour groups (sample + whether its pixels are LowRes & in image)
+        float4 sc[3][3];
+        float sd[3][3];
+        bool ok[3][3];
+#pragma unroll
+        for (int dj = 0; dj < 3; dj++)
+#pragma unroll
+            for (int di = 0; di < 3; di++) {
+                // pixel of that group adjacent to this group: column 2gx-1, (2gx..2gx+1), 2gx+2
+                const int pi = (di == 0) ? i0 - 1 : (di == 1 ? i0 : i0 + 2);
+                const int pj = (dj == 0) ? j0 - 1 : (dj == 1 ? j0 : j0 + 2);
+                bool good = pi >= 0 && pj >= 0 && pi < v.W && pj < v.H;
+                if (good) good = v.cls[(pj / T) * v.tw + (pi / T)] == kLow;
+                ok[dj][di] = good;
+                if (good) {
+                    const size_t li = (size_t)v.low_off + (size_t)(pj >> 1) * v.low_w + (pi >> 1);
+                    sc[dj][di] = fb.low_rgba[li];
+                    sd[dj][di] = fb.low_depth[li];
+                } else {
+                    sc[dj][di] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    sd[dj][di] = 0.0f;
+                }
+            }
+#pragma unroll
+        for (int b = 0; b < 2; b++)
+#pragma unroll
+            for (int a = 0; a < 2; a++) {
+                float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f}, ws = 0.0f;
+#pragma unroll
+                for (int ddj = -1; ddj <= 1; ddj++)
+#pragma unroll
+                    for (int ddi = -1; ddi <= 1; ddi++) {
+                        // neighbour pixel (2gx+a+ddi, 2gy+b+ddj) -> neighbour group slot
+                        const int si = (a + ddi < 0) ? 0 : ((a + ddi > 1) ? 2 : 1);
+                        const int sj = (b + ddj < 0) ? 0 : ((b + ddj > 1) ? 2 : 1);
+                        // pixel-level in-image test for the pixels inside this group's own column/row
+                        const int pi = i0 + a + ddi, pj = j0 + b + ddj;
+                        if (!ok[sj][si] || pi >= v.W || pj >= v.H) continue;
+                        const float w = (float)((2 - abs(ddi)) * (2 - abs(ddj)));
+                        acc[0] = fmaf(w, sc[sj][si].x, acc[0]);
+                        acc[1] = fmaf(w, sc[sj][si].y, acc[1]);
+                        acc[2] = fmaf(w, sc[sj][si].z, acc[2]);
+                        acc[3] = fmaf(w, sc[sj][si].w, acc[3]);
+                        acc[4] = fmaf(w, sd[sj][si], acc[4]);
+                        ws += w;
+                    }
+                const float inv = 1.0f / ws;
+                outc[b][a] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+                outd[b][a] = acc[4] * inv;
+            }
     }
-    float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f}, ws = 0.0f;
 #pragma unroll
-    for (int dj = -1; dj <= 1; dj++)
-#pragma unroll
-        for (int di = -1; di <= 1; di++) {
-            const int ii = i + di, jj = j + dj;
-            if (ii < 0 || jj < 0 || ii >= v.W || jj >= v.H) continue;
-            if (v.cls[(jj / T) * v.tw + (ii / T)] != kLow) continue;
-            const float w = (float)((2 - abs(di)) * (2 - abs(dj)));
-            const size_t li = (size_t)v.low_off + (size_t)(jj >> 1) * v.low_w + (ii >> 1);
-            const float4 p = fb.low_rgba[li];
-            acc[0] = fmaf(w, p.x, acc[0]);
-            acc[1] = fmaf(w, p.y, acc[1]);
-            acc[2] = fmaf(w, p.z, acc[2]);
-            acc[3] = fmaf(w, p.w, acc[3]);
-            acc[4] = fmaf(w, fb.low_depth[li], acc[4]);
-            ws += w;
+    for (int b = 0; b < 2; b++) {
+        const int j = j0 + b;
+        if (j >= v.H) continue;
+        const size_t row = (size_t)v.pix_off + (size_t)j * v.W;
+        if (i0 + 1 < v.W) {
+            reinterpret_cast<float4*>(rgba)[row + i0] = outc[b][0];
+            reinterpret_cast<float4*>(rgba)[row + i0 + 1] = outc[b][1];
+            depth[row + i0] = outd[b][0];
+            depth[row + i0 + 1] = outd[b][1];
+        } else {
+            reinterpret_cast<float4*>(rgba)[row + i0] = outc[b][0];
+            depth[row + i0] = outd[b][0];
         }
-    const float inv = 1.0f / ws;
-    reinterpret_cast<float4*>(rgba)[gi] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-    depth[gi] = acc[4] * inv;
+    }
 }
 
 void launch_compose(const FrameParams& fp, FrameBufs fb, float* rgba, float* depth, cudaStream_t st) {
-    int64_t total = 0;
-    for (int i = 0; i < fp.n_views; i++) total += (int64_t)fp.v[i].W * fp.v[i].H;
-    if (total == 0) return;
+    if (fp.n_views == 0) return;
+    const ViewParams& last = fp.v[fp.n_views - 1];
+    const int64_t total = last.low_off + (int64_t)last.low_w * ((last.H + 1) / 2);
     k_compose<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(fp, fb, rgba, depth, total);
 }
 

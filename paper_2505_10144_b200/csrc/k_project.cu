@@ -189,70 +189,103 @@ struct TileSplat {
     float A[6], bx, by, bz;
 };
 
+// Eq.4 on one polygon edge p -> p + d with t clamped to [0,1];
+// keeps the running minimum (strictly smaller q wins: earlier edge on ties).
+__device__ __forceinline__ void eq4_edge(const TileSplat& s, float ppx, float ppy, float qx, float qy, float& qmin,
+                                         float& hx, float& hy) {
+    const float ddx = qx - ppx, ddy = qy - ppy;
+    const float cdx = fmaf(s.C0, ddx, s.C1 * ddy), cdy = fmaf(s.C1, ddx, s.C2 * ddy);
+    const float den = fmaf(ddx, cdx, ddy * cdy);
+    const float nmr = -fmaf(ppx, cdx, ppy * cdy);
+    float t;
+    if (nmr <= 0.0f || !(den > 0.0f)) t = 0.0f;
+    else if (nmr >= den) t = 1.0f;
+    else t = nmr / den;
+    const float X = fmaf(t, ddx, ppx), Y = fmaf(t, ddy, ppy);
+    const float cX = fmaf(s.C0, X, s.C1 * Y), cY = fmaf(s.C1, X, s.C2 * Y);
+    const float q = fmaf(X, cX, Y * cY);
+    if (q < qmin) { qmin = q; hx = X; hy = Y; }
+}
+
 // O7: Eq.4 on the optimal-plane polygon of the tile, corner
 // rays clipped at s >= eps (DESIGN R8); returns keep and d_hat.
+// Fast path: all four corners in front (the common case) -> unrolled quad.
 __device__ bool tile_test(const TileSplat& s, const ViewParams& v, int x0, int y0, int x1, int y1, float& dhx,
                           float& dhy, float& dhz) {
-    float dx[4], dy[4], sv[4];
-    const int cxs[4] = {x0, x1, x1, x0}, cys[4] = {y0, y0, y1, y1};
+    const float ax = ((float)x0 - v.cx) / v.fx, bx = ((float)x1 - v.cx) / v.fx;
+    const float ay = ((float)y0 - v.cy) / v.fy, by = ((float)y1 - v.cy) / v.fy;
+    float dx[4] = {ax, bx, bx, ax}, dy[4] = {ay, ay, by, by}, sv[4];
     int nin = 0;
 #pragma unroll
     for (int k = 0; k < 4; k++) {
-        dx[k] = ((float)cxs[k] - v.cx) / v.fx;
-        dy[k] = ((float)cys[k] - v.cy) / v.fy;
         sv[k] = fmaf(s.ux, dx[k], fmaf(s.uy, dy[k], s.uz));
         nin += (sv[k] >= s.eps) ? 1 : 0;
     }
     if (nin == 0) return false;
-    float px[5], py[5];
-    int n = 0;
-#pragma unroll
-    for (int k = 0; k < 4; k++) {
-        const int k1 = (k + 1) & 3;
-        const bool ia = sv[k] >= s.eps, ib = sv[k1] >= s.eps;
-        if (ia) { px[n] = dx[k]; py[n] = dy[k]; n++; }
-        if (ia != ib) {
-            const int a = ia ? k : k1, b = ia ? k1 : k;
-            const float t = (sv[a] - s.eps) / (sv[a] - sv[b]);
-            px[n] = fmaf(t, dx[b] - dx[a], dx[a]);
-            py[n] = fmaf(t, dy[b] - dy[a], dy[a]);
-            n++;
-        }
-    }
-    float yx[5], yy[5];
-    for (int k = 0; k < n; k++) {
-        const float sk = dot3(s.ux, s.uy, s.uz, px[k], py[k], 1.0f);
-        yx[k] = dot3(s.e1x, 0.0f, s.e1z, px[k], py[k], 1.0f) / sk;
-        yy[k] = dot3(s.e2x, s.e2y, s.e2z, px[k], py[k], 1.0f) / sk;
-    }
-    int npos = 0, nneg = 0;
-    for (int k = 0; k < n; k++) {
-        const int k1 = (k + 1 == n) ? 0 : k + 1;
-        const float ddx = yx[k1] - yx[k], ddy = yy[k1] - yy[k];
-        const float cr = fmaf(ddy, yx[k], -(ddx * yy[k]));
-        npos += (cr >= 0.0f) ? 1 : 0;
-        nneg += (cr <= 0.0f) ? 1 : 0;
-    }
     float hx = 0.0f, hy = 0.0f, qmin;
-    if (npos == n || nneg == n) {
-        qmin = 0.0f;
+    if (nin == 4) {
+        float yx[4], yy[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const float is = 1.0f / dot3(s.ux, s.uy, s.uz, dx[k], dy[k], 1.0f);
+            yx[k] = dot3(s.e1x, 0.0f, s.e1z, dx[k], dy[k], 1.0f) * is;
+            yy[k] = dot3(s.e2x, s.e2y, s.e2z, dx[k], dy[k], 1.0f) * is;
+        }
+        int npos = 0, nneg = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int k1 = (k + 1) & 3;
+            const float ddx = yx[k1] - yx[k], ddy = yy[k1] - yy[k];
+            const float cr = fmaf(ddy, yx[k], -(ddx * yy[k]));
+            npos += (cr >= 0.0f) ? 1 : 0;
+            nneg += (cr <= 0.0f) ? 1 : 0;
+        }
+        if (npos == 4 || nneg == 4) {
+            qmin = 0.0f;
+        } else {
+            qmin = __int_as_float(0x7f800000);
+#pragma unroll
+            for (int k = 0; k < 4; k++) eq4_edge(s, yx[k], yy[k], yx[(k + 1) & 3], yy[(k + 1) & 3], qmin, hx, hy);
+        }
     } else {
-        qmin = __int_as_float(0x7f800000);
+        // partially behind the clip level: Sutherland-Hodgman against s >= eps
+        float px[5], py[5];
+        int n = 0;
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int k1 = (k + 1) & 3;
+            const bool ia = sv[k] >= s.eps, ib = sv[k1] >= s.eps;
+            if (ia) { px[n] = dx[k]; py[n] = dy[k]; n++; }
+            if (ia != ib) {
+                const int a = ia ? k : k1, b = ia ? k1 : k;
+                const float t = (sv[a] - s.eps) / (sv[a] - sv[b]);
+                px[n] = fmaf(t, dx[b] - dx[a], dx[a]);
+                py[n] = fmaf(t, dy[b] - dy[a], dy[a]);
+                n++;
+            }
+        }
+        float yx[5], yy[5];
+        for (int k = 0; k < n; k++) {
+            const float is = 1.0f / dot3(s.ux, s.uy, s.uz, px[k], py[k], 1.0f);
+            yx[k] = dot3(s.e1x, 0.0f, s.e1z, px[k], py[k], 1.0f) * is;
+            yy[k] = dot3(s.e2x, s.e2y, s.e2z, px[k], py[k], 1.0f) * is;
+        }
+        int npos = 0, nneg = 0;
         for (int k = 0; k < n; k++) {
             const int k1 = (k + 1 == n) ? 0 : k + 1;
-            const float ppx = yx[k], ppy = yy[k];
             const float ddx = yx[k1] - yx[k], ddy = yy[k1] - yy[k];
-            const float cdx = fmaf(s.C0, ddx, s.C1 * ddy), cdy = fmaf(s.C1, ddx, s.C2 * ddy);
-            const float den = fmaf(ddx, cdx, ddy * cdy);
-            const float nmr = -fmaf(ppx, cdx, ppy * cdy);
-            float t;
-            if (nmr <= 0.0f || !(den > 0.0f)) t = 0.0f;
-            else if (nmr >= den) t = 1.0f;
-            else t = nmr / den;
-            const float X = fmaf(t, ddx, ppx), Y = fmaf(t, ddy, ppy);
-            const float cX = fmaf(s.C0, X, s.C1 * Y), cY = fmaf(s.C1, X, s.C2 * Y);
-            const float q = fmaf(X, cX, Y * cY);
-            if (q < qmin) { qmin = q; hx = X; hy = Y; }
+            const float cr = fmaf(ddy, yx[k], -(ddx * yy[k]));
+            npos += (cr >= 0.0f) ? 1 : 0;
+            nneg += (cr <= 0.0f) ? 1 : 0;
+        }
+        if (npos == n || nneg == n) {
+            qmin = 0.0f;
+        } else {
+            qmin = __int_as_float(0x7f800000);
+            for (int k = 0; k < n; k++) {
+                const int k1 = (k + 1 == n) ? 0 : k + 1;
+                eq4_edge(s, yx[k], yy[k], yx[k1], yy[k1], qmin, hx, hy);
+            }
         }
     }
     dhx = fmaf(hy, s.e2x, fmaf(hx, s.e1x, s.ux));
@@ -309,15 +342,21 @@ __device__ void sh_color(const SceneDev& sc, int64_t g, int64_t N, int ncoef, fl
             basis[15] = -0.5900435899266435f * dx * (xx - 3.0f * yy);
         }
     }
-    float acc[3] = {0.0f, 0.0f, 0.0f};
-    const int nfl = ncoef * 3;
-    for (int c4 = 0; c4 * 4 < nfl; c4++) {
-        const float4 q = __ldg(&sc.sh[(size_t)c4 * N + g]);
-        const float vals[4] = {q.x, q.y, q.z, q.w};
+    // all coefficients into registers (compile-time indices: no local memory)
+    float shv[48];
+    const float4* src = sc.sh + (size_t)g * sc.sh_chunks;
 #pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const int f = c4 * 4 + k;
-            if (f < nfl) acc[f % 3] = fmaf(basis[f / 3], vals[k], acc[f % 3]);
+    for (int c4 = 0; c4 < 12; c4++) {
+        const float4 q = (c4 < sc.sh_chunks) ? __ldg(src + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        shv[4 * c4] = q.x; shv[4 * c4 + 1] = q.y; shv[4 * c4 + 2] = q.z; shv[4 * c4 + 3] = q.w;
+    }
+    float acc[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int k = 0; k < 16; k++) {
+        if (k < ncoef) {
+            acc[0] = fmaf(basis[k], shv[3 * k], acc[0]);
+            acc[1] = fmaf(basis[k], shv[3 * k + 1], acc[1]);
+            acc[2] = fmaf(basis[k], shv[3 * k + 2], acc[2]);
         }
     }
 #pragma unroll
@@ -337,12 +376,25 @@ __device__ __forceinline__ void load_gauss(const SceneDev& sc, int64_t g, int64_
 }
 
 // Step 1: per-Gaussian preprocess for all views + candidate tile counts.
-__global__ void __launch_bounds__(128) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb) {
+__global__ void __launch_bounds__(256, 2) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t N = fp.N;
     if (g >= N) return;
-    float4 m4, c0, c1, i0, i1;
-    load_gauss(sc, g, N, m4, c0, c1, i0, i1);
+    // near-plane test first (O1, same arithmetic as project_splat): the
+    // covariance / SH of a Gaussian behind every eye is never read
+    const float4 m4 = __ldg(&sc.mu[g]);
+    bool any = false;
+    for (int vi = 0; vi < fp.n_views; vi++) {
+        const ViewParams& v = fp.v[vi];
+        const float z = dot3(v.R[6], v.R[7], v.R[8], m4.x - v.o[0], m4.y - v.o[1], m4.z - v.o[2]);
+        any |= (z > fp.near_plane);
+    }
+    if (!any || m4.w < 0.0f) {
+        for (int vi = 0; vi < fp.n_views; vi++) fb.ntests[(size_t)vi * N + g] = 0;
+        return;
+    }
+    const float4 c0 = __ldg(&sc.cov[g]), c1 = __ldg(&sc.cov[N + g]);
+    const float4 i0 = __ldg(&sc.icov[g]), i1 = __ldg(&sc.icov[N + g]);
     for (int vi = 0; vi < fp.n_views; vi++) {
         const ViewParams& v = fp.v[vi];
         Proj p;
@@ -376,35 +428,24 @@ __global__ void __launch_bounds__(128) k_preprocess(SceneDev sc, FrameParams fp,
     }
 }
 
-__device__ __forceinline__ int64_t upper_bound_u32(const uint32_t* __restrict__ a, int64_t lo, int64_t hi,
-                                                   uint32_t x) {
-    while (lo < hi) {
-        const int64_t mid = (lo + hi) >> 1;
-        if (__ldg(a + mid) <= x) lo = mid + 1;
-        else hi = mid;
-    }
-    return lo;
-}
-
 // Step 3a: one thread per (Gaussian, candidate tile): Eq.4 test (O7) and key
 // (O8).  Candidates are laid out (view, g, tile row-major) by the scan of the
 // per-splat rect areas, so every thread does one test (load-balanced: big
 // footprints no longer serialise a thread).  Writes keep flag, key, value.
-__global__ void __launch_bounds__(256) k_tiletest(FrameParams fp, FrameBufs fb, int64_t test_cap) {
+// Candidate -> splat map: sid[toff[s] + i] = s for i < ntests[s].
+__global__ void k_fill_sid(FrameParams fp, FrameBufs fb, int64_t test_cap) {
     const int64_t VN = (int64_t)fp.n_views * fp.N;
+    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < VN; s += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t n = fb.ntests[s], a = fb.toff[s];
+        for (uint32_t i = 0; i < n && (int64_t)a + i < test_cap; i++) fb.sid[a + i] = (uint32_t)s;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_tiletest(FrameParams fp, FrameBufs fb, int64_t test_cap) {
     const int64_t total = min((int64_t)*fb.total_tests, test_cap);
-    const int lane = threadIdx.x & 31;
     const int T = fp.T;
-    for (int64_t tw0 = ((int64_t)blockIdx.x * blockDim.x) + (threadIdx.x & ~31); tw0 < total;
-         tw0 += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t t = tw0 + lane;
-        // warp-cooperative search: bracket the warp's splats, then search inside
-        const int64_t tw1 = min(tw0 + 31, total - 1);
-        int64_t b = 0;
-        if (lane < 2) b = upper_bound_u32(fb.toff, 0, VN, (uint32_t)(lane == 0 ? tw0 : tw1)) - 1;
-        const int64_t s_lo = __shfl_sync(0xffffffffu, b, 0), s_hi = __shfl_sync(0xffffffffu, b, 1);
-        if (t >= total) continue;
-        const int64_t sidx = upper_bound_u32(fb.toff, s_lo, s_hi + 1, (uint32_t)t) - 1;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t sidx = fb.sid[t];
         const uint32_t l = (uint32_t)(t - fb.toff[sidx]);
         const int vi = (int)(sidx / fp.N);
         const ViewParams& v = fp.v[vi];
@@ -513,7 +554,7 @@ __global__ void k_debug_splats(SceneDev sc, FrameParams fp, FrameBufs fb, int vi
 
 void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, cudaStream_t st) {
     if (fp.N == 0) return;
-    const int B = 128;
+    const int B = 256;
     k_preprocess<<<(unsigned)((fp.N + B - 1) / B), B, 0, st>>>(sc, fp, fb);
 }
 
@@ -529,7 +570,9 @@ static int sm_count() {
 }
 
 void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {
-    if ((int64_t)fp.n_views * fp.N == 0) return;
+    const int64_t VN = (int64_t)fp.n_views * fp.N;
+    if (VN == 0) return;
+    k_fill_sid<<<(unsigned)std::min<int64_t>((VN + 255) / 256, (int64_t)sm_count() * 16), 256, 0, st>>>(fp, fb, test_cap);
     k_tiletest<<<sm_count() * 8, 256, 0, st>>>(fp, fb, test_cap);
 }
 

@@ -46,7 +46,7 @@ struct vrs_context {
     float4* d_rec = nullptr;
     float4* d_col = nullptr;
     uint32_t *d_counts = nullptr, *d_ntests = nullptr, *d_toff = nullptr, *d_misc = nullptr;  // misc: pairs, overflow, tests
-    uint32_t *d_tflag = nullptr, *d_tpos = nullptr, *d_tval = nullptr;
+    uint32_t *d_tflag = nullptr, *d_tpos = nullptr, *d_tval = nullptr, *d_sid = nullptr;
     uint64_t* d_tkey = nullptr;
     int64_t test_cap = 0;
     uint64_t *d_keys = nullptr, *d_keys_alt = nullptr;
@@ -106,7 +106,7 @@ static vrs_status cuda_check(vrs_context* c, cudaError_t e, const char* where) {
 
 static void free_all(vrs_context* c) {
     void* ptrs[] = {c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_col, c->d_counts, c->d_ntests, c->d_toff, c->d_misc,
-                    c->d_tflag, c->d_tpos, c->d_tval, c->d_tkey,
+                    c->d_tflag, c->d_tpos, c->d_tval, c->d_tkey, c->d_sid,
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
                     c->d_sat, c->d_cls, c->d_items, c->d_nitems, c->d_out_rgba, c->d_out_depth};
@@ -155,6 +155,7 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     A(dalloc(&ctx->d_toff, (size_t)V * N));
     ctx->test_cap = 4 * P;
     A(dalloc(&ctx->d_tflag, (size_t)ctx->test_cap));
+    A(dalloc(&ctx->d_sid, (size_t)ctx->test_cap));
     A(dalloc(&ctx->d_tpos, (size_t)ctx->test_cap));
     A(dalloc(&ctx->d_tval, (size_t)ctx->test_cap));
     A(dalloc(&ctx->d_tkey, (size_t)ctx->test_cap));
@@ -264,7 +265,7 @@ vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_degree, 
     const int64_t nk = (int64_t)keep.size();
     cov.insert(cov.end(), cov_hi.begin(), cov_hi.end());
     icov.insert(icov.end(), icov_hi.begin(), icov_hi.end());
-    // SH: coefficient-major RGB flattened, [chunk][N] float4 (coalesced per chunk)
+    // SH: coefficient-major RGB flattened, [N][chunk] float4 (a visible Gaussian reads its own 48 floats)
     std::vector<float4> shd((size_t)chunks * std::max<int64_t>(nk, 1));
     for (int64_t r = 0; r < nk; r++) {
         const float* shc = sh + (size_t)keep[r] * nfl;
@@ -272,7 +273,7 @@ vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_degree, 
             float t[4] = {0, 0, 0, 0};
             for (int k = 0; k < 4; k++)
                 if (4 * c + k < nfl) t[k] = shc[4 * c + k];
-            shd[(size_t)c * nk + r] = make_float4(t[0], t[1], t[2], t[3]);
+            shd[(size_t)r * chunks + c] = make_float4(t[0], t[1], t[2], t[3]);
         }
     }
     // (re)allocate scene buffers
@@ -456,6 +457,7 @@ static FrameBufs frame_bufs(vrs_context* ctx) {
     fb.ntests = ctx->d_ntests;
     fb.toff = ctx->d_toff;
     fb.total_tests = ctx->d_misc + 2;
+    fb.sid = ctx->d_sid;
     fb.tflag = ctx->d_tflag;
     fb.tpos = ctx->d_tpos;
     fb.tkey = ctx->d_tkey;

@@ -62,7 +62,7 @@ struct SceneDev {
     const float4* mu;        // [N] mu.xyz, q_cut
     const float4* cov;       // [2][N] (xx,xy,xz,yy) (yz,zz,sigma,0)
     const float4* icov;      // [2][N] (xx,xy,xz,yy) (yz,zz,0,0)
-    const float4* sh;        // [chunks][N]
+    const float4* sh;        // [N][chunks]
     int32_t sh_chunks;
 };
 
@@ -71,6 +71,7 @@ struct FrameBufs {
     uint32_t* ntests;        // [V*N] candidate (Gaussian, tile) tests = rect area
     uint32_t* toff;          // [V*N] exclusive scan of ntests
     uint32_t* total_tests;   // [1] (device)
+    uint32_t* sid;           // [test_cap] candidate -> splat (view*N + g)
     uint32_t* tflag;         // [test_cap] keep flags
     uint32_t* tpos;          // [test_cap] exclusive scan of tflag = pair position
     uint64_t* tkey;          // [test_cap] key of kept candidates
