@@ -375,28 +375,68 @@ __device__ __forceinline__ void load_gauss(const SceneDev& sc, int64_t g, int64_
     i1 = __ldg(&sc.icov[N + g]);
 }
 
-// Step 1: per-Gaussian preprocess for all views + candidate tile counts.
-__global__ void __launch_bounds__(256, 2) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb) {
+// Step 1a: cheap conservative cull over all Gaussians and views.  The
+// footprint of a Gaussian lies in the cone of half-angle beta' around u with
+// tan^2 beta' = q_cut (s_max^2 / r^2 + 0.3 / f_min^2) >= q_cut lambda_max(Sigma_2)
+// (lambda_max(E^T Sigma_c E) <= s_max^2, dilation <= 0.3/f^2), so a view whose
+// frustum misses that (inflated) cone is also culled by the exact O6(a) test:
+// culling here never changes results, it only compacts the work of step 1b.
+__global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, FrameBufs fb) {
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t N = fp.N;
-    if (g >= N) return;
-    // near-plane test first (O1, same arithmetic as project_splat): the
-    // covariance / SH of a Gaussian behind every eye is never read
-    const float4 m4 = __ldg(&sc.mu[g]);
-    bool any = false;
+    const bool in = g < N;
+    float4 m4 = make_float4(0.f, 0.f, 0.f, -1.0f);
+    float smax = 0.0f;
+    if (in) {
+        m4 = __ldg(&sc.mu[g]);
+        smax = __ldg(&sc.cov[N + g]).w;
+    }
+    const int lane = threadIdx.x & 31;
     for (int vi = 0; vi < fp.n_views; vi++) {
         const ViewParams& v = fp.v[vi];
-        const float z = dot3(v.R[6], v.R[7], v.R[8], m4.x - v.o[0], m4.y - v.o[1], m4.z - v.o[2]);
-        any |= (z > fp.near_plane);
+        bool pass = false;
+        if (in && m4.w >= 0.0f) {
+            const float vx = m4.x - v.o[0], vy = m4.y - v.o[1], vz = m4.z - v.o[2];
+            const float mx = dot3(v.R[0], v.R[1], v.R[2], vx, vy, vz);
+            const float my = dot3(v.R[3], v.R[4], v.R[5], vx, vy, vz);
+            const float mz = dot3(v.R[6], v.R[7], v.R[8], vx, vy, vz);
+            if (mz > fp.near_plane) {
+                const float r2 = dot3(mx, my, mz, mx, my, mz);
+                const float tan2 = m4.w * (smax * smax / r2 + v.dil);
+                const float sinb = sqrtf(tan2 / (1.0f + tan2)) * 1.01f + 2e-3f;
+                const float ir = rsqrtf(r2);
+                const float ux = mx * ir, uy = my * ir, uz = mz * ir;
+                pass = true;
+#pragma unroll
+                for (int k = 0; k < 4; k++)
+                    pass = pass && (v.plane[k][0] * ux + v.plane[k][1] * uy + v.plane[k][2] * uz >= -sinb);
+            }
+        }
+        if (in && !pass) fb.ntests[(size_t)vi * N + g] = 0;
+        // warp-aggregated append of (view, g) to the work list
+        const unsigned m = __ballot_sync(0xffffffffu, pass);
+        if (m) {
+            uint32_t base = 0;
+            if (lane == 0) base = atomicAdd(fb.cand_count, (uint32_t)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, 0);
+            if (pass) fb.cand[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)((int64_t)vi * N + g);
+        }
     }
-    if (!any || m4.w < 0.0f) {
-        for (int vi = 0; vi < fp.n_views; vi++) fb.ntests[(size_t)vi * N + g] = 0;
-        return;
-    }
-    const float4 c0 = __ldg(&sc.cov[g]), c1 = __ldg(&sc.cov[N + g]);
-    const float4 i0 = __ldg(&sc.icov[g]), i1 = __ldg(&sc.icov[N + g]);
-    for (int vi = 0; vi < fp.n_views; vi++) {
+}
+
+// Step 1b: exact per-(view, Gaussian) preprocess of the compacted candidates:
+// projection, footprint, candidate tile count, splat record and SH colour.
+__global__ void __launch_bounds__(256, 2) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb) {
+    const int64_t N = fp.N;
+    const uint32_t nc = *fb.cand_count;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
+        const uint32_t sidx = fb.cand[i];
+        const int vi = (int)(sidx / N);
+        const int64_t g = (int64_t)sidx - (int64_t)vi * N;
         const ViewParams& v = fp.v[vi];
+        const float4 m4 = __ldg(&sc.mu[g]);
+        const float4 c0 = __ldg(&sc.cov[g]), c1 = __ldg(&sc.cov[N + g]);
+        const float4 i0 = __ldg(&sc.icov[g]), i1 = __ldg(&sc.icov[N + g]);
         Proj p;
         project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
         // number of (Gaussian, tile) candidates = rect area, 0 if the rect holds no
@@ -405,7 +445,7 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(SceneDev sc, FrameParams 
         if (p.valid && p.rect[0] <= p.rect[2] && p.rect[1] <= p.rect[3] &&
             sat_count(v.sat, v.tw + 1, p.rect[0], p.rect[1], p.rect[2], p.rect[3]) > 0)
             cnt = (uint32_t)((p.rect[2] - p.rect[0] + 1) * (p.rect[3] - p.rect[1] + 1));
-        fb.ntests[(size_t)vi * N + g] = cnt;
+        fb.ntests[sidx] = cnt;
         if (cnt == 0) continue;
         float rgb[3];
         {
@@ -413,7 +453,7 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(SceneDev sc, FrameParams 
             const float inv = 1.0f / sqrtf(dot3(dx, dy, dz, dx, dy, dz));
             sh_color(sc, g, N, fp.sh_coeffs, dx * inv, dy * inv, dz * inv, rgb);
         }
-        float4* rec = fb.rec + ((size_t)vi * N + g) * kRecF4;
+        float4* rec = fb.rec + (size_t)sidx * kRecF4;
         const uint32_t r01 = (uint32_t)p.rect[0] | ((uint32_t)p.rect[1] << 16);
         const uint32_t r23 = (uint32_t)p.rect[2] | ((uint32_t)p.rect[3] << 16);
         rec[0] = make_float4(p.u[0], p.u[1], p.u[2], p.qcut);
@@ -424,7 +464,7 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(SceneDev sc, FrameParams 
         rec[5] = make_float4(p.bv[2], p.sigma, p.eps, __uint_as_float(r01));
         rec[6] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(r23));
         rec[7] = make_float4(p.bbox[0], p.bbox[1], p.bbox[2], p.bbox[3]);
-        fb.col[(size_t)vi * N + g] = make_float4(rgb[0], rgb[1], rgb[2], 0.0f);
+        fb.col[sidx] = make_float4(rgb[0], rgb[1], rgb[2], 0.0f);
     }
 }
 
@@ -555,7 +595,12 @@ __global__ void k_debug_splats(SceneDev sc, FrameParams fp, FrameBufs fb, int vi
 void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, cudaStream_t st) {
     if (fp.N == 0) return;
     const int B = 256;
-    k_preprocess<<<(unsigned)((fp.N + B - 1) / B), B, 0, st>>>(sc, fp, fb);
+    cudaMemsetAsync(fb.cand_count, 0, 4, st);
+    k_cull<<<(unsigned)((fp.N + B - 1) / B), B, 0, st>>>(sc, fp, fb);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    k_preprocess<<<sms * 4, B, 0, st>>>(sc, fp, fb);
 }
 
 static int sm_count() {

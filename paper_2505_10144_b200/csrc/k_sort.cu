@@ -21,12 +21,14 @@ constexpr int kRadix = 256;
 constexpr int kWarps = kSortThreads / 32;
 constexpr uint32_t kStAgg = 1u << 30, kStPre = 2u << 30, kStMask = (1u << 30) - 1;
 
+// Status words are self-contained (flag + value): relaxed GPU-scope
+// accesses suffice and avoid the L1 invalidation an acquire load implies.
 __device__ __forceinline__ void st_release32(uint32_t* p, uint32_t v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ uint32_t ld_acquire32(const uint32_t* p) {
     uint32_t v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
 }  // namespace
@@ -67,25 +69,33 @@ __global__ void k_sort_hist_scan(uint32_t* hist) {
     h[t] = s[t] - v;
 }
 
-__global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint64_t* __restrict__ kin,
-                                                           const uint32_t* __restrict__ vin, uint64_t* __restrict__ kout,
-                                                           uint32_t* __restrict__ vout,
-                                                           const uint32_t* __restrict__ n_dev, int64_t cap, int pass,
-                                                           const uint32_t* __restrict__ digit_off, uint32_t* status,
-                                                           uint32_t* counter) {
-    __shared__ uint32_t s_wh[kWarps][kRadix];  // per-warp digit counts -> exclusive offsets
-    __shared__ uint32_t s_gbase[kRadix];
-    __shared__ uint32_t s_tile;
+struct OnesweepSmem {
+    uint32_t wh[kWarps][kRadix];    // per-warp digit counts -> exclusive offsets
+    uint32_t tstart[kRadix];        // tile-local exclusive digit offsets
+    uint32_t gbase[kRadix];         // global position of the tile's first key of each digit
+    uint64_t k[kSortTile];          // tile keys in digit-sorted order (staged scatter)
+    uint32_t v[kSortTile];
+    uint32_t tile;
+};
+
+__global__ void __launch_bounds__(kSortThreads, 2) k_onesweep(const uint64_t* __restrict__ kin,
+                                                              const uint32_t* __restrict__ vin,
+                                                              uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                                              const uint32_t* __restrict__ n_dev, int64_t cap,
+                                                              int pass, const uint32_t* __restrict__ digit_off,
+                                                              uint32_t* status, uint32_t* counter) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int shift = 8 * pass;
     const int64_t n = min((int64_t)*n_dev, cap);
     const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
     const uint32_t lt_mask = (1u << lane) - 1u;
     while (true) {
-        if (tid == 0) s_tile = atomicAdd(counter, 1u);
-        for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&s_wh[0][0])[i] = 0;
+        if (tid == 0) S.tile = atomicAdd(counter, 1u);
+        for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&S.wh[0][0])[i] = 0;
         __syncthreads();
-        const int64_t tile = s_tile;
+        const int64_t tile = S.tile;
         if (tile >= ntiles) break;
         const int64_t wbase = tile * kSortTile + (int64_t)warp * (kSortItems * 32);
         uint64_t key[kSortItems];
@@ -95,7 +105,7 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint64_t* __res
         for (int i = 0; i < kSortItems; i++) {
             const int64_t idx = wbase + i * 32 + lane;
             const bool ok = idx < n;
-            key[i] = ok ? kin[idx] : 0ull;
+            key[i] = ok ? kin[idx] : ~0ull;
             val[i] = ok ? vin[idx] : 0u;
         }
         // warp-local stable ranking in (item, lane) order
@@ -105,51 +115,87 @@ __global__ void __launch_bounds__(kSortThreads) k_onesweep(const uint64_t* __res
             const bool ok = idx < n;
             const uint32_t d = (uint32_t)(key[i] >> shift) & 0xffu;
             const uint32_t peers = __match_any_sync(0xffffffffu, ok ? d : (0x100u + lane));
-            const uint32_t old = ok ? s_wh[warp][d] : 0u;
+            const uint32_t old = ok ? S.wh[warp][d] : 0u;
             __syncwarp();
-            if (ok && (peers & lt_mask) == 0) s_wh[warp][d] = old + __popc(peers);
+            if (ok && (peers & lt_mask) == 0) S.wh[warp][d] = old + __popc(peers);
             __syncwarp();
             rank[i] = old + __popc(peers & lt_mask);
         }
         __syncthreads();
-        // per digit: exclusive over warps, tile total, publish + look-back
-        {
-            const int d = tid;  // kSortThreads == kRadix
-            uint32_t tot = 0;
+        // per digit (thread d): exclusive over warps, tile total; publish; look back
+        const int d = tid;  // kSortThreads == kRadix
+        uint32_t tot = 0;
 #pragma unroll
-            for (int w = 0; w < kWarps; w++) {
-                const uint32_t c = s_wh[w][d];
-                s_wh[w][d] = tot;
-                tot += c;
-            }
-            uint32_t* st = status + (size_t)tile * kRadix + d;
-            uint32_t excl = 0;
-            if (tile == 0) {
-                st_release32(st, kStPre | tot);
-            } else {
-                st_release32(st, kStAgg | tot);
-                int64_t j = tile - 1;
-                while (true) {
-                    uint32_t s;
-                    do { s = ld_acquire32(status + (size_t)j * kRadix + d); } while ((s & ~kStMask) == 0);
-                    excl += s & kStMask;
-                    if ((s & ~kStMask) == kStPre) break;
-                    j--;
+        for (int w = 0; w < kWarps; w++) {
+            const uint32_t c = S.wh[w][d];
+            S.wh[w][d] = tot;
+            tot += c;
+        }
+        uint32_t* st = status + (size_t)tile * kRadix + d;
+        uint32_t excl = 0;
+        if (tile == 0) {
+            st_release32(st, kStPre | tot);
+        } else {
+            st_release32(st, kStAgg | tot);
+            // decoupled look-back, four predecessors in flight per round trip
+            int64_t j = tile - 1;
+            while (true) {
+                uint32_t sv[4];
+#pragma unroll
+                for (int k = 0; k < 4; k++)
+                    sv[k] = (j - k >= 0) ? ld_acquire32(status + (size_t)(j - k) * kRadix + d) : kStPre;
+                int k = 0;
+                bool fin = false;
+#pragma unroll
+                for (; k < 4; k++) {
+                    const uint32_t f = sv[k] & ~kStMask;
+                    if (f == 0) break;
+                    excl += sv[k] & kStMask;
+                    if (f == kStPre) { fin = true; break; }
                 }
-                st_release32(st, kStPre | (excl + tot));
+                if (fin) break;
+                j -= k;
             }
-            s_gbase[d] = digit_off[pass * kRadix + d] + excl;
+            st_release32(st, kStPre | (excl + tot));
+        }
+        S.gbase[d] = digit_off[pass * kRadix + d] + excl;
+        // tile-local exclusive scan of the digit totals
+        S.tstart[d] = tot;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t run = 0;
+            for (int c = 0; c < kRadix; c += 32) {
+                const uint32_t v0 = S.tstart[c + lane];
+                uint32_t inc = v0;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                S.tstart[c + lane] = run + inc - v0;
+                run += __shfl_sync(0xffffffffu, inc, 31);
+            }
         }
         __syncthreads();
+        // stage keys in digit-sorted order, then write runs coalesced
 #pragma unroll
         for (int i = 0; i < kSortItems; i++) {
             const int64_t idx = wbase + i * 32 + lane;
             if (idx < n) {
-                const uint32_t d = (uint32_t)(key[i] >> shift) & 0xffu;
-                const uint32_t pos = s_gbase[d] + s_wh[warp][d] + rank[i];
-                kout[pos] = key[i];
-                vout[pos] = val[i];
+                const uint32_t dd = (uint32_t)(key[i] >> shift) & 0xffu;
+                const uint32_t lp = S.tstart[dd] + S.wh[warp][dd] + rank[i];
+                S.k[lp] = key[i];
+                S.v[lp] = val[i];
             }
+        }
+        __syncthreads();
+        const int cnt = (int)min((int64_t)kSortTile, n - tile * kSortTile);
+        for (int i = tid; i < cnt; i += kSortThreads) {
+            const uint64_t kk = S.k[i];
+            const uint32_t dd = (uint32_t)(kk >> shift) & 0xffu;
+            const uint32_t pos = S.gbase[dd] + (uint32_t)i - S.tstart[dd];
+            kout[pos] = kk;
+            vout[pos] = S.v[i];
         }
         __syncthreads();
     }
@@ -187,12 +233,18 @@ void launch_sort(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* v
     cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * 8, st);
     k_sort_hist<<<sms * 2, kSortThreads, 0, st>>>(keys, n_dev, cap, passes, s.hist);
     k_sort_hist_scan<<<passes, kRadix, 0, st>>>(s.hist);
-    const unsigned grid = (unsigned)std::min<int64_t>(max_tiles, (int64_t)sms * 4);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(OnesweepSmem));
+        attr = true;
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(max_tiles, (int64_t)sms * 2);
     uint64_t *ka = keys, *kb = keys_alt;
     uint32_t *va = vals, *vb = vals_alt;
     for (int p = 0; p < passes; p++) {
         cudaMemsetAsync(s.status, 0, sizeof(uint32_t) * (size_t)max_tiles * kRadix, st);
-        k_onesweep<<<grid, kSortThreads, 0, st>>>(ka, va, kb, vb, n_dev, cap, p, s.hist, s.status, s.counters + p);
+        k_onesweep<<<grid, kSortThreads, sizeof(OnesweepSmem), st>>>(ka, va, kb, vb, n_dev, cap, p, s.hist, s.status,
+                                                                      s.counters + p);
         std::swap(ka, kb);
         std::swap(va, vb);
     }

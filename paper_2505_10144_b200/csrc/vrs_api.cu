@@ -2,6 +2,7 @@
 // visibility masks, per-eye static setup cache and the per-frame launch
 // sequence preprocess -> scan -> duplicate -> onesweep sort -> ranges ->
 // blend -> compose, all enqueued on the caller's stream with no host sync.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -45,6 +46,7 @@ struct vrs_context {
     // frame buffers
     float4* d_rec = nullptr;
     float4* d_col = nullptr;
+    uint32_t* d_cand = nullptr;
     uint32_t *d_counts = nullptr, *d_ntests = nullptr, *d_toff = nullptr, *d_misc = nullptr;  // misc: pairs, overflow, tests
     uint32_t *d_tflag = nullptr, *d_tpos = nullptr, *d_tval = nullptr, *d_sid = nullptr;
     uint64_t* d_tkey = nullptr;
@@ -105,7 +107,7 @@ static vrs_status cuda_check(vrs_context* c, cudaError_t e, const char* where) {
     } while (0)
 
 static void free_all(vrs_context* c) {
-    void* ptrs[] = {c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_col, c->d_counts, c->d_ntests, c->d_toff, c->d_misc,
+    void* ptrs[] = {c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_col, c->d_cand, c->d_counts, c->d_ntests, c->d_toff, c->d_misc,
                     c->d_tflag, c->d_tpos, c->d_tval, c->d_tkey, c->d_sid,
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
@@ -150,6 +152,7 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
     A(dalloc(&ctx->d_rec, (size_t)V * N * kRecF4));
     A(dalloc(&ctx->d_col, (size_t)V * N));
+    A(dalloc(&ctx->d_cand, (size_t)V * N));
     A(dalloc(&ctx->d_counts, (size_t)V * N));
     A(dalloc(&ctx->d_ntests, (size_t)V * N));
     A(dalloc(&ctx->d_toff, (size_t)V * N));
@@ -253,11 +256,12 @@ vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_degree, 
             ok = ok && std::isfinite(c6[e2]) && std::isfinite(i6[e2]);
         }
         if (!ok) continue;
+        const double smax = std::sqrt(std::max(s2[0], std::max(s2[1], s2[2])));
         const float sg = (float)(1.0 / (1.0 + std::exp(-(double)logits[i])));
         const float qc = (float)(2.0 * std::log(255.0 * (double)sg));
         mu.push_back(make_float4(m[0], m[1], m[2], qc));
         cov.push_back(make_float4(c6[0], c6[1], c6[2], c6[3]));
-        cov_hi.push_back(make_float4(c6[4], c6[5], sg, 0.0f));
+        cov_hi.push_back(make_float4(c6[4], c6[5], sg, (float)(smax * (1.0 + 1e-6))));
         icov.push_back(make_float4(i6[0], i6[1], i6[2], i6[3]));
         icov_hi.push_back(make_float4(i6[4], i6[5], 0.0f, 0.0f));
         keep.push_back(i);
@@ -399,6 +403,17 @@ static vrs_status prepare_frame(vrs_context* ctx, int nv, const vrs_camera* cams
             v.rx = fov[vi].radius[0]; v.ry = fov[vi].radius[1];
             v.ramp = fov[vi].ramp;
         }
+        {   // frustum side planes (inward unit normals) and dilation bound, for k_cull
+            const double xl = (0.0 - c.cx) / c.fx, xr = ((double)c.width - c.cx) / c.fx;
+            const double yt = (0.0 - c.cy) / c.fy, yb = ((double)c.height - c.cy) / c.fy;
+            const double Nn[4][3] = {{1.0, 0.0, -xl}, {-1.0, 0.0, xr}, {0.0, 1.0, -yt}, {0.0, -1.0, yb}};
+            for (int k = 0; k < 4; k++) {
+                const double nn = std::sqrt(Nn[k][0] * Nn[k][0] + Nn[k][1] * Nn[k][1] + Nn[k][2] * Nn[k][2]);
+                for (int i = 0; i < 3; i++) v.plane[k][i] = (float)(Nn[k][i] / nn);
+            }
+            const double fmin = std::min(c.fx, c.fy);
+            v.dil = (float)(0.3 / (fmin * fmin) * 1.01);
+        }
         v.pix_off = pix_off;
         v.low_off = (int64_t)vi * ctx->low_px_view;
         v.low_w = (c.width + 1) / 2;
@@ -454,6 +469,8 @@ static FrameBufs frame_bufs(vrs_context* ctx) {
     FrameBufs fb{};
     fb.rec = ctx->d_rec;
     fb.col = ctx->d_col;
+    fb.cand = ctx->d_cand;
+    fb.cand_count = ctx->d_misc + 3;
     fb.ntests = ctx->d_ntests;
     fb.toff = ctx->d_toff;
     fb.total_tests = ctx->d_misc + 2;

@@ -34,6 +34,8 @@ struct ViewParams {
     int32_t tile_base;       // global tile id offset (views concatenated)
     int32_t fovea;           // foveation on
     float gx, gy, rx, ry, ramp;
+    float plane[4][3];       // inward unit normals of the 4 frustum side planes (camera frame)
+    float dil;               // 0.3 / min(fx, fy)^2: dilation bound for the conservative cull
     int64_t pix_off;         // pixel offset of this view in the output buffers
     int64_t low_off;         // offset of this view in the low-res sample planes
     int32_t low_w;           // low-res plane width ((W+1)/2)
@@ -60,7 +62,7 @@ struct FrameParams {
 
 struct SceneDev {
     const float4* mu;        // [N] mu.xyz, q_cut
-    const float4* cov;       // [2][N] (xx,xy,xz,yy) (yz,zz,sigma,0)
+    const float4* cov;       // [2][N] (xx,xy,xz,yy) (yz,zz,sigma,s_max)
     const float4* icov;      // [2][N] (xx,xy,xz,yy) (yz,zz,0,0)
     const float4* sh;        // [N][chunks]
     int32_t sh_chunks;
@@ -68,6 +70,8 @@ struct SceneDev {
 
 struct FrameBufs {
     float4* rec;             // [V][N][8]
+    uint32_t* cand;          // [V*N] (view*N + g) passing the conservative cull
+    uint32_t* cand_count;    // [1]
     uint32_t* ntests;        // [V*N] candidate (Gaussian, tile) tests = rect area
     uint32_t* toff;          // [V*N] exclusive scan of ntests
     uint32_t* total_tests;   // [1] (device)
