@@ -42,14 +42,16 @@ void launch_ranges(const uint64_t* keys, const uint32_t* n_dev, int64_t cap, uin
 
 namespace {
 
+constexpr int kBatch = 64;  // splat records staged per shared-memory batch
+
 struct BlendSmem {
-    float4 r0[kBlend];   // u.xyz, q_cut
-    float4 r1[kBlend];   // e1.x, e1.z, e2.x, e2.y
-    float4 r2[kBlend];   // e2.z, C00, C01, C11
-    float4 r3[kBlend];   // A a, b, c, p
-    float4 r4[kBlend];   // A e, f, b.x, b.y
-    float4 r5[kBlend];   // b.z, sigma, g (bits), -
-    uint32_t mask[kBlend];
+    float4 r0[kBatch];   // u.xyz, q_cut
+    float4 r1[kBatch];   // e1.x, e1.z, e2.x, e2.y
+    float4 r2[kBatch];   // e2.z, C00, C01, C11
+    float4 r3[kBatch];   // A a, b, c, p
+    float4 r4[kBatch];   // A e, f, b.x, b.y
+    float4 r5[kBatch];   // b.z, sigma, g (bits), -
+    uint32_t mask[kBatch];
     float4 wblock[8];    // per-warp sample extent xmin, xmax, ymin, ymax (pixel coords)
     // per-thread resort window: ring of K slots, (tau, g) packed into one
     // order-preserving 64-bit key, alpha alongside; [slot][thread] layout is
@@ -91,7 +93,7 @@ __device__ __forceinline__ float key_tau(unsigned long long key) {
 }  // namespace
 
 template <bool kCounters>
-__global__ void __launch_bounds__(kBlend, 2) k_blend(FrameParams fp, FrameBufs fb, float* __restrict__ rgba,
+__global__ void __launch_bounds__(kBlend, 4) k_blend(FrameParams fp, FrameBufs fb, float* __restrict__ rgba,
                                                       float* __restrict__ depth) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BlendSmem& S = *reinterpret_cast<BlendSmem*>(smem_raw);
@@ -171,10 +173,10 @@ __global__ void __launch_bounds__(kBlend, 2) k_blend(FrameParams fp, FrameBufs f
         done = Tr < kTmin;
     };
 
-    for (uint32_t base = rb; base < re; base += kBlend) {
+    for (uint32_t base = rb; base < re; base += kBatch) {
         __syncthreads();
         const uint32_t idx = base + tid;
-        if (idx < re) {
+        if (tid < kBatch && idx < re) {
             uint32_t g = __ldg(fb.vals + idx);
             g = (g < (uint32_t)fp.N) ? g : 0u;  // memory safety after a capacity overflow only
             const float4* rp = recv + (size_t)g * kRecF4;
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(kBlend, 2) k_blend(FrameParams fp, FrameBufs f
             S.mask[tid] = fp.no_cull ? 0xffu : m;
         }
         if (__syncthreads_count(!done) == 0) break;
-        const int nb = min((int)(re - base), kBlend);
+        const int nb = min((int)(re - base), kBatch);
         for (int c = 0; c < nb; c += 32) {
             if (__all_sync(0xffffffffu, done)) break;
             const bool rel = (c + lane < nb) && ((S.mask[c + lane] >> warp) & 1u);
