@@ -77,50 +77,53 @@ def make_workload(cfg_name):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clock + throttle reasons sampled (NVML, every 5 ms) during the timed region."""
 
-    def __init__(self, index=0):
+    HW_SLOWDOWN, SW_THERMAL, HW_THERMAL, SW_POWER = 0x8, 0x20, 0x40, 0x4
+
+    def __init__(self, index=0, period=0.005):
         self.index = index
+        self.period = period
         self.rows = []
-        self.proc = None
+        self._stop = threading.Event()
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 7:
-                self.rows.append(parts)
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.rows.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join(timeout=1)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = {self.HW_SLOWDOWN: "hw_slowdown", self.HW_THERMAL: "hw_thermal_slowdown",
+                 self.SW_THERMAL: "sw_thermal_slowdown", self.SW_POWER: "sw_power_cap"}
+        reasons = sorted({n for _, r in self.rows for bit, n in names.items() if r & bit})
+        return {"sm_mhz": statistics.median([r[0] for r in self.rows]), "sm_max_mhz": self.max_sm,
+                "reasons": reasons, "samples": len(self.rows), "source": "NVML, 5 ms period"}
 
 
 def measured_peaks():
@@ -206,20 +209,10 @@ def main():
         _, cams, fov, masks = None, None, None, None
         scene = None
     if world > 1:
-        n = cfg["n"]
-        k = (cfg["sh"] + 1) ** 2
-        bufs = {"means": (n, 3), "quats": (n, 4), "log_scales": (n, 3), "logits": (n,), "sh": (n, k, 3)}
-        tens = {}
-        for name, shape in bufs.items():
-            if rank == 0:
-                t = torch.from_numpy(np.ascontiguousarray(getattr(scene, name))).cuda()
-            else:
-                t = torch.empty(shape, dtype=torch.float32, device="cuda")
-            dist.broadcast(t, 0)
-            tens[name] = t.cpu().numpy()
+        from paper_2505_10144_b200.parallel import broadcast_scene
+        scene = broadcast_scene(scene, cfg["n"], cfg["sh"], device=torch.device("cuda", local))
         if rank != 0:
-            scene = sg.RawScene(tens["means"], tens["quats"], tens["log_scales"], tens["logits"], tens["sh"], cfg["sh"])
-            _, cams, fov, masks = (None,) + make_cams_only(args.config)
+            cams, fov, masks = make_cams_only(args.config)
     from paper_2505_10144_b200 import Renderer
 
     W = max(c.width for c in cams)

@@ -300,3 +300,46 @@ def test_capacity_overflow_reported(vrs):
     with pytest.raises(vrs.VrsError) as e:
         r.stats()
     assert e.value.status == vrs.vrs.VRS_E_CAPACITY
+
+
+def _quest_workload(seed, n, scale_mul, fovea, T, masks):
+    scene = sg.vr_room(seed, n, scale_mul=scale_mul, sh_degree=3)
+    cams = sg.stereo_pair(masks=masks)
+    fov = [sg.quest_fovea()] * 2 if fovea else None
+    mk = {0: sg.ellipse_mask(sg.QUEST_W, sg.QUEST_H), 1: sg.ellipse_mask(sg.QUEST_W, sg.QUEST_H)} if masks else {}
+    return scene, cams, fov, mk
+
+
+def test_c2_full_size_parity(vrs, oracle_mod):
+    """Config C2 at full size, in bench.py's launch configuration: 500k SH3,
+    stereo 2x2064x2208, 110 deg, foveated, masks, T_a = 32.  Pair list, ranges
+    and per-splat counts bit-exact; EVERY output pixel of both eyes within the
+    tolerances; workload counters equal."""
+    scene, cams, fov, mk = _quest_workload(2, 500_000, 1.0, True, 32, True)
+    r, o, g, oi = render_both(vrs, oracle_mod, scene, cams, fov, T=32, masks=mk, max_pairs=6 << 20)
+    assert_lists_equal(r, o)
+    assert_images_close(g, oi)
+    st, ost = r.stats(), o.stats()
+    for k in ("pairs", "samples", "contributions", "overflow_samples", "work_items", "visible_splats"):
+        assert st[k] == ost[k], (k, st[k], ost[k])
+    assert abs(st["terminated_samples"] - ost["terminated_samples"]) <= 1e-4 * ost["samples"]
+    assert abs(st["evaluations"] - ost["evaluations"]) <= 1e-4 * ost["evaluations"]
+
+
+def test_c3_full_size_sampled_parity(vrs, oracle_mod):
+    """Config C3 at full size (3M Gaussians, stereo, no foveation, T_a = 16):
+    pair list bit-exact, 20k sampled output pixels within tolerance."""
+    scene, cams, fov, mk = _quest_workload(3, 3_000_000, (1 / 6) ** 0.5, False, 16, False)
+    r, o, g, _ = render_both(vrs, oracle_mod, scene, cams, None, T=16, max_pairs=16 << 20, oracle_render=False)
+    k, v = r.vrs_debug_pairs(True)
+    ok, ov = o.pairs(True)
+    assert np.array_equal(k, ok) and np.array_equal(v, ov)
+    assert np.array_equal(r.vrs_debug_ranges(), o.ranges())
+    rs = np.random.default_rng(0)
+    n = 20000
+    vxy = np.stack([rs.integers(0, 2, n), rs.integers(0, sg.QUEST_W, n), rs.integers(0, sg.QUEST_H, n)], 1)
+    orgba, odep = o.render_pixels(vxy)
+    grgba = np.stack([g[vv][0][yy, xx] for vv, xx, yy in vxy])
+    gdep = np.array([g[vv][1][yy, xx] for vv, xx, yy in vxy])
+    assert np.abs(grgba - orgba).max() <= RGB_TOL
+    assert (np.abs(gdep - odep) - DEPTH_REL * np.abs(odep)).max() <= 1e-6
