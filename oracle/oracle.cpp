@@ -143,6 +143,27 @@ static inline float chart_num(const float* e1, const float* e2, const float* C, 
     return std::fmaf(ex, cx, ey * cy);
 }
 
+/* alpha = min(0.99, sigma * exp(-q/2)) with q = num / s^2, in the
+ * contract's deterministic binary32 form (DESIGN reading R9): exp(-q/2) =
+ * 2^x, x = (num * -0.5 log2 e) / s^2, split x = n + f (n = floor x), 2^f by a
+ * fixed degree-5 polynomial (relative error 1.5e-7), scaled by 2^n exactly.
+ * Transmittance T_k = T_{k-1} * (1 - alpha_k) is then identical on every
+ * implementation, so the T < 1e-4 termination decision is exact. */
+static inline float alpha_of(float num, float ss, float sigma) {
+    float x = std::fmax((num * -0.72134752f) / ss, -64.0f);  // NaN/-inf guard (s*s underflow)
+    float fl = std::floor(x);
+    float f = x - fl;
+    float p = 0.00187757565f;
+    p = std::fmaf(p, f, 0.00898934249f);
+    p = std::fmaf(p, f, 0.0558263175f);
+    p = std::fmaf(p, f, 0.240153611f);
+    p = std::fmaf(p, f, 0.693153083f);
+    p = std::fmaf(p, f, 0.99999994f);
+    float e = std::ldexp(p, (int)fl);
+    float a = sigma * e;
+    return a < 0.99f ? a : 0.99f;
+}
+
 /* 3x3 symmetric (xx,xy,xz,yy,yz,zz) conjugation W S W^T, R6 "3x3 products":
  * T = W*S first, then T*W^T, each entry a dot3. */
 static void conj3(const float* W, const float* S6, float* out6) {
@@ -523,7 +544,7 @@ struct SampleStats { int64_t evals = 0, contribs = 0, overflow = 0, term = 0; };
  * sorted by (tau, g); overflow pops the minimum and blends it
  * front-to-back (Eq.2 with product transmittance, L2); stop once T < 1e-4,
  * checked after blending (L11); drain at stream end. */
-struct WEnt { float tau; uint32_t g; double alpha; };
+struct WEnt { float tau; uint32_t g; float alpha; };
 
 static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, float ys, SampleStats& st) {
     const ViewState& vs = O.views[view];
@@ -534,15 +555,16 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
     const int K = O.p.window_k;
     uint32_t b = O.ranges[2 * gtile], e = O.ranges[2 * gtile + 1];
     std::vector<WEnt> win;
-    double T = 1.0, C[3] = {0, 0, 0}, D = 0.0;
+    float T = 1.0f;  // transmittance: binary32 product (exact decision, R9)
+    double C[3] = {0, 0, 0}, D = 0.0;
     bool done = false, overflowed = false;
     auto blend = [&](const WEnt& w) {
         const Splat& sp = vs.splats[w.g];
-        double wt = w.alpha * T;
+        double wt = (double)w.alpha * (double)T;
         for (int c = 0; c < 3; c++) C[c] += (double)sp.rgb[c] * wt;
         D += (double)w.tau * dn * wt;
-        T *= (1.0 - w.alpha);
-        if (T < 1e-4) done = true;
+        T = T * (1.0f - w.alpha);
+        if (T < 1e-4f) done = true;
     };
     for (uint32_t i = b; i < e && !done; i++) {
         st.evals++;
@@ -553,8 +575,7 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
         float num = chart_num(sp.e1, sp.e2, sp.C, dray);
         float ss = s * s;
         if (!(num <= sp.qcut * ss)) continue;  // alpha < 1/255, division-free (R3)
-        double q = (double)num / ((double)s * (double)s);
-        double alpha = std::min(0.99, (double)sp.sigma * std::exp(-0.5 * q));
+        float alpha = alpha_of(num, ss, sp.sigma);  // P:254, L10, R9
         float den = quad3(sp.A, x, y, 1.0f);
         float dtb = std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2]));
         float tau = dtb / den;  // depth of max density along this pixel's ray
@@ -576,10 +597,10 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
     if (overflowed) st.overflow++;
     if (done) st.term++;
     Px out;
-    out.r = C[0] + T * O.p.background[0];
-    out.g = C[1] + T * O.p.background[1];
-    out.b = C[2] + T * O.p.background[2];
-    out.a = 1.0 - T;
+    out.r = C[0] + (double)T * O.p.background[0];
+    out.g = C[1] + (double)T * O.p.background[1];
+    out.b = C[2] + (double)T * O.p.background[2];
+    out.a = 1.0 - (double)T;
     out.d = D;
     return out;
 }
@@ -998,8 +1019,7 @@ int orc_render_bruteforce(void* h, int view, float* rgba, float* depth) {
                 float dray[3] = {x, y, 1.0f};
                 float num = chart_num(sp.e1, sp.e2, sp.C, dray);
                 if (!(num <= sp.qcut * (s * s))) continue;
-                double q = (double)num / ((double)s * (double)s);
-                double alpha = std::min(0.99, (double)sp.sigma * std::exp(-0.5 * q));
+                float alpha = alpha_of(num, s * s, sp.sigma);
                 float den = quad3(sp.A, x, y, 1.0f);
                 float dtb = std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2]));
                 all.push_back(WEnt{std::fmax(dtb / den, -1e30f) + 0.0f, (uint32_t)g, alpha});
@@ -1007,20 +1027,21 @@ int orc_render_bruteforce(void* h, int view, float* rgba, float* depth) {
             std::stable_sort(all.begin(), all.end(), [](const WEnt& a, const WEnt& c) {
                 return a.tau < c.tau || (a.tau == c.tau && a.g < c.g);
             });
-            double T = 1.0, C[3] = {0, 0, 0}, D = 0.0;
+            float T = 1.0f;
+            double C[3] = {0, 0, 0}, D = 0.0;
             for (const WEnt& w : all) {
                 const Splat& sp = vs.splats[w.g];
-                double wt = w.alpha * T;
+                double wt = (double)w.alpha * (double)T;
                 for (int c = 0; c < 3; c++) C[c] += (double)sp.rgb[c] * wt;
                 D += (double)w.tau * dn * wt;
-                T *= (1.0 - w.alpha);
-                if (T < 1e-4) break;
+                T = T * (1.0f - w.alpha);
+                if (T < 1e-4f) break;
             }
             size_t k = (size_t)j * v.width + i;
-            rgba[4 * k + 0] = (float)(C[0] + T * O.p.background[0]);
-            rgba[4 * k + 1] = (float)(C[1] + T * O.p.background[1]);
-            rgba[4 * k + 2] = (float)(C[2] + T * O.p.background[2]);
-            rgba[4 * k + 3] = (float)(1.0 - T);
+            rgba[4 * k + 0] = (float)(C[0] + (double)T * O.p.background[0]);
+            rgba[4 * k + 1] = (float)(C[1] + (double)T * O.p.background[1]);
+            rgba[4 * k + 2] = (float)(C[2] + (double)T * O.p.background[2]);
+            rgba[4 * k + 3] = (float)(1.0 - (double)T);
             depth[k] = (float)D;
         }
     return 0;

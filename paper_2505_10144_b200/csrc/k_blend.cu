@@ -85,6 +85,23 @@ __device__ __forceinline__ float fast_ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
+// alpha = min(0.99, sigma * 2^x), x = (num * -0.5 log2 e) / s^2: the
+// contract's deterministic binary32 exp (DESIGN R9) -- the oracle evaluates the
+// identical operations, so transmittance and the T < 1e-4 stop are exact.
+__device__ __forceinline__ float alpha_of(float num, float ss, float sigma) {
+    const float x = fmaxf(__fdiv_rn(num * -0.72134752f, ss), -64.0f);  // NaN/-inf guard (s*s underflow)
+    const float fl = floorf(x);
+    const float f = x - fl;
+    float p = 0.00187757565f;
+    p = fmaf(p, f, 0.00898934249f);
+    p = fmaf(p, f, 0.0558263175f);
+    p = fmaf(p, f, 0.240153611f);
+    p = fmaf(p, f, 0.693153083f);
+    p = fmaf(p, f, 0.99999994f);
+    const float e = __int_as_float(__float_as_int(p) + ((int)fl << 23));  // p * 2^n, exact (normal range)
+    const float a = sigma * e;
+    return a < kAlphaMax ? a : kAlphaMax;
+}
 __device__ __forceinline__ float key_tau(unsigned long long key) {
     const uint32_t k = (uint32_t)(key >> 32);
     return __uint_as_float(k ^ (((int32_t)k < 0) ? 0x80000000u : 0xffffffffu));
@@ -160,7 +177,7 @@ __global__ void __launch_bounds__(kBlend, 4) k_blend(FrameParams fp, FrameBufs f
     float Tr = 1.0f, Cr = 0.0f, Cg = 0.0f, Cb = 0.0f, Dd = 0.0f;
     bool done = false;
     uint32_t hk = 0;  // byte offset of the ring head
-    uint32_t n_contrib = 0, stop_pos = re;
+    uint32_t n_contrib = 0, stop_pos = re - 1;  // entry whose insertion stopped the sample (re-1: ran out)
 
     auto blend_one = [&](unsigned long long key, float a) {
         const float4 col = __ldg(colv + (uint32_t)key);
@@ -213,8 +230,7 @@ __global__ void __launch_bounds__(kBlend, 4) k_blend(FrameParams fp, FrameBufs f
                 if (!(s > 0.0f) || !(num <= a0.w * ss)) continue;
                 // contribution: alpha (tolerance-only), tau (decision, IEEE division)
                 const float4 a3 = S.r3[j], a4 = S.r4[j], a5 = S.r5[j];
-                const float q = num * fast_rcp(ss);
-                const float alpha = fminf(kAlphaMax, a5.y * fast_ex2(-0.72134752044448170368f * q));
+                const float alpha = alpha_of(num, ss, a5.y);
                 const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
                 const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, a5.x));
                 const unsigned long long key = order_key(__fdiv_rn(dtb, den), __float_as_uint(a5.z));
