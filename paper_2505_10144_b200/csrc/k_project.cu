@@ -526,15 +526,39 @@ __global__ void __launch_bounds__(256) k_tiletest(FrameParams fp, FrameBufs fb, 
 
 // Step 3b: compaction of the kept candidates at their scanned positions:
 // the pair list in (view, g, tile row-major) emission order.
-__global__ void k_compact(FrameBufs fb, int64_t test_cap, int64_t pair_cap, uint64_t* __restrict__ keys,
-                          uint32_t* __restrict__ vals) {
+__global__ void __launch_bounds__(256) k_compact(FrameBufs fb, int64_t test_cap, int64_t pair_cap,
+                                                 uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                                 uint32_t* __restrict__ hist, int passes) {
+    // also accumulates the onesweep digit histograms of the emitted keys (fused
+    // "global histogram" pass of the sort: the keys are read here anyway)
+    __shared__ uint32_t s_h[8][256];
+    if (hist)
+        for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&s_h[0][0])[i] = 0;
+    __syncthreads();
     const int64_t total = min((int64_t)*fb.total_tests, test_cap);
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         if (!fb.tflag[t]) continue;
         const uint32_t pos = fb.tpos[t];
         if (pos < pair_cap) {
-            keys[pos] = fb.tkey[t];
+            const uint64_t k = fb.tkey[t];
+            keys[pos] = k;
             vals[pos] = fb.tval[t];
+            if (hist) {  // warp-aggregated (the top digits have few distinct values)
+                const unsigned act = __activemask();
+                const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+                for (int p = 0; p < passes; p++) {
+                    const uint32_t d = (uint32_t)(k >> (8 * p)) & 0xffu;
+                    const unsigned peers = __match_any_sync(act, d);
+                    if ((peers & lt) == 0) atomicAdd(&s_h[p][d], (uint32_t)__popc(peers));
+                }
+            }
+        }
+    }
+    if (hist) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
+            const uint32_t c = (&s_h[0][0])[i];
+            if (c) atomicAdd(&hist[i], c);
         }
     }
 }
@@ -622,8 +646,9 @@ void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cuda
 }
 
 void launch_compact(FrameBufs fb, int64_t test_cap, int64_t pair_cap, uint64_t* keys, uint32_t* vals,
-                    cudaStream_t st) {
-    k_compact<<<sm_count() * 8, 256, 0, st>>>(fb, test_cap, pair_cap, keys, vals);
+                    uint32_t* hist, int passes, cudaStream_t st) {
+    if (hist) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 8 * 256, st);
+    k_compact<<<sm_count() * 8, 256, 0, st>>>(fb, test_cap, pair_cap, keys, vals, hist, passes);
 }
 
 void launch_counts(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {

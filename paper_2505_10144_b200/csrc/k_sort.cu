@@ -52,38 +52,34 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __re
     }
 }
 
-// Exclusive scan of each pass's 256 bins (in place).
-__global__ void k_sort_hist_scan(uint32_t* hist) {
-    __shared__ uint32_t s[kRadix];
-    uint32_t* h = hist + blockIdx.x * kRadix;
-    const int t = threadIdx.x;
-    const uint32_t v = h[t];
-    s[t] = v;
-    __syncthreads();
-    for (int o = 1; o < kRadix; o <<= 1) {
-        uint32_t a = t >= o ? s[t - o] : 0u;
-        __syncthreads();
-        s[t] += a;
-        __syncthreads();
-    }
-    h[t] = s[t] - v;
-}
-
 struct OnesweepSmem {
     uint32_t wh[kWarps][kRadix];    // per-warp digit counts -> exclusive offsets
     uint32_t tstart[kRadix];        // tile-local exclusive digit offsets
     uint32_t gbase[kRadix];         // global position of the tile's first key of each digit
+    uint32_t doff[kRadix];          // global exclusive digit offsets of this pass
     uint64_t k[kSortTile];          // tile keys in digit-sorted order (staged scatter)
     uint32_t v[kSortTile];
     uint32_t tile;
 };
 
-__global__ void __launch_bounds__(kSortThreads, 2) k_onesweep(const uint64_t* __restrict__ kin,
+// 64-bit look-back status: epoch (frame/pass tag, so no per-pass memset) |
+// flag (1 = tile aggregate, 2 = inclusive prefix) | 32-bit count.
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(const uint64_t* __restrict__ kin,
                                                               const uint32_t* __restrict__ vin,
                                                               uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
                                                               const uint32_t* __restrict__ n_dev, int64_t cap,
-                                                              int pass, const uint32_t* __restrict__ digit_off,
-                                                              uint32_t* status, uint32_t* counter) {
+                                                              int pass, const uint32_t* __restrict__ hist,
+                                                              unsigned long long* status, uint32_t* counter,
+                                                              uint32_t epoch) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     OnesweepSmem& S = *reinterpret_cast<OnesweepSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -91,6 +87,28 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_onesweep(const uint64_t* __
     const int64_t n = min((int64_t)*n_dev, cap);
     const int64_t ntiles = (n + kSortTile - 1) / kSortTile;
     const uint32_t lt_mask = (1u << lane) - 1u;
+    const unsigned long long ep = (unsigned long long)epoch << 34;
+    const unsigned long long kAgg = ep | (1ull << 32), kPre = ep | (2ull << 32);
+    // global digit offsets of this pass (exclusive scan of the histogram)
+    {
+        const uint32_t h = hist[pass * kRadix + tid];
+        S.doff[tid] = h;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t run = 0;
+            for (int c = 0; c < kRadix; c += 32) {
+                const uint32_t v0 = S.doff[c + lane];
+                uint32_t inc = v0;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                    if (lane >= o) inc += y;
+                }
+                S.doff[c + lane] = run + inc - v0;
+                run += __shfl_sync(0xffffffffu, inc, 31);
+            }
+        }
+    }
     while (true) {
         if (tid == 0) S.tile = atomicAdd(counter, 1u);
         for (int i = tid; i < kWarps * kRadix; i += kSortThreads) (&S.wh[0][0])[i] = 0;
@@ -99,14 +117,11 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_onesweep(const uint64_t* __
         if (tile >= ntiles) break;
         const int64_t wbase = tile * kSortTile + (int64_t)warp * (kSortItems * 32);
         uint64_t key[kSortItems];
-        uint32_t val[kSortItems];
         uint32_t rank[kSortItems];
 #pragma unroll
         for (int i = 0; i < kSortItems; i++) {
             const int64_t idx = wbase + i * 32 + lane;
-            const bool ok = idx < n;
-            key[i] = ok ? kin[idx] : ~0ull;
-            val[i] = ok ? vin[idx] : 0u;
+            key[i] = (idx < n) ? kin[idx] : ~0ull;
         }
         // warp-local stable ranking in (item, lane) order
 #pragma unroll
@@ -122,7 +137,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_onesweep(const uint64_t* __
             rank[i] = old + __popc(peers & lt_mask);
         }
         __syncthreads();
-        // per digit (thread d): exclusive over warps, tile total; publish; look back
+        // per digit (thread d): exclusive over warps and tile total; publish the aggregate early
         const int d = tid;  // kSortThreads == kRadix
         uint32_t tot = 0;
 #pragma unroll
@@ -131,38 +146,11 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_onesweep(const uint64_t* __
             S.wh[w][d] = tot;
             tot += c;
         }
-        uint32_t* st = status + (size_t)tile * kRadix + d;
-        uint32_t excl = 0;
-        if (tile == 0) {
-            st_release32(st, kStPre | tot);
-        } else {
-            st_release32(st, kStAgg | tot);
-            // decoupled look-back, four predecessors in flight per round trip
-            int64_t j = tile - 1;
-            while (true) {
-                uint32_t sv[4];
-#pragma unroll
-                for (int k = 0; k < 4; k++)
-                    sv[k] = (j - k >= 0) ? ld_acquire32(status + (size_t)(j - k) * kRadix + d) : kStPre;
-                int k = 0;
-                bool fin = false;
-#pragma unroll
-                for (; k < 4; k++) {
-                    const uint32_t f = sv[k] & ~kStMask;
-                    if (f == 0) break;
-                    excl += sv[k] & kStMask;
-                    if (f == kStPre) { fin = true; break; }
-                }
-                if (fin) break;
-                j -= k;
-            }
-            st_release32(st, kStPre | (excl + tot));
-        }
-        S.gbase[d] = digit_off[pass * kRadix + d] + excl;
-        // tile-local exclusive scan of the digit totals
+        unsigned long long* st = status + (size_t)tile * kRadix + d;
+        st_status(st, (tile == 0 ? kPre : kAgg) | tot);
         S.tstart[d] = tot;
         __syncthreads();
-        if (warp == 0) {
+        if (warp == 0) {  // tile-local exclusive scan of the digit totals
             uint32_t run = 0;
             for (int c = 0; c < kRadix; c += 32) {
                 const uint32_t v0 = S.tstart[c + lane];
@@ -177,7 +165,7 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_onesweep(const uint64_t* __
             }
         }
         __syncthreads();
-        // stage keys in digit-sorted order, then write runs coalesced
+        // stage keys/values in digit-sorted order (frees the registers before the look-back)
 #pragma unroll
         for (int i = 0; i < kSortItems; i++) {
             const int64_t idx = wbase + i * 32 + lane;
@@ -185,9 +173,33 @@ __global__ void __launch_bounds__(kSortThreads, 2) k_onesweep(const uint64_t* __
                 const uint32_t dd = (uint32_t)(key[i] >> shift) & 0xffu;
                 const uint32_t lp = S.tstart[dd] + S.wh[warp][dd] + rank[i];
                 S.k[lp] = key[i];
-                S.v[lp] = val[i];
+                S.v[lp] = vin[idx];
             }
         }
+        // decoupled look-back for digit d, four predecessors in flight per round trip
+        uint32_t excl = 0;
+        if (tile > 0) {
+            int64_t j = tile - 1;
+            while (true) {
+                unsigned long long sv[4];
+#pragma unroll
+                for (int k = 0; k < 4; k++)
+                    sv[k] = (j - k >= 0) ? ld_status(status + (size_t)(j - k) * kRadix + d) : kPre;
+                int k = 0;
+                bool fin = false;
+#pragma unroll
+                for (; k < 4; k++) {
+                    const unsigned long long e = sv[k] & ~0xffffffffull;
+                    if (e != kAgg && e != kPre) break;  // not yet published in this epoch
+                    excl += (uint32_t)sv[k];
+                    if (e == kPre) { fin = true; break; }
+                }
+                if (fin) break;
+                j -= k;
+            }
+            st_status(st, kPre | (excl + tot));
+        }
+        S.gbase[d] = S.doff[d] + excl;
         __syncthreads();
         const int cnt = (int)min((int64_t)kSortTile, n - tile * kSortTile);
         for (int i = tid; i < cnt; i += kSortThreads) {
@@ -210,7 +222,7 @@ __global__ void k_copy_pairs(const uint64_t* __restrict__ ks, const uint32_t* __
     }
 }
 
-size_t sort_status_words(int64_t cap) { return (size_t)((cap + kSortTile - 1) / kSortTile + 1) * kRadix; }
+size_t sort_status_words(int64_t cap) { return 2 * ((size_t)((cap + kSortTile - 1) / kSortTile + 1) * kRadix); }
 
 static int g_num_sms = 0;
 static int num_sms() {
@@ -224,27 +236,31 @@ static int num_sms() {
 }
 
 void launch_sort(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, const uint32_t* n_dev,
-                 int64_t cap, int key_bits, SortScratch s, cudaStream_t st) {
+                 int64_t cap, int key_bits, SortScratch s, cudaStream_t st, bool hist_ready) {
     const int passes = (key_bits + 7) / 8;
     if (passes <= 0 || cap <= 0) return;
     const int sms = num_sms();
     const int64_t max_tiles = (cap + kSortTile - 1) / kSortTile;
-    cudaMemsetAsync(s.hist, 0, sizeof(uint32_t) * 8 * kRadix, st);
     cudaMemsetAsync(s.counters, 0, sizeof(uint32_t) * 8, st);
-    k_sort_hist<<<sms * 2, kSortThreads, 0, st>>>(keys, n_dev, cap, passes, s.hist);
-    k_sort_hist_scan<<<passes, kRadix, 0, st>>>(s.hist);
+    if (!hist_ready) {
+        cudaMemsetAsync(s.hist, 0, sizeof(uint32_t) * 8 * kRadix, st);
+        k_sort_hist<<<sms * 2, kSortThreads, 0, st>>>(keys, n_dev, cap, passes, s.hist);
+    }
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(OnesweepSmem));
         attr = true;
     }
-    const unsigned grid = (unsigned)std::min<int64_t>(max_tiles, (int64_t)sms * 2);
+    const unsigned grid = (unsigned)std::min<int64_t>(max_tiles, (int64_t)sms * 3);
     uint64_t *ka = keys, *kb = keys_alt;
     uint32_t *va = vals, *vb = vals_alt;
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(s.status);
     for (int p = 0; p < passes; p++) {
-        cudaMemsetAsync(s.status, 0, sizeof(uint32_t) * (size_t)max_tiles * kRadix, st);
-        k_onesweep<<<grid, kSortThreads, sizeof(OnesweepSmem), st>>>(ka, va, kb, vb, n_dev, cap, p, s.hist, s.status,
-                                                                      s.counters + p);
+        const uint32_t epoch = (++*s.epoch) & 0x3fffffffu;
+        if (epoch == 1)  // (re)start of the epoch sequence: clear stale tags once
+            cudaMemsetAsync(status, 0, sizeof(unsigned long long) * (size_t)max_tiles * kRadix, st);
+        k_onesweep<<<grid, kSortThreads, sizeof(OnesweepSmem), st>>>(ka, va, kb, vb, n_dev, cap, p, s.hist, status,
+                                                                      s.counters + p, epoch);
         std::swap(ka, kb);
         std::swap(va, vb);
     }

@@ -60,6 +60,7 @@ struct vrs_context {
     unsigned long long* d_stats = nullptr;
     uint32_t* d_scan_scratch = nullptr;
     SortScratch sort{};
+    uint32_t sort_epoch = 0;
     // per-view static setup
     int32_t* d_vis = nullptr;     // [V][max_tiles]
     uint32_t* d_sat = nullptr;    // [V][max_sat]
@@ -176,6 +177,7 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     A(dalloc(&ctx->sort.status, sort_status_words(P)));
     A(dalloc(&ctx->sort.counters, 8));
     ctx->sort.max_tiles = (P + 4095) / 4096;
+    ctx->sort.epoch = &ctx->sort_epoch;
     A(dalloc(&ctx->d_vis, (size_t)V * ctx->max_tiles_view));
     A(dalloc(&ctx->d_cls, (size_t)V * ctx->max_tiles_view));
     A(dalloc(&ctx->d_sat, (size_t)V * ctx->max_sat_view));
@@ -523,10 +525,10 @@ static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* ca
     if (tm) CK(cudaEventRecord(ctx->ev[2], st));
     launch_tiletest(fp, fb, ctx->test_cap, st);
     launch_scan(fb.tflag, fb.tpos, fb.total, fb.total_tests, ctx->test_cap, ctx->d_scan_scratch, st);
-    launch_compact(fb, ctx->test_cap, fp.pair_cap, fb.keys, fb.vals, st);
+    const int key_bits = key_bits_for(ctx->last_tiles);
+    launch_compact(fb, ctx->test_cap, fp.pair_cap, fb.keys, fb.vals, ctx->sort.hist, (key_bits + 7) / 8, st);
     if (tm) CK(cudaEventRecord(ctx->ev[3], st));
-    launch_sort(fb.keys, fb.vals, fb.keys_alt, fb.vals_alt, fb.total, fp.pair_cap, key_bits_for(ctx->last_tiles),
-                ctx->sort, st);
+    launch_sort(fb.keys, fb.vals, fb.keys_alt, fb.vals_alt, fb.total, fp.pair_cap, key_bits, ctx->sort, st, true);
     if (tm) CK(cudaEventRecord(ctx->ev[4], st));
     launch_ranges(fb.keys, fb.total, fp.pair_cap, fb.ranges, ctx->last_tiles, st);
     if (tm) CK(cudaEventRecord(ctx->ev[5], st));
@@ -654,7 +656,8 @@ vrs_status vrs_debug_pairs(vrs_context* ctx, int32_t sorted, uint64_t* keys, uin
         CK(cudaMemcpy(vals, ctx->d_vals, 4 * n, cudaMemcpyDeviceToHost));
     } else {
         // re-run the compaction (emission order) into the alternate buffers
-        launch_compact(frame_bufs(ctx), ctx->test_cap, ctx->cfg.max_pairs, ctx->d_keys_alt, ctx->d_vals_alt, st);
+        launch_compact(frame_bufs(ctx), ctx->test_cap, ctx->cfg.max_pairs, ctx->d_keys_alt, ctx->d_vals_alt, nullptr, 0,
+                       st);
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(st));
         CK(cudaMemcpy(keys, ctx->d_keys_alt, 8 * n, cudaMemcpyDeviceToHost));
@@ -718,7 +721,7 @@ vrs_status vrs_sort_pairs(vrs_context* ctx, uint64_t* keys, uint32_t* vals, int6
     uint32_t* d_n = ctx->d_misc + 4;
     CK(cudaMemcpyAsync(d_n, &nn, 4, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
-    launch_sort(keys, vals, ctx->d_keys_alt, ctx->d_vals_alt, d_n, n, key_bits, ctx->sort, st);
+    launch_sort(keys, vals, ctx->d_keys_alt, ctx->d_vals_alt, d_n, n, key_bits, ctx->sort, st, false);
     CK(cudaGetLastError());
     return VRS_OK;
 }

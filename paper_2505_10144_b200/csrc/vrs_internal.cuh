@@ -103,19 +103,21 @@ void launch_scan(const uint32_t* in, uint32_t* out, uint32_t* total, const uint3
                  uint32_t* scratch, cudaStream_t st);
 size_t scan_scratch_words(int64_t n);
 void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st);
+// hist (optional): [8][256] digit histograms of the emitted keys for `passes` 8-bit digits
 void launch_compact(FrameBufs fb, int64_t test_cap, int64_t pair_cap, uint64_t* keys, uint32_t* vals,
-                    cudaStream_t st);
+                    uint32_t* hist, int passes, cudaStream_t st);
 void launch_counts(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st);
 struct SortScratch {
-    uint32_t* hist;          // [8][256]
-    uint32_t* status;        // [passes][max_tiles][256]
+    uint32_t* hist;          // [8][256] digit histograms (may be filled by k_compact)
+    uint32_t* status;        // [max_tiles][256] u64 epoch-tagged look-back words
     uint32_t* counters;      // [8]
+    uint32_t* epoch;         // host-side pass counter (tags status words; no per-pass memset)
     int64_t max_tiles;
 };
 size_t sort_status_words(int64_t cap);
 // Sort n_dev (device count, capped at cap) pairs by key bits [0, key_bits); result in (keys, vals).
 void launch_sort(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, const uint32_t* n_dev,
-                 int64_t cap, int key_bits, SortScratch s, cudaStream_t st);
+                 int64_t cap, int key_bits, SortScratch s, cudaStream_t st, bool hist_ready);
 void launch_ranges(const uint64_t* keys, const uint32_t* n_dev, int64_t cap, uint32_t* ranges, int64_t n_tiles,
                    cudaStream_t st);
 void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
