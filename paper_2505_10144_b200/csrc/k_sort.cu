@@ -33,7 +33,10 @@ __device__ __forceinline__ uint32_t ld_acquire32(const uint32_t* p) {
 }
 }  // namespace
 
-// Digit histograms of every pass in one read of the keys.
+// Digit histograms of every pass in one read of the keys.  Each thread reads
+// 8 consecutive keys and run-length aggregates equal digits in registers
+// before touching shared memory (the high digits -- view/tile rows, depth
+// exponent -- repeat along the emission order and would serialise atomics).
 __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __restrict__ keys,
                                                             const uint32_t* __restrict__ n_dev, int64_t cap,
                                                             int passes, uint32_t* hist) {
@@ -41,9 +44,39 @@ __global__ void __launch_bounds__(kSortThreads) k_sort_hist(const uint64_t* __re
     for (int i = threadIdx.x; i < 8 * kRadix; i += blockDim.x) (&s_h[0][0])[i] = 0;
     __syncthreads();
     const int64_t n = min((int64_t)*n_dev, cap);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint64_t k = keys[i];
-        for (int p = 0; p < passes; p++) atomicAdd(&s_h[p][(k >> (8 * p)) & 0xff], 1u);
+    constexpr int R = 8;
+    for (int64_t base = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * R; base < n;
+         base += (int64_t)gridDim.x * blockDim.x * R) {
+        uint64_t k[R];
+        if (base + R <= n && (reinterpret_cast<uintptr_t>(keys) & 15) == 0) {
+            const ulonglong2* p = reinterpret_cast<const ulonglong2*>(keys + base);
+#pragma unroll
+            for (int i = 0; i < R / 2; i++) {
+                const ulonglong2 q = p[i];
+                k[2 * i] = q.x;
+                k[2 * i + 1] = q.y;
+            }
+        } else {
+#pragma unroll
+            for (int i = 0; i < R; i++) k[i] = (base + i < n) ? keys[base + i] : 0ull;
+        }
+        const int m = (int)min((int64_t)R, n - base);
+        for (int p = 0; p < passes; p++) {
+            uint32_t cur = (uint32_t)(k[0] >> (8 * p)) & 0xffu, run = 1;
+#pragma unroll
+            for (int i = 1; i < R; i++) {
+                if (i >= m) break;
+                const uint32_t d = (uint32_t)(k[i] >> (8 * p)) & 0xffu;
+                if (d == cur) {
+                    run++;
+                } else {
+                    atomicAdd(&s_h[p][cur], run);
+                    cur = d;
+                    run = 1;
+                }
+            }
+            atomicAdd(&s_h[p][cur], run);
+        }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < passes * kRadix; i += blockDim.x) {

@@ -526,9 +526,9 @@ static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* ca
     launch_tiletest(fp, fb, ctx->test_cap, st);
     launch_scan(fb.tflag, fb.tpos, fb.total, fb.total_tests, ctx->test_cap, ctx->d_scan_scratch, st);
     const int key_bits = key_bits_for(ctx->last_tiles);
-    launch_compact(fb, ctx->test_cap, fp.pair_cap, fb.keys, fb.vals, ctx->sort.hist, (key_bits + 7) / 8, st);
+    launch_compact(fb, ctx->test_cap, fp.pair_cap, fb.keys, fb.vals, nullptr, 0, st);
     if (tm) CK(cudaEventRecord(ctx->ev[3], st));
-    launch_sort(fb.keys, fb.vals, fb.keys_alt, fb.vals_alt, fb.total, fp.pair_cap, key_bits, ctx->sort, st, true);
+    launch_sort(fb.keys, fb.vals, fb.keys_alt, fb.vals_alt, fb.total, fp.pair_cap, key_bits, ctx->sort, st, false);
     if (tm) CK(cudaEventRecord(ctx->ev[4], st));
     launch_ranges(fb.keys, fb.total, fp.pair_cap, fb.ranges, ctx->last_tiles, st);
     if (tm) CK(cudaEventRecord(ctx->ev[5], st));
