@@ -143,14 +143,18 @@ static inline float chart_num(const float* e1, const float* e2, const float* C, 
     return std::fmaf(ex, cx, ey * cy);
 }
 
-/* alpha = min(0.99, sigma * exp(-q/2)) with q = num / s^2, in the
- * contract's deterministic binary32 form (DESIGN reading R9): exp(-q/2) =
- * 2^x, x = (num * -0.5 log2 e) / s^2, split x = n + f (n = floor x), 2^f by a
- * fixed degree-5 polynomial (relative error 1.5e-7), scaled by 2^n exactly.
- * Transmittance T_k = T_{k-1} * (1 - alpha_k) is then identical on every
- * implementation, so the T < 1e-4 termination decision is exact. */
-static inline float alpha_of(float num, float ss, float sigma) {
-    float x = std::fmax((num * -0.72134752f) / ss, -64.0f);  // NaN/-inf guard (s*s underflow)
+/* Per-sample alpha and depth in the contract's binary32 form (DESIGN R9):
+ * one IEEE reciprocal r = 1/(s^2 * den) serves both quotients,
+ *   x   = (num * -0.5 log2 e) * (den * r)      (= -q/2 log2 e, q = num/s^2)
+ *   tau = dtb * (s^2 * r)                       (= dtb / den, StopThePop depth)
+ * alpha = min(0.99, sigma * 2^x), 2^x = 2^n * p(f), n = floor x,
+ * p a fixed degree-5 polynomial (relative error 1.5e-7), scaled exactly.  All
+ * implementations therefore produce identical alpha and transmittance
+ * T_k = T_{k-1} * (1 - alpha_k), so the T < 1e-4 stop is an exact decision. */
+struct SampleAT { float alpha, tau; };
+static inline SampleAT sample_alpha_tau(float num, float ss, float den, float dtb, float sigma) {
+    float r = 1.0f / (ss * den);
+    float x = std::fmax((num * -0.72134752f) * (den * r), -64.0f);  // NaN/-inf guard
     float fl = std::floor(x);
     float f = x - fl;
     float p = 0.00187757565f;
@@ -161,7 +165,10 @@ static inline float alpha_of(float num, float ss, float sigma) {
     p = std::fmaf(p, f, 0.99999994f);
     float e = std::ldexp(p, (int)fl);
     float a = sigma * e;
-    return a < 0.99f ? a : 0.99f;
+    SampleAT o;
+    o.alpha = a < 0.99f ? a : 0.99f;
+    o.tau = std::fmax(dtb * (ss * r), -1e30f) + 0.0f;  // canonical: NaN/-inf -> -1e30, -0 -> +0 (R4)
+    return o;
 }
 
 /* 3x3 symmetric (xx,xy,xz,yy,yz,zz) conjugation W S W^T, R6 "3x3 products":
@@ -575,11 +582,11 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
         float num = chart_num(sp.e1, sp.e2, sp.C, dray);
         float ss = s * s;
         if (!(num <= sp.qcut * ss)) continue;  // alpha < 1/255, division-free (R3)
-        float alpha = alpha_of(num, ss, sp.sigma);  // P:254, L10, R9
         float den = quad3(sp.A, x, y, 1.0f);
         float dtb = std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2]));
-        float tau = dtb / den;  // depth of max density along this pixel's ray
-        tau = std::fmax(tau, -1e30f) + 0.0f;  // canonical: NaN/-inf -> -1e30, -0 -> +0 (DESIGN R4)
+        SampleAT at = sample_alpha_tau(num, ss, den, dtb, sp.sigma);  // P:254, L10, R9
+        float alpha = at.alpha;
+        float tau = at.tau;  // depth of max density along this pixel's ray (O10)
         st.contribs++;
         WEnt ent{tau, g, alpha};
         auto pos = std::upper_bound(win.begin(), win.end(), ent, [](const WEnt& a, const WEnt& c) {
@@ -1019,10 +1026,10 @@ int orc_render_bruteforce(void* h, int view, float* rgba, float* depth) {
                 float dray[3] = {x, y, 1.0f};
                 float num = chart_num(sp.e1, sp.e2, sp.C, dray);
                 if (!(num <= sp.qcut * (s * s))) continue;
-                float alpha = alpha_of(num, s * s, sp.sigma);
                 float den = quad3(sp.A, x, y, 1.0f);
                 float dtb = std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2]));
-                all.push_back(WEnt{std::fmax(dtb / den, -1e30f) + 0.0f, (uint32_t)g, alpha});
+                SampleAT at = sample_alpha_tau(num, s * s, den, dtb, sp.sigma);
+                all.push_back(WEnt{at.tau, (uint32_t)g, at.alpha});
             }
             std::stable_sort(all.begin(), all.end(), [](const WEnt& a, const WEnt& c) {
                 return a.tau < c.tau || (a.tau == c.tau && a.g < c.g);
@@ -1103,7 +1110,9 @@ float orc_sample_depth(void* h, int view, int64_t g, float xs, float ys) {
     float x = (xs - vs.v.cx) / vs.v.fx, y = (ys - vs.v.cy) / vs.v.fy;
     float den = quad3(sp.A, x, y, 1.0f);
     float dtb = std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2]));
-    return dtb / den;
+    float s = std::fmaf(sp.u[0], x, std::fmaf(sp.u[1], y, sp.u[2]));
+    float d[3] = {x, y, 1.0f};
+    return sample_alpha_tau(chart_num(sp.e1, sp.e2, sp.C, d), s * s, den, dtb, sp.sigma).tau;
 }
 
 }  // extern "C"

@@ -85,11 +85,14 @@ __device__ __forceinline__ float fast_ex2(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
     return r;
 }
-// alpha = min(0.99, sigma * 2^x), x = (num * -0.5 log2 e) / s^2: the
-// contract's deterministic binary32 exp (DESIGN R9) -- the oracle evaluates the
+// Per-sample alpha and depth (DESIGN R9): one IEEE reciprocal of s^2*den
+// serves x = -q/2 log2 e and tau = dtb/den; alpha = min(0.99, sigma 2^x) with
+// the contract's deterministic binary32 exp2 -- the oracle evaluates the
 // identical operations, so transmittance and the T < 1e-4 stop are exact.
-__device__ __forceinline__ float alpha_of(float num, float ss, float sigma) {
-    const float x = fmaxf(__fdiv_rn(num * -0.72134752f, ss), -64.0f);  // NaN/-inf guard (s*s underflow)
+__device__ __forceinline__ float alpha_tau(float num, float ss, float den, float dtb, float sigma, float& tau) {
+    const float r = __frcp_rn(ss * den);
+    const float x = fmaxf((num * -0.72134752f) * (den * r), -64.0f);  // NaN/-inf guard
+    tau = dtb * (ss * r);
     const float fl = floorf(x);
     const float f = x - fl;
     float p = 0.00187757565f;
@@ -230,10 +233,11 @@ __global__ void __launch_bounds__(kBlend, 4) k_blend(FrameParams fp, FrameBufs f
                 if (!(s > 0.0f) || !(num <= a0.w * ss)) continue;
                 // contribution: alpha (tolerance-only), tau (decision, IEEE division)
                 const float4 a3 = S.r3[j], a4 = S.r4[j], a5 = S.r5[j];
-                const float alpha = alpha_of(num, ss, a5.y);
                 const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
                 const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, a5.x));
-                const unsigned long long key = order_key(__fdiv_rn(dtb, den), __float_as_uint(a5.z));
+                float tau;
+                const float alpha = alpha_tau(num, ss, den, dtb, a5.y, tau);
+                const unsigned long long key = order_key(tau, __float_as_uint(a5.z));
                 if (kCounters) n_contrib++;
                 // insert, then pop the minimum of the K+1 entries
                 const unsigned long long kh = WK(hk);
