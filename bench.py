@@ -150,6 +150,7 @@ def cpu_baseline(scene, cams, fov, masks, T, budget_s=15.0):
     n = 512
     t_pix, done = 0.0, 0
     while t_prep + t_pix < budget_s and done < total_px:
+        n = min(n, total_px - done)
         vxy = np.stack([rs.integers(0, len(cams), n), rs.integers(0, cams[0].width, n),
                         rs.integers(0, cams[0].height, n)], 1)
         t0 = time.perf_counter()
@@ -177,7 +178,8 @@ def run_reference(args):
         if s >= args.warmup:
             vals.append(r)
     v = statistics.median([r["value"] for r in vals])
-    line = {"metric": METRIC, "value": v, "unit": vals[0]["unit"], "n_gpus": args.gpus, "steps": args.steps,
+    line = {"metric": METRIC if args.config == "c2" else METRIC + f" [{args.config}]", "value": v,
+            "unit": vals[0]["unit"], "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": {"workload": args.config, "desc": cfg["desc"]},
@@ -310,7 +312,10 @@ def main():
         n_views = len(cams)
         key_bits = 32 + int(np.ceil(np.log2(max(2, sum(((c.width + cfg["T"] - 1) // cfg["T"]) *
                                                         ((c.height + cfg["T"] - 1) // cfg["T"]) for c in cams)))))
-        launches_per_step = 7 + 2 + (key_bits + 7) // 8 + (1 if ((key_bits + 7) // 8) % 2 else 0)
+        # k_cull, k_preprocess, k_scan, k_fill_sid, k_tiletest, k_scan, k_compact, k_sort_hist,
+        # passes x k_onesweep (+ k_copy_pairs if odd), k_ranges, k_blend, k_compose
+        passes = (key_bits + 7) // 8
+        launches_per_step = 11 + passes + (passes % 2)
         line = {
             "metric": METRIC if args.config == "c2" else METRIC + f" [{args.config}]",
             "value": world * 1000.0 / ms_max,

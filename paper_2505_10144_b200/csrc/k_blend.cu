@@ -367,11 +367,11 @@ __global__ void k_compose(FrameParams fp, FrameBufs fb, float* __restrict__ rgba
     int vi = 0;
     while (vi + 1 < fp.n_views && gi >= fp.v[vi + 1].low_off) vi++;
     const ViewParams& v = fp.v[vi];
-    const int64_t k = gi - v.low_off;
-    const int gx = (int)(k % v.low_w), gy = (int)(k / v.low_w);
+    const uint32_t k = (uint32_t)(gi - v.low_off);
+    const int gx = (int)(k % (uint32_t)v.low_w), gy = (int)(k / (uint32_t)v.low_w);
     if (2 * gy >= v.H) return;  // gap between views' low-res planes
-    const int T = fp.T, i0 = 2 * gx, j0 = 2 * gy;
-    const int c = v.cls[(j0 / T) * v.tw + (i0 / T)];
+    const int tsh = (fp.T == 32) ? 5 : 4, i0 = 2 * gx, j0 = 2 * gy;  // T is 16 or 32
+    const int c = v.cls[(j0 >> tsh) * v.tw + (i0 >> tsh)];
     if (c == kHigh || c == kHybrid) return;
     float4 outc[2][2];
     float outd[2][2];
@@ -396,7 +396,7 @@ __global__ void k_compose(FrameParams fp, FrameBufs fb, float* __restrict__ rgba
                 const int pi = (di == 0) ? i0 - 1 : (di == 1 ? i0 : i0 + 2);
                 const int pj = (dj == 0) ? j0 - 1 : (dj == 1 ? j0 : j0 + 2);
                 bool good = pi >= 0 && pj >= 0 && pi < v.W && pj < v.H;
-                if (good) good = v.cls[(pj / T) * v.tw + (pi / T)] == kLow;
+                if (good) good = v.cls[(pj >> tsh) * v.tw + (pi >> tsh)] == kLow;
                 ok[dj][di] = good;
                 if (good) {
                     const size_t li = (size_t)v.low_off + (size_t)(pj >> 1) * v.low_w + (pi >> 1);

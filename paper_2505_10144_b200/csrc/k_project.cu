@@ -431,7 +431,8 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(SceneDev sc, FrameParams 
     const uint32_t nc = *fb.cand_count;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
         const uint32_t sidx = fb.cand[i];
-        const int vi = (int)(sidx / N);
+        int vi = 0;  // view = number of view blocks of N below sidx (no 64-bit division)
+        while (vi + 1 < fp.n_views && (int64_t)sidx >= (int64_t)(vi + 1) * N) vi++;
         const int64_t g = (int64_t)sidx - (int64_t)vi * N;
         const ViewParams& v = fp.v[vi];
         const float4 m4 = __ldg(&sc.mu[g]);
@@ -487,7 +488,8 @@ __global__ void __launch_bounds__(256) k_tiletest(FrameParams fp, FrameBufs fb, 
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t sidx = fb.sid[t];
         const uint32_t l = (uint32_t)(t - fb.toff[sidx]);
-        const int vi = (int)(sidx / fp.N);
+        int vi = 0;
+        while (vi + 1 < fp.n_views && sidx >= (int64_t)(vi + 1) * fp.N) vi++;
         const ViewParams& v = fp.v[vi];
         const float4* rec = fb.rec + (size_t)sidx * kRecF4;
         const float4 r0 = __ldg(rec + 0), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2), r5 = __ldg(rec + 5),

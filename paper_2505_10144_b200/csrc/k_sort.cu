@@ -209,19 +209,20 @@ __global__ void __launch_bounds__(kSortThreads, 3) k_onesweep(const uint64_t* __
                 S.v[lp] = vin[idx];
             }
         }
-        // decoupled look-back for digit d, four predecessors in flight per round trip
+        // decoupled look-back for digit d, kLook predecessors in flight per round trip
         uint32_t excl = 0;
         if (tile > 0) {
+            constexpr int kLook = 16;
             int64_t j = tile - 1;
             while (true) {
-                unsigned long long sv[4];
+                unsigned long long sv[kLook];
 #pragma unroll
-                for (int k = 0; k < 4; k++)
+                for (int k = 0; k < kLook; k++)
                     sv[k] = (j - k >= 0) ? ld_status(status + (size_t)(j - k) * kRadix + d) : kPre;
                 int k = 0;
                 bool fin = false;
 #pragma unroll
-                for (; k < 4; k++) {
+                for (; k < kLook; k++) {
                     const unsigned long long e = sv[k] & ~0xffffffffull;
                     if (e != kAgg && e != kPre) break;  // not yet published in this epoch
                     excl += (uint32_t)sv[k];
