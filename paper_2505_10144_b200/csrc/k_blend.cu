@@ -37,7 +37,7 @@ void launch_ranges(const uint64_t* keys, const uint32_t* n_dev, int64_t cap, uin
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    k_ranges<<<sms * 4, 256, 0, st>>>(keys, n_dev, cap, ranges, n_tiles);
+    k_ranges<<<sms * 16, 256, 0, st>>>(keys, n_dev, cap, ranges, n_tiles);
 }
 
 namespace {

@@ -342,21 +342,20 @@ __device__ void sh_color(const SceneDev& sc, int64_t g, int64_t N, int ncoef, fl
             basis[15] = -0.5900435899266435f * dx * (xx - 3.0f * yy);
         }
     }
-    // all coefficients into registers (compile-time indices: no local memory)
-    float shv[48];
+    // accumulate chunk by chunk (4 floats of the coefficient-major RGB array at
+    // a time; all indices compile-time: no local memory, few live registers)
     const float4* src = sc.sh + (size_t)g * sc.sh_chunks;
-#pragma unroll
-    for (int c4 = 0; c4 < 12; c4++) {
-        const float4 q = (c4 < sc.sh_chunks) ? __ldg(src + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
-        shv[4 * c4] = q.x; shv[4 * c4 + 1] = q.y; shv[4 * c4 + 2] = q.z; shv[4 * c4 + 3] = q.w;
-    }
     float acc[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
-    for (int k = 0; k < 16; k++) {
-        if (k < ncoef) {
-            acc[0] = fmaf(basis[k], shv[3 * k], acc[0]);
-            acc[1] = fmaf(basis[k], shv[3 * k + 1], acc[1]);
-            acc[2] = fmaf(basis[k], shv[3 * k + 2], acc[2]);
+    for (int c4 = 0; c4 < 12; c4++) {
+        if (c4 < sc.sh_chunks) {
+            const float4 q = __ldg(src + c4);
+            const float qv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int f = 4 * c4 + k;  // coefficient f / 3, channel f % 3
+                if (f / 3 < ncoef) acc[f % 3] = fmaf(basis[f / 3], qv[k], acc[f % 3]);
+            }
         }
     }
 #pragma unroll
@@ -391,7 +390,9 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
         m4 = __ldg(&sc.mu[g]);
         smax = __ldg(&sc.cov[N + g]).w;
     }
-    const int lane = threadIdx.x & 31;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __shared__ uint32_t s_wcnt[32];
+    __shared__ uint32_t s_base;
     for (int vi = 0; vi < fp.n_views; vi++) {
         const ViewParams& v = fp.v[vi];
         bool pass = false;
@@ -413,20 +414,30 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
             }
         }
         if (in && !pass) fb.ntests[(size_t)vi * N + g] = 0;
-        // warp-aggregated append of (view, g) to the work list
+        // block-aggregated append of (view, g) to the work list: one global
+        // atomic per block and view (a single hot counter serialises otherwise)
         const unsigned m = __ballot_sync(0xffffffffu, pass);
-        if (m) {
-            uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(fb.cand_count, (uint32_t)__popc(m));
-            base = __shfl_sync(0xffffffffu, base, 0);
-            if (pass) fb.cand[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)((int64_t)vi * N + g);
+        if (lane == 0) s_wcnt[warp] = (uint32_t)__popc(m);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t tot = 0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); w++) {
+                const uint32_t c = s_wcnt[w];
+                s_wcnt[w] = tot;
+                tot += c;
+            }
+            s_base = tot ? atomicAdd(fb.cand_count, tot) : 0u;
         }
+        __syncthreads();
+        if (pass)
+            fb.cand[s_base + s_wcnt[warp] + __popc(m & ((1u << lane) - 1u))] = (uint32_t)((int64_t)vi * N + g);
+        __syncthreads();
     }
 }
 
 // Step 1b: exact per-(view, Gaussian) preprocess of the compacted candidates:
 // projection, footprint, candidate tile count, splat record and SH colour.
-__global__ void __launch_bounds__(256, 2) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb) {
+__global__ void __launch_bounds__(256, 3) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb) {
     const int64_t N = fp.N;
     const uint32_t nc = *fb.cand_count;
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
@@ -469,116 +480,187 @@ __global__ void __launch_bounds__(256, 2) k_preprocess(SceneDev sc, FrameParams 
     }
 }
 
-// Step 3a: one thread per (Gaussian, candidate tile): Eq.4 test (O7) and key
-// (O8).  Candidates are laid out (view, g, tile row-major) by the scan of the
-// per-splat rect areas, so every thread does one test (load-balanced: big
-// footprints no longer serialise a thread).  Writes keep flag, key, value.
-// Candidate -> splat map: sid[toff[s] + i] = s for i < ntests[s].
-__global__ void k_fill_sid(FrameParams fp, FrameBufs fb, int64_t test_cap) {
-    const int64_t VN = (int64_t)fp.n_views * fp.N;
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < VN; s += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t n = fb.ntests[s], a = fb.toff[s];
-        for (uint32_t i = 0; i < n && (int64_t)a + i < test_cap; i++) fb.sid[a + i] = (uint32_t)s;
-    }
+// Step 3 (fused): one thread per (Gaussian, candidate tile): Eq.4 test (O7)
+// and key (O8), then single-pass stream compaction of the kept candidates
+// with decoupled look-back (blocks take 512-candidate tiles in order from a
+// counter, publish their keep count, look back for their offset and write
+// the pairs directly in (view, g, tile row-major) emission order).  The
+// onesweep digit histograms of the emitted keys are accumulated on the way.
+// Candidates are laid out by the scan of the per-splat rect areas, which also
+// wrote the (splat, rect-local index) of every candidate (sidk).
+namespace {
+constexpr int kTT = 256;           // threads per block
+constexpr int kTTItems = 2;        // candidates per thread (independent: ILP)
+constexpr int kTTTile = kTT * kTTItems;
+__device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+}  // namespace
+
+__device__ __forceinline__ bool test_candidate(const FrameParams& fp, const FrameBufs& fb, unsigned long long sk,
+                                               uint64_t& key, uint32_t& gout) {
+    const uint32_t sidx = (uint32_t)sk, l = (uint32_t)(sk >> 32);
+    int vi = 0;
+    while (vi + 1 < fp.n_views && (int64_t)sidx >= (int64_t)(vi + 1) * fp.N) vi++;
+    const ViewParams& v = fp.v[vi];
+    const float4* rec = fb.rec + (size_t)sidx * kRecF4;
+    const float4 r0 = __ldg(rec + 0), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2), r5 = __ldg(rec + 5),
+                 r6 = __ldg(rec + 6);
+    const uint32_t r01 = __float_as_uint(r5.w), r23 = __float_as_uint(r6.w);
+    const int tx0 = r01 & 0xffff, ty0 = r01 >> 16, tx1 = r23 & 0xffff;
+    const int rw = tx1 - tx0 + 1;
+    const int tx = tx0 + (int)(l % (uint32_t)rw), ty = ty0 + (int)(l / (uint32_t)rw);
+    if (!v.vis[ty * v.tw + tx]) return false;
+    TileSplat s;
+    s.ux = r0.x; s.uy = r0.y; s.uz = r0.z; s.qcut = r0.w;
+    s.e1x = r1.x; s.e1z = r1.y; s.e2x = r1.z; s.e2y = r1.w;
+    s.e2z = r2.x; s.C0 = r2.y; s.C1 = r2.z; s.C2 = r2.w;
+    s.eps = r5.z;
+    const int T = fp.T, x0 = tx * T, y0 = ty * T;
+    float hx, hy, hz;
+    if (!tile_test(s, v, x0, y0, min(x0 + T, v.W), min(y0 + T, v.H), hx, hy, hz)) return false;
+    const float4 r3 = __ldg(rec + 3), r4 = __ldg(rec + 4);
+    s.A[0] = r3.x; s.A[1] = r3.y; s.A[2] = r3.z; s.A[3] = r3.w;
+    s.A[4] = r4.x; s.A[5] = r4.y; s.bx = r4.z; s.by = r4.w; s.bz = r5.x;
+    const float td = tile_depth(s, hx, hy, hz, fp.near_plane);
+    const uint64_t tile = (uint64_t)(v.tile_base + ty * v.tw + tx);
+    key = (tile << 32) | (uint64_t)__float_as_uint(td);
+    gout = (uint32_t)((int64_t)sidx - (int64_t)vi * fp.N);
+    return true;
 }
 
-__global__ void __launch_bounds__(256) k_tiletest(FrameParams fp, FrameBufs fb, int64_t test_cap) {
+__global__ void __launch_bounds__(kTT) k_tiletest(FrameParams fp, FrameBufs fb, int64_t test_cap, uint64_t* keys,
+                                                  uint32_t* vals, uint32_t* hist, int passes,
+                                                  unsigned long long* status, uint32_t* counter, uint32_t epoch) {
+    __shared__ uint32_t s_h[8][256];
+    __shared__ uint32_t s_wc[kTT / 32 * kTTItems];
+    __shared__ uint32_t s_tile, s_excl;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned long long ep = (unsigned long long)epoch << 34;
+    const unsigned long long kAgg = ep | (1ull << 32), kPre = ep | (2ull << 32);
+    if (hist)
+        for (int i = tid; i < 8 * 256; i += kTT) (&s_h[0][0])[i] = 0;
     const int64_t total = min((int64_t)*fb.total_tests, test_cap);
-    const int T = fp.T;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t sidx = fb.sid[t];
-        const uint32_t l = (uint32_t)(t - fb.toff[sidx]);
-        int vi = 0;
-        while (vi + 1 < fp.n_views && sidx >= (int64_t)(vi + 1) * fp.N) vi++;
-        const ViewParams& v = fp.v[vi];
-        const float4* rec = fb.rec + (size_t)sidx * kRecF4;
-        const float4 r0 = __ldg(rec + 0), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2), r5 = __ldg(rec + 5),
-                     r6 = __ldg(rec + 6);
-        const uint32_t r01 = __float_as_uint(r5.w), r23 = __float_as_uint(r6.w);
-        const int tx0 = r01 & 0xffff, ty0 = r01 >> 16, tx1 = r23 & 0xffff;
-        const int rw = tx1 - tx0 + 1;
-        const int tx = tx0 + (int)(l % (uint32_t)rw), ty = ty0 + (int)(l / (uint32_t)rw);
-        uint32_t keep = 0;
-        uint64_t key = 0;
-        if (v.vis[ty * v.tw + tx]) {
-            TileSplat s;
-            s.ux = r0.x; s.uy = r0.y; s.uz = r0.z; s.qcut = r0.w;
-            s.e1x = r1.x; s.e1z = r1.y; s.e2x = r1.z; s.e2y = r1.w;
-            s.e2z = r2.x; s.C0 = r2.y; s.C1 = r2.z; s.C2 = r2.w;
-            s.eps = r5.z;
-            const int x0 = tx * T, y0 = ty * T;
-            float hx, hy, hz;
-            if (tile_test(s, v, x0, y0, min(x0 + T, v.W), min(y0 + T, v.H), hx, hy, hz)) {
-                const float4 r3 = __ldg(rec + 3), r4 = __ldg(rec + 4);
-                s.A[0] = r3.x; s.A[1] = r3.y; s.A[2] = r3.z; s.A[3] = r3.w;
-                s.A[4] = r4.x; s.A[5] = r4.y; s.bx = r4.z; s.by = r4.w; s.bz = r5.x;
-                const float td = tile_depth(s, hx, hy, hz, fp.near_plane);
-                const uint64_t tile = (uint64_t)(v.tile_base + ty * v.tw + tx);
-                key = (tile << 32) | (uint64_t)__float_as_uint(td);
-                keep = 1;
+    const int64_t ntiles = (total + kTTTile - 1) / kTTTile;
+    while (true) {
+        if (tid == 0) s_tile = atomicAdd(counter, 1u);
+        __syncthreads();
+        const int64_t tile = s_tile;
+        if (tile >= ntiles) break;
+        uint64_t key[kTTItems];
+        uint32_t gv[kTTItems];
+        bool keep[kTTItems];
+#pragma unroll
+        for (int it = 0; it < kTTItems; it++) {
+            const int64_t t = tile * kTTTile + it * kTT + tid;
+            keep[it] = false;
+            key[it] = 0;
+            gv[it] = 0;
+            if (t < total) keep[it] = test_candidate(fp, fb, fb.sidk[t], key[it], gv[it]);
+        }
+        // tile-local exclusive positions in candidate order (item-major, then thread)
+        uint32_t wbits[kTTItems];
+#pragma unroll
+        for (int it = 0; it < kTTItems; it++) {
+            wbits[it] = __ballot_sync(0xffffffffu, keep[it]);
+            if (lane == 0) s_wc[it * (kTT / 32) + warp] = __popc(wbits[it]);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            constexpr int nw = kTT / 32 * kTTItems;  // 16 warp-slots
+            const uint32_t c = (lane < nw) ? s_wc[lane] : 0u;
+            uint32_t inc = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += y;
+            }
+            const uint32_t agg = __shfl_sync(0xffffffffu, inc, 31);
+            if (lane < nw) s_wc[lane] = inc - c;
+            // publish + warp-wide decoupled look-back
+            uint32_t excl = 0;
+            if (tile == 0) {
+                if (lane == 0) st_relaxed64(&status[0], kPre | agg);
+            } else {
+                if (lane == 0) st_relaxed64(&status[tile], kAgg | agg);
+                int64_t j = tile - 1;
+                while (true) {
+                    const int64_t jj = j - lane;
+                    unsigned long long sv = kPre;
+                    if (jj >= 0) {
+                        do {
+                            sv = ld_relaxed64(&status[jj]);
+                        } while ((sv & ~0xffffffffull) != kAgg && (sv & ~0xffffffffull) != kPre);
+                    }
+                    const unsigned pre = __ballot_sync(0xffffffffu, (sv & ~0xffffffffull) == kPre);
+                    const int stop = pre ? (__ffs(pre) - 1) : 31;
+                    uint32_t val = (lane <= stop) ? (uint32_t)sv : 0u;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+                    excl += val;
+                    if (pre) break;
+                    j -= 32;
+                }
+                if (lane == 0) st_relaxed64(&status[tile], kPre | (excl + agg));
+            }
+            if (lane == 0) {
+                s_excl = excl;
+                if (tile == ntiles - 1) *fb.total = excl + agg;
             }
         }
-        fb.tflag[t] = keep;
-        if (keep) {
-            fb.tkey[t] = key;
-            fb.tval[t] = (uint32_t)(sidx - (int64_t)vi * fp.N);
-        }
-    }
-}
-
-// Step 3b: compaction of the kept candidates at their scanned positions:
-// the pair list in (view, g, tile row-major) emission order.
-__global__ void __launch_bounds__(256) k_compact(FrameBufs fb, int64_t test_cap, int64_t pair_cap,
-                                                 uint64_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                                 uint32_t* __restrict__ hist, int passes) {
-    // also accumulates the onesweep digit histograms of the emitted keys (fused
-    // "global histogram" pass of the sort: the keys are read here anyway)
-    __shared__ uint32_t s_h[8][256];
-    if (hist)
-        for (int i = threadIdx.x; i < 8 * 256; i += blockDim.x) (&s_h[0][0])[i] = 0;
-    __syncthreads();
-    const int64_t total = min((int64_t)*fb.total_tests, test_cap);
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-        if (!fb.tflag[t]) continue;
-        const uint32_t pos = fb.tpos[t];
-        if (pos < pair_cap) {
-            const uint64_t k = fb.tkey[t];
-            keys[pos] = k;
-            vals[pos] = fb.tval[t];
-            if (hist) {  // warp-aggregated (the top digits have few distinct values)
-                const unsigned act = __activemask();
-                const unsigned lt = (1u << (threadIdx.x & 31)) - 1u;
+        __syncthreads();
+        const uint32_t excl = s_excl;
+#pragma unroll
+        for (int it = 0; it < kTTItems; it++) {
+            if (keep[it]) {
+                const uint32_t pos = excl + s_wc[it * (kTT / 32) + warp] + __popc(wbits[it] & lt);
+                if (pos < fp.pair_cap) {
+                    keys[pos] = key[it];
+                    vals[pos] = gv[it];
+                }
+            }
+            if (hist) {  // digit histograms: one atomic per warp when the digit is warp-uniform
+                const unsigned m = wbits[it];
                 for (int p = 0; p < passes; p++) {
-                    const uint32_t d = (uint32_t)(k >> (8 * p)) & 0xffu;
-                    const unsigned peers = __match_any_sync(act, d);
-                    if ((peers & lt) == 0) atomicAdd(&s_h[p][d], (uint32_t)__popc(peers));
+                    const uint32_t d = (uint32_t)(key[it] >> (8 * p)) & 0xffu;
+                    const uint32_t dmin = __reduce_min_sync(0xffffffffu, keep[it] ? d : 0xffffffffu);
+                    const uint32_t dmax = __reduce_max_sync(0xffffffffu, keep[it] ? d : 0u);
+                    if (dmin == dmax) {
+                        if (lane == 0 && m) atomicAdd(&s_h[p][dmin], (uint32_t)__popc(m));
+                    } else if (keep[it]) {
+                        atomicAdd(&s_h[p][d], 1u);
+                    }
                 }
             }
         }
+        __syncthreads();
     }
     if (hist) {
         __syncthreads();
-        for (int i = threadIdx.x; i < passes * 256; i += blockDim.x) {
+        for (int i = tid; i < passes * 256; i += kTT) {
             const uint32_t c = (&s_h[0][0])[i];
             if (c) atomicAdd(&hist[i], c);
         }
     }
 }
 
-// Exact per-(view, g) pair counts (parity hook / statistics only).
+// Exact per-(view, g) pair counts (parity hook / statistics only): the
+// pairs of a splat are contiguous in emission order, so its count is the
+// number of emitted pairs whose candidate falls in its candidate range;
+// computed by a binary search of the splat range in the candidate->pair map.
 __global__ void k_counts(FrameParams fp, FrameBufs fb, int64_t test_cap) {
-    const int64_t VN = (int64_t)fp.n_views * fp.N;
     const int64_t total = min((int64_t)*fb.total_tests, test_cap);
-    const uint32_t pairs = *fb.total;
-    for (int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; s < VN; s += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t n = fb.ntests[s], a = fb.toff[s];
-        uint32_t c = 0;
-        if (n && (int64_t)a < total) {
-            const uint32_t pa = fb.tpos[a];
-            const uint32_t pb = ((int64_t)a + n < total) ? fb.tpos[a + n] : pairs;
-            c = pb - pa;
-        }
-        fb.counts[s] = c;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+        uint64_t key;
+        uint32_t g;
+        const unsigned long long sk = fb.sidk[t];
+        if (test_candidate(fp, fb, sk, key, g)) atomicAdd(&fb.counts[(uint32_t)sk], 1u);
     }
 }
 
@@ -626,7 +708,7 @@ void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    k_preprocess<<<sms * 4, B, 0, st>>>(sc, fp, fb);
+    k_preprocess<<<sms * 6, B, 0, st>>>(sc, fp, fb);
 }
 
 static int sm_count() {
@@ -640,23 +722,24 @@ static int sm_count() {
     return n;
 }
 
-void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {
-    const int64_t VN = (int64_t)fp.n_views * fp.N;
-    if (VN == 0) return;
-    k_fill_sid<<<(unsigned)std::min<int64_t>((VN + 255) / 256, (int64_t)sm_count() * 16), 256, 0, st>>>(fp, fb, test_cap);
-    k_tiletest<<<sm_count() * 8, 256, 0, st>>>(fp, fb, test_cap);
-}
-
-void launch_compact(FrameBufs fb, int64_t test_cap, int64_t pair_cap, uint64_t* keys, uint32_t* vals,
-                    uint32_t* hist, int passes, cudaStream_t st) {
+void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, uint64_t* keys, uint32_t* vals,
+                     uint32_t* hist, int passes, unsigned long long* status, uint32_t* counter, uint32_t epoch,
+                     cudaStream_t st) {
+    if ((int64_t)fp.n_views * fp.N == 0) {
+        cudaMemsetAsync(fb.total, 0, 4, st);
+        return;
+    }
     if (hist) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 8 * 256, st);
-    k_compact<<<sm_count() * 8, 256, 0, st>>>(fb, test_cap, pair_cap, keys, vals, hist, passes);
+    cudaMemsetAsync(counter, 0, 4, st);
+    cudaMemsetAsync(fb.total, 0, 4, st);  // stays 0 when there is no candidate at all
+    k_tiletest<<<sm_count() * 8, kTT, 0, st>>>(fp, fb, test_cap, keys, vals, hist, passes, status, counter, epoch);
 }
 
 void launch_counts(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {
     const int64_t n = (int64_t)fp.n_views * fp.N;
     if (n == 0) return;
-    k_counts<<<(unsigned)std::min<int64_t>((n + 255) / 256, 65535), 256, 0, st>>>(fp, fb, test_cap);
+    cudaMemsetAsync(fb.counts, 0, sizeof(uint32_t) * n, st);
+    k_counts<<<sm_count() * 8, 256, 0, st>>>(fp, fb, test_cap);
 }
 
 void launch_debug_splats(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int view, float* out,

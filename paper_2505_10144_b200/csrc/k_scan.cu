@@ -32,7 +32,8 @@ __device__ __forceinline__ unsigned long long ld_acquire(const unsigned long lon
 // device, so the scanned length need not be known on the host) is covered.
 __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restrict__ in, uint32_t* __restrict__ out,
                                                        uint32_t* total, const uint32_t* __restrict__ n_dev,
-                                                       int64_t cap, unsigned long long* scratch) {
+                                                       int64_t cap, unsigned long long* scratch,
+                                                       unsigned long long* __restrict__ expand, int64_t expand_cap) {
     __shared__ uint32_t s_tile, s_excl;
     __shared__ uint32_t s_warp[kScanThreads / 32];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -108,7 +109,18 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restric
         }
         __syncthreads();
         uint32_t run = s_excl + wpre + inc - tsum;
-        if (base + kScanItems <= n && ((reinterpret_cast<uintptr_t>(out + base) & 15) == 0)) {
+        if (expand) {  // candidate -> (element, local index) map
+            uint32_t o = run;
+#pragma unroll 1
+            for (int k = 0; k < kScanItems; k++) {
+                const unsigned long long e = (unsigned long long)(base + k);
+                for (uint32_t j = 0; j < v[k] && (int64_t)o + j < expand_cap; j++)
+                    expand[o + j] = e | ((unsigned long long)j << 32);
+                o += v[k];
+            }
+        }
+        if (!out) {
+        } else if (base + kScanItems <= n && ((reinterpret_cast<uintptr_t>(out + base) & 15) == 0)) {
             uint4* p = reinterpret_cast<uint4*>(out + base);
 #pragma unroll
             for (int k = 0; k < kScanItems / 4; k++) {
@@ -134,7 +146,7 @@ __global__ void __launch_bounds__(kScanThreads) k_scan(const uint32_t* __restric
 size_t scan_scratch_words(int64_t n) { return (size_t)((n + kScanTile - 1) / kScanTile) + 2; }
 
 void launch_scan(const uint32_t* in, uint32_t* out, uint32_t* total, const uint32_t* n_dev, int64_t cap,
-                 uint32_t* scratch32, cudaStream_t st) {
+                 uint32_t* scratch32, cudaStream_t st, unsigned long long* expand, int64_t expand_cap) {
     unsigned long long* scratch = reinterpret_cast<unsigned long long*>(scratch32);
     if (cap <= 0) {
         cudaMemsetAsync(total, 0, 4, st);
@@ -150,7 +162,7 @@ void launch_scan(const uint32_t* in, uint32_t* out, uint32_t* total, const uint3
     const int64_t tiles = (cap + kScanTile - 1) / kScanTile;
     cudaMemsetAsync(scratch, 0, (size_t)(tiles + 1) * 8, st);
     const int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * 4);
-    k_scan<<<(unsigned)grid, kScanThreads, 0, st>>>(in, out, total, n_dev, cap, scratch);
+    k_scan<<<(unsigned)grid, kScanThreads, 0, st>>>(in, out, total, n_dev, cap, scratch, expand, expand_cap);
 }
 
 }  // namespace vrs

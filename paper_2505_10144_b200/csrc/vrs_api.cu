@@ -48,8 +48,9 @@ struct vrs_context {
     float4* d_col = nullptr;
     uint32_t* d_cand = nullptr;
     uint32_t *d_counts = nullptr, *d_ntests = nullptr, *d_toff = nullptr, *d_misc = nullptr;  // misc: pairs, overflow, tests
-    uint32_t *d_tflag = nullptr, *d_tpos = nullptr, *d_tval = nullptr, *d_sid = nullptr;
-    uint64_t* d_tkey = nullptr;
+    unsigned long long* d_sidk = nullptr;    // [test_cap] candidate map
+    unsigned long long* d_tt_status = nullptr;  // fused tile-test look-back words
+    uint32_t tt_epoch = 0;
     int64_t test_cap = 0;
     uint64_t *d_keys = nullptr, *d_keys_alt = nullptr;
     uint32_t *d_vals = nullptr, *d_vals_alt = nullptr;
@@ -109,7 +110,7 @@ static vrs_status cuda_check(vrs_context* c, cudaError_t e, const char* where) {
 
 static void free_all(vrs_context* c) {
     void* ptrs[] = {c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_col, c->d_cand, c->d_counts, c->d_ntests, c->d_toff, c->d_misc,
-                    c->d_tflag, c->d_tpos, c->d_tval, c->d_tkey, c->d_sid,
+                    c->d_sidk, c->d_tt_status,
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
                     c->d_sat, c->d_cls, c->d_items, c->d_nitems, c->d_out_rgba, c->d_out_depth};
@@ -158,11 +159,8 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     A(dalloc(&ctx->d_ntests, (size_t)V * N));
     A(dalloc(&ctx->d_toff, (size_t)V * N));
     ctx->test_cap = 4 * P;
-    A(dalloc(&ctx->d_tflag, (size_t)ctx->test_cap));
-    A(dalloc(&ctx->d_sid, (size_t)ctx->test_cap));
-    A(dalloc(&ctx->d_tpos, (size_t)ctx->test_cap));
-    A(dalloc(&ctx->d_tval, (size_t)ctx->test_cap));
-    A(dalloc(&ctx->d_tkey, (size_t)ctx->test_cap));
+    A(dalloc(&ctx->d_sidk, (size_t)ctx->test_cap));
+    A(dalloc(&ctx->d_tt_status, (size_t)(ctx->test_cap / 512 + 2)));
     A(dalloc(&ctx->d_misc, 8));
     A(dalloc(&ctx->d_keys, (size_t)P));
     A(dalloc(&ctx->d_keys_alt, (size_t)P));
@@ -467,6 +465,16 @@ static int key_bits_for(int64_t tiles) {
     return 32 + b;
 }
 
+// Look-back words of the fused tile test, epoch-tagged (cleared once per wrap).
+static unsigned long long* tt_status(vrs_context* ctx, cudaStream_t st) {
+    ctx->tt_epoch = (ctx->tt_epoch + 1) & 0x3fffffffu;
+    if (ctx->tt_epoch <= 1) {
+        ctx->tt_epoch = 1;
+        cudaMemsetAsync(ctx->d_tt_status, 0, sizeof(unsigned long long) * (size_t)(ctx->test_cap / 512 + 2), st);
+    }
+    return ctx->d_tt_status;
+}
+
 static FrameBufs frame_bufs(vrs_context* ctx) {
     FrameBufs fb{};
     fb.rec = ctx->d_rec;
@@ -476,11 +484,7 @@ static FrameBufs frame_bufs(vrs_context* ctx) {
     fb.ntests = ctx->d_ntests;
     fb.toff = ctx->d_toff;
     fb.total_tests = ctx->d_misc + 2;
-    fb.sid = ctx->d_sid;
-    fb.tflag = ctx->d_tflag;
-    fb.tpos = ctx->d_tpos;
-    fb.tkey = ctx->d_tkey;
-    fb.tval = ctx->d_tval;
+    fb.sidk = ctx->d_sidk;
     fb.counts = ctx->d_counts;
     fb.total = ctx->d_misc;
     fb.overflow = ctx->d_misc + 1;
@@ -521,14 +525,15 @@ static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* ca
     if (ctx->counters) CK(cudaMemsetAsync(ctx->d_stats, 0, 8 * sizeof(unsigned long long), st));
     launch_preprocess(sc, fp, fb, st);
     if (tm) CK(cudaEventRecord(ctx->ev[1], st));
-    launch_scan(fb.ntests, fb.toff, fb.total_tests, nullptr, (int64_t)nv * fp.N, ctx->d_scan_scratch, st);
+    launch_scan(fb.ntests, fb.toff, fb.total_tests, nullptr, (int64_t)nv * fp.N, ctx->d_scan_scratch, st, fb.sidk,
+                ctx->test_cap);
     if (tm) CK(cudaEventRecord(ctx->ev[2], st));
-    launch_tiletest(fp, fb, ctx->test_cap, st);
-    launch_scan(fb.tflag, fb.tpos, fb.total, fb.total_tests, ctx->test_cap, ctx->d_scan_scratch, st);
     const int key_bits = key_bits_for(ctx->last_tiles);
-    launch_compact(fb, ctx->test_cap, fp.pair_cap, fb.keys, fb.vals, nullptr, 0, st);
+    unsigned long long* tts = tt_status(ctx, st);  // (advances the epoch)
+    launch_tiletest(fp, fb, ctx->test_cap, fb.keys, fb.vals, ctx->sort.hist, (key_bits + 7) / 8, tts,
+                    ctx->sort.counters + 7, ctx->tt_epoch, st);
     if (tm) CK(cudaEventRecord(ctx->ev[3], st));
-    launch_sort(fb.keys, fb.vals, fb.keys_alt, fb.vals_alt, fb.total, fp.pair_cap, key_bits, ctx->sort, st, false);
+    launch_sort(fb.keys, fb.vals, fb.keys_alt, fb.vals_alt, fb.total, fp.pair_cap, key_bits, ctx->sort, st, true);
     if (tm) CK(cudaEventRecord(ctx->ev[4], st));
     launch_ranges(fb.keys, fb.total, fp.pair_cap, fb.ranges, ctx->last_tiles, st);
     if (tm) CK(cudaEventRecord(ctx->ev[5], st));
@@ -655,9 +660,14 @@ vrs_status vrs_debug_pairs(vrs_context* ctx, int32_t sorted, uint64_t* keys, uin
         CK(cudaMemcpy(keys, ctx->d_keys, 8 * n, cudaMemcpyDeviceToHost));
         CK(cudaMemcpy(vals, ctx->d_vals, 4 * n, cudaMemcpyDeviceToHost));
     } else {
-        // re-run the compaction (emission order) into the alternate buffers
-        launch_compact(frame_bufs(ctx), ctx->test_cap, ctx->cfg.max_pairs, ctx->d_keys_alt, ctx->d_vals_alt, nullptr, 0,
-                       st);
+        // re-run the fused tests + compaction (emission order) into the alternate buffers
+        FrameBufs fb = frame_bufs(ctx);
+        uint32_t saved = 0;
+        CK(cudaMemcpy(&saved, ctx->d_misc, 4, cudaMemcpyDeviceToHost));
+        unsigned long long* tts = tt_status(ctx, st);
+        launch_tiletest(ctx->fp, fb, ctx->test_cap, ctx->d_keys_alt, ctx->d_vals_alt, nullptr, 0, tts,
+                        ctx->sort.counters + 7, ctx->tt_epoch, st);
+        CK(cudaMemcpyAsync(ctx->d_misc, &saved, 4, cudaMemcpyHostToDevice, st));
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(st));
         CK(cudaMemcpy(keys, ctx->d_keys_alt, 8 * n, cudaMemcpyDeviceToHost));

@@ -75,11 +75,7 @@ struct FrameBufs {
     uint32_t* ntests;        // [V*N] candidate (Gaussian, tile) tests = rect area
     uint32_t* toff;          // [V*N] exclusive scan of ntests
     uint32_t* total_tests;   // [1] (device)
-    uint32_t* sid;           // [test_cap] candidate -> splat (view*N + g)
-    uint32_t* tflag;         // [test_cap] keep flags
-    uint32_t* tpos;          // [test_cap] exclusive scan of tflag = pair position
-    uint64_t* tkey;          // [test_cap] key of kept candidates
-    uint32_t* tval;          // [test_cap] Gaussian index of kept candidates
+    unsigned long long* sidk;  // [test_cap] candidate -> (splat view*N+g) | (rect-local tile index << 32)
     uint32_t* counts;        // [V*N] exact pair counts (parity hook only)
     uint32_t* total;         // [1] pair total (device)
     uint32_t* overflow;      // [1] capacity overflow flag
@@ -99,13 +95,16 @@ void launch_setup_view(const uint8_t* mask, int mask_w, ViewParams vp, int T, in
                        int32_t* cls, uint32_t* items, int32_t* n_items_dev, cudaStream_t st);
 void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, cudaStream_t st);
 // Exclusive scan of n = min(*n_dev, cap) u32 (n_dev may be null: n = cap); *total = sum.
+// out may be null.  expand (optional): for element e with count c at offset o,
+// expand[o + j] = e | (j << 32) for j < c (and o + j < expand_cap).
 void launch_scan(const uint32_t* in, uint32_t* out, uint32_t* total, const uint32_t* n_dev, int64_t cap,
-                 uint32_t* scratch, cudaStream_t st);
+                 uint32_t* scratch, cudaStream_t st, unsigned long long* expand = nullptr,
+                 int64_t expand_cap = 0);
 size_t scan_scratch_words(int64_t n);
-void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st);
-// hist (optional): [8][256] digit histograms of the emitted keys for `passes` 8-bit digits
-void launch_compact(FrameBufs fb, int64_t test_cap, int64_t pair_cap, uint64_t* keys, uint32_t* vals,
-                    uint32_t* hist, int passes, cudaStream_t st);
+// Fused Eq.4 tests + keys + stream compaction (+ onesweep digit histograms when hist != null).
+void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, uint64_t* keys, uint32_t* vals,
+                     uint32_t* hist, int passes, unsigned long long* status, uint32_t* counter, uint32_t epoch,
+                     cudaStream_t st);
 void launch_counts(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st);
 struct SortScratch {
     uint32_t* hist;          // [8][256] digit histograms (may be filled by k_compact)
