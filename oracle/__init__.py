@@ -20,7 +20,7 @@ STAT_NAMES = ["pairs", "samples", "evaluations", "contributions", "overflow_samp
 # splat record field slices (oracle.cpp orc_get_splats)
 SPLAT_FIELDS = {"valid": slice(0, 1), "muc": slice(1, 4), "u": slice(4, 7), "e1": slice(7, 10),
                 "e2": slice(10, 13), "S2": slice(13, 16), "C": slice(16, 19), "eps": slice(19, 20),
-                "A": slice(25, 31), "bv": slice(31, 34), "rgb": slice(34, 37), "sigma": slice(37, 38),
+                "m2": slice(20, 22), "Cp": slice(22, 25), "A": slice(25, 31), "bv": slice(31, 34), "rgb": slice(34, 37), "sigma": slice(37, 38),
                 "qcut": slice(38, 39), "rect": slice(39, 43), "bbox": slice(43, 47), "count": slice(47, 48)}
 
 
@@ -145,13 +145,14 @@ class Oracle:
             lib().orc_set_mask(self.h, slot, m.shape[1], m.shape[0], _p(m))
 
     def prepare(self, cams, foveas=None, assign_tile=16, window_k=16, near=0.2, background=(0, 0, 0),
-                threads=0):
+                threads=0, projection=0):
         foveas = foveas if foveas is not None else [None] * len(cams)
         arr = (_View * len(cams))(*[make_view(c, f) for c, f in zip(cams, foveas)])
         p = _Params()
         p.assign_tile, p.window_k, p.near_plane = assign_tile, window_k, near
         p.background[:] = list(background)
         p.threads = threads
+        p.projection = projection
         rc = lib().orc_prepare(self.h, len(cams), C.cast(arr, C.c_void_p), C.cast(C.pointer(p), C.c_void_p))
         if rc != 0:
             raise ValueError(f"orc_prepare rc={rc}")

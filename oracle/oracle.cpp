@@ -95,6 +95,8 @@ struct Splat {
     int rect[4] = {0, 0, -1, -1};  // tx0, ty0, tx1, ty1 (inclusive); empty if tx0 > tx1
     float bbox[4] = {0, 0, 0, 0};  // conservative pixel extent xmin, xmax, ymin, ymax
     uint32_t count = 0;
+    // EWA baseline (projection = 1, config C5): pixel-space mean and conic
+    float m2[2] = {0, 0}, Cp[3] = {0, 0, 0};
 };
 
 enum { CLS_HIGH = 0, CLS_LOW = 1, CLS_HYBRID = 2, CLS_INVIS = 3 };
@@ -152,9 +154,7 @@ static inline float chart_num(const float* e1, const float* e2, const float* C, 
  * implementations therefore produce identical alpha and transmittance
  * T_k = T_{k-1} * (1 - alpha_k), so the T < 1e-4 stop is an exact decision. */
 struct SampleAT { float alpha, tau; };
-static inline SampleAT sample_alpha_tau(float num, float ss, float den, float dtb, float sigma) {
-    float r = 1.0f / (ss * den);
-    float x = std::fmax((num * -0.72134752f) * (den * r), -64.0f);  // NaN/-inf guard
+static inline float alpha_of_x(float x, float sigma) {
     float fl = std::floor(x);
     float f = x - fl;
     float p = 0.00187757565f;
@@ -165,10 +165,25 @@ static inline SampleAT sample_alpha_tau(float num, float ss, float den, float dt
     p = std::fmaf(p, f, 0.99999994f);
     float e = std::ldexp(p, (int)fl);
     float a = sigma * e;
+    return a < 0.99f ? a : 0.99f;
+}
+static inline SampleAT sample_alpha_tau(float num, float ss, float den, float dtb, float sigma) {
+    float r = 1.0f / (ss * den);
+    float x = std::fmax((num * -0.72134752f) * (den * r), -64.0f);  // NaN/-inf guard
     SampleAT o;
-    o.alpha = a < 0.99f ? a : 0.99f;
+    o.alpha = alpha_of_x(x, sigma);
     o.tau = std::fmax(dtb * (ss * r), -1e30f) + 0.0f;  // canonical: NaN/-inf -> -1e30, -0 -> +0 (R4)
     return o;
+}
+/* EWA baseline per sample (q directly in pixels; one IEEE division for tau). */
+static inline SampleAT sample_alpha_tau_ewa(float q, float den, float dtb, float sigma) {
+    SampleAT o;
+    o.alpha = alpha_of_x(std::fmax(q * -0.72134752f, -64.0f), sigma);
+    o.tau = std::fmax(dtb / den, -1e30f) + 0.0f;
+    return o;
+}
+static inline float ewa_q(const float* C, float dx, float dy) {
+    return std::fmaf(dx, std::fmaf(C[0], dx, C[1] * dy), dy * std::fmaf(C[1], dx, C[2] * dy));
 }
 
 /* 3x3 symmetric (xx,xy,xz,yy,yz,zz) conjugation W S W^T, R6 "3x3 products":
@@ -215,6 +230,79 @@ static void sh_color(const float* shc, int deg, const double dir[3], float out[3
     }
 }
 
+/* Shared tail of O5/O6 for both projections: depth coefficients and colour. */
+static void depth_and_colour(const Scene& S, const orc_view& v, int64_t g, Splat& sp) {
+    const float* mu = &S.mu[3 * g];
+    float Ai[6];
+    conj3(v.R, &S.icov[6 * g], Ai);  // A = W Sigma_w^-1 W^T = Sigma_c^-1
+    sp.A[0] = Ai[0];
+    sp.A[1] = 2.0f * Ai[1];
+    sp.A[2] = Ai[3];
+    sp.A[3] = 2.0f * Ai[2];
+    sp.A[4] = 2.0f * Ai[4];
+    sp.A[5] = Ai[5];
+    float Am[3][3] = {{Ai[0], Ai[1], Ai[2]}, {Ai[1], Ai[3], Ai[4]}, {Ai[2], Ai[4], Ai[5]}};
+    for (int i = 0; i < 3; i++) sp.bv[i] = dot3(Am[i], sp.muc);
+    double d[3] = {(double)mu[0] - v.o[0], (double)mu[1] - v.o[1], (double)mu[2] - v.o[2]};
+    double nd = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    for (int i = 0; i < 3; i++) d[i] /= nd;
+    sh_color(&S.sh[(size_t)g * S.ncoef * 3], S.deg, d, sp.rgb);
+}
+
+/* Pixel bbox [xmin,xmax]x[ymin,ymax] (already expanded) -> bbox + tile rect (O6d). */
+static void set_rect(const Oracle& O, const ViewState& vs, double xmin, double xmax, double ymin, double ymax,
+                     Splat& sp) {
+    const double W = vs.v.width, H = vs.v.height;
+    sp.bbox[0] = (float)std::max(xmin, -2.0); sp.bbox[1] = (float)std::min(xmax, W + 2.0);
+    sp.bbox[2] = (float)std::max(ymin, -2.0); sp.bbox[3] = (float)std::min(ymax, H + 2.0);
+    const int T_a = O.p.assign_tile;
+    if (xmax < 0.0 || ymax < 0.0 || xmin > W || ymin > H) return;  // empty rect
+    sp.rect[0] = std::max(0, (int)std::floor(std::max(xmin, 0.0) / T_a));
+    sp.rect[1] = std::max(0, (int)std::floor(std::max(ymin, 0.0) / T_a));
+    sp.rect[2] = std::min(vs.tw - 1, (int)std::floor(std::min(xmax, W) / T_a));
+    sp.rect[3] = std::min(vs.th - 1, (int)std::floor(std::min(ymax, H) / T_a));
+}
+
+/* EWA baseline (Eq.3; SURVEY "EWA mode", config C5): the 3DGS
+ * local-affine projection Sigma_2D = J W Sigma W^T J^T + 0.3 I in pixels
+ * ([ext] 3DGS computeCov2D, with its 1.3 tan(fov/2) clamp of the Jacobian
+ * point), per-sample q = D^T C D from the projected mean, tiles tested in
+ * screen space (StopThePop's original tile culling). */
+static void preprocess_ewa(const Oracle& O, const ViewState& vs, int64_t g, Splat& sp) {
+    const Scene& S = O.sc;
+    const orc_view& v = vs.v;
+    float Sc[6];
+    conj3(v.R, &S.cov[6 * g], Sc);
+    const float z = sp.muc[2];
+    const float limx = 1.3f * ((0.5f * (float)v.width) / v.fx), limy = 1.3f * ((0.5f * (float)v.height) / v.fy);
+    const float txtz = sp.muc[0] / z, tytz = sp.muc[1] / z;
+    const float tx = std::fmin(limx, std::fmax(-limx, txtz)) * z;
+    const float ty = std::fmin(limy, std::fmax(-limy, tytz)) * z;
+    const float zz = z * z;
+    const float J00 = v.fx / z, J02 = -(v.fx * tx) / zz, J11 = v.fy / z, J12 = -(v.fy * ty) / zz;
+    // rows of J Sigma_c (Sigma_c = xx,xy,xz,yy,yz,zz)
+    const float a0 = std::fmaf(J00, Sc[0], J02 * Sc[2]), a1 = std::fmaf(J00, Sc[1], J02 * Sc[4]),
+                a2 = std::fmaf(J00, Sc[2], J02 * Sc[5]);
+    const float b1 = std::fmaf(J11, Sc[3], J12 * Sc[4]), b2 = std::fmaf(J11, Sc[4], J12 * Sc[5]);
+    float c00 = std::fmaf(a0, J00, a2 * J02), c01 = std::fmaf(a1, J11, a2 * J12), c11 = std::fmaf(b1, J11, b2 * J12);
+    c00 = c00 + 0.3f;
+    c11 = c11 + 0.3f;
+    sp.S2[0] = c00; sp.S2[1] = c01; sp.S2[2] = c11;
+    const float det = std::fmaf(c00, c11, -(c01 * c01));
+    if (!(det > 0.0f)) return;
+    const float idet = 1.0f / det;
+    sp.Cp[0] = c11 * idet;
+    sp.Cp[1] = -c01 * idet;
+    sp.Cp[2] = c00 * idet;
+    sp.m2[0] = std::fmaf(v.fx, sp.muc[0] / z, v.cx);
+    sp.m2[1] = std::fmaf(v.fy, sp.muc[1] / z, v.cy);
+    depth_and_colour(S, v, g, sp);
+    sp.valid = 1;
+    // footprint: axis extents of D^T C D <= q_cut are sqrt(q_cut Sigma_ii), + 1 px
+    const double rx = std::sqrt((double)sp.qcut * c00), ry = std::sqrt((double)sp.qcut * c11);
+    set_rect(O, vs, sp.m2[0] - rx - 1.0, sp.m2[0] + rx + 1.0, sp.m2[1] - ry - 1.0, sp.m2[1] + ry + 1.0, sp);
+}
+
 /* O1-O6 for one Gaussian in one view. */
 static void preprocess_one(const Oracle& O, const ViewState& vs, int64_t g, Splat& sp) {
     const Scene& S = O.sc;
@@ -227,6 +315,10 @@ static void preprocess_one(const Oracle& O, const ViewState& vs, int64_t g, Spla
     sp.qcut = S.qcut[g];
     sp.sigma = S.sigma[g];
     if (!(sp.muc[2] > O.p.near_plane) || sp.qcut < 0.0f) return;
+    if (O.p.projection == 1) {
+        preprocess_ewa(O, vs, g, sp);
+        return;
+    }
     // O2 optimal plane: tangent plane of the unit sphere at o, perpendicular
     // to o->mu.  u = mu_c / r, basis e1, e2.
     float r2 = dot3(sp.muc, sp.muc);
@@ -272,22 +364,7 @@ static void preprocess_one(const Oracle& O, const ViewState& vs, int64_t g, Spla
     // (1-eps^2)/eps^2 >= 4 (1 + q_cut tr(Sigma_2)) - 1 > q_cut * lambda_max / lambda... i.e.
     // q >= tan^2 / lambda_max(Sigma_2) > q_cut (tr >= lambda_max), DESIGN R8.
     sp.eps = 0.5f / std::sqrt(std::fmaf(sp.qcut, s00 + s11, 1.0f));
-    float Ai[6];
-    conj3(v.R, &S.icov[6 * g], Ai);  // A = W Sigma_w^-1 W^T = Sigma_c^-1
-    sp.A[0] = Ai[0];
-    sp.A[1] = 2.0f * Ai[1];
-    sp.A[2] = Ai[3];
-    sp.A[3] = 2.0f * Ai[2];
-    sp.A[4] = 2.0f * Ai[4];
-    sp.A[5] = Ai[5];
-    float Am[3][3] = {{Ai[0], Ai[1], Ai[2]}, {Ai[1], Ai[3], Ai[4]}, {Ai[2], Ai[4], Ai[5]}};
-    for (int i = 0; i < 3; i++) sp.bv[i] = dot3(Am[i], sp.muc);
-    {   // colour: SH along the world-space direction o -> mu (L18)
-        double d[3] = {(double)mu[0] - v.o[0], (double)mu[1] - v.o[1], (double)mu[2] - v.o[2]};
-        double nd = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
-        for (int i = 0; i < 3; i++) d[i] /= nd;
-        sh_color(&S.sh[(size_t)g * S.ncoef * 3], S.deg, d, sp.rgb);
-    }
+    depth_and_colour(S, v, g, sp);
     // O6(a) cone vs frustum side planes (conservative, double, margin 1e-4).
     double S00 = s00, S01 = s01, S11 = s11;
     double lmax = 0.5 * (S00 + S11) + std::sqrt(0.25 * (S00 - S11) * (S00 - S11) + S01 * S01);
@@ -350,15 +427,49 @@ static void preprocess_one(const Oracle& O, const ViewState& vs, int64_t g, Spla
     }
     if (whole) { xmin = -1.0; xmax = W + 1.0; ymin = -1.0; ymax = H + 1.0; }
     // O6(d) expand by 1 px, inclusive coarse-tile rect, clamp.
-    xmin -= 1.0; xmax += 1.0; ymin -= 1.0; ymax += 1.0;
-    sp.bbox[0] = (float)std::max(xmin, -2.0); sp.bbox[1] = (float)std::min(xmax, W + 2.0);
-    sp.bbox[2] = (float)std::max(ymin, -2.0); sp.bbox[3] = (float)std::min(ymax, H + 2.0);
-    const int T_a = O.p.assign_tile;
-    if (xmax < 0.0 || ymax < 0.0 || xmin > W || ymin > H) return;  // empty rect
-    sp.rect[0] = std::max(0, (int)std::floor(std::max(xmin, 0.0) / T_a));
-    sp.rect[1] = std::max(0, (int)std::floor(std::max(ymin, 0.0) / T_a));
-    sp.rect[2] = std::min(vs.tw - 1, (int)std::floor(std::min(xmax, W) / T_a));
-    sp.rect[3] = std::min(vs.th - 1, (int)std::floor(std::min(ymax, H) / T_a));
+    set_rect(O, vs, xmin - 1.0, xmax + 1.0, ymin - 1.0, ymax + 1.0, sp);
+}
+
+/* Minimum of the 2D quadratic X^T C X over a convex polygon (vertices relative
+ * to the Gaussian's mean): 0 if the mean (origin) is inside (all edge cross
+ * products share a sign), else Eq.4 on every edge with t
+ * clamped to [0,1], strictly smaller q wins (earlier edge on ties). */
+static void poly_min(const float* C, const float* yx, const float* yy, int n, float* qmin_out, float* hx_out,
+                     float* hy_out) {
+    // mean (chart origin) inside the convex polygon: all edge cross products share a sign
+    int npos = 0, nneg = 0;
+    for (int k = 0; k < n; k++) {
+        int k1 = (k + 1 == n) ? 0 : k + 1;
+        float ddx = yx[k1] - yx[k], ddy = yy[k1] - yy[k];
+        float cr = std::fmaf(ddy, yx[k], -(ddx * yy[k]));
+        if (cr >= 0.0f) npos++;
+        if (cr <= 0.0f) nneg++;
+    }
+    float hx, hy, qmin;
+    if (npos == n || nneg == n) {
+        hx = 0.0f; hy = 0.0f; qmin = 0.0f;  // x_hat = mu_2D (P:371)
+    } else {
+        qmin = INFINITY; hx = 0.0f; hy = 0.0f;
+        for (int k = 0; k < n; k++) {  // Eq.4 on every edge, t clamped to [0,1]
+            int k1 = (k + 1 == n) ? 0 : k + 1;
+            float ppx = yx[k], ppy = yy[k];
+            float ddx = yx[k1] - yx[k], ddy = yy[k1] - yy[k];
+            float cdx = std::fmaf(C[0], ddx, C[1] * ddy), cdy = std::fmaf(C[1], ddx, C[2] * ddy);
+            float den = std::fmaf(ddx, cdx, ddy * cdy);
+            float nmr = -std::fmaf(ppx, cdx, ppy * cdy);  // d^T C (mu2D - p), mu2D = 0
+            float t;
+            if (nmr <= 0.0f || !(den > 0.0f)) t = 0.0f;
+            else if (nmr >= den) t = 1.0f;
+            else t = nmr / den;
+            float X = std::fmaf(t, ddx, ppx), Y = std::fmaf(t, ddy, ppy);
+            float cX = std::fmaf(C[0], X, C[1] * Y), cY = std::fmaf(C[1], X, C[2] * Y);
+            float q = std::fmaf(X, cX, Y * cY);
+            if (q < qmin) { qmin = q; hx = X; hy = Y; }
+        }
+    }
+    *qmin_out = qmin;
+    *hx_out = hx;
+    *hy_out = hy;
 }
 
 /* O7 (Eq.4) on the Gaussian's optimal plane; returns keep and
@@ -405,39 +516,30 @@ static bool tile_test(const Splat& sp, const orc_view& v, int x0, int y0, int x1
         yx[k] = dot3(sp.e1, d) * is;
         yy[k] = dot3(sp.e2, d) * is;
     }
-    // mean (chart origin) inside the convex polygon: all edge cross products share a sign
-    int npos = 0, nneg = 0;
-    for (int k = 0; k < n; k++) {
-        int k1 = (k + 1 == n) ? 0 : k + 1;
-        float ddx = yx[k1] - yx[k], ddy = yy[k1] - yy[k];
-        float cr = std::fmaf(ddy, yx[k], -(ddx * yy[k]));
-        if (cr >= 0.0f) npos++;
-        if (cr <= 0.0f) nneg++;
-    }
     float hx, hy, qmin;
-    if (npos == n || nneg == n) {
-        hx = 0.0f; hy = 0.0f; qmin = 0.0f;  // x_hat = mu_2D (P:371)
-    } else {
-        qmin = INFINITY; hx = 0.0f; hy = 0.0f;
-        for (int k = 0; k < n; k++) {  // Eq.4 on every edge, t clamped to [0,1]
-            int k1 = (k + 1 == n) ? 0 : k + 1;
-            float ppx = yx[k], ppy = yy[k];
-            float ddx = yx[k1] - yx[k], ddy = yy[k1] - yy[k];
-            float cdx = std::fmaf(sp.C[0], ddx, sp.C[1] * ddy), cdy = std::fmaf(sp.C[1], ddx, sp.C[2] * ddy);
-            float den = std::fmaf(ddx, cdx, ddy * cdy);
-            float nmr = -std::fmaf(ppx, cdx, ppy * cdy);  // d^T C (mu2D - p), mu2D = 0
-            float t;
-            if (nmr <= 0.0f || !(den > 0.0f)) t = 0.0f;
-            else if (nmr >= den) t = 1.0f;
-            else t = nmr / den;
-            float X = std::fmaf(t, ddx, ppx), Y = std::fmaf(t, ddy, ppy);
-            float cX = std::fmaf(sp.C[0], X, sp.C[1] * Y), cY = std::fmaf(sp.C[1], X, sp.C[2] * Y);
-            float q = std::fmaf(X, cX, Y * cY);
-            if (q < qmin) { qmin = q; hx = X; hy = Y; }
-        }
-    }
+    poly_min(sp.C, yx, yy, n, &qmin, &hx, &hy);
     *qmin_out = qmin;
     for (int i = 0; i < 3; i++) dhat[i] = std::fmaf(hy, sp.e2[i], std::fmaf(hx, sp.e1[i], sp.u[i]));
+    return qmin <= sp.qcut * 1.001f;
+}
+
+/* EWA baseline O7: StopThePop's screen-space tile test: the tile's
+ * pixel-edge rectangle relative to the projected mean, the same polygon
+ * minimum in pixel units; the ray through x_hat gives the key depth. */
+static bool tile_test_ewa(const Splat& sp, const orc_view& v, int x0, int y0, int x1, int y1, float* qmin_out,
+                          float dhat[3]) {
+    const int cx_[4] = {x0, x1, x1, x0}, cy_[4] = {y0, y0, y1, y1};
+    float yx[4], yy[4];
+    for (int k = 0; k < 4; k++) {
+        yx[k] = (float)cx_[k] - sp.m2[0];
+        yy[k] = (float)cy_[k] - sp.m2[1];
+    }
+    float hx, hy, qmin;
+    poly_min(sp.Cp, yx, yy, 4, &qmin, &hx, &hy);
+    *qmin_out = qmin;
+    dhat[0] = ((sp.m2[0] + hx) - v.cx) / v.fx;
+    dhat[1] = ((sp.m2[1] + hy) - v.cy) / v.fy;
+    dhat[2] = 1.0f;
     return qmin <= sp.qcut * 1.001f;
 }
 
@@ -536,7 +638,9 @@ static void for_kept_tiles(const Oracle& O, const ViewState& vs, const Splat& sp
             if (!vs.vis[(size_t)ty * vs.tw + tx]) continue;
             int x0 = tx * T, y0 = ty * T, x1 = std::min(x0 + T, vs.v.width), y1 = std::min(y0 + T, vs.v.height);
             float qmin, dh[3];
-            if (tile_test(sp, vs.v, x0, y0, x1, y1, &qmin, dh)) f(tx, ty, dh);
+            const bool keep = (O.p.projection == 1) ? tile_test_ewa(sp, vs.v, x0, y0, x1, y1, &qmin, dh)
+                                                     : tile_test(sp, vs.v, x0, y0, x1, y1, &qmin, dh);
+            if (keep) f(tx, ty, dh);
         }
 }
 
@@ -577,14 +681,22 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
         st.evals++;
         uint32_t g = O.vals[i];
         const Splat& sp = vs.splats[g];
-        float s = std::fmaf(sp.u[0], x, std::fmaf(sp.u[1], y, sp.u[2]));
-        if (!(s > 0.0f)) continue;
-        float num = chart_num(sp.e1, sp.e2, sp.C, dray);
-        float ss = s * s;
-        if (!(num <= sp.qcut * ss)) continue;  // alpha < 1/255, division-free (R3)
-        float den = quad3(sp.A, x, y, 1.0f);
-        float dtb = std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2]));
-        SampleAT at = sample_alpha_tau(num, ss, den, dtb, sp.sigma);  // P:254, L10, R9
+        SampleAT at;
+        if (O.p.projection == 1) {  // EWA baseline: q from the projected mean in pixels
+            float q = ewa_q(sp.Cp, xs - sp.m2[0], ys - sp.m2[1]);
+            if (!(q <= sp.qcut)) continue;
+            at = sample_alpha_tau_ewa(q, quad3(sp.A, x, y, 1.0f),
+                                      std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2])), sp.sigma);
+        } else {
+            float s = std::fmaf(sp.u[0], x, std::fmaf(sp.u[1], y, sp.u[2]));
+            if (!(s > 0.0f)) continue;
+            float num = chart_num(sp.e1, sp.e2, sp.C, dray);
+            float ss = s * s;
+            if (!(num <= sp.qcut * ss)) continue;  // alpha < 1/255, division-free (R3)
+            float den = quad3(sp.A, x, y, 1.0f);
+            float dtb = std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2]));
+            at = sample_alpha_tau(num, ss, den, dtb, sp.sigma);  // P:254, L10, R9
+        }
         float alpha = at.alpha;
         float tau = at.tau;  // depth of max density along this pixel's ray (O10)
         st.contribs++;
@@ -765,6 +877,7 @@ int orc_prepare(void* h, int n_views, const orc_view* views, const orc_params* p
     Oracle& O = *(Oracle*)h;
     O.p = *p;
     if (O.p.assign_tile != 16 && O.p.assign_tile != 32) return 1;
+    if (O.p.projection != 0 && O.p.projection != 1) return 4;
     O.views.assign(n_views, ViewState());
     O.ntiles = 0;
     for (int v = 0; v < n_views; v++) {
@@ -896,6 +1009,7 @@ void orc_get_splats(void* h, int view, float* out) {
             o[13 + i] = s.S2[i]; o[16 + i] = s.C[i]; o[31 + i] = s.bv[i]; o[34 + i] = s.rgb[i];
         }
         o[19] = s.eps;
+        o[20] = s.m2[0]; o[21] = s.m2[1]; o[22] = s.Cp[0]; o[23] = s.Cp[1]; o[24] = s.Cp[2];
         for (int i = 0; i < 6; i++) o[25 + i] = s.A[i];
         o[37] = s.sigma; o[38] = s.qcut;
         for (int i = 0; i < 4; i++) { o[39 + i] = (float)s.rect[i]; o[43 + i] = s.bbox[i]; }
@@ -1021,14 +1135,21 @@ int orc_render_bruteforce(void* h, int view, float* rgba, float* depth) {
             for (int64_t g = 0; g < N; g++) {
                 const Splat& sp = vs.splats[g];
                 if (!sp.valid) continue;
-                float s = std::fmaf(sp.u[0], x, std::fmaf(sp.u[1], y, sp.u[2]));
-                if (!(s > 0.0f)) continue;
-                float dray[3] = {x, y, 1.0f};
-                float num = chart_num(sp.e1, sp.e2, sp.C, dray);
-                if (!(num <= sp.qcut * (s * s))) continue;
                 float den = quad3(sp.A, x, y, 1.0f);
                 float dtb = std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2]));
-                SampleAT at = sample_alpha_tau(num, s * s, den, dtb, sp.sigma);
+                SampleAT at;
+                if (O.p.projection == 1) {
+                    float q = ewa_q(sp.Cp, ((float)i + 0.5f) - sp.m2[0], ((float)j + 0.5f) - sp.m2[1]);
+                    if (!(q <= sp.qcut)) continue;
+                    at = sample_alpha_tau_ewa(q, den, dtb, sp.sigma);
+                } else {
+                    float s = std::fmaf(sp.u[0], x, std::fmaf(sp.u[1], y, sp.u[2]));
+                    if (!(s > 0.0f)) continue;
+                    float dray[3] = {x, y, 1.0f};
+                    float num = chart_num(sp.e1, sp.e2, sp.C, dray);
+                    if (!(num <= sp.qcut * (s * s))) continue;
+                    at = sample_alpha_tau(num, s * s, den, dtb, sp.sigma);
+                }
                 all.push_back(WEnt{at.tau, (uint32_t)g, at.alpha});
             }
             std::stable_sort(all.begin(), all.end(), [](const WEnt& a, const WEnt& c) {
@@ -1060,7 +1181,8 @@ int orc_tile_test(void* h, int view, int64_t g, int x0, int y0, int x1, int y1, 
     const Splat& sp = vs.splats[g];
     if (!sp.valid) { out[0] = -1.0f; return 0; }
     float qmin = 0.0f, dh[3] = {0, 0, 0};
-    bool keep = tile_test(sp, vs.v, x0, y0, x1, y1, &qmin, dh);
+    bool keep = (O.p.projection == 1) ? tile_test_ewa(sp, vs.v, x0, y0, x1, y1, &qmin, dh)
+                                       : tile_test(sp, vs.v, x0, y0, x1, y1, &qmin, dh);
     out[0] = keep ? 1.0f : 0.0f;
     out[1] = qmin;
     out[2] = tile_depth(sp, dh, O.p.near_plane);

@@ -503,3 +503,76 @@ def test_keys_sorted_stable_and_ranges(oracle_mod):
     # emission order: view-major, then g ascending
     view_of = (ku >> np.uint64(32)).astype(np.int64) // (8 * 6)
     assert np.all(np.diff(view_of) >= 0)
+
+
+# --------------------------------------------------------------------- EWA baseline (config C5)
+
+@pytest.mark.parametrize("f,s,z,sigma,dc", [(64.0, 0.1, 4.0, 0.9, 0.3), (40.0, 0.3, 7.0, 0.99, 1.2)])
+def test_ewa_P1_onaxis_closed_form(oracle_mod, f, s, z, sigma, dc):
+    """EWA mode (Eq.3) on the optical axis: J = (f/z)[I 0], so
+    q = |D|^2/(f^2 s^2/z^2 + 0.3) exactly like P1."""
+    W = H = 64
+    sc = scene_from([[0, 0, z]], s, opacities=sigma, dc=[dc] * 3)
+    o = oracle_mod.Oracle(sc).prepare([identity_camera(W, H, f)], assign_tile=16, projection=1)
+    (img, dep), = o.render()
+    jj, ii = np.mgrid[0:H, 0:W]
+    dx, dy = ii + 0.5 - W / 2, jj + 0.5 - H / 2
+    q = (dx ** 2 + dy ** 2) / (f * f * s * s / (z * z) + 0.3)
+    a = np.minimum(0.99, sigma * np.exp(-q / 2))
+    qcut = 2 * math.log(255 * np.float32(sigma))
+    inside = q <= qcut * (1 - 1e-5)
+    np.testing.assert_allclose(img[..., 3][inside], a[inside], rtol=2e-5, atol=1e-7)
+    assert np.all(img[..., 3][q > qcut * (1 + 1e-5)] == 0)
+
+
+@pytest.mark.parametrize("seed", list(range(100, 110)))
+def test_ewa_P9_windowed_equals_bruteforce(oracle_mod, seed):
+    """P9 for the EWA mode: tile lists sound, windowed = tile-free full sort."""
+    sc, cam = tiny_set(seed)
+    o = oracle_mod.Oracle(sc).prepare([cam], assign_tile=16, window_k=64, projection=1)
+    (img, dep), = o.render()
+    bf, bd = o.bruteforce(0)
+    assert np.array_equal(img, bf) and np.array_equal(dep, bd)
+
+
+def test_ewa_culling_sound(oracle_mod):
+    """P4 for the EWA mode: a culled screen tile has no pixel-space point with
+    q <= q_cut (dense 64x64 sampling, double)."""
+    sc = sg.random_scene(1, n=300)
+    cam = identity_camera(128, 128, 64.0)
+    o = oracle_mod.Oracle(sc).prepare([cam], assign_tile=16, projection=1)
+    sps = o.splats(0)
+    lin = np.linspace(0, 1, 64)
+    ncull = 0
+    for g in range(0, 300, 3):
+        sp = sps[g]
+        if sp[0] == 0:
+            continue
+        m, C = sp[20:22].astype(np.float64), sp[22:25].astype(np.float64)
+        for ty in range(8):
+            for tx in range(8):
+                r = o.tile_test(0, g, tx * 16, ty * 16, tx * 16 + 16, ty * 16 + 16)
+                if r["keep"] == 0:
+                    ncull += 1
+                    X = tx * 16 + 16 * lin[None, :] - m[0]
+                    Y = ty * 16 + 16 * lin[:, None] - m[1]
+                    q = C[0] * X * X + 2 * C[1] * X * Y + C[2] * Y * Y
+                    assert q.min() > sp[38]
+    assert ncull > 100
+
+
+def test_large_fov_identity_distinguishes_op_from_ewa(oracle_mod):
+    """The paper's large-FOV protocol (App. D): the 3x-resolution
+    crop equals the normal render for Optimal Projection (pin P13) but not for
+    the EWA local-affine projection, whose error grows off-axis."""
+    sc = sg.random_scene(6, n=800, z_range=(1.5, 6.0), xy_frac=2.0)
+    W, H = 64, 48
+    small = identity_camera(W, H, 40.0)
+    large = identity_camera(3 * W, 3 * H, 40.0, cx=small.cx + W, cy=small.cy + H)
+    res = {}
+    for proj in (0, 1):
+        (a, _), = oracle_mod.Oracle(sc).prepare([small], assign_tile=16, projection=proj).render()
+        (b, _), = oracle_mod.Oracle(sc).prepare([large], assign_tile=16, projection=proj).render()
+        res[proj] = np.abs(a - b[H:2 * H, W:2 * W]).max()
+    assert res[0] == 0.0
+    assert res[1] > 1e-3
