@@ -69,7 +69,8 @@ typedef struct {
     int32_t max_height;
     int32_t window_k;        /* per-sample StopThePop resort window; only 16 is compiled */
     int32_t assign_tile;     /* 16 or 32: Gaussian/tile assignment size */
-    int32_t projection;      /* 0 = Optimal Projection (only mode; EWA is a later row) */
+    int32_t projection;      /* 0 = Optimal Projection (the method); 1 = EWA local-affine baseline
+                                (Eq.3; 3DGS computeCov2D; config C5 comparison) */
     float near_plane;        /* view-space near cull, 0.2 */
     float background[3];     /* composited under residual transmittance; (0,0,0) */
 } vrs_config;

@@ -89,10 +89,7 @@ __device__ __forceinline__ float fast_ex2(float x) {
 // serves x = -q/2 log2 e and tau = dtb/den; alpha = min(0.99, sigma 2^x) with
 // the contract's deterministic binary32 exp2 -- the oracle evaluates the
 // identical operations, so transmittance and the T < 1e-4 stop are exact.
-__device__ __forceinline__ float alpha_tau(float num, float ss, float den, float dtb, float sigma, float& tau) {
-    const float r = __frcp_rn(ss * den);
-    const float x = fmaxf((num * -0.72134752f) * (den * r), -64.0f);  // NaN/-inf guard
-    tau = dtb * (ss * r);
+__device__ __forceinline__ float alpha_of_x(float x, float sigma) {
     const float fl = floorf(x);
     const float f = x - fl;
     float p = 0.00187757565f;
@@ -105,6 +102,12 @@ __device__ __forceinline__ float alpha_tau(float num, float ss, float den, float
     const float a = sigma * e;
     return a < kAlphaMax ? a : kAlphaMax;
 }
+__device__ __forceinline__ float alpha_tau(float num, float ss, float den, float dtb, float sigma, float& tau) {
+    const float r = __frcp_rn(ss * den);
+    const float x = fmaxf((num * -0.72134752f) * (den * r), -64.0f);  // NaN/-inf guard
+    tau = dtb * (ss * r);
+    return alpha_of_x(x, sigma);
+}
 __device__ __forceinline__ float key_tau(unsigned long long key) {
     const uint32_t k = (uint32_t)(key >> 32);
     return __uint_as_float(k ^ (((int32_t)k < 0) ? 0x80000000u : 0xffffffffu));
@@ -112,7 +115,7 @@ __device__ __forceinline__ float key_tau(unsigned long long key) {
 
 }  // namespace
 
-template <bool kCounters>
+template <bool kCounters, bool kEwa>
 __global__ void __launch_bounds__(kBlend, 4) k_blend(FrameParams fp, FrameBufs fb, float* __restrict__ rgba,
                                                       float* __restrict__ depth) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -223,20 +226,33 @@ __global__ void __launch_bounds__(kBlend, 4) k_blend(FrameParams fp, FrameBufs f
                 const int j = c + __ffs(bits) - 1;
                 bits &= bits - 1;
                 if (done) continue;
-                const float4 a0 = S.r0[j], a1 = S.r1[j], a2 = S.r2[j];
-                const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
-                const float ex = fmaf(a1.x, x, a1.y);
-                const float ey = fmaf(a1.z, x, fmaf(a1.w, y, a2.x));
-                const float cx = fmaf(a2.y, ex, a2.z * ey), cy = fmaf(a2.z, ex, a2.w * ey);
-                const float num = fmaf(ex, cx, ey * cy);
-                const float ss = s * s;
-                if (!(s > 0.0f) || !(num <= a0.w * ss)) continue;
-                // contribution: alpha (tolerance-only), tau (decision, IEEE division)
-                const float4 a3 = S.r3[j], a4 = S.r4[j], a5 = S.r5[j];
-                const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
-                const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, a5.x));
-                float tau;
-                const float alpha = alpha_tau(num, ss, den, dtb, a5.y, tau);
+                float alpha, tau;
+                if (kEwa) {  // EWA baseline: q from the projected mean in pixels
+                    const float4 a0 = S.r0[j], a1 = S.r1[j];
+                    const float dxp = xs - a0.x, dyp = ys - a0.y;
+                    const float q = fmaf(dxp, fmaf(a0.w, dxp, a1.x * dyp), dyp * fmaf(a1.x, dxp, a1.y * dyp));
+                    if (!(q <= a0.z)) continue;
+                    const float4 a3 = S.r3[j], a4 = S.r4[j], a5 = S.r5[j];
+                    const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
+                    const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, a5.x));
+                    tau = __fdiv_rn(dtb, den);
+                    alpha = alpha_of_x(fmaxf(q * -0.72134752f, -64.0f), a5.y);
+                } else {
+                    const float4 a0 = S.r0[j], a1 = S.r1[j], a2 = S.r2[j];
+                    const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
+                    const float ex = fmaf(a1.x, x, a1.y);
+                    const float ey = fmaf(a1.z, x, fmaf(a1.w, y, a2.x));
+                    const float cx = fmaf(a2.y, ex, a2.z * ey), cy = fmaf(a2.z, ex, a2.w * ey);
+                    const float num = fmaf(ex, cx, ey * cy);
+                    const float ss = s * s;
+                    if (!(s > 0.0f) || !(num <= a0.w * ss)) continue;
+                    // contribution: alpha and tau (R9: one IEEE reciprocal, exact on both sides)
+                    const float4 a3 = S.r3[j], a4 = S.r4[j];
+                    const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
+                    const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, S.r5[j].x));
+                    alpha = alpha_tau(num, ss, den, dtb, S.r5[j].y, tau);
+                }
+                const float4 a5 = S.r5[j];
                 const unsigned long long key = order_key(tau, __float_as_uint(a5.z));
                 if (kCounters) n_contrib++;
                 // insert, then pop the minimum of the K+1 entries
@@ -344,14 +360,19 @@ void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* r
     const size_t smem = sizeof(BlendSmem);
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(k_blend<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_blend<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_blend<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr_set = true;
     }
-    if (fp.counters)
-        k_blend<true><<<total_items, kBlend, smem, st>>>(fp, fb, rgba, depth);
-    else
-        k_blend<false><<<total_items, kBlend, smem, st>>>(fp, fb, rgba, depth);
+    if (fp.ewa) {
+        if (fp.counters) k_blend<true, true><<<total_items, kBlend, smem, st>>>(fp, fb, rgba, depth);
+        else k_blend<false, true><<<total_items, kBlend, smem, st>>>(fp, fb, rgba, depth);
+    } else {
+        if (fp.counters) k_blend<true, false><<<total_items, kBlend, smem, st>>>(fp, fb, rgba, depth);
+        else k_blend<false, false><<<total_items, kBlend, smem, st>>>(fp, fb, rgba, depth);
+    }
 }
 
 // Step 7: periphery reconstruction: nearest-neighbour upsample of the

@@ -21,7 +21,82 @@ struct Proj {
     float sigma, qcut;
     int rect[4];
     float bbox[4];
+    float m2[2], Cp[3];  // EWA baseline: pixel mean and conic
 };
+
+__device__ __forceinline__ void set_rect(const ViewParams& v, int T, double xmin, double xmax, double ymin,
+                                         double ymax, Proj& p) {
+    const double W = v.W, H = v.H;
+    p.bbox[0] = (float)fmax(xmin, -2.0); p.bbox[1] = (float)fmin(xmax, W + 2.0);
+    p.bbox[2] = (float)fmax(ymin, -2.0); p.bbox[3] = (float)fmin(ymax, H + 2.0);
+    if (xmax < 0.0 || ymax < 0.0 || xmin > W || ymin > H) return;
+    p.rect[0] = max(0, (int)floor(fmax(xmin, 0.0) / T));
+    p.rect[1] = max(0, (int)floor(fmax(ymin, 0.0) / T));
+    p.rect[2] = min(v.tw - 1, (int)floor(fmin(xmax, W) / T));
+    p.rect[3] = min(v.th - 1, (int)floor(fmin(ymax, H) / T));
+}
+
+// Sigma_c = W Sigma W^T (T = W*Sigma, then T*W^T, each entry a dot3)
+__device__ __forceinline__ void conj3(const ViewParams& v, float4 a, float4 b, float Sc[3][3]) {
+    const float S[3][3] = {{a.x, a.y, a.z}, {a.y, a.w, b.x}, {a.z, b.x, b.y}};
+    float Tm[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = 0; j < 3; j++) Tm[i][j] = dot3(v.R[3 * i], v.R[3 * i + 1], v.R[3 * i + 2], S[0][j], S[1][j], S[2][j]);
+#pragma unroll
+    for (int i = 0; i < 3; i++)
+#pragma unroll
+        for (int j = i; j < 3; j++) Sc[i][j] = dot3(Tm[i][0], Tm[i][1], Tm[i][2], v.R[3 * j], v.R[3 * j + 1], v.R[3 * j + 2]);
+    Sc[1][0] = Sc[0][1]; Sc[2][0] = Sc[0][2]; Sc[2][1] = Sc[1][2];
+}
+
+// EWA baseline (Eq.3; 3DGS computeCov2D with its 1.3 tan(fov/2)
+// clamp, SURVEY "EWA mode", config C5): pixel-space conic from the local-affine
+// Jacobian at the clamped mean, + 0.3 px^2, screen-space footprint.
+__device__ void project_splat_ewa(const ViewParams& v, float4 m4, float4 c0, float4 c1, float4 i0, float4 i1,
+                                  int T, float near_plane, Proj& p) {
+    p.valid = 0;
+    p.rect[0] = 0; p.rect[1] = 0; p.rect[2] = -1; p.rect[3] = -1;
+    p.qcut = m4.w;
+    p.sigma = c1.z;
+    const float vx = m4.x - v.o[0], vy = m4.y - v.o[1], vz = m4.z - v.o[2];
+    p.muc[0] = dot3(v.R[0], v.R[1], v.R[2], vx, vy, vz);
+    p.muc[1] = dot3(v.R[3], v.R[4], v.R[5], vx, vy, vz);
+    p.muc[2] = dot3(v.R[6], v.R[7], v.R[8], vx, vy, vz);
+    if (!(p.muc[2] > near_plane) || p.qcut < 0.0f) return;
+    float Sc[3][3];
+    conj3(v, c0, c1, Sc);
+    const float z = p.muc[2];
+    const float limx = 1.3f * ((0.5f * (float)v.W) / v.fx), limy = 1.3f * ((0.5f * (float)v.H) / v.fy);
+    const float txtz = p.muc[0] / z, tytz = p.muc[1] / z;
+    const float tx = fminf(limx, fmaxf(-limx, txtz)) * z;
+    const float ty = fminf(limy, fmaxf(-limy, tytz)) * z;
+    const float zz = z * z;
+    const float J00 = v.fx / z, J02 = -(v.fx * tx) / zz, J11 = v.fy / z, J12 = -(v.fy * ty) / zz;
+    const float a0 = fmaf(J00, Sc[0][0], J02 * Sc[0][2]), a1 = fmaf(J00, Sc[0][1], J02 * Sc[1][2]),
+                a2 = fmaf(J00, Sc[0][2], J02 * Sc[2][2]);
+    const float b1 = fmaf(J11, Sc[1][1], J12 * Sc[1][2]), b2 = fmaf(J11, Sc[1][2], J12 * Sc[2][2]);
+    float c00 = fmaf(a0, J00, a2 * J02), c01 = fmaf(a1, J11, a2 * J12), c11 = fmaf(b1, J11, b2 * J12);
+    c00 = c00 + 0.3f;
+    c11 = c11 + 0.3f;
+    p.S2[0] = c00; p.S2[1] = c01; p.S2[2] = c11;
+    const float det = fmaf(c00, c11, -(c01 * c01));
+    if (!(det > 0.0f)) return;
+    const float idet = 1.0f / det;
+    p.Cp[0] = c11 * idet; p.Cp[1] = -c01 * idet; p.Cp[2] = c00 * idet;
+    p.m2[0] = fmaf(v.fx, p.muc[0] / z, v.cx);
+    p.m2[1] = fmaf(v.fy, p.muc[1] / z, v.cy);
+    float Ai[3][3];
+    conj3(v, i0, i1, Ai);
+    p.A[0] = Ai[0][0]; p.A[1] = 2.0f * Ai[0][1]; p.A[2] = Ai[1][1];
+    p.A[3] = 2.0f * Ai[0][2]; p.A[4] = 2.0f * Ai[1][2]; p.A[5] = Ai[2][2];
+#pragma unroll
+    for (int i = 0; i < 3; i++) p.bv[i] = dot3(Ai[i][0], Ai[i][1], Ai[i][2], p.muc[0], p.muc[1], p.muc[2]);
+    p.valid = 1;
+    const double rx = sqrt((double)p.qcut * c00), ry = sqrt((double)p.qcut * c11);
+    set_rect(v, T, p.m2[0] - rx - 1.0, p.m2[0] + rx + 1.0, p.m2[1] - ry - 1.0, p.m2[1] + ry + 1.0, p);
+}
 
 // O1-O6 (DESIGN "Numerics contract"): view transform and near cull,
 // optimal-plane frame, projected covariance with pixel-mapped dilation,
@@ -173,14 +248,7 @@ __device__ void project_splat(const ViewParams& v, float4 m4, float4 c0, float4 
         }
     }
     if (whole) { xmin = -1.0; xmax = W + 1.0; ymin = -1.0; ymax = H + 1.0; }
-    xmin -= 1.0; xmax += 1.0; ymin -= 1.0; ymax += 1.0;
-    p.bbox[0] = (float)fmax(xmin, -2.0); p.bbox[1] = (float)fmin(xmax, W + 2.0);
-    p.bbox[2] = (float)fmax(ymin, -2.0); p.bbox[3] = (float)fmin(ymax, H + 2.0);
-    if (xmax < 0.0 || ymax < 0.0 || xmin > W || ymin > H) return;
-    p.rect[0] = max(0, (int)floor(fmax(xmin, 0.0) / T));
-    p.rect[1] = max(0, (int)floor(fmax(ymin, 0.0) / T));
-    p.rect[2] = min(v.tw - 1, (int)floor(fmin(xmax, W) / T));
-    p.rect[3] = min(v.th - 1, (int)floor(fmin(ymax, H) / T));
+    set_rect(v, T, xmin - 1.0, xmax + 1.0, ymin - 1.0, ymax + 1.0, p);
 }
 
 // Splat fields needed by the tile test and the key.
@@ -207,6 +275,43 @@ __device__ __forceinline__ void eq4_edge(const TileSplat& s, float ppx, float pp
     if (q < qmin) { qmin = q; hx = X; hy = Y; }
 }
 
+// Minimum of X^T C X over a quad (vertices relative to the mean): 0 if the
+// mean is inside, else Eq.4 on the four edges.
+__device__ __forceinline__ void quad_min(const TileSplat& s, const float yx[4], const float yy[4], float& qmin,
+                                         float& hx, float& hy) {
+    int npos = 0, nneg = 0;
+#pragma unroll
+    for (int k = 0; k < 4; k++) {
+        const int k1 = (k + 1) & 3;
+        const float ddx = yx[k1] - yx[k], ddy = yy[k1] - yy[k];
+        const float cr = fmaf(ddy, yx[k], -(ddx * yy[k]));
+        npos += (cr >= 0.0f) ? 1 : 0;
+        nneg += (cr <= 0.0f) ? 1 : 0;
+    }
+    if (npos == 4 || nneg == 4) {
+        qmin = 0.0f;
+    } else {
+        qmin = __int_as_float(0x7f800000);
+#pragma unroll
+        for (int k = 0; k < 4; k++) eq4_edge(s, yx[k], yy[k], yx[(k + 1) & 3], yy[(k + 1) & 3], qmin, hx, hy);
+    }
+}
+
+// EWA baseline O7: StopThePop's screen-space tile test: the tile
+// rectangle relative to the projected mean, Eq.4 in pixel units (C = pixel
+// conic, stored in C0..C2; mean in ux, uy); key ray through x_hat.
+__device__ bool tile_test_ewa(const TileSplat& s, const ViewParams& v, int x0, int y0, int x1, int y1, float& dhx,
+                              float& dhy, float& dhz) {
+    const float ax = (float)x0 - s.ux, bx = (float)x1 - s.ux, ay = (float)y0 - s.uy, by = (float)y1 - s.uy;
+    const float yx[4] = {ax, bx, bx, ax}, yy[4] = {ay, ay, by, by};
+    float hx = 0.0f, hy = 0.0f, qmin;
+    quad_min(s, yx, yy, qmin, hx, hy);
+    dhx = ((s.ux + hx) - v.cx) / v.fx;
+    dhy = ((s.uy + hy) - v.cy) / v.fy;
+    dhz = 1.0f;
+    return qmin <= s.qcut * kO7Margin;
+}
+
 // O7: Eq.4 on the optimal-plane polygon of the tile, corner
 // rays clipped at s >= eps (DESIGN R8); returns keep and d_hat.
 // Fast path: all four corners in front (the common case) -> unrolled quad.
@@ -231,22 +336,7 @@ __device__ bool tile_test(const TileSplat& s, const ViewParams& v, int x0, int y
             yx[k] = dot3(s.e1x, 0.0f, s.e1z, dx[k], dy[k], 1.0f) * is;
             yy[k] = dot3(s.e2x, s.e2y, s.e2z, dx[k], dy[k], 1.0f) * is;
         }
-        int npos = 0, nneg = 0;
-#pragma unroll
-        for (int k = 0; k < 4; k++) {
-            const int k1 = (k + 1) & 3;
-            const float ddx = yx[k1] - yx[k], ddy = yy[k1] - yy[k];
-            const float cr = fmaf(ddy, yx[k], -(ddx * yy[k]));
-            npos += (cr >= 0.0f) ? 1 : 0;
-            nneg += (cr <= 0.0f) ? 1 : 0;
-        }
-        if (npos == 4 || nneg == 4) {
-            qmin = 0.0f;
-        } else {
-            qmin = __int_as_float(0x7f800000);
-#pragma unroll
-            for (int k = 0; k < 4; k++) eq4_edge(s, yx[k], yy[k], yx[(k + 1) & 3], yy[(k + 1) & 3], qmin, hx, hy);
-        }
+        quad_min(s, yx, yy, qmin, hx, hy);
     } else {
         // partially behind the clip level: Sutherland-Hodgman against s >= eps
         float px[5], py[5];
@@ -401,7 +491,9 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
             const float mx = dot3(v.R[0], v.R[1], v.R[2], vx, vy, vz);
             const float my = dot3(v.R[3], v.R[4], v.R[5], vx, vy, vz);
             const float mz = dot3(v.R[6], v.R[7], v.R[8], vx, vy, vz);
-            if (mz > fp.near_plane) {
+            if (mz > fp.near_plane && fp.ewa) {
+                pass = true;  // EWA baseline: screen-space footprint decides (no cone)
+            } else if (mz > fp.near_plane) {
                 const float r2 = dot3(mx, my, mz, mx, my, mz);
                 const float tan2 = m4.w * (smax * smax / r2 + v.dil);
                 const float sinb = sqrtf(tan2 / (1.0f + tan2)) * 1.01f + 2e-3f;
@@ -450,7 +542,8 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneDev sc, FrameParams 
         const float4 c0 = __ldg(&sc.cov[g]), c1 = __ldg(&sc.cov[N + g]);
         const float4 i0 = __ldg(&sc.icov[g]), i1 = __ldg(&sc.icov[N + g]);
         Proj p;
-        project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
+        if (fp.ewa) project_splat_ewa(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
+        else project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
         // number of (Gaussian, tile) candidates = rect area, 0 if the rect holds no
         // visible tile (SAT); the exact Eq.4 tests run load-balanced in k_tiletest
         uint32_t cnt = 0;
@@ -468,9 +561,16 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneDev sc, FrameParams 
         float4* rec = fb.rec + (size_t)sidx * kRecF4;
         const uint32_t r01 = (uint32_t)p.rect[0] | ((uint32_t)p.rect[1] << 16);
         const uint32_t r23 = (uint32_t)p.rect[2] | ((uint32_t)p.rect[3] << 16);
-        rec[0] = make_float4(p.u[0], p.u[1], p.u[2], p.qcut);
-        rec[1] = make_float4(p.e1[0], p.e1[2], p.e2[0], p.e2[1]);
-        rec[2] = make_float4(p.e2[2], p.C[0], p.C[1], p.C[2]);
+        if (fp.ewa) {
+            rec[0] = make_float4(p.m2[0], p.m2[1], p.qcut, p.Cp[0]);
+            rec[1] = make_float4(p.Cp[1], p.Cp[2], 0.0f, 0.0f);
+            rec[2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            p.eps = 0.0f;
+        } else {
+            rec[0] = make_float4(p.u[0], p.u[1], p.u[2], p.qcut);
+            rec[1] = make_float4(p.e1[0], p.e1[2], p.e2[0], p.e2[1]);
+            rec[2] = make_float4(p.e2[2], p.C[0], p.C[1], p.C[2]);
+        }
         rec[3] = make_float4(p.A[0], p.A[1], p.A[2], p.A[3]);
         rec[4] = make_float4(p.A[4], p.A[5], p.bv[0], p.bv[1]);
         rec[5] = make_float4(p.bv[2], p.sigma, p.eps, __uint_as_float(r01));
@@ -517,13 +617,18 @@ __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const Fram
     const int tx = tx0 + (int)(l % (uint32_t)rw), ty = ty0 + (int)(l / (uint32_t)rw);
     if (!v.vis[ty * v.tw + tx]) return false;
     TileSplat s;
-    s.ux = r0.x; s.uy = r0.y; s.uz = r0.z; s.qcut = r0.w;
-    s.e1x = r1.x; s.e1z = r1.y; s.e2x = r1.z; s.e2y = r1.w;
-    s.e2z = r2.x; s.C0 = r2.y; s.C1 = r2.z; s.C2 = r2.w;
-    s.eps = r5.z;
     const int T = fp.T, x0 = tx * T, y0 = ty * T;
     float hx, hy, hz;
-    if (!tile_test(s, v, x0, y0, min(x0 + T, v.W), min(y0 + T, v.H), hx, hy, hz)) return false;
+    if (fp.ewa) {  // record: (m.x, m.y, q_cut, Cp0) (Cp1, Cp2, -, -)
+        s.ux = r0.x; s.uy = r0.y; s.qcut = r0.z; s.C0 = r0.w; s.C1 = r1.x; s.C2 = r1.y;
+        if (!tile_test_ewa(s, v, x0, y0, min(x0 + T, v.W), min(y0 + T, v.H), hx, hy, hz)) return false;
+    } else {
+        s.ux = r0.x; s.uy = r0.y; s.uz = r0.z; s.qcut = r0.w;
+        s.e1x = r1.x; s.e1z = r1.y; s.e2x = r1.z; s.e2y = r1.w;
+        s.e2z = r2.x; s.C0 = r2.y; s.C1 = r2.z; s.C2 = r2.w;
+        s.eps = r5.z;
+        if (!tile_test(s, v, x0, y0, min(x0 + T, v.W), min(y0 + T, v.H), hx, hy, hz)) return false;
+    }
     const float4 r3 = __ldg(rec + 3), r4 = __ldg(rec + 4);
     s.A[0] = r3.x; s.A[1] = r3.y; s.A[2] = r3.z; s.A[3] = r3.w;
     s.A[4] = r4.x; s.A[5] = r4.y; s.bx = r4.z; s.by = r4.w; s.bz = r5.x;
@@ -677,7 +782,9 @@ __global__ void k_debug_splats(SceneDev sc, FrameParams fp, FrameBufs fb, int vi
     for (int i = 0; i < 6; i++) p.A[i] = 0.0f;
     for (int i = 0; i < 4; i++) p.bbox[i] = 0.0f;
     p.eps = 0.0f;
-    project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
+    p.m2[0] = p.m2[1] = p.Cp[0] = p.Cp[1] = p.Cp[2] = 0.0f;
+    if (fp.ewa) project_splat_ewa(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
+    else project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
     float* o = out + g * 48;
     for (int i = 0; i < 48; i++) o[i] = 0.0f;
     o[0] = (float)p.valid;
@@ -686,6 +793,7 @@ __global__ void k_debug_splats(SceneDev sc, FrameParams fp, FrameBufs fb, int vi
         o[13 + i] = p.S2[i]; o[16 + i] = p.C[i]; o[31 + i] = p.bv[i];
     }
     o[19] = p.eps;
+    o[20] = p.m2[0]; o[21] = p.m2[1]; o[22] = p.Cp[0]; o[23] = p.Cp[1]; o[24] = p.Cp[2];
     for (int i = 0; i < 6; i++) o[25 + i] = p.A[i];
     o[37] = p.sigma; o[38] = p.qcut;
     for (int i = 0; i < 4; i++) { o[39 + i] = (float)p.rect[i]; o[43 + i] = p.bbox[i]; }

@@ -133,7 +133,7 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     *out = nullptr;
     if (cfg->max_views < 1 || cfg->max_views > VRS_MAX_VIEWS || cfg->max_gaussians < 0 || cfg->max_pairs < 1 ||
         cfg->max_pairs >= (int64_t)1 << 30 || cfg->max_width < 1 || cfg->max_height < 1 ||
-        (cfg->assign_tile != 16 && cfg->assign_tile != 32) || cfg->window_k != kWindow || cfg->projection != 0 ||
+        (cfg->assign_tile != 16 && cfg->assign_tile != 32) || cfg->window_k != kWindow || (cfg->projection != 0 && cfg->projection != 1) ||
         !(cfg->near_plane > 0.0f) || (int64_t)cfg->max_views * cfg->max_gaussians >= ((int64_t)1 << 32))
         return VRS_E_INVALID_ARG;
     vrs_context* ctx = new vrs_context();
@@ -379,6 +379,7 @@ static vrs_status prepare_frame(vrs_context* ctx, int nv, const vrs_camera* cams
     fp.sh_coeffs = (ctx->deg + 1) * (ctx->deg + 1);
     fp.counters = ctx->counters;
     fp.no_cull = ctx->no_cull;
+    fp.ewa = ctx->cfg.projection;
     fp.N = ctx->N;
     fp.pair_cap = ctx->cfg.max_pairs;
     fp.near_plane = ctx->cfg.near_plane;

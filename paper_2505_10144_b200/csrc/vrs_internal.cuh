@@ -53,6 +53,7 @@ struct FrameParams {
     int32_t sh_coeffs;       // (deg+1)^2
     int32_t counters;        // instrumentation on
     int32_t no_cull;         // test hook: disable the warp-block footprint skip (P12)
+    int32_t ewa;             // projection: 0 = Optimal Projection, 1 = EWA baseline (config C5)
     int64_t N;
     int64_t pair_cap;
     float near_plane;

@@ -124,12 +124,12 @@ class Renderer:
     """One vrs_context (one device).  Thin object wrapper over the C ABI."""
 
     def __init__(self, max_gaussians, max_views=2, max_pairs=1 << 22, max_width=2064, max_height=2208,
-                 assign_tile=16, device=0, near_plane=0.2, background=(0.0, 0.0, 0.0), window_k=16):
+                 assign_tile=16, device=0, near_plane=0.2, background=(0.0, 0.0, 0.0), window_k=16, projection=0):
         L = lib()
         cfg = vrs_config()
         cfg.device, cfg.max_views, cfg.max_gaussians, cfg.max_pairs = device, max_views, max_gaussians, max_pairs
         cfg.max_width, cfg.max_height, cfg.window_k, cfg.assign_tile = max_width, max_height, window_k, assign_tile
-        cfg.projection, cfg.near_plane = 0, near_plane
+        cfg.projection, cfg.near_plane = projection, near_plane
         cfg.background[:] = list(background)
         h = C.c_void_p()
         st = L.vrs_create(C.byref(cfg), C.byref(h))

@@ -30,11 +30,11 @@ def vrs():
 
 
 def render_both(vrs, oracle_mod, scene, cams, foveas=None, T=16, masks=None, max_pairs=1 << 22, counters=True,
-                no_cull=False, oracle_render=True):
+                no_cull=False, oracle_render=True, projection=0):
     W = max(c.width for c in cams)
     H = max(c.height for c in cams)
     r = vrs.Renderer(max_gaussians=max(scene.n, 1), max_views=len(cams), max_pairs=max_pairs, max_width=W,
-                     max_height=H, assign_tile=T)
+                     max_height=H, assign_tile=T, projection=projection)
     r.upload(scene)
     o = oracle_mod.Oracle(scene)
     for slot, m in (masks or {}).items():
@@ -44,7 +44,7 @@ def render_both(vrs, oracle_mod, scene, cams, foveas=None, T=16, masks=None, max
     rgba, depth = r.render(cams, foveas)
     torch.cuda.synchronize()
     g_imgs = vrs.vrs.split_views(rgba.cpu().numpy(), depth.cpu().numpy(), cams)
-    o.prepare(cams, foveas, assign_tile=T)
+    o.prepare(cams, foveas, assign_tile=T, projection=projection)
     o_imgs = o.render() if oracle_render else None
     return r, o, g_imgs, o_imgs
 
@@ -341,3 +341,32 @@ def test_c3_full_size_sampled_parity(vrs, oracle_mod):
     gdep = np.array([g[vv][1][yy, xx] for vv, xx, yy in vxy])
     assert np.abs(grgba - orgba).max() <= RGB_TOL
     assert (np.abs(gdep - odep) - DEPTH_REL * np.abs(odep)).max() <= 1e-6
+
+
+# --------------------------------------------------------------------- EWA baseline (config C5)
+
+@pytest.mark.parametrize("seed", [0, 3])
+def test_ewa_parity_small(vrs, oracle_mod, seed):
+    """EWA baseline mode (config C5's comparison): pairs bit-exact, images within tolerance."""
+    scene = sg.random_scene(seed, n=1000, sh_degree=3, xy_frac=1.5)
+    cam = sg.look_camera((0, 0, 0), f=48.0, width=160, height=128)
+    r, o, g, oi = render_both(vrs, oracle_mod, scene, [cam], projection=1)
+    assert_lists_equal(r, o)
+    assert_images_close(g, oi)
+    gs, os_ = r.vrs_debug_splats(0), o.splats(0)
+    valid = os_[:, 0] == 1
+    assert np.array_equal(gs[:, 0], os_[:, 0])
+    assert np.array_equal(gs[valid][:, 20:25], os_[valid][:, 20:25])
+
+
+@pytest.mark.parametrize("hfov", [90.0, 160.0])
+def test_ewa_wide_fov_foveated_stereo(vrs, oracle_mod, hfov):
+    """C5-style FoV sweep end points on a reduced vr_room, OP and EWA, foveated stereo."""
+    scene = sg.vr_room(5, 30000, sh_degree=3)
+    W, H = 256, 256
+    cams = sg.stereo_pair(width=W, height=H, hfov_deg=hfov, masks=False)
+    fov = [sg.Fovea((W / 2, H / 2), (W / 4, H / 4), 0.1)] * 2
+    for proj in (0, 1):
+        r, o, g, oi = render_both(vrs, oracle_mod, scene, cams, fov, T=32, projection=proj)
+        assert_lists_equal(r, o)
+        assert_images_close(g, oi)
