@@ -45,6 +45,11 @@ CONFIGS = {
                desc="3M vr_room SH3 (scales x0.408), stereo 2x2064x2208, 110deg, no foveation"),
     "c1": dict(n=1000, scale_mul=None, sh=0, fovea=False, T=16, masks=False, seed=0,
                desc="1000 random Gaussians SH0, one 128x128 view, 90deg, 16x16 tiles"),
+    "c4": dict(n=1_000_000, scale_mul=0.707, sh=3, fovea=True, T=32, masks=True, seed=4, trajectory=True,
+               desc="1M vr_room SH3 (scales x0.707), 360-pose head trajectory = 720 views, stereo pairs "
+                    "sharded by rank, foveated"),
+    "c5": dict(n=500_000, scale_mul=1.0, sh=3, fovea=True, T=32, masks=False, seed=2,
+               desc="C2 scene, FoV sweep 90-160 deg, Optimal Projection vs EWA baseline"),
 }
 METRIC = "stereo frames/sec (2x2064x2208, foveated) at 500k Gaussians; ms/stage"
 
@@ -56,11 +61,25 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="vrs", choices=["vrs", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--projection", type=int, default=0, help="0 = Optimal Projection, 1 = EWA baseline")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
     ap.add_argument("--quiet", action="store_true")
     return ap.parse_args()
+
+
+def step_cams(cfg_name, cams, step, rank=0, world=1):
+    """Cameras of timed step ``step``: fixed for C1/C2/C3; for C4 the rank's
+    contiguous shard of the 360-pose trajectory (a stereo pair never split),
+    visited cyclically."""
+    if not CONFIGS[cfg_name].get("trajectory"):
+        return cams
+    from paper_2505_10144_b200.parallel import shard_range
+    a, b = shard_range(360, world, rank)
+    t = a + (step % max(1, b - a))
+    head, yaw, pitch, roll = sg.trajectory_pose(t)
+    return sg.stereo_pair(head, yaw, pitch, roll, masks=True)
 
 
 def make_workload(cfg_name):
@@ -189,10 +208,54 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_c5(args):
+    """Config C5: FoV sweep 90-160 deg on the C2 scene, Optimal Projection vs the
+    EWA baseline: pairs per eye, blend ms and frame ms per FoV (one GPU)."""
+    import torch
+    from paper_2505_10144_b200 import Renderer
+    cfg = CONFIGS["c5"]
+    scene = sg.vr_room(cfg["seed"], cfg["n"], sh_degree=cfg["sh"])
+    fov = [sg.quest_fovea()] * 2
+    rows = []
+    stream = torch.cuda.Stream()
+    for proj in (0, 1):
+        r = Renderer(max_gaussians=scene.n, max_views=2, max_pairs=24 << 20, max_width=sg.QUEST_W,
+                     max_height=sg.QUEST_H, assign_tile=32, projection=proj)
+        r.upload(scene)
+        rgba, depth = r.alloc_outputs(sg.stereo_pair(masks=False))
+        for hfov in range(90, 161, 10):
+            cams = sg.stereo_pair(hfov_deg=float(hfov), masks=False)
+            r.vrs_set_instrumentation(counters=1, timing=0)
+            r.render(cams, fov, rgba, depth, stream=stream)
+            st = r.stats()
+            r.vrs_set_instrumentation(counters=0, timing=1)
+            for _ in range(args.warmup):
+                r.render(cams, fov, rgba, depth, stream=stream)
+            ms, blend = [], []
+            for _ in range(args.steps):
+                r.render(cams, fov, rgba, depth, stream=stream)
+                t = r.stats()["stage_ms"]
+                ms.append(t[7])
+                blend.append(t[5])
+            rows.append({"projection": "OP" if proj == 0 else "EWA", "hfov": hfov,
+                         "pairs_per_eye": st["pairs"] / 2, "contributions": st["contributions"],
+                         "frame_ms": float(np.median(ms)), "blend_ms": float(np.median(blend))})
+        r.close()
+    op110 = [x for x in rows if x["projection"] == "OP" and x["hfov"] == 110][0]
+    line = {"metric": "C5 FoV sweep (OP vs EWA): stereo frames/s at 110 deg OP; pairs/eye and blend ms per FoV",
+            "value": 1000.0 / op110["frame_ms"], "unit": "stereo frames/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": op110["frame_ms"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "c5", "desc": cfg["desc"]}, "sweep": rows}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.config == "c5":
+        return run_c5(args)
     import torch
     import torch.distributed as dist
 
@@ -219,8 +282,8 @@ def main():
 
     W = max(c.width for c in cams)
     H = max(c.height for c in cams)
-    r = Renderer(max_gaussians=scene.n, max_views=len(cams), max_pairs=16 << 20 if cfg["n"] > 1e6 else 6 << 20,
-                 max_width=W, max_height=H, assign_tile=cfg["T"], device=local)
+    r = Renderer(max_gaussians=scene.n, max_views=len(cams), max_pairs=16 << 20 if cfg["n"] > 1e6 else 8 << 20,
+                 max_width=W, max_height=H, assign_tile=cfg["T"], device=local, projection=args.projection)
     r.upload(scene)
     for k, m in masks.items():
         r.set_mask(k, m)
@@ -235,9 +298,9 @@ def main():
     counters = r.stats()
     r.vrs_set_instrumentation(counters=0, timing=1)
 
-    for _ in range(args.warmup):
+    for w in range(args.warmup):
         with torch.cuda.stream(stream):
-            r.render(cams, fov, rgba, depth, stream=stream)
+            r.render(step_cams(args.config, cams, w, rank, world), fov, rgba, depth, stream=stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -250,8 +313,9 @@ def main():
             with torch.cuda.stream(stream):
                 if not args.no_flush:
                     flush.fill_(s & 0xff)
+                cs = step_cams(args.config, cams, s, rank, world)
                 ev0[s].record(stream)
-                r.render(cams, fov, rgba, depth, stream=stream)
+                r.render(cs, fov, rgba, depth, stream=stream)
                 ev1[s].record(stream)
             st = r.stats()  # syncs the stream; outside the event pair
             stage.append(st["stage_ms"])
