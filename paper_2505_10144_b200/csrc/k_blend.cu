@@ -116,7 +116,13 @@ __device__ __forceinline__ float key_tau(unsigned long long key) {
 }  // namespace
 
 template <bool kCounters, bool kEwa>
-__global__ void __launch_bounds__(kBlend, 4) k_blend(FrameParams fp, FrameBufs fb, float* __restrict__ rgba,
+#ifndef VRS_BLEND_MINB
+#define VRS_BLEND_MINB 4
+#endif
+#ifndef VRS_BLEND_PREFETCH
+#define VRS_BLEND_PREFETCH 0
+#endif
+__global__ void __launch_bounds__(kBlend, VRS_BLEND_MINB) k_blend(FrameParams fp, FrameBufs fb, float* __restrict__ rgba,
                                                       float* __restrict__ depth) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BlendSmem& S = *reinterpret_cast<BlendSmem*>(smem_raw);
@@ -185,13 +191,14 @@ __global__ void __launch_bounds__(kBlend, 4) k_blend(FrameParams fp, FrameBufs f
     uint32_t hk = 0;  // byte offset of the ring head
     uint32_t n_contrib = 0, stop_pos = re - 1;  // entry whose insertion stopped the sample (re-1: ran out)
 
+    const char* __restrict__ colb = reinterpret_cast<const char*>(colv);
     auto blend_one = [&](unsigned long long key, float a) {
-        const float4 col = __ldg(colv + (uint32_t)key);
+        const float4 col = __ldg(reinterpret_cast<const float4*>(colb + ((uint32_t)key) * 16ull));
         const float wgt = a * Tr;
         Cr = fmaf(col.x, wgt, Cr);
         Cg = fmaf(col.y, wgt, Cg);
         Cb = fmaf(col.z, wgt, Cb);
-        Dd = fmaf(key_tau(key) * dn, wgt, Dd);
+        Dd = fmaf(key_tau(key), wgt, Dd);  // ray-distance factor |d| applied once at the end
         Tr = Tr * (1.0f - a);
         done = Tr < kTmin;
     };
@@ -222,30 +229,27 @@ __global__ void __launch_bounds__(kBlend, 4) k_blend(FrameParams fp, FrameBufs f
             if (__all_sync(0xffffffffu, done)) break;
             const bool rel = (c + lane < nb) && ((S.mask[c + lane] >> warp) & 1u);
             unsigned bits = __ballot_sync(0xffffffffu, rel);
-            while (bits) {
-                const int j = c + __ffs(bits) - 1;
-                bits &= bits - 1;
-                if (done) continue;
+            // process entry j (its r0..r2 already in registers); `return` = skip
+            auto process = [&](const int j, const float4 a0, const float4 a1, const float4 a2) {
+                if (done) return;
                 float alpha, tau;
                 if (kEwa) {  // EWA baseline: q from the projected mean in pixels
-                    const float4 a0 = S.r0[j], a1 = S.r1[j];
                     const float dxp = xs - a0.x, dyp = ys - a0.y;
                     const float q = fmaf(dxp, fmaf(a0.w, dxp, a1.x * dyp), dyp * fmaf(a1.x, dxp, a1.y * dyp));
-                    if (!(q <= a0.z)) continue;
+                    if (!(q <= a0.z)) return;
                     const float4 a3 = S.r3[j], a4 = S.r4[j], a5 = S.r5[j];
                     const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
                     const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, a5.x));
                     tau = __fdiv_rn(dtb, den);
                     alpha = alpha_of_x(fmaxf(q * -0.72134752f, -64.0f), a5.y);
                 } else {
-                    const float4 a0 = S.r0[j], a1 = S.r1[j], a2 = S.r2[j];
                     const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
                     const float ex = fmaf(a1.x, x, a1.y);
                     const float ey = fmaf(a1.z, x, fmaf(a1.w, y, a2.x));
                     const float cx = fmaf(a2.y, ex, a2.z * ey), cy = fmaf(a2.z, ex, a2.w * ey);
                     const float num = fmaf(ex, cx, ey * cy);
                     const float ss = s * s;
-                    if (!(s > 0.0f) || !(num <= a0.w * ss)) continue;
+                    if (!(s > 0.0f) || !(num <= a0.w * ss)) return;
                     // contribution: alpha and tau (R9: one IEEE reciprocal, exact on both sides)
                     const float4 a3 = S.r3[j], a4 = S.r4[j];
                     const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
@@ -261,7 +265,7 @@ __global__ void __launch_bounds__(kBlend, 4) k_blend(FrameParams fp, FrameBufs f
                 const float ah = WA(hk);
                 blend_one(direct ? key : kh, direct ? alpha : ah);
                 if (kCounters && done) stop_pos = base + j;
-                if (direct || done) continue;
+                if (direct || done) return;
                 hk = (hk + kSlotBytes) & kRingMask;
                 // insertion from the tail (entries arrive nearly sorted)
                 uint32_t jo = (hk + (kWindow - 2) * kSlotBytes) & kRingMask;
@@ -277,7 +281,40 @@ __global__ void __launch_bounds__(kBlend, 4) k_blend(FrameParams fp, FrameBufs f
                 const uint32_t dst = (jo + kSlotBytes) & kRingMask;
                 WK(dst) = key;
                 WA(dst) = alpha;
+            };
+#if VRS_BLEND_PREFETCH
+            // software pipeline: the next entry's coefficients are loaded before
+            // the current entry is processed (hides the shared-memory latency)
+            if (bits) {
+                int j = c + __ffs(bits) - 1;
+                bits &= bits - 1;
+                float4 a0 = S.r0[j], a1 = S.r1[j], a2 = kEwa ? a1 : S.r2[j];
+                while (true) {
+                    const bool more = bits != 0;
+                    int jn = j;
+                    float4 b0 = a0, b1 = a1, b2 = a2;
+                    if (more) {
+                        jn = c + __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        b0 = S.r0[jn];
+                        b1 = S.r1[jn];
+                        if (!kEwa) b2 = S.r2[jn];
+                    }
+                    process(j, a0, a1, a2);
+                    if (!more) break;
+                    j = jn;
+                    a0 = b0;
+                    a1 = b1;
+                    a2 = b2;
+                }
             }
+#else
+            while (bits) {
+                const int j = c + __ffs(bits) - 1;
+                bits &= bits - 1;
+                process(j, S.r0[j], S.r1[j], kEwa ? S.r1[j] : S.r2[j]);
+            }
+#endif
         }
     }
     // drain the window in order (sentinels pop as no-ops)
@@ -289,6 +326,7 @@ __global__ void __launch_bounds__(kBlend, 4) k_blend(FrameParams fp, FrameBufs f
 #undef WK
 #undef WA
     // outputs
+    Dd = Dd * dn;
     const float oR = Cr + Tr * fp.bg[0], oG = Cg + Tr * fp.bg[1], oB = Cb + Tr * fp.bg[2], oA = 1.0f - Tr;
     if (kind == kItemLow) {
         if (px < v.W && py < v.H) {

@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvrs.so")
+LIB_PATH = os.environ.get("VRS_LIB") or os.path.join(_HERE, "libvrs.so")  # VRS_LIB: tuning variants
 
 VRS_OK, VRS_E_INVALID_ARG, VRS_E_INGEST, VRS_E_CUDA, VRS_E_OOM, VRS_E_CAPACITY, VRS_E_STATE = range(7)
 VRS_MAX_VIEWS = 8
