@@ -177,6 +177,12 @@ VRS_API vrs_status vrs_debug_splats(vrs_context* ctx, int32_t view, float* out, 
 /* Per coarse tile class (0 High, 1 Low, 2 Hybrid, 3 Invisible) and visibility bit. */
 VRS_API vrs_status vrs_debug_tile_info(vrs_context* ctx, int32_t view, int32_t* cls, int32_t* vis, int64_t capacity);
 
+/* Largest tile (in pairs) the binned sort sorts in shared memory; larger
+ * tiles are sorted in chunks of that size and merged in global memory.  A
+ * power of two in [64, 4096] (default 4096); lowering it only exercises the
+ * merge path (results are identical).  Applies from the next frame. */
+VRS_API vrs_status vrs_debug_set_sort_smem_cap(vrs_context* ctx, int32_t cap);
+
 /* ---- primitives exposed for tests (DEVICE pointers, enqueued on stream) ---- */
 /* Stable LSD onesweep radix sort of n (key, value) pairs in place by the low
  * key_bits bits of the key (n <= max_pairs).  */

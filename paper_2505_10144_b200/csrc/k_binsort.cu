@@ -1,0 +1,342 @@
+// Step 4 ("instantiated ... this arrangement is sorted
+// ... ranges"): the (tile, depth) sort of the Gaussian/tile pairs as a binned
+// per-tile sort instead of a global radix sort.
+//
+// The fused tile test (k_project.cu) already knows every pair's tile, so it
+// counts pairs per tile with one atomic each and keeps the returned arrival
+// rank.  Then:
+//   k_tile_scan  one block: exclusive scan of the per-tile counts -> ranges
+//                (empty tiles (0, 0), as the oracle reports them), the list
+//                of non-empty tiles, and the counters zeroed for the next frame;
+//   k_bucket     pair i -> bucket[range_begin(tile) + rank_i] = (depth bits << 32) | g;
+//   k_tile_sort  one block per tile: the tile's (depth bits, g) keys sorted in
+//                shared memory by a bitonic network (tiles larger than the
+//                shared-memory capacity: sorted chunks merged along merge paths
+//                in global memory), written back as (tile << 32 | depth, g).
+// (depth bits, g) is unique inside a tile, so the result does not depend on
+// the atomic arrival order and equals the stable (tile, depth) sort of the
+// (view, g, tile) emission order -- the oracle's order, bit for bit.
+// Traffic: counts + pairs read twice and written twice (~40 B/pair), against
+// ~6 read+write passes (~150 B/pair) for the 46-bit LSD radix sort it replaces.
+#include "vrs_internal.cuh"
+
+namespace vrs {
+
+namespace {
+constexpr int kScanT = 1024;
+constexpr int kScanPer = 8;
+constexpr int kScanRound = kScanT * kScanPer;
+constexpr int kBinT = 256;
+constexpr int kWarpSortMax = 256;  // tiles up to this size: one warp, keys in registers (E <= 8)
+
+// Ascending bitonic sort of s[0, P), P a power of two >= 64, by a block of NT
+// threads.  Compare-exchange i of a stage with distance j <= 32 touches only
+// the 64-element block i >> 5, and thread t always owns blocks (t >> 5) + k *
+// NT/32, so such stages synchronise the warp only; a block barrier is needed
+// when this or the previous stage crosses warps (j > 32, or j = 32 after 64).
+template <int NT>
+__device__ __forceinline__ void bitonic_sort_smem(uint64_t* s, uint32_t P) {
+    const uint32_t tid = threadIdx.x;
+    for (uint32_t k = 2; k <= P; k <<= 1) {
+        for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+            if (j > 32 || (j == 32 && k > 64)) __syncthreads();
+            else __syncwarp();
+            for (uint32_t i = tid; i < (P >> 1); i += NT) {
+                const uint32_t ix = ((i & ~(j - 1)) << 1) | (i & (j - 1)), iy = ix | j;
+                const uint64_t a = s[ix], b = s[iy];
+                if ((a > b) == ((ix & k) == 0)) {
+                    s[ix] = b;
+                    s[iy] = a;
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// out[0, na+nb) = merge of the sorted (unique-key) runs a and b; each thread
+// of the block finds its merge-path split by binary search and merges its
+// share serially.
+__device__ __forceinline__ void merge_block(const uint64_t* a, uint32_t na, const uint64_t* b, uint32_t nb,
+                                            uint64_t* out) {
+    const uint32_t m = na + nb;
+    const uint32_t d0 = (uint32_t)((uint64_t)m * threadIdx.x / blockDim.x);
+    const uint32_t d1 = (uint32_t)((uint64_t)m * (threadIdx.x + 1) / blockDim.x);
+    if (d0 >= d1) return;
+    uint32_t lo = d0 > nb ? d0 - nb : 0u, hi = min(d0, na);
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (a[mid] < b[d0 - 1 - mid]) lo = mid + 1;
+        else hi = mid;
+    }
+    uint32_t i = lo, j = d0 - lo;
+    for (uint32_t d = d0; d < d1; d++) {
+        const bool ta = j >= nb || (i < na && a[i] < b[j]);
+        out[d] = ta ? a[i++] : b[j++];
+    }
+}
+// One warp sorts one tile of n <= 32*E keys held in registers (blocked
+// layout: lane l holds elements l*E .. l*E+E-1; padding ~0 sorts last):
+// bitonic stages with distance j < E are register compare-exchanges, the
+// others exchange with lane l ^ (j/E) by shuffles.  No shared memory, no
+// barriers.
+template <int E>
+__device__ __forceinline__ void warp_sort_tile(const uint64_t* __restrict__ bk, uint32_t n, uint64_t tk,
+                                               uint64_t* __restrict__ kout, uint32_t* __restrict__ vout,
+                                               uint64_t* sw, int lane) {
+    // coalesced (striped) global access, transposed through shared memory
+    // (row stride E+1 keeps both orders at the 2-wavefront minimum)
+    uint64_t x[E];
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint32_t idx = (uint32_t)(e * 32 + lane);
+        sw[(idx / E) * (E + 1) + idx % E] = idx < n ? bk[idx] : ~0ull;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; e++) x[e] = sw[lane * (E + 1) + e];
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < E) {
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    if ((e & j) == 0) {
+                        const bool asc = ((lane * E + e) & k) == 0;
+                        const uint64_t a = x[e], b = x[e | j];
+                        const bool sw_ = (a > b) == asc;
+                        x[e] = sw_ ? b : a;
+                        x[e | j] = sw_ ? a : b;
+                    }
+                }
+            } else {
+                const int jl = j / E;
+                const bool keep_min = ((lane & jl) == 0) == (((lane * E) & k) == 0);
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    const uint64_t y = __shfl_xor_sync(0xffffffffu, x[e], jl);
+                    x[e] = keep_min ? (x[e] < y ? x[e] : y) : (x[e] < y ? y : x[e]);
+                }
+            }
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; e++) sw[lane * (E + 1) + e] = x[e];
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint32_t idx = (uint32_t)(e * 32 + lane);
+        if (idx < n) {
+            const uint64_t v = sw[(idx / E) * (E + 1) + idx % E];
+            kout[idx] = tk | (v >> 32);
+            vout[idx] = (uint32_t)v;
+        }
+    }
+    __syncwarp();
+}
+}  // namespace
+
+__global__ void __launch_bounds__(kScanT) k_tile_scan(uint32_t* __restrict__ cnt, int64_t n_tiles,
+                                                      uint32_t* __restrict__ ranges, uint32_t* __restrict__ list,
+                                                      uint32_t* __restrict__ list_n, int64_t list_cap,
+                                                      uint32_t small_max) {
+    __shared__ uint32_t s_c[kScanRound];
+    __shared__ uint32_t s_w[kScanT / 32];
+    __shared__ uint32_t s_nb, s_ns;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_nb = s_ns = 0;
+    uint32_t carry = 0;
+    for (int64_t r0 = 0; r0 < n_tiles; r0 += kScanRound) {
+        const int m = (int)min((int64_t)kScanRound, n_tiles - r0);
+        for (int i = tid; i < m; i += kScanT) {  // coalesced, and re-zero for the next frame
+            s_c[i] = cnt[r0 + i];
+            cnt[r0 + i] = 0u;
+        }
+        __syncthreads();
+        uint32_t v[kScanPer], sum = 0;
+#pragma unroll
+        for (int k = 0; k < kScanPer; k++) {
+            const int idx = tid * kScanPer + k;
+            v[k] = idx < m ? s_c[idx] : 0u;
+            sum += v[k];
+        }
+        uint32_t inc = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        if (lane == 31) s_w[warp] = inc;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = s_w[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            s_w[lane] = w;
+        }
+        __syncthreads();
+        uint32_t excl = carry + (warp ? s_w[warp - 1] : 0u) + inc - sum;
+#pragma unroll
+        for (int k = 0; k < kScanPer; k++) {  // tile starts replace the counts (all were read above)
+            const int idx = tid * kScanPer + k;
+            if (idx < m) s_c[idx] = excl;
+            excl += v[k];
+        }
+        const uint32_t carry_next = carry + s_w[kScanT / 32 - 1];
+        __syncthreads();
+        const unsigned lt = (1u << lane) - 1u;
+        for (int i0 = 0; i0 < m; i0 += kScanT) {  // coalesced (start, end) stores + list appends
+            const int i = i0 + tid;
+            uint32_t c = 0, st = 0;
+            if (i < m) {
+                st = s_c[i];
+                c = (i + 1 < m ? s_c[i + 1] : carry_next) - st;
+                reinterpret_cast<uint2*>(ranges)[r0 + i] = c ? make_uint2(st, st + c) : make_uint2(0u, 0u);
+            }
+            const uint32_t t = (uint32_t)(r0 + i);
+            const unsigned mb = __ballot_sync(0xffffffffu, c > small_max);
+            const unsigned ms = __ballot_sync(0xffffffffu, c != 0u && c <= small_max);
+            uint32_t bb = 0, bs = 0;
+            if (lane == 0) {  // one shared atomic per warp and class (list order is irrelevant)
+                if (mb) bb = atomicAdd(&s_nb, (uint32_t)__popc(mb));
+                if (ms) bs = atomicAdd(&s_ns, (uint32_t)__popc(ms));
+            }
+            bb = __shfl_sync(0xffffffffu, bb, 0);
+            bs = __shfl_sync(0xffffffffu, bs, 0);
+            if ((mb >> lane) & 1u) list[bb + __popc(mb & lt)] = t;                     // big tiles from the front
+            if ((ms >> lane) & 1u) list[list_cap - 1 - (bs + __popc(ms & lt))] = t;  // small ones from the back
+        }
+        carry = carry_next;
+        __syncthreads();
+    }
+    if (tid == 0) {
+        list_n[0] = s_nb;
+        list_n[1] = s_ns;
+        list_n[2] = 0u;  // k_tile_sort's small-tile work counter
+    }
+}
+
+__global__ void __launch_bounds__(256) k_bucket(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
+                                                const uint32_t* __restrict__ rank, const uint32_t* __restrict__ n_dev,
+                                                int64_t cap, const uint32_t* __restrict__ ranges,
+                                                uint64_t* __restrict__ bucket) {
+    const int64_t n = min((int64_t)*n_dev, cap);
+    constexpr int U = 4;  // independent items per thread (latency hiding)
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * U) {
+        uint64_t k[U];
+        uint32_t r[U], v[U], b[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int64_t i = i0 + u * stride;
+            k[u] = i < n ? keys[i] : 0ull;
+            r[u] = i < n ? rank[i] : 0u;
+            v[u] = i < n ? vals[i] : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) b[u] = (i0 + u * stride < n) ? ranges[2 * (size_t)(uint32_t)(k[u] >> 32)] : 0u;
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            if (i0 + u * stride < n) bucket[b[u] + r[u]] = (k[u] << 32) | v[u];
+    }
+}
+
+__global__ void __launch_bounds__(kBinT, 4) k_tile_sort(const uint32_t* __restrict__ list,
+                                                     const uint32_t* __restrict__ list_n, int64_t list_cap,
+                                                     const uint32_t* __restrict__ ranges, uint64_t* bucket,
+                                                     uint64_t* keys, uint32_t* __restrict__ vals, uint32_t cap_smem,
+                                                     uint32_t* work) {
+    extern __shared__ __align__(16) uint64_t s_k[];
+    const uint32_t tid = threadIdx.x;
+    const uint32_t nbig = list_n[0], nsmall = list_n[1];
+    // big tiles (> kWarpSortMax pairs): one block each, shared memory / merge path
+    for (uint32_t w = blockIdx.x; w < nbig; w += gridDim.x) {
+        const uint32_t t = list[w];
+        const uint32_t off = ranges[2 * (size_t)t], n = ranges[2 * (size_t)t + 1] - off;
+        const uint64_t tk = (uint64_t)t << 32;
+        uint64_t* bk = bucket + off;
+        for (uint32_t c0 = 0; c0 < n; c0 += cap_smem) {
+            const uint32_t m = min(cap_smem, n - c0);
+            uint32_t P = 64;
+            while (P < m) P <<= 1;
+            __syncthreads();  // the previous tile/chunk is done with s_k
+            for (uint32_t i = tid; i < P; i += kBinT) s_k[i] = i < m ? bk[c0 + i] : ~0ull;
+            __syncthreads();
+            bitonic_sort_smem<kBinT>(s_k, P);
+            if (n <= cap_smem) {
+                for (uint32_t i = tid; i < m; i += kBinT) {
+                    const uint64_t k = s_k[i];
+                    keys[off + i] = tk | (k >> 32);
+                    vals[off + i] = (uint32_t)k;
+                }
+            } else {
+                for (uint32_t i = tid; i < m; i += kBinT) bk[c0 + i] = s_k[i];
+            }
+        }
+        if (n > cap_smem) {  // merge the sorted chunks: bucket <-> keys ping-pong over this tile's range
+            uint64_t* src = bk;
+            uint64_t* dst = keys + off;
+            for (uint32_t L = cap_smem; L < n; L <<= 1) {
+                __syncthreads();
+                for (uint32_t s0 = 0; s0 < n; s0 += 2 * L) {
+                    const uint32_t na = min(L, n - s0), nb = min(L, n - s0 - na);
+                    merge_block(src + s0, na, src + s0 + na, nb, dst + s0);
+                }
+                uint64_t* tmp = src;
+                src = dst;
+                dst = tmp;
+            }
+            __syncthreads();
+            for (uint32_t i = tid; i < n; i += kBinT) {  // (in place when src is keys: same element, same thread)
+                const uint64_t k = src[i];
+                keys[off + i] = tk | (k >> 32);
+                vals[off + i] = (uint32_t)k;
+            }
+        }
+    }
+    // small tiles: one warp each, taken dynamically (warp-private slice of s_k)
+    const int lane = (int)(tid & 31u);
+    __syncthreads();  // the block path is done with s_k
+    uint64_t* sw = s_k + (tid >> 5) * (32 * 9);
+    while (true) {
+        uint32_t w = 0;
+        if (lane == 0) w = atomicAdd(work, 1u);
+        w = __shfl_sync(0xffffffffu, w, 0);
+        if (w >= nsmall) break;
+        const uint32_t t = list[list_cap - 1 - w];
+        const uint32_t off = ranges[2 * (size_t)t], n = ranges[2 * (size_t)t + 1] - off;
+        const uint64_t tk = (uint64_t)t << 32;
+        if (n <= 64) warp_sort_tile<2>(bucket + off, n, tk, keys + off, vals + off, sw, lane);
+        else if (n <= 128) warp_sort_tile<4>(bucket + off, n, tk, keys + off, vals + off, sw, lane);
+        else warp_sort_tile<8>(bucket + off, n, tk, keys + off, vals + off, sw, lane);
+    }
+}
+
+static int sms_now() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
+
+void launch_binsort(FrameBufs fb, int64_t cap, int64_t n_tiles, BinScratch b, cudaStream_t st) {
+    if (n_tiles <= 0) return;
+    cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kBinCap * 8));
+    const int sms = sms_now();
+    k_tile_scan<<<1, kScanT, 0, st>>>(b.tile_cnt, n_tiles, fb.ranges, b.list, b.list_n, b.max_tiles,
+                                      min(b.cap_smem, (uint32_t)kWarpSortMax));
+    k_bucket<<<sms * 8, 256, 0, st>>>(fb.keys, fb.vals, b.rank, fb.total, cap, fb.ranges, fb.keys_alt);
+    k_tile_sort<<<sms * 4, kBinT, kBinCap * 8, st>>>(b.list, b.list_n, b.max_tiles, fb.ranges, fb.keys_alt, fb.keys,
+                                                     fb.vals, b.cap_smem, b.list_n + 2);
+}
+
+}  // namespace vrs

@@ -584,8 +584,9 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneDev sc, FrameParams 
 // and key (O8), then single-pass stream compaction of the kept candidates
 // with decoupled look-back (blocks take 512-candidate tiles in order from a
 // counter, publish their keep count, look back for their offset and write
-// the pairs directly in (view, g, tile row-major) emission order).  The
-// onesweep digit histograms of the emitted keys are accumulated on the way.
+// the pairs directly in (view, g, tile row-major) emission order).
+// When tile_cnt is given, every written pair also takes its rank inside its
+// tile from a per-tile counter (the binned sort's bucket slot, k_binsort.cu).
 // Candidates are laid out by the scan of the per-splat rect areas, which also
 // wrote the (splat, rect-local index) of every candidate (sidk).
 namespace {
@@ -640,17 +641,14 @@ __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const Fram
 }
 
 __global__ void __launch_bounds__(kTT) k_tiletest(FrameParams fp, FrameBufs fb, int64_t test_cap, uint64_t* keys,
-                                                  uint32_t* vals, uint32_t* hist, int passes,
+                                                  uint32_t* vals, uint32_t* tile_cnt, uint32_t* rank,
                                                   unsigned long long* status, uint32_t* counter, uint32_t epoch) {
-    __shared__ uint32_t s_h[8][256];
     __shared__ uint32_t s_wc[kTT / 32 * kTTItems];
     __shared__ uint32_t s_tile, s_excl;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
     const unsigned long long ep = (unsigned long long)epoch << 34;
     const unsigned long long kAgg = ep | (1ull << 32), kPre = ep | (2ull << 32);
-    if (hist)
-        for (int i = tid; i < 8 * 256; i += kTT) (&s_h[0][0])[i] = 0;
     const int64_t total = min((int64_t)*fb.total_tests, test_cap);
     const int64_t ntiles = (total + kTTTile - 1) / kTTTile;
     while (true) {
@@ -728,30 +726,11 @@ __global__ void __launch_bounds__(kTT) k_tiletest(FrameParams fp, FrameBufs fb, 
                 if (pos < fp.pair_cap) {
                     keys[pos] = key[it];
                     vals[pos] = gv[it];
-                }
-            }
-            if (hist) {  // digit histograms: one atomic per warp when the digit is warp-uniform
-                const unsigned m = wbits[it];
-                for (int p = 0; p < passes; p++) {
-                    const uint32_t d = (uint32_t)(key[it] >> (8 * p)) & 0xffu;
-                    const uint32_t dmin = __reduce_min_sync(0xffffffffu, keep[it] ? d : 0xffffffffu);
-                    const uint32_t dmax = __reduce_max_sync(0xffffffffu, keep[it] ? d : 0u);
-                    if (dmin == dmax) {
-                        if (lane == 0 && m) atomicAdd(&s_h[p][dmin], (uint32_t)__popc(m));
-                    } else if (keep[it]) {
-                        atomicAdd(&s_h[p][d], 1u);
-                    }
+                    if (tile_cnt) rank[pos] = atomicAdd(&tile_cnt[(uint32_t)(key[it] >> 32)], 1u);
                 }
             }
         }
         __syncthreads();
-    }
-    if (hist) {
-        __syncthreads();
-        for (int i = tid; i < passes * 256; i += kTT) {
-            const uint32_t c = (&s_h[0][0])[i];
-            if (c) atomicAdd(&hist[i], c);
-        }
     }
 }
 
@@ -831,16 +810,16 @@ static int sm_count() {
 }
 
 void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, uint64_t* keys, uint32_t* vals,
-                     uint32_t* hist, int passes, unsigned long long* status, uint32_t* counter, uint32_t epoch,
-                     cudaStream_t st) {
+                     uint32_t* tile_cnt, uint32_t* rank, unsigned long long* status, uint32_t* counter,
+                     uint32_t epoch, cudaStream_t st) {
     if ((int64_t)fp.n_views * fp.N == 0) {
         cudaMemsetAsync(fb.total, 0, 4, st);
         return;
     }
-    if (hist) cudaMemsetAsync(hist, 0, sizeof(uint32_t) * 8 * 256, st);
     cudaMemsetAsync(counter, 0, 4, st);
     cudaMemsetAsync(fb.total, 0, 4, st);  // stays 0 when there is no candidate at all
-    k_tiletest<<<sm_count() * 8, kTT, 0, st>>>(fp, fb, test_cap, keys, vals, hist, passes, status, counter, epoch);
+    k_tiletest<<<sm_count() * 8, kTT, 0, st>>>(fp, fb, test_cap, keys, vals, tile_cnt, rank, status, counter,
+                                                   epoch);
 }
 
 void launch_counts(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {

@@ -62,6 +62,7 @@ struct vrs_context {
     uint32_t* d_scan_scratch = nullptr;
     SortScratch sort{};
     uint32_t sort_epoch = 0;
+    BinScratch bin{};
     // per-view static setup
     int32_t* d_vis = nullptr;     // [V][max_tiles]
     uint32_t* d_sat = nullptr;    // [V][max_sat]
@@ -113,6 +114,7 @@ static void free_all(vrs_context* c) {
                     c->d_sidk, c->d_tt_status,
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
+                    c->bin.tile_cnt, c->bin.rank, c->bin.list, c->bin.list_n,
                     c->d_sat, c->d_cls, c->d_items, c->d_nitems, c->d_out_rgba, c->d_out_depth};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -176,6 +178,12 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     A(dalloc(&ctx->sort.counters, 8));
     ctx->sort.max_tiles = (P + 4095) / 4096;
     ctx->sort.epoch = &ctx->sort_epoch;
+    ctx->bin.max_tiles = V * ctx->max_tiles_view;
+    ctx->bin.cap_smem = kBinCap;
+    A(dalloc(&ctx->bin.tile_cnt, (size_t)ctx->bin.max_tiles));
+    A(dalloc(&ctx->bin.rank, (size_t)P));
+    A(dalloc(&ctx->bin.list, (size_t)ctx->bin.max_tiles));
+    A(dalloc(&ctx->bin.list_n, 4));
     A(dalloc(&ctx->d_vis, (size_t)V * ctx->max_tiles_view));
     A(dalloc(&ctx->d_cls, (size_t)V * ctx->max_tiles_view));
     A(dalloc(&ctx->d_sat, (size_t)V * ctx->max_sat_view));
@@ -188,6 +196,7 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
         return (e == cudaErrorMemoryAllocation) ? VRS_E_OOM : VRS_E_CUDA;
     }
     cudaMemset(ctx->d_misc, 0, 32);
+    cudaMemset(ctx->bin.tile_cnt, 0, sizeof(uint32_t) * ctx->bin.max_tiles);  // k_tile_scan re-zeroes per frame
     *out = ctx;
     return VRS_OK;
 }
@@ -529,14 +538,13 @@ static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* ca
     launch_scan(fb.ntests, fb.toff, fb.total_tests, nullptr, (int64_t)nv * fp.N, ctx->d_scan_scratch, st, fb.sidk,
                 ctx->test_cap);
     if (tm) CK(cudaEventRecord(ctx->ev[2], st));
-    const int key_bits = key_bits_for(ctx->last_tiles);
     unsigned long long* tts = tt_status(ctx, st);  // (advances the epoch)
-    launch_tiletest(fp, fb, ctx->test_cap, fb.keys, fb.vals, ctx->sort.hist, (key_bits + 7) / 8, tts,
+    launch_tiletest(fp, fb, ctx->test_cap, fb.keys, fb.vals, ctx->bin.tile_cnt, ctx->bin.rank, tts,
                     ctx->sort.counters + 7, ctx->tt_epoch, st);
     if (tm) CK(cudaEventRecord(ctx->ev[3], st));
-    launch_sort(fb.keys, fb.vals, fb.keys_alt, fb.vals_alt, fb.total, fp.pair_cap, key_bits, ctx->sort, st, true);
+    // binned per-tile sort; its tile-count scan also writes the ranges ("ranges" stage ~ 0)
+    launch_binsort(fb, fp.pair_cap, ctx->last_tiles, ctx->bin, st);
     if (tm) CK(cudaEventRecord(ctx->ev[4], st));
-    launch_ranges(fb.keys, fb.total, fp.pair_cap, fb.ranges, ctx->last_tiles, st);
     if (tm) CK(cudaEventRecord(ctx->ev[5], st));
     launch_blend(fp, fb, total_items, rgba, depth, st);
     if (tm) CK(cudaEventRecord(ctx->ev[6], st));
@@ -646,6 +654,14 @@ vrs_status vrs_debug_counts(vrs_context* ctx, uint32_t* counts, int64_t capacity
     return VRS_OK;
 }
 
+vrs_status vrs_debug_set_sort_smem_cap(vrs_context* ctx, int32_t cap) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    if (cap < 64 || cap > (int32_t)kBinCap || (cap & (cap - 1)))
+        return fail(ctx, VRS_E_INVALID_ARG, "sort smem cap must be a power of two in [64, 4096]");
+    ctx->bin.cap_smem = (uint32_t)cap;
+    return VRS_OK;
+}
+
 vrs_status vrs_debug_pairs(vrs_context* ctx, int32_t sorted, uint64_t* keys, uint32_t* vals, int64_t capacity,
                            int64_t* n_out) {
     if (!ctx || !keys || !vals) return VRS_E_INVALID_ARG;
@@ -666,7 +682,7 @@ vrs_status vrs_debug_pairs(vrs_context* ctx, int32_t sorted, uint64_t* keys, uin
         uint32_t saved = 0;
         CK(cudaMemcpy(&saved, ctx->d_misc, 4, cudaMemcpyDeviceToHost));
         unsigned long long* tts = tt_status(ctx, st);
-        launch_tiletest(ctx->fp, fb, ctx->test_cap, ctx->d_keys_alt, ctx->d_vals_alt, nullptr, 0, tts,
+        launch_tiletest(ctx->fp, fb, ctx->test_cap, ctx->d_keys_alt, ctx->d_vals_alt, nullptr, nullptr, tts,
                         ctx->sort.counters + 7, ctx->tt_epoch, st);
         CK(cudaMemcpyAsync(ctx->d_misc, &saved, 4, cudaMemcpyHostToDevice, st));
         CK(cudaGetLastError());

@@ -20,7 +20,7 @@ VRS_MAX_VIEWS = 8
 EXPORTS = ["vrs_abi_version", "vrs_create", "vrs_destroy", "vrs_last_error", "vrs_upload_gaussians",
            "vrs_set_visibility_mask", "vrs_render_views", "vrs_render_views_host", "vrs_set_instrumentation",
            "vrs_get_frame_stats", "vrs_debug_counts", "vrs_debug_pairs", "vrs_debug_ranges", "vrs_debug_splats",
-           "vrs_debug_tile_info", "vrs_sort_pairs", "vrs_exclusive_scan"]
+           "vrs_debug_tile_info", "vrs_debug_set_sort_smem_cap", "vrs_sort_pairs", "vrs_exclusive_scan"]
 
 
 class VrsError(RuntimeError):
@@ -86,6 +86,7 @@ def lib():
             "vrs_debug_ranges": (i32, [vp, vp, i64, C.POINTER(C.c_int64)]),
             "vrs_debug_splats": (i32, [vp, i32, vp, i64]),
             "vrs_debug_tile_info": (i32, [vp, i32, vp, vp, i64]),
+            "vrs_debug_set_sort_smem_cap": (i32, [vp, i32]),
             "vrs_sort_pairs": (i32, [vp, vp, vp, i64, i32, vp]),
             "vrs_exclusive_scan": (i32, [vp, vp, vp, vp, i64, vp]),
         }
@@ -274,6 +275,9 @@ class Renderer:
         cls, vis = np.zeros(tw * th, np.int32), np.zeros(tw * th, np.int32)
         self._check(lib().vrs_debug_tile_info(self.h, view, _np_ptr(cls), _np_ptr(vis), tw * th))
         return cls.reshape(th, tw), vis.reshape(th, tw)
+
+    def vrs_debug_set_sort_smem_cap(self, cap):
+        self._check(lib().vrs_debug_set_sort_smem_cap(self.h, int(cap)))
 
     # ---- primitives
     def vrs_sort_pairs(self, keys, vals, key_bits=64, stream=None):

@@ -201,6 +201,36 @@ def test_warp_culling_never_changes_results(vrs, oracle_mod):
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
 
+@pytest.mark.parametrize("cap", [64, 128])
+def test_binned_sort_merge_path_parity(vrs, oracle_mod, cap):
+    """Binned sort: tiles larger than the shared-memory capacity are sorted in
+    chunks and merged in global memory; forcing a tiny capacity sends most
+    tiles of a dense foveated stereo frame through that path -- sorted pairs,
+    ranges and images must still equal the oracle's exactly."""
+    scene = sg.vr_room(8, 20000, sh_degree=1)
+    W, H = 256, 192
+    cams = sg.stereo_pair(width=W, height=H, masks=False)
+    fov = [sg.Fovea((W / 2, H / 2), (W / 4, H / 4), 0.1)] * 2
+    r = vrs.Renderer(max_gaussians=scene.n, max_views=2, max_pairs=1 << 22, max_width=W, max_height=H,
+                     assign_tile=32)
+    r.upload(scene)
+    r.vrs_debug_set_sort_smem_cap(cap)
+    rgba, depth = r.render(cams, fov)
+    torch.cuda.synchronize()
+    o = oracle_mod.Oracle(scene)
+    o.prepare(cams, fov, assign_tile=32)
+    rng = o.ranges()
+    assert (rng[:, 1] - rng[:, 0]).max() > 2 * cap, "test needs tiles spanning several merge rounds"
+    k, v = r.vrs_debug_pairs(True)
+    ok, ov = o.pairs(True)
+    assert np.array_equal(k, ok) and np.array_equal(v, ov)
+    assert np.array_equal(r.vrs_debug_ranges(), rng)
+    g = vrs.vrs.split_views(rgba.cpu().numpy(), depth.cpu().numpy(), cams)
+    assert_images_close(g, o.render())
+    with pytest.raises(Exception):
+        r.vrs_debug_set_sort_smem_cap(100)  # not a power of two
+
+
 def test_determinism(vrs):
     """P14: two renders are byte-identical."""
     scene = sg.vr_room(4, 30000)
