@@ -166,7 +166,8 @@ VRS_API vrs_status vrs_get_frame_stats(vrs_context* ctx, vrs_frame_stats* out);
 /* Per-(view, Gaussian) exact pair counts of the last frame, n_views*N u32. */
 VRS_API vrs_status vrs_debug_counts(vrs_context* ctx, uint32_t* counts, int64_t capacity, int64_t* n_out);
 /* Pair keys ((global tile << 32) | f32 bits of the tile depth) and values
- * (Gaussian index), sorted (sorted=1) or in emission order (sorted=0). */
+ * (Gaussian index), sorted by (key, value) (sorted=1) or as emitted by the
+ * tile test (sorted=0; the emission order is arbitrary). */
 VRS_API vrs_status vrs_debug_pairs(vrs_context* ctx, int32_t sorted, uint64_t* keys, uint32_t* vals, int64_t capacity,
                            int64_t* n_out);
 /* [start, end) per global tile (views concatenated), 2 u32 per tile. */

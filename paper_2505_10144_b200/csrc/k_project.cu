@@ -505,7 +505,6 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
                     pass = pass && (v.plane[k][0] * ux + v.plane[k][1] * uy + v.plane[k][2] * uz >= -sinb);
             }
         }
-        if (in && !pass) fb.ntests[(size_t)vi * N + g] = 0;
         // block-aggregated append of (view, g) to the work list: one global
         // atomic per block and view (a single hot counter serialises otherwise)
         const unsigned m = __ballot_sync(0xffffffffu, pass);
@@ -529,78 +528,115 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
 
 // Step 1b: exact per-(view, Gaussian) preprocess of the compacted candidates:
 // projection, footprint, candidate tile count, splat record and SH colour.
-__global__ void __launch_bounds__(256, 3) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb) {
+// Step 2 (fused): each block scans its 256 candidate-tile counts, reserves
+// their total in the test list with one atomic and writes the expansion
+// (splat view*N+g | rect-local tile index << 32) cooperatively, every output
+// slot finding its owner by binary search over the block prefix (balanced
+// and coalesced whatever the rect sizes).  The list order across blocks is
+// arbitrary: the binned sort makes the final pair order independent of it.
+__global__ void __launch_bounds__(256, 3) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb, int64_t test_cap) {
+    __shared__ uint32_t s_inc[256];
+    __shared__ uint32_t s_sidx[256];
+    __shared__ uint32_t s_w[8];
+    __shared__ uint32_t s_base;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t N = fp.N;
     const uint32_t nc = *fb.cand_count;
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nc; i += gridDim.x * blockDim.x) {
-        const uint32_t sidx = fb.cand[i];
-        int vi = 0;  // view = number of view blocks of N below sidx (no 64-bit division)
-        while (vi + 1 < fp.n_views && (int64_t)sidx >= (int64_t)(vi + 1) * N) vi++;
-        const int64_t g = (int64_t)sidx - (int64_t)vi * N;
-        const ViewParams& v = fp.v[vi];
-        const float4 m4 = __ldg(&sc.mu[g]);
-        const float4 c0 = __ldg(&sc.cov[g]), c1 = __ldg(&sc.cov[N + g]);
-        const float4 i0 = __ldg(&sc.icov[g]), i1 = __ldg(&sc.icov[N + g]);
-        Proj p;
-        if (fp.ewa) project_splat_ewa(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
-        else project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
-        // number of (Gaussian, tile) candidates = rect area, 0 if the rect holds no
-        // visible tile (SAT); the exact Eq.4 tests run load-balanced in k_tiletest
-        uint32_t cnt = 0;
-        if (p.valid && p.rect[0] <= p.rect[2] && p.rect[1] <= p.rect[3] &&
-            sat_count(v.sat, v.tw + 1, p.rect[0], p.rect[1], p.rect[2], p.rect[3]) > 0)
-            cnt = (uint32_t)((p.rect[2] - p.rect[0] + 1) * (p.rect[3] - p.rect[1] + 1));
-        fb.ntests[sidx] = cnt;
-        if (cnt == 0) continue;
-        float rgb[3];
-        {
-            const float dx = m4.x - v.o[0], dy = m4.y - v.o[1], dz = m4.z - v.o[2];
-            const float inv = 1.0f / sqrtf(dot3(dx, dy, dz, dx, dy, dz));
-            sh_color(sc, g, N, fp.sh_coeffs, dx * inv, dy * inv, dz * inv, rgb);
+    for (uint32_t b0 = blockIdx.x * 256u; b0 < nc; b0 += gridDim.x * 256u) {
+        const uint32_t i = b0 + tid;
+        uint32_t cnt = 0, sidx = 0;
+        if (i < nc) {
+            sidx = fb.cand[i];
+            int vi = 0;  // view = number of view blocks of N below sidx (no 64-bit division)
+            while (vi + 1 < fp.n_views && (int64_t)sidx >= (int64_t)(vi + 1) * N) vi++;
+            const int64_t g = (int64_t)sidx - (int64_t)vi * N;
+            const ViewParams& v = fp.v[vi];
+            const float4 m4 = __ldg(&sc.mu[g]);
+            const float4 c0 = __ldg(&sc.cov[g]), c1 = __ldg(&sc.cov[N + g]);
+            const float4 i0 = __ldg(&sc.icov[g]), i1 = __ldg(&sc.icov[N + g]);
+            Proj p;
+            if (fp.ewa) project_splat_ewa(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
+            else project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
+            // number of (Gaussian, tile) candidates = rect area, 0 if the rect holds no
+            // visible tile (SAT); the exact Eq.4 tests run load-balanced in k_tiletest
+            if (p.valid && p.rect[0] <= p.rect[2] && p.rect[1] <= p.rect[3] &&
+                sat_count(v.sat, v.tw + 1, p.rect[0], p.rect[1], p.rect[2], p.rect[3]) > 0)
+                cnt = (uint32_t)((p.rect[2] - p.rect[0] + 1) * (p.rect[3] - p.rect[1] + 1));
+            if (cnt) {
+                float rgb[3];
+                {
+                    const float dx = m4.x - v.o[0], dy = m4.y - v.o[1], dz = m4.z - v.o[2];
+                    const float inv = 1.0f / sqrtf(dot3(dx, dy, dz, dx, dy, dz));
+                    sh_color(sc, g, N, fp.sh_coeffs, dx * inv, dy * inv, dz * inv, rgb);
+                }
+                float4* rec = fb.rec + (size_t)sidx * kRecF4;
+                const uint32_t r01 = (uint32_t)p.rect[0] | ((uint32_t)p.rect[1] << 16);
+                const uint32_t r23 = (uint32_t)p.rect[2] | ((uint32_t)p.rect[3] << 16);
+                if (fp.ewa) {
+                    rec[0] = make_float4(p.m2[0], p.m2[1], p.qcut, p.Cp[0]);
+                    rec[1] = make_float4(p.Cp[1], p.Cp[2], 0.0f, 0.0f);
+                    rec[2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                    p.eps = 0.0f;
+                } else {
+                    rec[0] = make_float4(p.u[0], p.u[1], p.u[2], p.qcut);
+                    rec[1] = make_float4(p.e1[0], p.e1[2], p.e2[0], p.e2[1]);
+                    rec[2] = make_float4(p.e2[2], p.C[0], p.C[1], p.C[2]);
+                }
+                rec[3] = make_float4(p.A[0], p.A[1], p.A[2], p.A[3]);
+                rec[4] = make_float4(p.A[4], p.A[5], p.bv[0], p.bv[1]);
+                rec[5] = make_float4(p.bv[2], p.sigma, p.eps, __uint_as_float(r01));
+                rec[6] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(r23));
+                rec[7] = make_float4(p.bbox[0], p.bbox[1], p.bbox[2], p.bbox[3]);
+                fb.col[sidx] = make_float4(rgb[0], rgb[1], rgb[2], 0.0f);
+            }
         }
-        float4* rec = fb.rec + (size_t)sidx * kRecF4;
-        const uint32_t r01 = (uint32_t)p.rect[0] | ((uint32_t)p.rect[1] << 16);
-        const uint32_t r23 = (uint32_t)p.rect[2] | ((uint32_t)p.rect[3] << 16);
-        if (fp.ewa) {
-            rec[0] = make_float4(p.m2[0], p.m2[1], p.qcut, p.Cp[0]);
-            rec[1] = make_float4(p.Cp[1], p.Cp[2], 0.0f, 0.0f);
-            rec[2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-            p.eps = 0.0f;
-        } else {
-            rec[0] = make_float4(p.u[0], p.u[1], p.u[2], p.qcut);
-            rec[1] = make_float4(p.e1[0], p.e1[2], p.e2[0], p.e2[1]);
-            rec[2] = make_float4(p.e2[2], p.C[0], p.C[1], p.C[2]);
+        // block inclusive scan of the counts
+        uint32_t inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
         }
-        rec[3] = make_float4(p.A[0], p.A[1], p.A[2], p.A[3]);
-        rec[4] = make_float4(p.A[4], p.A[5], p.bv[0], p.bv[1]);
-        rec[5] = make_float4(p.bv[2], p.sigma, p.eps, __uint_as_float(r01));
-        rec[6] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(r23));
-        rec[7] = make_float4(p.bbox[0], p.bbox[1], p.bbox[2], p.bbox[3]);
-        fb.col[sidx] = make_float4(rgb[0], rgb[1], rgb[2], 0.0f);
+        if (lane == 31) s_w[warp] = inc;
+        __syncthreads();
+        uint32_t wpre = 0, tot = 0;
+#pragma unroll
+        for (int w = 0; w < 8; w++) {
+            wpre += (w < warp) ? s_w[w] : 0u;
+            tot += s_w[w];
+        }
+        s_inc[tid] = wpre + inc;
+        s_sidx[tid] = sidx;
+        if (tid == 0) s_base = tot ? atomicAdd(fb.total_tests, tot) : 0u;
+        __syncthreads();
+        const uint32_t base = s_base;
+        for (uint32_t o = tid; o < tot; o += 256u) {
+            int lo = 0, hi = 255;  // owner: first e with s_inc[e] > o
+            while (lo < hi) {
+                const int mid = (lo + hi) >> 1;
+                if (s_inc[mid] > o) hi = mid;
+                else lo = mid + 1;
+            }
+            const uint32_t excl = lo ? s_inc[lo - 1] : 0u;
+            const int64_t pos = (int64_t)base + o;
+            if (pos < test_cap) fb.sidk[pos] = (unsigned long long)s_sidx[lo] | ((unsigned long long)(o - excl) << 32);
+        }
+        __syncthreads();
     }
 }
 
 // Step 3 (fused): one thread per (Gaussian, candidate tile): Eq.4 test (O7)
-// and key (O8), then single-pass stream compaction of the kept candidates
-// with decoupled look-back (blocks take 512-candidate tiles in order from a
-// counter, publish their keep count, look back for their offset and write
-// the pairs directly in (view, g, tile row-major) emission order).
-// When tile_cnt is given, every written pair also takes its rank inside its
-// tile from a per-tile counter (the binned sort's bucket slot, k_binsort.cu).
-// Candidates are laid out by the scan of the per-splat rect areas, which also
-// wrote the (splat, rect-local index) of every candidate (sidk).
+// and key (O8), then stream compaction of the kept candidates (blocks take
+// 512-candidate tiles from a counter and reserve their output with one
+// atomic; the emission order is therefore arbitrary, and irrelevant: the
+// binned sort orders by (tile, depth, g)).  When tile_cnt is given, every
+// written pair also takes its rank inside its tile from a per-tile counter
+// (its bucket slot, k_binsort.cu).  Candidates come from the expansion the
+// preprocess wrote (sidk: splat | rect-local tile index << 32).
 namespace {
 constexpr int kTT = 256;           // threads per block
 constexpr int kTTItems = 2;        // candidates per thread (independent: ILP)
 constexpr int kTTTile = kTT * kTTItems;
-__device__ __forceinline__ void st_relaxed64(unsigned long long* p, unsigned long long v) {
-    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_relaxed64(const unsigned long long* p) {
-    unsigned long long v;
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-    return v;
-}
 }  // namespace
 
 __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const FrameBufs& fb, unsigned long long sk,
@@ -642,13 +678,11 @@ __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const Fram
 
 __global__ void __launch_bounds__(kTT) k_tiletest(FrameParams fp, FrameBufs fb, int64_t test_cap, uint64_t* keys,
                                                   uint32_t* vals, uint32_t* tile_cnt, uint32_t* rank,
-                                                  unsigned long long* status, uint32_t* counter, uint32_t epoch) {
+                                                  uint32_t* counter) {
     __shared__ uint32_t s_wc[kTT / 32 * kTTItems];
-    __shared__ uint32_t s_tile, s_excl;
+    __shared__ uint32_t s_tile, s_base;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const unsigned long long ep = (unsigned long long)epoch << 34;
-    const unsigned long long kAgg = ep | (1ull << 32), kPre = ep | (2ull << 32);
     const int64_t total = min((int64_t)*fb.total_tests, test_cap);
     const int64_t ntiles = (total + kTTTile - 1) / kTTTile;
     while (true) {
@@ -667,7 +701,7 @@ __global__ void __launch_bounds__(kTT) k_tiletest(FrameParams fp, FrameBufs fb, 
             gv[it] = 0;
             if (t < total) keep[it] = test_candidate(fp, fb, fb.sidk[t], key[it], gv[it]);
         }
-        // tile-local exclusive positions in candidate order (item-major, then thread)
+        // block-local positions, one global atomic per block tile for the base
         uint32_t wbits[kTTItems];
 #pragma unroll
         for (int it = 0; it < kTTItems; it++) {
@@ -686,43 +720,14 @@ __global__ void __launch_bounds__(kTT) k_tiletest(FrameParams fp, FrameBufs fb, 
             }
             const uint32_t agg = __shfl_sync(0xffffffffu, inc, 31);
             if (lane < nw) s_wc[lane] = inc - c;
-            // publish + warp-wide decoupled look-back
-            uint32_t excl = 0;
-            if (tile == 0) {
-                if (lane == 0) st_relaxed64(&status[0], kPre | agg);
-            } else {
-                if (lane == 0) st_relaxed64(&status[tile], kAgg | agg);
-                int64_t j = tile - 1;
-                while (true) {
-                    const int64_t jj = j - lane;
-                    unsigned long long sv = kPre;
-                    if (jj >= 0) {
-                        do {
-                            sv = ld_relaxed64(&status[jj]);
-                        } while ((sv & ~0xffffffffull) != kAgg && (sv & ~0xffffffffull) != kPre);
-                    }
-                    const unsigned pre = __ballot_sync(0xffffffffu, (sv & ~0xffffffffull) == kPre);
-                    const int stop = pre ? (__ffs(pre) - 1) : 31;
-                    uint32_t val = (lane <= stop) ? (uint32_t)sv : 0u;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-                    excl += val;
-                    if (pre) break;
-                    j -= 32;
-                }
-                if (lane == 0) st_relaxed64(&status[tile], kPre | (excl + agg));
-            }
-            if (lane == 0) {
-                s_excl = excl;
-                if (tile == ntiles - 1) *fb.total = excl + agg;
-            }
+            if (lane == 0) s_base = agg ? atomicAdd(fb.total, agg) : 0u;
         }
         __syncthreads();
-        const uint32_t excl = s_excl;
+        const uint32_t base = s_base;
 #pragma unroll
         for (int it = 0; it < kTTItems; it++) {
             if (keep[it]) {
-                const uint32_t pos = excl + s_wc[it * (kTT / 32) + warp] + __popc(wbits[it] & lt);
+                const uint32_t pos = base + s_wc[it * (kTT / 32) + warp] + __popc(wbits[it] & lt);
                 if (pos < fp.pair_cap) {
                     keys[pos] = key[it];
                     vals[pos] = gv[it];
@@ -730,7 +735,6 @@ __global__ void __launch_bounds__(kTT) k_tiletest(FrameParams fp, FrameBufs fb, 
                 }
             }
         }
-        __syncthreads();
     }
 }
 
@@ -787,7 +791,8 @@ __global__ void k_debug_splats(SceneDev sc, FrameParams fp, FrameBufs fb, int vi
     }
 }
 
-void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, cudaStream_t st) {
+void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {
+    cudaMemsetAsync(fb.total_tests, 0, 4, st);
     if (fp.N == 0) return;
     const int B = 256;
     cudaMemsetAsync(fb.cand_count, 0, 4, st);
@@ -795,7 +800,7 @@ void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, 
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    k_preprocess<<<sms * 6, B, 0, st>>>(sc, fp, fb);
+    k_preprocess<<<sms * 6, B, 0, st>>>(sc, fp, fb, test_cap);
 }
 
 static int sm_count() {
@@ -810,16 +815,11 @@ static int sm_count() {
 }
 
 void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, uint64_t* keys, uint32_t* vals,
-                     uint32_t* tile_cnt, uint32_t* rank, unsigned long long* status, uint32_t* counter,
-                     uint32_t epoch, cudaStream_t st) {
-    if ((int64_t)fp.n_views * fp.N == 0) {
-        cudaMemsetAsync(fb.total, 0, 4, st);
-        return;
-    }
+                     uint32_t* tile_cnt, uint32_t* rank, uint32_t* counter, cudaStream_t st) {
+    cudaMemsetAsync(fb.total, 0, 4, st);  // pair total: block atomics below
+    if ((int64_t)fp.n_views * fp.N == 0) return;
     cudaMemsetAsync(counter, 0, 4, st);
-    cudaMemsetAsync(fb.total, 0, 4, st);  // stays 0 when there is no candidate at all
-    k_tiletest<<<sm_count() * 8, kTT, 0, st>>>(fp, fb, test_cap, keys, vals, tile_cnt, rank, status, counter,
-                                                   epoch);
+    k_tiletest<<<sm_count() * 8, kTT, 0, st>>>(fp, fb, test_cap, keys, vals, tile_cnt, rank, counter);
 }
 
 void launch_counts(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {

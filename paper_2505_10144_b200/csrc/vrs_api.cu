@@ -47,10 +47,8 @@ struct vrs_context {
     float4* d_rec = nullptr;
     float4* d_col = nullptr;
     uint32_t* d_cand = nullptr;
-    uint32_t *d_counts = nullptr, *d_ntests = nullptr, *d_toff = nullptr, *d_misc = nullptr;  // misc: pairs, overflow, tests
+    uint32_t *d_counts = nullptr, *d_misc = nullptr;  // misc: pairs, overflow, tests, candidates
     unsigned long long* d_sidk = nullptr;    // [test_cap] candidate map
-    unsigned long long* d_tt_status = nullptr;  // fused tile-test look-back words
-    uint32_t tt_epoch = 0;
     int64_t test_cap = 0;
     uint64_t *d_keys = nullptr, *d_keys_alt = nullptr;
     uint32_t *d_vals = nullptr, *d_vals_alt = nullptr;
@@ -110,8 +108,8 @@ static vrs_status cuda_check(vrs_context* c, cudaError_t e, const char* where) {
     } while (0)
 
 static void free_all(vrs_context* c) {
-    void* ptrs[] = {c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_col, c->d_cand, c->d_counts, c->d_ntests, c->d_toff, c->d_misc,
-                    c->d_sidk, c->d_tt_status,
+    void* ptrs[] = {c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_col, c->d_cand, c->d_counts, c->d_misc,
+                    c->d_sidk,
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
                     c->bin.tile_cnt, c->bin.rank, c->bin.list, c->bin.list_n,
@@ -158,11 +156,8 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     A(dalloc(&ctx->d_col, (size_t)V * N));
     A(dalloc(&ctx->d_cand, (size_t)V * N));
     A(dalloc(&ctx->d_counts, (size_t)V * N));
-    A(dalloc(&ctx->d_ntests, (size_t)V * N));
-    A(dalloc(&ctx->d_toff, (size_t)V * N));
     ctx->test_cap = 4 * P;
     A(dalloc(&ctx->d_sidk, (size_t)ctx->test_cap));
-    A(dalloc(&ctx->d_tt_status, (size_t)(ctx->test_cap / 512 + 2)));
     A(dalloc(&ctx->d_misc, 8));
     A(dalloc(&ctx->d_keys, (size_t)P));
     A(dalloc(&ctx->d_keys_alt, (size_t)P));
@@ -469,30 +464,12 @@ static vrs_status prepare_frame(vrs_context* ctx, int nv, const vrs_camera* cams
     return VRS_OK;
 }
 
-static int key_bits_for(int64_t tiles) {
-    int b = 0;
-    while (((int64_t)1 << b) < tiles) b++;
-    return 32 + b;
-}
-
-// Look-back words of the fused tile test, epoch-tagged (cleared once per wrap).
-static unsigned long long* tt_status(vrs_context* ctx, cudaStream_t st) {
-    ctx->tt_epoch = (ctx->tt_epoch + 1) & 0x3fffffffu;
-    if (ctx->tt_epoch <= 1) {
-        ctx->tt_epoch = 1;
-        cudaMemsetAsync(ctx->d_tt_status, 0, sizeof(unsigned long long) * (size_t)(ctx->test_cap / 512 + 2), st);
-    }
-    return ctx->d_tt_status;
-}
-
 static FrameBufs frame_bufs(vrs_context* ctx) {
     FrameBufs fb{};
     fb.rec = ctx->d_rec;
     fb.col = ctx->d_col;
     fb.cand = ctx->d_cand;
     fb.cand_count = ctx->d_misc + 3;
-    fb.ntests = ctx->d_ntests;
-    fb.toff = ctx->d_toff;
     fb.total_tests = ctx->d_misc + 2;
     fb.sidk = ctx->d_sidk;
     fb.counts = ctx->d_counts;
@@ -533,14 +510,11 @@ static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* ca
     if (tm) CK(cudaEventRecord(ctx->ev[0], st));
     CK(cudaMemsetAsync(ctx->d_misc + 1, 0, 4, st));
     if (ctx->counters) CK(cudaMemsetAsync(ctx->d_stats, 0, 8 * sizeof(unsigned long long), st));
-    launch_preprocess(sc, fp, fb, st);
+    launch_preprocess(sc, fp, fb, ctx->test_cap, st);  // (the candidate scan is fused into it: "scan" stage ~ 0)
     if (tm) CK(cudaEventRecord(ctx->ev[1], st));
-    launch_scan(fb.ntests, fb.toff, fb.total_tests, nullptr, (int64_t)nv * fp.N, ctx->d_scan_scratch, st, fb.sidk,
-                ctx->test_cap);
     if (tm) CK(cudaEventRecord(ctx->ev[2], st));
-    unsigned long long* tts = tt_status(ctx, st);  // (advances the epoch)
-    launch_tiletest(fp, fb, ctx->test_cap, fb.keys, fb.vals, ctx->bin.tile_cnt, ctx->bin.rank, tts,
-                    ctx->sort.counters + 7, ctx->tt_epoch, st);
+    launch_tiletest(fp, fb, ctx->test_cap, fb.keys, fb.vals, ctx->bin.tile_cnt, ctx->bin.rank,
+                    ctx->sort.counters + 7, st);
     if (tm) CK(cudaEventRecord(ctx->ev[3], st));
     // binned per-tile sort; its tile-count scan also writes the ranges ("ranges" stage ~ 0)
     launch_binsort(fb, fp.pair_cap, ctx->last_tiles, ctx->bin, st);
@@ -679,12 +653,8 @@ vrs_status vrs_debug_pairs(vrs_context* ctx, int32_t sorted, uint64_t* keys, uin
     } else {
         // re-run the fused tests + compaction (emission order) into the alternate buffers
         FrameBufs fb = frame_bufs(ctx);
-        uint32_t saved = 0;
-        CK(cudaMemcpy(&saved, ctx->d_misc, 4, cudaMemcpyDeviceToHost));
-        unsigned long long* tts = tt_status(ctx, st);
-        launch_tiletest(ctx->fp, fb, ctx->test_cap, ctx->d_keys_alt, ctx->d_vals_alt, nullptr, nullptr, tts,
-                        ctx->sort.counters + 7, ctx->tt_epoch, st);
-        CK(cudaMemcpyAsync(ctx->d_misc, &saved, 4, cudaMemcpyHostToDevice, st));
+        launch_tiletest(ctx->fp, fb, ctx->test_cap, ctx->d_keys_alt, ctx->d_vals_alt, nullptr, nullptr,
+                        ctx->sort.counters + 7, st);  // (re-derives the same pair total)
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(st));
         CK(cudaMemcpy(keys, ctx->d_keys_alt, 8 * n, cudaMemcpyDeviceToHost));

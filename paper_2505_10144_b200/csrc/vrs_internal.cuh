@@ -73,8 +73,6 @@ struct FrameBufs {
     float4* rec;             // [V][N][8]
     uint32_t* cand;          // [V*N] (view*N + g) passing the conservative cull
     uint32_t* cand_count;    // [1]
-    uint32_t* ntests;        // [V*N] candidate (Gaussian, tile) tests = rect area
-    uint32_t* toff;          // [V*N] exclusive scan of ntests
     uint32_t* total_tests;   // [1] (device)
     unsigned long long* sidk;  // [test_cap] candidate -> (splat view*N+g) | (rect-local tile index << 32)
     uint32_t* counts;        // [V*N] exact pair counts (parity hook only)
@@ -94,7 +92,8 @@ struct FrameBufs {
 // ----------------------------------------------------------------- launchers
 void launch_setup_view(const uint8_t* mask, int mask_w, ViewParams vp, int T, int32_t* vis, uint32_t* sat,
                        int32_t* cls, uint32_t* items, int32_t* n_items_dev, cudaStream_t st);
-void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, cudaStream_t st);
+// Cull + preprocess + candidate expansion into fb.sidk (total in fb.total_tests).
+void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st);
 // Exclusive scan of n = min(*n_dev, cap) u32 (n_dev may be null: n = cap); *total = sum.
 // out may be null.  expand (optional): for element e with count c at offset o,
 // expand[o + j] = e | (j << 32) for j < c (and o + j < expand_cap).
@@ -105,8 +104,7 @@ size_t scan_scratch_words(int64_t n);
 // Fused Eq.4 tests + keys + stream compaction; with tile_cnt != null every
 // written pair also gets rank[pos] = its arrival rank in tile_cnt[tile].
 void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, uint64_t* keys, uint32_t* vals,
-                     uint32_t* tile_cnt, uint32_t* rank, unsigned long long* status, uint32_t* counter,
-                     uint32_t epoch, cudaStream_t st);
+                     uint32_t* tile_cnt, uint32_t* rank, uint32_t* counter, cudaStream_t st);
 void launch_counts(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st);
 struct SortScratch {
     uint32_t* hist;          // [8][256] digit histograms (may be filled by k_compact)

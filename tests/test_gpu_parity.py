@@ -61,9 +61,12 @@ def assert_images_close(g_imgs, o_imgs):
 
 def assert_lists_equal(r, o):
     assert np.array_equal(r.vrs_debug_counts(), o.counts()), "per-(view,g) pair counts differ"
+    # emitted (unsorted) pairs: the GPU emits in arbitrary block order, so the
+    # multisets are compared (the sorted list below is compared in order)
     ku, vu = r.vrs_debug_pairs(False)
     oku, ovu = o.pairs(False)
-    assert np.array_equal(ku, oku) and np.array_equal(vu, ovu), "emitted pairs differ"
+    gi, oi = np.lexsort((vu, ku)), np.lexsort((ovu, oku))
+    assert np.array_equal(ku[gi], oku[oi]) and np.array_equal(vu[gi], ovu[oi]), "emitted pairs differ"
     k, v = r.vrs_debug_pairs(True)
     ok, ov = o.pairs(True)
     assert np.array_equal(k, ok), "sorted keys differ"
