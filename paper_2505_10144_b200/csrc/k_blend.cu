@@ -91,6 +91,7 @@ __device__ __forceinline__ float fast_ex2(float x) {
 // identical operations, so transmittance and the T < 1e-4 stop are exact.
 __device__ __forceinline__ float alpha_of_x(float x, float sigma) {
     const float fl = floorf(x);
+    const int n = (int)fl;
     const float f = x - fl;
     float p = 0.00187757565f;
     p = fmaf(p, f, 0.00898934249f);
@@ -98,7 +99,7 @@ __device__ __forceinline__ float alpha_of_x(float x, float sigma) {
     p = fmaf(p, f, 0.240153611f);
     p = fmaf(p, f, 0.693153083f);
     p = fmaf(p, f, 0.99999994f);
-    const float e = __int_as_float(__float_as_int(p) + ((int)fl << 23));  // p * 2^n, exact (normal range)
+    const float e = __int_as_float(__float_as_int(p) + (n << 23));  // p * 2^n, exact (normal range)
     const float a = sigma * e;
     return a < kAlphaMax ? a : kAlphaMax;
 }
@@ -191,9 +192,10 @@ __global__ void __launch_bounds__(kBlend, VRS_BLEND_MINB) k_blend(FrameParams fp
     uint32_t hk = 0;  // byte offset of the ring head
     uint32_t n_contrib = 0, stop_pos = re - 1;  // entry whose insertion stopped the sample (re-1: ran out)
 
-    const char* __restrict__ colb = reinterpret_cast<const char*>(colv);
     auto blend_one = [&](unsigned long long key, float a) {
-        const float4 col = __ldg(reinterpret_cast<const float4*>(colb + ((uint32_t)key) * 16ull));
+        const float4* cp;  // colv + g as one 32x32->64 multiply-add
+        asm("mad.wide.u32 %0, %1, 16, %2;" : "=l"(cp) : "r"((uint32_t)key), "l"(colv));
+        const float4 col = __ldg(cp);
         const float wgt = a * Tr;
         Cr = fmaf(col.x, wgt, Cr);
         Cg = fmaf(col.y, wgt, Cg);
@@ -267,18 +269,21 @@ __global__ void __launch_bounds__(kBlend, VRS_BLEND_MINB) k_blend(FrameParams fp
                 if (kCounters && done) stop_pos = base + j;
                 if (direct || done) return;
                 hk = (hk + kSlotBytes) & kRingMask;
-                // insertion from the tail (entries arrive nearly sorted)
+                // insertion from the tail (entries arrive nearly sorted); dst
+                // is the hole, starting at the popped head's slot
                 uint32_t jo = (hk + (kWindow - 2) * kSlotBytes) & kRingMask;
+                uint32_t dst = (jo + kSlotBytes) & kRingMask;
+                unsigned long long kj = WK(jo);
+                int left = kWindow - 1;
 #pragma unroll 1
-                for (int left = kWindow - 1; left > 0; left--) {
-                    const unsigned long long kj = WK(jo);
-                    if (kj <= key) break;
-                    const uint32_t dst = (jo + kSlotBytes) & kRingMask;
+                while (kj > key) {
                     WK(dst) = kj;
                     WA(dst) = WA(jo);
-                    jo = (jo + kRingMask) & kRingMask;
+                    dst = jo;
+                    if (--left == 0) break;
+                    jo = (jo - kSlotBytes) & kRingMask;
+                    kj = WK(jo);
                 }
-                const uint32_t dst = (jo + kSlotBytes) & kRingMask;
                 WK(dst) = key;
                 WA(dst) = alpha;
             };
@@ -466,22 +471,22 @@ __global__ void k_compose(FrameParams fp, FrameBufs fb, float* __restrict__ rgba
                     sd[dj][di] = 0.0f;
                 }
             }
+        // Pixels of one group share its sample, so the 3x3 taps of pixel
+        // (i0+a, j0+b) collapse onto 2x2 neighbour groups with summed
+        // separable weights: a = 0 -> groups {-1: 1, 0: 2 + [i0+1 < W]},
+        // a = 1 -> {0: 3, +1: 1} (pixel-level in-image tests folded in).
+        const float wx[2][3] = {{1.0f, (i0 + 1 < v.W) ? 3.0f : 2.0f, 0.0f}, {0.0f, 3.0f, 1.0f}};
+        const float wy[2][3] = {{1.0f, (j0 + 1 < v.H) ? 3.0f : 2.0f, 0.0f}, {0.0f, 3.0f, 1.0f}};
 #pragma unroll
         for (int b = 0; b < 2; b++)
 #pragma unroll
             for (int a = 0; a < 2; a++) {
                 float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f}, ws = 0.0f;
 #pragma unroll
-                for (int ddj = -1; ddj <= 1; ddj++)
+                for (int sj = b; sj < b + 2; sj++)
 #pragma unroll
-                    for (int ddi = -1; ddi <= 1; ddi++) {
-                        // neighbour pixel (2gx+a+ddi, 2gy+b+ddj) -> neighbour group slot
-                        const int si = (a + ddi < 0) ? 0 : ((a + ddi > 1) ? 2 : 1);
-                        const int sj = (b + ddj < 0) ? 0 : ((b + ddj > 1) ? 2 : 1);
-                        // pixel-level in-image test for the pixels inside this group's own column/row
-                        const int pi = i0 + a + ddi, pj = j0 + b + ddj;
-                        if (!ok[sj][si] || pi >= v.W || pj >= v.H) continue;
-                        const float w = (float)((2 - abs(ddi)) * (2 - abs(ddj)));
+                    for (int si = a; si < a + 2; si++) {
+                        const float w = ok[sj][si] ? wx[a][si] * wy[b][sj] : 0.0f;
                         acc[0] = fmaf(w, sc[sj][si].x, acc[0]);
                         acc[1] = fmaf(w, sc[sj][si].y, acc[1]);
                         acc[2] = fmaf(w, sc[sj][si].z, acc[2]);

@@ -534,7 +534,16 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
 // slot finding its owner by binary search over the block prefix (balanced
 // and coalesced whatever the rect sizes).  The list order across blocks is
 // arbitrary: the binned sort makes the final pair order independent of it.
-__global__ void __launch_bounds__(256, 3) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb, int64_t test_cap) {
+#ifndef VRS_PP_MINB
+#define VRS_PP_MINB 3
+#endif
+#ifndef VRS_TT_HOIST
+#define VRS_TT_HOIST 0
+#endif
+#ifndef VRS_TT_MINB
+#define VRS_TT_MINB 4
+#endif
+__global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb, int64_t test_cap) {
     __shared__ uint32_t s_inc[256];
     __shared__ uint32_t s_sidx[256];
     __shared__ uint32_t s_w[8];
@@ -551,6 +560,11 @@ __global__ void __launch_bounds__(256, 3) k_preprocess(SceneDev sc, FrameParams 
             while (vi + 1 < fp.n_views && (int64_t)sidx >= (int64_t)(vi + 1) * N) vi++;
             const int64_t g = (int64_t)sidx - (int64_t)vi * N;
             const ViewParams& v = fp.v[vi];
+            {  // the SH lines are needed after the projection: start fetching them into L2 now
+                const char* shp = reinterpret_cast<const char*>(sc.sh + (size_t)g * sc.sh_chunks);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(shp));
+                if (sc.sh_chunks > 4) asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + 128));
+            }
             const float4 m4 = __ldg(&sc.mu[g]);
             const float4 c0 = __ldg(&sc.cov[g]), c1 = __ldg(&sc.cov[N + g]);
             const float4 i0 = __ldg(&sc.icov[g]), i1 = __ldg(&sc.icov[N + g]);
@@ -648,6 +662,9 @@ __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const Fram
     const float4* rec = fb.rec + (size_t)sidx * kRecF4;
     const float4 r0 = __ldg(rec + 0), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2), r5 = __ldg(rec + 5),
                  r6 = __ldg(rec + 6);
+#if VRS_TT_HOIST
+    const float4 r3 = __ldg(rec + 3), r4 = __ldg(rec + 4);  // issued with the others: one latency level less
+#endif
     const uint32_t r01 = __float_as_uint(r5.w), r23 = __float_as_uint(r6.w);
     const int tx0 = r01 & 0xffff, ty0 = r01 >> 16, tx1 = r23 & 0xffff;
     const int rw = tx1 - tx0 + 1;
@@ -666,7 +683,9 @@ __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const Fram
         s.eps = r5.z;
         if (!tile_test(s, v, x0, y0, min(x0 + T, v.W), min(y0 + T, v.H), hx, hy, hz)) return false;
     }
+#if !VRS_TT_HOIST
     const float4 r3 = __ldg(rec + 3), r4 = __ldg(rec + 4);
+#endif
     s.A[0] = r3.x; s.A[1] = r3.y; s.A[2] = r3.z; s.A[3] = r3.w;
     s.A[4] = r4.x; s.A[5] = r4.y; s.bx = r4.z; s.by = r4.w; s.bz = r5.x;
     const float td = tile_depth(s, hx, hy, hz, fp.near_plane);
@@ -676,7 +695,7 @@ __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const Fram
     return true;
 }
 
-__global__ void __launch_bounds__(kTT) k_tiletest(FrameParams fp, FrameBufs fb, int64_t test_cap, uint64_t* keys,
+__global__ void __launch_bounds__(kTT, VRS_TT_MINB) k_tiletest(FrameParams fp, FrameBufs fb, int64_t test_cap, uint64_t* keys,
                                                   uint32_t* vals, uint32_t* tile_cnt, uint32_t* rank,
                                                   uint32_t* counter) {
     __shared__ uint32_t s_wc[kTT / 32 * kTTItems];
