@@ -50,6 +50,9 @@ CONFIGS = {
                     "sharded by rank, foveated"),
     "c5": dict(n=500_000, scale_mul=1.0, sh=3, fovea=True, T=32, masks=False, seed=2,
                desc="C2 scene, FoV sweep 90-160 deg, Optimal Projection vs EWA baseline"),
+    "c6": dict(n=500_000, scale_mul=1.0, sh=3, fovea=True, T=32, masks=True, seed=2, two_pass=True,
+               desc="C2 workload rendered with the paper's two-pass foveated baseline (App. A): full-res "
+                    "centre crop + half-res masked periphery, bilinear upsample + blend (SURVEY N1)"),
 }
 METRIC = "stereo frames/sec (2x2064x2208, foveated) at 500k Gaussians; ms/stage"
 
@@ -282,8 +285,11 @@ def main():
 
     W = max(c.width for c in cams)
     H = max(c.height for c in cams)
-    r = Renderer(max_gaussians=scene.n, max_views=len(cams), max_pairs=16 << 20 if cfg["n"] > 1e6 else 8 << 20,
+    two_pass = bool(cfg.get("two_pass"))
+    r = Renderer(max_gaussians=scene.n, max_views=len(cams) * (2 if two_pass else 1),
+                 max_pairs=16 << 20 if cfg["n"] > 1e6 or two_pass else 8 << 20,
                  max_width=W, max_height=H, assign_tile=cfg["T"], device=local, projection=args.projection)
+    render = r.render_two_pass if two_pass else r.render
     r.upload(scene)
     for k, m in masks.items():
         r.set_mask(k, m)
@@ -294,13 +300,13 @@ def main():
     # counters run (outside timing): workload counters for the roofline
     r.vrs_set_instrumentation(counters=1, timing=0)
     with torch.cuda.stream(stream):
-        r.render(cams, fov, rgba, depth, stream=stream)
+        render(cams, fov, rgba, depth, stream=stream)
     counters = r.stats()
     r.vrs_set_instrumentation(counters=0, timing=1)
 
     for w in range(args.warmup):
         with torch.cuda.stream(stream):
-            r.render(step_cams(args.config, cams, w, rank, world), fov, rgba, depth, stream=stream)
+            render(step_cams(args.config, cams, w, rank, world), fov, rgba, depth, stream=stream)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -315,7 +321,7 @@ def main():
                     flush.fill_(s & 0xff)
                 cs = step_cams(args.config, cams, s, rank, world)
                 ev0[s].record(stream)
-                r.render(cs, fov, rgba, depth, stream=stream)
+                render(cs, fov, rgba, depth, stream=stream)
                 ev1[s].record(stream)
             st = r.stats()  # syncs the stream; outside the event pair
             stage.append(st["stage_ms"])
@@ -338,14 +344,24 @@ def main():
         px = sum(c.width * c.height for c in cams)
         hr = torch.empty((px, 4), dtype=torch.float32).pin_memory()
         hd = torch.empty(px, dtype=torch.float32).pin_memory()
+
+        def render_to_host():
+            if two_pass:  # public Python API: device render, then D2H into pinned memory on the same stream
+                with torch.cuda.stream(stream):
+                    render(cams, fov, rgba, depth, stream=stream)
+                    hr.copy_(rgba, non_blocking=True)
+                    hd.copy_(depth, non_blocking=True)
+                stream.synchronize()
+            else:
+                r.render_host(cams, fov, hr, hd, stream=stream)
         for _ in range(2):
-            r.render_host(cams, fov, hr, hd, stream=stream)
+            render_to_host()
         n_e2e = min(args.steps, 20)
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(n_e2e):
-            r.render_host(cams, fov, hr, hd, stream=stream)
+            render_to_host()
         e2e_s = (time.perf_counter() - t0) / n_e2e
         e_t = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         if world > 1:
@@ -353,7 +369,8 @@ def main():
         cam_bytes = len(cams) * (72 + 24)
         e2e = {"value": world / float(e_t.item()), "unit": "stereo frames/s" if len(cams) == 2 else "frames/s",
                "h2d_bytes_per_step": cam_bytes, "d2h_bytes_per_step": int(px * 20),
-               "note": "vrs_render_views_host: render + D2H of RGBA f32 + depth f32 into pinned host memory; "
+               "note": ("render_two_pass into device buffers + D2H copies on the stream" if two_pass else
+                        "vrs_render_views_host: render + D2H") + " of RGBA f32 + depth f32 into pinned host memory; "
                        "camera/fovea structs travel as kernel parameters"}
 
     if rank == 0:
@@ -374,12 +391,9 @@ def main():
             except Exception:
                 traffic = None
         n_views = len(cams)
-        key_bits = 32 + int(np.ceil(np.log2(max(2, sum(((c.width + cfg["T"] - 1) // cfg["T"]) *
-                                                        ((c.height + cfg["T"] - 1) // cfg["T"]) for c in cams)))))
-        # k_cull, k_preprocess, k_scan, k_fill_sid, k_tiletest, k_scan, k_compact, k_sort_hist,
-        # passes x k_onesweep (+ k_copy_pairs if odd), k_ranges, k_blend, k_compose
-        passes = (key_bits + 7) // 8
-        launches_per_step = 11 + passes + (passes % 2)
+        # k_cull, k_preprocess, k_tiletest, k_tile_scan, k_bucket, k_tile_sort, k_blend, k_compose
+        # (+ k_two_pass_combine for the two-pass baseline)
+        launches_per_step = 8 + (1 if two_pass else 0)
         line = {
             "metric": METRIC if args.config == "c2" else METRIC + f" [{args.config}]",
             "value": world * 1000.0 / ms_max,
@@ -406,7 +420,7 @@ def main():
             "context": {"paper_rtx4090_ms_per_stereo_frame_0.5M_scenes": [9.89, 12.19],
                         "paper_headline": "72+ FPS on RTX 4090 at 2x2064x2272 (P:91, P:107)"},
         }
-        if not args.no_cpu_baseline and world == 1:
+        if not args.no_cpu_baseline and world == 1 and not two_pass:
             line["cpu_baseline"] = cpu_baseline(scene, cams, fov, masks, cfg["T"])
         print(json.dumps(line), flush=True)
     if world > 1:

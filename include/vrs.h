@@ -154,6 +154,24 @@ VRS_API vrs_status vrs_render_views(vrs_context* ctx, int32_t n_views, const vrs
 VRS_API vrs_status vrs_render_views_host(vrs_context* ctx, int32_t n_views, const vrs_camera* cams,
                                  const vrs_fovea* fovea, float* rgba_host, float* depth_host, void* stream);
 
+/* Two-pass foveated baseline (App. A), for
+ * comparison with the single-pass path.  For every view i (fovea[i] must be
+ * enabled): pass 1 renders the pixels with a non-zero fovea blend weight (the
+ * rectangle of half-extents radius*(1 + 2*ramp) around the centre, plus one
+ * pixel, clipped to the view) at full resolution through a cropped camera
+ * (principal point shifted by the integer rectangle origin: identical pixel
+ * rays); pass 2 renders the whole view at half resolution (focal lengths and
+ * principal point halved, ceil(W/2) x ceil(H/2)) with the view's visibility
+ * mask reduced by a 2x2 OR.  Both passes of all views run as ONE frame of
+ * 2*n_views views (so max_views >= 2*n_views, and the frame statistics and
+ * debug hooks describe that frame).  The output (same layout as
+ * vrs_render_views) is up(P2) blended with P1 by the fovea weight w:
+ * w*P1 + (1-w)*up(P2) per RGBA and depth channel, up() the bilinear upsample
+ * with pixel-centre alignment (full-resolution pixel i samples pass-2
+ * coordinate (i - 0.5)/2) and edge clamping.  Errors as vrs_render_views. */
+VRS_API vrs_status vrs_render_views_two_pass(vrs_context* ctx, int32_t n_views, const vrs_camera* cams,
+                                     const vrs_fovea* fovea, float* rgba, float* depth, void* stream);
+
 /* Detailed counters (evaluations, contributions, overflow) cost atomics;
  * stage timing costs events.  Both off by default. */
 VRS_API vrs_status vrs_set_instrumentation(vrs_context* ctx, int32_t counters, int32_t timing);

@@ -70,9 +70,17 @@ struct vrs_context {
     int64_t max_sat_view = 0;
     ViewSetup vs[VRS_MAX_VIEWS];
     // masks
-    uint8_t* d_mask[VRS_MAX_MASK_SLOTS] = {};
-    int mask_w[VRS_MAX_MASK_SLOTS] = {}, mask_h[VRS_MAX_MASK_SLOTS] = {};
-    uint64_t mask_gen[VRS_MAX_MASK_SLOTS] = {};
+    // slots [0, VRS_MAX_MASK_SLOTS): user masks; [VRS_MAX_MASK_SLOTS, 2x): their
+    // half-resolution versions for the two-pass baseline (built on demand)
+    uint8_t* d_mask[2 * VRS_MAX_MASK_SLOTS] = {};
+    int mask_w[2 * VRS_MAX_MASK_SLOTS] = {}, mask_h[2 * VRS_MAX_MASK_SLOTS] = {};
+    uint64_t mask_gen[2 * VRS_MAX_MASK_SLOTS] = {};
+    uint64_t half_src_gen[VRS_MAX_MASK_SLOTS] = {};  // user generation the half mask was built from
+    bool internal_masks = false;                     // validate_camera accepts the half slots
+    // two-pass baseline pass images
+    float4* d_tp_rgba = nullptr;
+    float* d_tp_depth = nullptr;
+    size_t tp_px_cap = 0;
     uint64_t gen_counter = 1;
     // last frame
     FrameParams fp{};
@@ -116,8 +124,10 @@ static void free_all(vrs_context* c) {
                     c->d_sat, c->d_cls, c->d_items, c->d_nitems, c->d_out_rgba, c->d_out_depth};
     for (void* p : ptrs)
         if (p) cudaFree(p);
-    for (int i = 0; i < VRS_MAX_MASK_SLOTS; i++)
+    for (int i = 0; i < 2 * VRS_MAX_MASK_SLOTS; i++)
         if (c->d_mask[i]) cudaFree(c->d_mask[i]);
+    if (c->d_tp_rgba) cudaFree(c->d_tp_rgba);
+    if (c->d_tp_depth) cudaFree(c->d_tp_depth);
     if (c->ev_created)
         for (auto& e : c->ev) cudaEventDestroy(e);
 }
@@ -360,7 +370,8 @@ static vrs_status validate_camera(vrs_context* ctx, const vrs_camera& c, const v
         return fail(ctx, VRS_E_INVALID_ARG, "bad intrinsics / position");
     if (c.width < 1 || c.height < 1 || c.width > ctx->cfg.max_width || c.height > ctx->cfg.max_height)
         return fail(ctx, VRS_E_INVALID_ARG, "view size exceeds max_width/max_height");
-    if (c.mask_slot >= VRS_MAX_MASK_SLOTS) return fail(ctx, VRS_E_INVALID_ARG, "mask slot");
+    if (c.mask_slot >= (ctx->internal_masks ? 2 * VRS_MAX_MASK_SLOTS : VRS_MAX_MASK_SLOTS))
+        return fail(ctx, VRS_E_INVALID_ARG, "mask slot");
     if (c.mask_slot >= 0 && ctx->d_mask[c.mask_slot] &&
         (ctx->mask_w[c.mask_slot] != c.width || ctx->mask_h[c.mask_slot] != c.height))
         return fail(ctx, VRS_E_INVALID_ARG, "mask resolution differs from view resolution");
@@ -558,6 +569,115 @@ vrs_status vrs_render_views_host(vrs_context* ctx, int32_t n_views, const vrs_ca
     CK(cudaMemcpyAsync(rgba_host, ctx->d_out_rgba, sizeof(float) * 4 * px, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(depth_host, ctx->d_out_depth, sizeof(float) * px, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    return VRS_OK;
+}
+
+/* the two-pass foveated baseline. */
+static void two_pass_rect(const vrs_camera& c, const vrs_fovea& f, int& i0, int& j0, int& i1, int& j1) {
+    // pixels with a non-zero blend weight lie within radius * (1 + 2 ramp) of
+    // the centre (fovea_weight); one pixel of margin on each side
+    const double ex = (double)f.radius[0] * (1.0 + 2.0 * (double)f.ramp);
+    const double ey = (double)f.radius[1] * (1.0 + 2.0 * (double)f.ramp);
+    i0 = (int)std::min(std::max(0.0, std::floor((double)f.center[0] - ex) - 1.0), (double)c.width - 1.0);
+    j0 = (int)std::min(std::max(0.0, std::floor((double)f.center[1] - ey) - 1.0), (double)c.height - 1.0);
+    i1 = (int)std::max(std::min((double)c.width, std::ceil((double)f.center[0] + ex) + 1.0), (double)i0 + 1.0);
+    j1 = (int)std::max(std::min((double)c.height, std::ceil((double)f.center[1] + ey) + 1.0), (double)j0 + 1.0);
+}
+
+vrs_status vrs_render_views_two_pass(vrs_context* ctx, int32_t n_views, const vrs_camera* cams,
+                                     const vrs_fovea* fovea, float* rgba, float* depth, void* stream) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    if (ctx->sticky != VRS_OK) return ctx->sticky;
+    if (n_views < 1 || 2 * n_views > ctx->cfg.max_views || !cams || !fovea || !rgba || !depth)
+        return fail(ctx, VRS_E_INVALID_ARG, "two-pass needs fovea, outputs and max_views >= 2 * n_views");
+    for (int i = 0; i < n_views; i++) {
+        if (!fovea[i].enabled) return fail(ctx, VRS_E_INVALID_ARG, "two-pass needs an enabled fovea per view");
+        vrs_status s = validate_camera(ctx, cams[i], &fovea[i]);
+        if (s != VRS_OK) return s;
+    }
+    CK(cudaSetDevice(ctx->cfg.device));
+    cudaStream_t st = (cudaStream_t)stream;
+    vrs_camera pc[VRS_MAX_VIEWS];
+    TwoPassParams tp{};
+    tp.n = n_views;
+    int64_t out_off = 0, p1_px = 0, p2_px = 0;
+    for (int i = 0; i < n_views; i++) {
+        const vrs_camera& c = cams[i];
+        int i0, j0, i1, j1;
+        two_pass_rect(c, fovea[i], i0, j0, i1, j1);
+        // pass 1: cropped camera, pixel (a, b) = parent pixel (i0 + a, j0 + b)
+        vrs_camera c1 = c;
+        c1.cx = c.cx - (float)i0;
+        c1.cy = c.cy - (float)j0;
+        c1.width = i1 - i0;
+        c1.height = j1 - j0;
+        c1.mask_slot = -1;
+        // pass 2: half resolution (sample (a, b) at parent position (2a + 1, 2b + 1)), half mask
+        vrs_camera c2 = c;
+        c2.fx = c.fx * 0.5f;
+        c2.fy = c.fy * 0.5f;
+        c2.cx = c.cx * 0.5f;
+        c2.cy = c.cy * 0.5f;
+        c2.width = (c.width + 1) / 2;
+        c2.height = (c.height + 1) / 2;
+        c2.mask_slot = -1;
+        const int ms = c.mask_slot;
+        if (ms >= 0 && ctx->d_mask[ms]) {
+            const int hs = VRS_MAX_MASK_SLOTS + ms;
+            if (!ctx->d_mask[hs] || ctx->half_src_gen[ms] != ctx->mask_gen[ms] || ctx->mask_w[hs] != c2.width ||
+                ctx->mask_h[hs] != c2.height) {
+                if (ctx->d_mask[hs]) CK(cudaFree(ctx->d_mask[hs]));
+                ctx->d_mask[hs] = nullptr;
+                CK(dalloc(&ctx->d_mask[hs], (size_t)c2.width * c2.height));
+                launch_mask_half(ctx->d_mask[ms], c.width, c.height, ctx->d_mask[hs], c2.width, c2.height, st);
+                CK(cudaGetLastError());
+                ctx->mask_w[hs] = c2.width;
+                ctx->mask_h[hs] = c2.height;
+                ctx->mask_gen[hs] = ctx->gen_counter++;
+                ctx->half_src_gen[ms] = ctx->mask_gen[ms];
+            }
+            c2.mask_slot = hs;
+        }
+        pc[i] = c1;
+        pc[n_views + i] = c2;
+        TwoPassView& t = tp.v[i];
+        t.W = c.width; t.H = c.height;
+        t.i0 = i0; t.j0 = j0; t.w1 = c1.width; t.h1 = c1.height;
+        t.W2 = c2.width; t.H2 = c2.height;
+        t.out_off = out_off;
+        t.p1_off = p1_px;
+        t.gx = fovea[i].center[0]; t.gy = fovea[i].center[1];
+        t.rx = fovea[i].radius[0]; t.ry = fovea[i].radius[1];
+        t.ramp = fovea[i].ramp;
+        out_off += (int64_t)c.width * c.height;
+        p1_px += (int64_t)c1.width * c1.height;
+        p2_px += (int64_t)c2.width * c2.height;
+    }
+    {   // pass images: all pass-1 views, then all pass-2 views (the render's view order)
+        int64_t o = p1_px;
+        for (int i = 0; i < n_views; i++) {
+            tp.v[i].p2_off = o;
+            o += (int64_t)tp.v[i].W2 * tp.v[i].H2;
+        }
+    }
+    const size_t tot = (size_t)(p1_px + p2_px);
+    if (tot > ctx->tp_px_cap) {
+        if (ctx->d_tp_rgba) cudaFree(ctx->d_tp_rgba);
+        if (ctx->d_tp_depth) cudaFree(ctx->d_tp_depth);
+        ctx->d_tp_rgba = nullptr;
+        ctx->d_tp_depth = nullptr;
+        ctx->tp_px_cap = 0;
+        CK(dalloc(&ctx->d_tp_rgba, tot));
+        CK(dalloc(&ctx->d_tp_depth, tot));
+        ctx->tp_px_cap = tot;
+    }
+    ctx->internal_masks = true;
+    vrs_status s = render_impl(ctx, 2 * n_views, pc, nullptr, reinterpret_cast<float*>(ctx->d_tp_rgba),
+                               ctx->d_tp_depth, st);
+    ctx->internal_masks = false;
+    if (s != VRS_OK) return s;
+    launch_two_pass_combine(tp, ctx->d_tp_rgba, ctx->d_tp_depth, rgba, depth, out_off, st);
+    CK(cudaGetLastError());
     return VRS_OK;
 }
 

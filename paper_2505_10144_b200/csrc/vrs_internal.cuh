@@ -133,6 +133,21 @@ struct BinScratch {
 void launch_binsort(FrameBufs fb, int64_t cap, int64_t n_tiles, BinScratch b, cudaStream_t st);
 void launch_ranges(const uint64_t* keys, const uint32_t* n_dev, int64_t cap, uint32_t* ranges, int64_t n_tiles,
                    cudaStream_t st);
+// Two-pass foveated baseline (k_twopass.cu).
+struct TwoPassView {
+    int32_t W, H;            // output view
+    int32_t i0, j0, w1, h1;  // pass-1 rectangle (full resolution)
+    int32_t W2, H2;          // pass-2 (half resolution) size
+    int64_t out_off, p1_off, p2_off;  // pixel offsets: output, pass-1 image, pass-2 image
+    float gx, gy, rx, ry, ramp;       // fovea (blend weight)
+};
+struct TwoPassParams {
+    int32_t n;
+    TwoPassView v[VRS_MAX_VIEWS];
+};
+void launch_mask_half(const uint8_t* src, int W, int H, uint8_t* dst, int W2, int H2, cudaStream_t st);
+void launch_two_pass_combine(const TwoPassParams& tp, const float4* prgba, const float* pdepth, float* rgba,
+                             float* depth, int64_t total, cudaStream_t st);
 void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
                   cudaStream_t st);
 void launch_compose(const FrameParams& fp, FrameBufs fb, float* rgba, float* depth, cudaStream_t st);

@@ -19,7 +19,7 @@ VRS_OK, VRS_E_INVALID_ARG, VRS_E_INGEST, VRS_E_CUDA, VRS_E_OOM, VRS_E_CAPACITY, 
 VRS_MAX_VIEWS = 8
 EXPORTS = ["vrs_abi_version", "vrs_create", "vrs_destroy", "vrs_last_error", "vrs_upload_gaussians",
            "vrs_set_visibility_mask", "vrs_render_views", "vrs_render_views_host", "vrs_set_instrumentation",
-           "vrs_get_frame_stats", "vrs_debug_counts", "vrs_debug_pairs", "vrs_debug_ranges", "vrs_debug_splats",
+           "vrs_render_views_two_pass", "vrs_get_frame_stats", "vrs_debug_counts", "vrs_debug_pairs", "vrs_debug_ranges", "vrs_debug_splats",
            "vrs_debug_tile_info", "vrs_debug_set_sort_smem_cap", "vrs_sort_pairs", "vrs_exclusive_scan"]
 
 
@@ -79,6 +79,7 @@ def lib():
             "vrs_set_visibility_mask": (i32, [vp, i32, i32, i32, vp]),
             "vrs_render_views": (i32, [vp, i32, vp, vp, vp, vp, vp]),
             "vrs_render_views_host": (i32, [vp, i32, vp, vp, vp, vp, vp]),
+            "vrs_render_views_two_pass": (i32, [vp, i32, vp, vp, vp, vp, vp]),
             "vrs_set_instrumentation": (i32, [vp, i32, i32]),
             "vrs_get_frame_stats": (i32, [vp, C.POINTER(vrs_frame_stats)]),
             "vrs_debug_counts": (i32, [vp, vp, i64, C.POINTER(C.c_int64)]),
@@ -213,6 +214,24 @@ class Renderer:
         return rgba, depth
 
     render = vrs_render_views
+
+    def vrs_render_views_two_pass(self, cams, foveas, rgba=None, depth=None, stream=None):
+        """Two-pass foveated baseline (App. A) into DEVICE tensors; same output layout as render()."""
+        import torch
+        if rgba is None or depth is None:
+            rgba, depth = self.alloc_outputs(cams)
+        carr, farr = self._views_structs(cams, foveas)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        self._check(lib().vrs_render_views_two_pass(self.h, len(cams), C.cast(carr, C.c_void_p),
+                                                    C.cast(farr, C.c_void_p) if farr is not None else None,
+                                                    C.c_void_p(rgba.data_ptr()), C.c_void_p(depth.data_ptr()),
+                                                    C.c_void_p(sp)))
+        self._views = None  # the last frame holds the 2n pass views
+        return rgba, depth
+
+    render_two_pass = vrs_render_views_two_pass
 
     def vrs_render_views_host(self, cams, foveas=None, rgba_host=None, depth_host=None, stream=None):
         """End-to-end path: outputs land in HOST buffers (numpy or pinned torch tensors)."""

@@ -403,3 +403,35 @@ def test_ewa_wide_fov_foveated_stereo(vrs, oracle_mod, hfov):
         r, o, g, oi = render_both(vrs, oracle_mod, scene, cams, fov, T=32, projection=proj)
         assert_lists_equal(r, o)
         assert_images_close(g, oi)
+
+
+@pytest.mark.parametrize("W,H,seed", [(320, 256, 13), (333, 251, 14)])
+def test_two_pass_baseline_parity(vrs, oracle_mod, W, H, seed):
+    """SURVEY §8f N1 (App. A): the two-pass foveated baseline through the C
+    ABI against oracle/twopass.py -- stereo, visibility masks (pass 2 only,
+    2x2-OR reduced), odd sizes; the 4-view pass frame's sorted pair list and
+    ranges bit-exact, every output pixel within the tolerances."""
+    from oracle import twopass as tpo
+    scene = sg.vr_room(seed, 20000, sh_degree=3)
+    f = sg.focal_for_hfov(W, 110.0)
+    cams = [sg.look_camera((x, 0, 0), 0.3, 0.1, 0.0, f=f, width=W, height=H, mask_slot=e)
+            for e, x in enumerate((-0.0315, 0.0315))]
+    fov = [sg.Fovea((W / 2, H / 2), (W / 4, H / 4), 0.10), sg.Fovea((W / 2 + 7.3, H / 2 - 5.1), (W / 5, H / 4), 0.2)]
+    masks = {0: sg.ellipse_mask(W, H), 1: sg.ellipse_mask(W, H, 1.0)}
+    r = vrs.Renderer(max_gaussians=scene.n, max_views=4, max_pairs=1 << 22, max_width=W, max_height=H,
+                     assign_tile=32)
+    r.upload(scene)
+    for s, m in masks.items():
+        r.set_mask(s, m)
+    rgba, depth = r.render_two_pass(cams, fov)
+    torch.cuda.synchronize()
+    g = vrs.vrs.split_views(rgba.cpu().numpy(), depth.cpu().numpy(), cams)
+    out, o = tpo.render_two_pass(oracle_mod, scene, cams, fov, masks=masks, assign_tile=32)
+    k, v = r.vrs_debug_pairs(True)
+    ok, ov = o.pairs(True)
+    assert np.array_equal(k, ok) and np.array_equal(v, ov)
+    assert np.array_equal(r.vrs_debug_ranges(), o.ranges())
+    assert_images_close(g, [(c.astype(np.float32), d.astype(np.float32)) for c, d in out])
+    # the second render reuses the cached half masks and per-eye setup
+    rgba2, depth2 = r.render_two_pass(cams, fov)
+    assert torch.equal(rgba, rgba2) and torch.equal(depth, depth2)
