@@ -42,7 +42,17 @@ void launch_ranges(const uint64_t* keys, const uint32_t* n_dev, int64_t cap, uin
 
 namespace {
 
-constexpr int kBatch = 64;  // splat records staged per shared-memory batch
+#ifndef VRS_BLEND_THREADS
+#define VRS_BLEND_THREADS 256
+#endif
+#ifndef VRS_BLEND_BATCH
+#define VRS_BLEND_BATCH 80
+#endif
+constexpr int kBT = VRS_BLEND_THREADS;   // threads per block: a whole 16x16 item, or half of it (16x8)
+constexpr int kSplit = 256 / kBT;        // blocks per item
+constexpr int kWarps = kBT / 32;
+constexpr int kBatch = VRS_BLEND_BATCH;  // splat records staged per shared-memory batch
+static_assert(kBatch <= kBT && (kSplit == 1 || kSplit == 2), "blend block shape");
 
 struct BlendSmem {
     float4 r0[kBatch];   // u.xyz, q_cut
@@ -52,16 +62,16 @@ struct BlendSmem {
     float4 r4[kBatch];   // A e, f, b.x, b.y
     float4 r5[kBatch];   // b.z, sigma, g (bits), -
     uint32_t mask[kBatch];
-    float4 wblock[8];    // per-warp sample extent xmin, xmax, ymin, ymax (pixel coords)
+    float4 wblock[kWarps];  // per-warp sample extent xmin, xmax, ymin, ymax (pixel coords)
     // per-thread resort window: ring of K slots, (tau, g) packed into one
     // order-preserving 64-bit key, alpha alongside; [slot][thread] layout is
     // bank-conflict free for any per-thread slot index
-    unsigned long long w_key[kWindow][kBlend];
-    float w_a[kWindow][kBlend];
+    unsigned long long w_key[kWindow][kBT];
+    float w_a[kWindow][kBT];
     unsigned long long cnt[4];
 };
 
-constexpr uint32_t kSlotBytes = kBlend * 8;                   // one ring slot of keys
+constexpr uint32_t kSlotBytes = kBT * 8;                   // one ring slot of keys
 constexpr uint32_t kRingMask = (kWindow - 1) * kSlotBytes;    // byte-offset ring mask
 static_assert((kWindow & (kWindow - 1)) == 0, "ring needs a power-of-two window");
 
@@ -118,19 +128,16 @@ __device__ __forceinline__ float key_tau(unsigned long long key) {
 
 template <bool kCounters, bool kEwa>
 #ifndef VRS_BLEND_MINB
-#define VRS_BLEND_MINB 4
+#define VRS_BLEND_MINB (1024 / VRS_BLEND_THREADS)
 #endif
-#ifndef VRS_BLEND_PREFETCH
-#define VRS_BLEND_PREFETCH 0
-#endif
-__global__ void __launch_bounds__(kBlend, VRS_BLEND_MINB) k_blend(FrameParams fp, FrameBufs fb, float* __restrict__ rgba,
+__global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, FrameBufs fb, float* __restrict__ rgba,
                                                       float* __restrict__ depth) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BlendSmem& S = *reinterpret_cast<BlendSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // locate the view and the item
     int vi = 0;
-    const int item = blockIdx.x;
+    const int item = blockIdx.x / kSplit, half = blockIdx.x % kSplit;  // half: rows 8-15 of the item
     while (vi + 1 < fp.n_views && item >= fp.v[vi + 1].item_off) vi++;
     const ViewParams& v = fp.v[vi];
     const uint32_t it = v.items[item - v.item_off];
@@ -138,7 +145,7 @@ __global__ void __launch_bounds__(kBlend, VRS_BLEND_MINB) k_blend(FrameParams fp
     const int T = fp.T;
     const int tx = tile % v.tw, ty = tile / v.tw;
     const int x0 = tx * T, y0 = ty * T;
-    const int lx = lane & 7, ly = lane >> 3, wx = (warp & 1) * 8, wy = (warp >> 1) * 4;
+    const int lx = lane & 7, ly = lane >> 3, wx = (warp & 1) * 8, wy = (warp >> 1) * 4 + half * 8;
     const int sx = wx + lx, sy = wy + ly;
     int px, py;  // pixel (full-rate) or group origin pixel (low)
     float xs, ys;
@@ -155,8 +162,8 @@ __global__ void __launch_bounds__(kBlend, VRS_BLEND_MINB) k_blend(FrameParams fp
         xs = (float)px + 0.5f;
         ys = (float)py + 0.5f;
     }
-    if (tid < 8) {
-        const int wwx = (tid & 1) * 8, wwy = (tid >> 1) * 4;
+    if (tid < kWarps) {
+        const int wwx = (tid & 1) * 8, wwy = (tid >> 1) * 4 + half * 8;
         float4 b;
         if (kind == kItemLow)
             b = make_float4((float)(x0 + 2 * wwx + 1), (float)(x0 + 2 * (wwx + 7) + 1), (float)(y0 + 2 * wwy + 1),
@@ -205,6 +212,70 @@ __global__ void __launch_bounds__(kBlend, VRS_BLEND_MINB) k_blend(FrameParams fp
         done = Tr < kTmin;
     };
 
+    // the contribution of one (sample, splat) pair with its alpha, depth and
+    // order key: insert into the window, pop the minimum
+    auto contribute = [&](const unsigned long long key, const float alpha, const uint32_t pos) {
+        if (kCounters) n_contrib++;
+        const unsigned long long kh = WK(hk);
+        const bool direct = key < kh;  // the new entry is the minimum
+        const float ah = WA(hk);
+        blend_one(direct ? key : kh, direct ? alpha : ah);
+        if (kCounters && done) stop_pos = pos;
+        if (direct || done) return;
+        hk = (hk + kSlotBytes) & kRingMask;
+        // insertion from the tail (entries arrive nearly sorted); dst
+        // is the hole, starting at the popped head's slot
+        uint32_t jo = (hk + (kWindow - 2) * kSlotBytes) & kRingMask;
+        uint32_t dst = (jo + kSlotBytes) & kRingMask;
+        unsigned long long kj = WK(jo);
+        int left = kWindow - 1;
+#pragma unroll 1
+        while (kj > key) {
+            WK(dst) = kj;
+            WA(dst) = WA(jo);
+            dst = jo;
+            if (--left == 0) break;
+            jo = (jo - kSlotBytes) & kRingMask;
+            kj = WK(jo);
+        }
+        WK(dst) = key;
+        WA(dst) = alpha;
+    };
+    // membership + alpha/tau of entry g for this sample; a3..a5 fetched only on contribution
+    auto evaluate = [&](const uint32_t pos, const uint32_t g, const float4 a0, const float4 a1, const float4 a2,
+                        auto&& load345) {
+        if (done) return;
+        float alpha, tau;
+        if (kEwa) {  // EWA baseline: q from the projected mean in pixels
+            const float dxp = xs - a0.x, dyp = ys - a0.y;
+            const float q = fmaf(dxp, fmaf(a0.w, dxp, a1.x * dyp), dyp * fmaf(a1.x, dxp, a1.y * dyp));
+            if (!(q <= a0.z)) return;
+            float4 a3, a4;
+            float2 a5;
+            load345(a3, a4, a5);
+            const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
+            const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, a5.x));
+            tau = __fdiv_rn(dtb, den);
+            alpha = alpha_of_x(fmaxf(q * -0.72134752f, -64.0f), a5.y);
+        } else {
+            const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
+            const float ex = fmaf(a1.x, x, a1.y);
+            const float ey = fmaf(a1.z, x, fmaf(a1.w, y, a2.x));
+            const float cx = fmaf(a2.y, ex, a2.z * ey), cy = fmaf(a2.z, ex, a2.w * ey);
+            const float num = fmaf(ex, cx, ey * cy);
+            const float ss = s * s;
+            if (!(s > 0.0f) || !(num <= a0.w * ss)) return;
+            // contribution: alpha and tau (R9: one IEEE reciprocal, exact on both sides)
+            float4 a3, a4;
+            float2 a5;
+            load345(a3, a4, a5);
+            const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
+            const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, a5.x));
+            alpha = alpha_tau(num, ss, den, dtb, a5.y, tau);
+        }
+        contribute(order_key(tau, g), alpha, pos);
+    };
+
     for (uint32_t base = rb; base < re; base += kBatch) {
         __syncthreads();
         const uint32_t idx = base + tid;
@@ -218,7 +289,7 @@ __global__ void __launch_bounds__(kBlend, VRS_BLEND_MINB) k_blend(FrameParams fp
             S.r5[tid] = make_float4(a5.x, a5.y, __uint_as_float(g), 0.0f);
             uint32_t m = 0;
 #pragma unroll
-            for (int w = 0; w < 8; w++) {
+            for (int w = 0; w < kWarps; w++) {
                 const float4 b = S.wblock[w];
                 const bool hit = !(a7.y < b.x || a7.x > b.y || a7.w < b.z || a7.z > b.w);
                 m |= hit ? (1u << w) : 0u;
@@ -231,95 +302,17 @@ __global__ void __launch_bounds__(kBlend, VRS_BLEND_MINB) k_blend(FrameParams fp
             if (__all_sync(0xffffffffu, done)) break;
             const bool rel = (c + lane < nb) && ((S.mask[c + lane] >> warp) & 1u);
             unsigned bits = __ballot_sync(0xffffffffu, rel);
-            // process entry j (its r0..r2 already in registers); `return` = skip
-            auto process = [&](const int j, const float4 a0, const float4 a1, const float4 a2) {
-                if (done) return;
-                float alpha, tau;
-                if (kEwa) {  // EWA baseline: q from the projected mean in pixels
-                    const float dxp = xs - a0.x, dyp = ys - a0.y;
-                    const float q = fmaf(dxp, fmaf(a0.w, dxp, a1.x * dyp), dyp * fmaf(a1.x, dxp, a1.y * dyp));
-                    if (!(q <= a0.z)) return;
-                    const float4 a3 = S.r3[j], a4 = S.r4[j], a5 = S.r5[j];
-                    const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
-                    const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, a5.x));
-                    tau = __fdiv_rn(dtb, den);
-                    alpha = alpha_of_x(fmaxf(q * -0.72134752f, -64.0f), a5.y);
-                } else {
-                    const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
-                    const float ex = fmaf(a1.x, x, a1.y);
-                    const float ey = fmaf(a1.z, x, fmaf(a1.w, y, a2.x));
-                    const float cx = fmaf(a2.y, ex, a2.z * ey), cy = fmaf(a2.z, ex, a2.w * ey);
-                    const float num = fmaf(ex, cx, ey * cy);
-                    const float ss = s * s;
-                    if (!(s > 0.0f) || !(num <= a0.w * ss)) return;
-                    // contribution: alpha and tau (R9: one IEEE reciprocal, exact on both sides)
-                    const float4 a3 = S.r3[j], a4 = S.r4[j];
-                    const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
-                    const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, S.r5[j].x));
-                    alpha = alpha_tau(num, ss, den, dtb, S.r5[j].y, tau);
-                }
-                const float4 a5 = S.r5[j];
-                const unsigned long long key = order_key(tau, __float_as_uint(a5.z));
-                if (kCounters) n_contrib++;
-                // insert, then pop the minimum of the K+1 entries
-                const unsigned long long kh = WK(hk);
-                const bool direct = key < kh;  // the new entry is the minimum
-                const float ah = WA(hk);
-                blend_one(direct ? key : kh, direct ? alpha : ah);
-                if (kCounters && done) stop_pos = base + j;
-                if (direct || done) return;
-                hk = (hk + kSlotBytes) & kRingMask;
-                // insertion from the tail (entries arrive nearly sorted); dst
-                // is the hole, starting at the popped head's slot
-                uint32_t jo = (hk + (kWindow - 2) * kSlotBytes) & kRingMask;
-                uint32_t dst = (jo + kSlotBytes) & kRingMask;
-                unsigned long long kj = WK(jo);
-                int left = kWindow - 1;
-#pragma unroll 1
-                while (kj > key) {
-                    WK(dst) = kj;
-                    WA(dst) = WA(jo);
-                    dst = jo;
-                    if (--left == 0) break;
-                    jo = (jo - kSlotBytes) & kRingMask;
-                    kj = WK(jo);
-                }
-                WK(dst) = key;
-                WA(dst) = alpha;
-            };
-#if VRS_BLEND_PREFETCH
-            // software pipeline: the next entry's coefficients are loaded before
-            // the current entry is processed (hides the shared-memory latency)
-            if (bits) {
-                int j = c + __ffs(bits) - 1;
-                bits &= bits - 1;
-                float4 a0 = S.r0[j], a1 = S.r1[j], a2 = kEwa ? a1 : S.r2[j];
-                while (true) {
-                    const bool more = bits != 0;
-                    int jn = j;
-                    float4 b0 = a0, b1 = a1, b2 = a2;
-                    if (more) {
-                        jn = c + __ffs(bits) - 1;
-                        bits &= bits - 1;
-                        b0 = S.r0[jn];
-                        b1 = S.r1[jn];
-                        if (!kEwa) b2 = S.r2[jn];
-                    }
-                    process(j, a0, a1, a2);
-                    if (!more) break;
-                    j = jn;
-                    a0 = b0;
-                    a1 = b1;
-                    a2 = b2;
-                }
-            }
-#else
             while (bits) {
                 const int j = c + __ffs(bits) - 1;
                 bits &= bits - 1;
-                process(j, S.r0[j], S.r1[j], kEwa ? S.r1[j] : S.r2[j]);
+                evaluate(base + j, __float_as_uint(S.r5[j].z), S.r0[j], S.r1[j], kEwa ? S.r1[j] : S.r2[j],
+                         [&](float4& a3, float4& a4, float2& a5) {
+                             a3 = S.r3[j];
+                             a4 = S.r4[j];
+                             const float4 t = S.r5[j];
+                             a5 = make_float2(t.x, t.y);
+                         });
             }
-#endif
         }
     }
     // drain the window in order (sentinels pop as no-ops)
@@ -401,6 +394,7 @@ void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* r
                   cudaStream_t st) {
     if (total_items <= 0) return;
     const size_t smem = sizeof(BlendSmem);
+    const unsigned grid = (unsigned)total_items * kSplit;
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(k_blend<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -410,11 +404,11 @@ void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* r
         attr_set = true;
     }
     if (fp.ewa) {
-        if (fp.counters) k_blend<true, true><<<total_items, kBlend, smem, st>>>(fp, fb, rgba, depth);
-        else k_blend<false, true><<<total_items, kBlend, smem, st>>>(fp, fb, rgba, depth);
+        if (fp.counters) k_blend<true, true><<<grid, kBT, smem, st>>>(fp, fb, rgba, depth);
+        else k_blend<false, true><<<grid, kBT, smem, st>>>(fp, fb, rgba, depth);
     } else {
-        if (fp.counters) k_blend<true, false><<<total_items, kBlend, smem, st>>>(fp, fb, rgba, depth);
-        else k_blend<false, false><<<total_items, kBlend, smem, st>>>(fp, fb, rgba, depth);
+        if (fp.counters) k_blend<true, false><<<grid, kBT, smem, st>>>(fp, fb, rgba, depth);
+        else k_blend<false, false><<<grid, kBT, smem, st>>>(fp, fb, rgba, depth);
     }
 }
 

@@ -407,6 +407,9 @@ __device__ __forceinline__ void proj_to_tilesplat(const Proj& p, TileSplat& s) {
 }
 
 // View-dependent colour: real SH through degree 3 (3DGS basis), +0.5, >= 0.
+// The coefficients come either from memory (src) or, already loaded, from q.
+__device__ __forceinline__ void sh_color_q(const float4 q4[12], int chunks, int ncoef, float dx, float dy, float dz,
+                                           float out[3]);
 __device__ void sh_color(const SceneDev& sc, int64_t g, int64_t N, int ncoef, float dx, float dy, float dz,
                          float out[3]) {
     const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
@@ -546,8 +549,8 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
 __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb, int64_t test_cap) {
     __shared__ uint32_t s_inc[256];
     __shared__ uint32_t s_sidx[256];
-    __shared__ uint32_t s_w[8];
-    __shared__ uint32_t s_base;
+    __shared__ uint32_t s_w[8], s_vw[8];
+    __shared__ uint32_t s_base, s_vbase;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int64_t N = fp.N;
     const uint32_t nc = *fb.cand_count;
@@ -560,11 +563,6 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
             while (vi + 1 < fp.n_views && (int64_t)sidx >= (int64_t)(vi + 1) * N) vi++;
             const int64_t g = (int64_t)sidx - (int64_t)vi * N;
             const ViewParams& v = fp.v[vi];
-            {  // the SH lines are needed after the projection: start fetching them into L2 now
-                const char* shp = reinterpret_cast<const char*>(sc.sh + (size_t)g * sc.sh_chunks);
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(shp));
-                if (sc.sh_chunks > 4) asm volatile("prefetch.global.L2 [%0];" ::"l"(shp + 128));
-            }
             const float4 m4 = __ldg(&sc.mu[g]);
             const float4 c0 = __ldg(&sc.cov[g]), c1 = __ldg(&sc.cov[N + g]);
             const float4 i0 = __ldg(&sc.icov[g]), i1 = __ldg(&sc.icov[N + g]);
@@ -577,12 +575,6 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
                 sat_count(v.sat, v.tw + 1, p.rect[0], p.rect[1], p.rect[2], p.rect[3]) > 0)
                 cnt = (uint32_t)((p.rect[2] - p.rect[0] + 1) * (p.rect[3] - p.rect[1] + 1));
             if (cnt) {
-                float rgb[3];
-                {
-                    const float dx = m4.x - v.o[0], dy = m4.y - v.o[1], dz = m4.z - v.o[2];
-                    const float inv = 1.0f / sqrtf(dot3(dx, dy, dz, dx, dy, dz));
-                    sh_color(sc, g, N, fp.sh_coeffs, dx * inv, dy * inv, dz * inv, rgb);
-                }
                 float4* rec = fb.rec + (size_t)sidx * kRecF4;
                 const uint32_t r01 = (uint32_t)p.rect[0] | ((uint32_t)p.rect[1] << 16);
                 const uint32_t r23 = (uint32_t)p.rect[2] | ((uint32_t)p.rect[3] << 16);
@@ -599,31 +591,40 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
                 rec[3] = make_float4(p.A[0], p.A[1], p.A[2], p.A[3]);
                 rec[4] = make_float4(p.A[4], p.A[5], p.bv[0], p.bv[1]);
                 rec[5] = make_float4(p.bv[2], p.sigma, p.eps, __uint_as_float(r01));
-                rec[6] = make_float4(rgb[0], rgb[1], rgb[2], __uint_as_float(r23));
+                rec[6] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(r23));  // (colour: k_color)
                 rec[7] = make_float4(p.bbox[0], p.bbox[1], p.bbox[2], p.bbox[3]);
-                fb.col[sidx] = make_float4(rgb[0], rgb[1], rgb[2], 0.0f);
             }
         }
-        // block inclusive scan of the counts
+        // block inclusive scan of the counts; visible splats (cnt > 0) counted alongside
         uint32_t inc = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
             if (lane >= o) inc += y;
         }
-        if (lane == 31) s_w[warp] = inc;
+        const unsigned vb = __ballot_sync(0xffffffffu, cnt != 0u);
+        if (lane == 31) {
+            s_w[warp] = inc;
+            s_vw[warp] = (uint32_t)__popc(vb);
+        }
         __syncthreads();
-        uint32_t wpre = 0, tot = 0;
+        uint32_t wpre = 0, tot = 0, vpre = 0, vtot = 0;
 #pragma unroll
         for (int w = 0; w < 8; w++) {
             wpre += (w < warp) ? s_w[w] : 0u;
             tot += s_w[w];
+            vpre += (w < warp) ? s_vw[w] : 0u;
+            vtot += s_vw[w];
         }
         s_inc[tid] = wpre + inc;
         s_sidx[tid] = sidx;
-        if (tid == 0) s_base = tot ? atomicAdd(fb.total_tests, tot) : 0u;
+        if (tid == 0) {
+            s_base = tot ? atomicAdd(fb.total_tests, tot) : 0u;
+            s_vbase = vtot ? atomicAdd(fb.vis_count, vtot) : 0u;
+        }
         __syncthreads();
         const uint32_t base = s_base;
+        if (cnt) fb.vis_list[s_vbase + vpre + __popc(vb & ((1u << lane) - 1u))] = sidx;
         for (uint32_t o = tid; o < tot; o += 256u) {
             int lo = 0, hi = 255;  // owner: first e with s_inc[e] > o
             while (lo < hi) {
@@ -810,8 +811,80 @@ __global__ void k_debug_splats(SceneDev sc, FrameParams fp, FrameBufs fb, int vi
     }
 }
 
+__device__ __forceinline__ void sh_color_q(const float4 q4[12], int chunks, int ncoef, float dx, float dy, float dz,
+                                           float out[3]) {
+    const float C0 = 0.28209479177387814f, C1 = 0.4886025119029199f;
+    float basis[16];
+    basis[0] = C0;
+    if (ncoef > 1) {
+        basis[1] = -C1 * dy; basis[2] = C1 * dz; basis[3] = -C1 * dx;
+    }
+    if (ncoef > 4) {
+        const float xx = dx * dx, yy = dy * dy, zz = dz * dz, xy = dx * dy, yz = dy * dz, xz = dx * dz;
+        basis[4] = 1.0925484305920792f * xy;
+        basis[5] = -1.0925484305920792f * yz;
+        basis[6] = 0.31539156525252005f * (2.0f * zz - xx - yy);
+        basis[7] = -1.0925484305920792f * xz;
+        basis[8] = 0.5462742152960396f * (xx - yy);
+        if (ncoef > 9) {
+            basis[9] = -0.5900435899266435f * dy * (3.0f * xx - yy);
+            basis[10] = 2.890611442640554f * xy * dz;
+            basis[11] = -0.4570457994644658f * dy * (4.0f * zz - xx - yy);
+            basis[12] = 0.3731763325901154f * dz * (2.0f * zz - 3.0f * xx - 3.0f * yy);
+            basis[13] = -0.4570457994644658f * dx * (4.0f * zz - xx - yy);
+            basis[14] = 1.445305721320277f * dz * (xx - yy);
+            basis[15] = -0.5900435899266435f * dx * (xx - 3.0f * yy);
+        }
+    }
+    float acc[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int c4 = 0; c4 < 12; c4++) {
+        if (c4 < chunks) {
+            const float qv[4] = {q4[c4].x, q4[c4].y, q4[c4].z, q4[c4].w};
+#pragma unroll
+            for (int k = 0; k < 4; k++) {
+                const int f = 4 * c4 + k;
+                if (f / 3 < ncoef) acc[f % 3] = fmaf(basis[f / 3], qv[k], acc[f % 3]);
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 3; c++) {
+        const float r = acc[c] + 0.5f;
+        out[c] = r > 0.0f ? r : 0.0f;
+    }
+}
+
+// Step 1c: view-dependent SH colour (Eq.2 colour term) of the
+// splats with at least one candidate tile, a streaming pass over the list the
+// preprocess appended them to (kept out of k_preprocess so its block scan
+// does not wait on the 192 B SH fetches).
+__global__ void __launch_bounds__(256) k_color(SceneDev sc, FrameParams fp, FrameBufs fb) {
+    const int64_t N = fp.N;
+    const uint32_t n = *fb.vis_count;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t sidx = fb.vis_list[i];
+        int vi = 0;
+        while (vi + 1 < fp.n_views && (int64_t)sidx >= (int64_t)(vi + 1) * N) vi++;
+        const int64_t g = (int64_t)sidx - (int64_t)vi * N;
+        const ViewParams& v = fp.v[vi];
+        // all loads first (the mean and every SH chunk are independent)
+        const float4 m4 = __ldg(&sc.mu[g]);
+        const float4* src = sc.sh + (size_t)g * sc.sh_chunks;
+        float4 q[12];
+#pragma unroll
+        for (int c4 = 0; c4 < 12; c4++) q[c4] = c4 < sc.sh_chunks ? __ldg(src + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float dx = m4.x - v.o[0], dy = m4.y - v.o[1], dz = m4.z - v.o[2];
+        const float inv = 1.0f / sqrtf(dot3(dx, dy, dz, dx, dy, dz));
+        float rgb[3];
+        sh_color_q(q, sc.sh_chunks, fp.sh_coeffs, dx * inv, dy * inv, dz * inv, rgb);
+        fb.col[sidx] = make_float4(rgb[0], rgb[1], rgb[2], 0.0f);
+    }
+}
+
 void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {
     cudaMemsetAsync(fb.total_tests, 0, 4, st);
+    cudaMemsetAsync(fb.vis_count, 0, 4, st);
     if (fp.N == 0) return;
     const int B = 256;
     cudaMemsetAsync(fb.cand_count, 0, 4, st);
@@ -820,6 +893,7 @@ void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     k_preprocess<<<sms * 6, B, 0, st>>>(sc, fp, fb, test_cap);
+    k_color<<<sms * 8, B, 0, st>>>(sc, fp, fb);
 }
 
 static int sm_count() {

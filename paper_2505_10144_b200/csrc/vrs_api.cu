@@ -47,7 +47,8 @@ struct vrs_context {
     float4* d_rec = nullptr;
     float4* d_col = nullptr;
     uint32_t* d_cand = nullptr;
-    uint32_t *d_counts = nullptr, *d_misc = nullptr;  // misc: pairs, overflow, tests, candidates
+    uint32_t *d_counts = nullptr, *d_misc = nullptr;  // misc: pairs, overflow, tests, candidates, visible
+    uint32_t* d_vis_list = nullptr;
     unsigned long long* d_sidk = nullptr;    // [test_cap] candidate map
     int64_t test_cap = 0;
     uint64_t *d_keys = nullptr, *d_keys_alt = nullptr;
@@ -116,7 +117,7 @@ static vrs_status cuda_check(vrs_context* c, cudaError_t e, const char* where) {
     } while (0)
 
 static void free_all(vrs_context* c) {
-    void* ptrs[] = {c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_col, c->d_cand, c->d_counts, c->d_misc,
+    void* ptrs[] = {c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_col, c->d_cand, c->d_counts, c->d_misc, c->d_vis_list,
                     c->d_sidk,
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
@@ -166,6 +167,7 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     A(dalloc(&ctx->d_col, (size_t)V * N));
     A(dalloc(&ctx->d_cand, (size_t)V * N));
     A(dalloc(&ctx->d_counts, (size_t)V * N));
+    A(dalloc(&ctx->d_vis_list, (size_t)V * N));
     ctx->test_cap = 4 * P;
     A(dalloc(&ctx->d_sidk, (size_t)ctx->test_cap));
     A(dalloc(&ctx->d_misc, 8));
@@ -481,6 +483,8 @@ static FrameBufs frame_bufs(vrs_context* ctx) {
     fb.col = ctx->d_col;
     fb.cand = ctx->d_cand;
     fb.cand_count = ctx->d_misc + 3;
+    fb.vis_list = ctx->d_vis_list;
+    fb.vis_count = ctx->d_misc + 4;
     fb.total_tests = ctx->d_misc + 2;
     fb.sidk = ctx->d_sidk;
     fb.counts = ctx->d_counts;

@@ -75,6 +75,8 @@ struct FrameBufs {
     uint32_t* cand_count;    // [1]
     uint32_t* total_tests;   // [1] (device)
     unsigned long long* sidk;  // [test_cap] candidate -> (splat view*N+g) | (rect-local tile index << 32)
+    uint32_t* vis_list;      // [V*N] (view*N + g) with >= 1 candidate tile (colour work list)
+    uint32_t* vis_count;     // [1]
     uint32_t* counts;        // [V*N] exact pair counts (parity hook only)
     uint32_t* total;         // [1] pair total (device)
     uint32_t* overflow;      // [1] capacity overflow flag
