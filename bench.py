@@ -27,6 +27,7 @@ import os
 import statistics
 import subprocess
 import sys
+import math
 import threading
 import time
 
@@ -50,6 +51,9 @@ CONFIGS = {
                     "sharded by rank, foveated"),
     "c5": dict(n=500_000, scale_mul=1.0, sh=3, fovea=True, T=32, masks=False, seed=2,
                desc="C2 scene, FoV sweep 90-160 deg, Optimal Projection vs EWA baseline"),
+    "c7": dict(n=500_000, scale_mul=1.0, sh=3, fovea=False, T=16, masks=False, seed=2,
+               desc="large-FOV protocol (App. D) on the C2 scene: per eye, crop [W,2W)x[H,2H) of the 3W x 3H "
+                    "render at the same pixel focal length vs the W x H render, Optimal Projection vs EWA"),
     "c6": dict(n=500_000, scale_mul=1.0, sh=3, fovea=True, T=32, masks=True, seed=2, two_pass=True,
                desc="C2 workload rendered with the paper's two-pass foveated baseline (App. A): full-res "
                     "centre crop + half-res masked periphery, bilinear upsample + blend (SURVEY N1)"),
@@ -211,6 +215,62 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_c7(args):
+    """Config C7: large-FOV protocol on the CUDA
+    path.  Both eyes of the C2 stereo pair are rendered at W x H and at 3W x 3H
+    with the same pixel focal length; the centre crop of the wide render casts
+    the original rays pixel for pixel, so a projection without error reproduces
+    the normal render exactly.  Reports crop-vs-normal PSNR (RGB) and max |diff|
+    per projection, and the wide-render time."""
+    import torch
+    from paper_2505_10144_b200 import Renderer
+    from paper_2505_10144_b200.protocol import centre_crop, psnr, wide_camera
+    from paper_2505_10144_b200.vrs import split_views
+    cfg = CONFIGS["c7"]
+    scene = sg.vr_room(cfg["seed"], cfg["n"], sh_degree=cfg["sh"])
+    cams = sg.stereo_pair(masks=False)
+    wides = [wide_camera(c) for c in cams]
+    rows = []
+    stream = torch.cuda.Stream()
+    for proj in (0, 1):
+        r = Renderer(max_gaussians=scene.n, max_views=2, max_pairs=48 << 20, max_width=wides[0].width,
+                     max_height=wides[0].height, assign_tile=cfg["T"], projection=proj)
+        r.upload(scene)
+        with torch.cuda.stream(stream):
+            a = r.render(cams, None, stream=stream)
+            normal = split_views(a[0].cpu().numpy(), a[1].cpu().numpy(), cams)
+            r.vrs_set_instrumentation(counters=0, timing=1)
+            rw, dw = r.alloc_outputs(wides)
+            for _ in range(max(args.warmup, 1)):
+                r.render(wides, None, rw, dw, stream=stream)
+            ms = []
+            for _ in range(max(args.steps // 4, 2)):
+                r.render(wides, None, rw, dw, stream=stream)
+                ms.append(r.stats()["stage_ms"][7])
+            wide = split_views(rw.cpu().numpy(), dw.cpu().numpy(), wides)
+        st = r.stats()
+        for e in range(2):
+            crop = centre_crop(wide[e][0], cams[e])
+            nrm = normal[e][0]
+            p = psnr(crop[..., :3], nrm[..., :3])
+            rows.append({"projection": "OP" if proj == 0 else "EWA", "eye": e,
+                         "crop_psnr_db": None if math.isinf(p) else p, "identical": bool(math.isinf(p)),
+                         "max_abs_rgb_diff": float(np.abs(crop[..., :3] - nrm[..., :3]).max()),
+                         "wide_pairs_per_eye": st["pairs"] / 2, "wide_stereo_ms": float(np.median(ms))})
+        r.close()
+        del rw, dw
+        torch.cuda.empty_cache()
+    ewa = [x["crop_psnr_db"] for x in rows if x["projection"] == "EWA"]
+    ewa_v = float(np.mean([x for x in ewa if x is not None])) if any(x is not None for x in ewa) else None
+    line = {"metric": "C7 large-FOV protocol: crop-vs-normal PSNR (dB) of the EWA baseline (OP: identical)",
+            "value": ewa_v, "unit": "dB", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "higher_is_better": True, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "c7", "desc": cfg["desc"], "gaussians": scene.n, "normal": [cams[0].width,
+                       cams[0].height], "wide": [wides[0].width, wides[0].height], "assign_tile": cfg["T"]},
+            "rows": rows}
+    print(json.dumps(line), flush=True)
+
+
 def run_c5(args):
     """Config C5: FoV sweep 90-160 deg on the C2 scene, Optimal Projection vs the
     EWA baseline: pairs per eye, blend ms and frame ms per FoV (one GPU)."""
@@ -259,6 +319,8 @@ def main():
         return run_reference(args)
     if args.config == "c5":
         return run_c5(args)
+    if args.config == "c7":
+        return run_c7(args)
     import torch
     import torch.distributed as dist
 
