@@ -2,29 +2,31 @@
 // ... ranges"): the (tile, depth) sort of the Gaussian/tile pairs as a binned
 // per-tile sort instead of a global radix sort.
 //
-// The fused tile test (k_project.cu) already knows every pair's tile, so it
-// counts pairs per tile with one atomic each and keeps the returned arrival
-// rank.  Then:
-//   k_tile_scan  one block: exclusive scan of the per-tile counts -> ranges
-//                (empty tiles (0, 0), as the oracle reports them), the list
-//                of non-empty tiles, and the counters zeroed for the next frame;
-//   k_bucket     pair i -> bucket[range_begin(tile) + rank_i] = (depth bits << 32) | g;
-//   k_tile_sort  one block per tile: the tile's (depth bits, g) keys sorted in
-//                shared memory by a bitonic network (tiles larger than the
-//                shared-memory capacity: sorted chunks merged along merge paths
-//                in global memory), written back as (tile << 32 | depth, g).
+// The tile test (k_project.cu k_tiletest_direct) already knows every pair's
+// tile: it takes the pair's arrival rank from the tile's counter and writes
+// (depth bits << 32 | g) straight into the tile's bucket slot (tile *
+// kTileCap + rank), or onto an overflow list past kTileCap.  Then:
+//   k_tile_scan   one block: exclusive scans of the per-tile counts -> ranges
+//                 (empty tiles (0, 0), as the oracle reports them; clamped to
+//                 the pair capacity), of the overflow counts -> overflow
+//                 offsets, the pair total, the list of non-empty tiles, and
+//                 the counters zeroed for the next frame;
+//   k_ovf_bucket  overflow pairs -> their per-tile overflow slots;
+//   k_tile_sort   one warp per tile of <= 256 pairs (keys in registers,
+//                 bitonic by shuffles), one block per larger tile (shared-
+//                 memory bitonic; beyond the shared-memory capacity sorted
+//                 chunks merged along merge paths in global memory), written
+//                 back as (tile << 32 | depth, g) at the tile's range.
 // (depth bits, g) is unique inside a tile, so the result does not depend on
 // the atomic arrival order and equals the stable (tile, depth) sort of the
 // (view, g, tile) emission order -- the oracle's order, bit for bit.
-// Traffic: counts + pairs read twice and written twice (~40 B/pair), against
-// ~6 read+write passes (~150 B/pair) for the 46-bit LSD radix sort it replaces.
 #include "vrs_internal.cuh"
 
 namespace vrs {
 
 namespace {
 constexpr int kScanT = 1024;
-constexpr int kScanPer = 8;
+constexpr int kScanPer = 4;
 constexpr int kScanRound = kScanT * kScanPer;
 constexpr int kBinT = 256;
 constexpr int kWarpSortMax = 256;  // tiles up to this size: one warp, keys in registers (E <= 8)
@@ -139,15 +141,17 @@ __device__ __forceinline__ void warp_sort_tile(const uint64_t* __restrict__ bk, 
 }  // namespace
 
 __global__ void __launch_bounds__(kScanT) k_tile_scan(uint32_t* __restrict__ cnt, int64_t n_tiles,
-                                                      uint32_t* __restrict__ ranges, uint32_t* __restrict__ list,
-                                                      uint32_t* __restrict__ list_n, int64_t list_cap,
-                                                      uint32_t small_max) {
-    __shared__ uint32_t s_c[kScanRound];
-    __shared__ uint32_t s_w[kScanT / 32];
+                                                      uint32_t* __restrict__ ranges, uint32_t* __restrict__ ovf_off,
+                                                      uint32_t* __restrict__ total, uint32_t cap,
+                                                      uint32_t* __restrict__ list, uint32_t* __restrict__ list_n,
+                                                      int64_t list_cap, uint32_t small_max) {
+    __shared__ uint32_t s_c[kScanRound];  // counts, then tile starts
+    __shared__ uint32_t s_o[kScanRound];  // overflow starts
+    __shared__ uint32_t s_w[kScanT / 32], s_wo[kScanT / 32];
     __shared__ uint32_t s_nb, s_ns;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (tid == 0) s_nb = s_ns = 0;
-    uint32_t carry = 0;
+    uint32_t carry = 0, ocarry = 0;
     for (int64_t r0 = 0; r0 < n_tiles; r0 += kScanRound) {
         const int m = (int)min((int64_t)kScanRound, n_tiles - r0);
         for (int i = tid; i < m; i += kScanT) {  // coalesced, and re-zero for the next frame
@@ -155,48 +159,71 @@ __global__ void __launch_bounds__(kScanT) k_tile_scan(uint32_t* __restrict__ cnt
             cnt[r0 + i] = 0u;
         }
         __syncthreads();
-        uint32_t v[kScanPer], sum = 0;
+        uint32_t v[kScanPer], sum = 0, osum = 0;
 #pragma unroll
         for (int k = 0; k < kScanPer; k++) {
             const int idx = tid * kScanPer + k;
             v[k] = idx < m ? s_c[idx] : 0u;
             sum += v[k];
+            osum += v[k] > kTileCap ? v[k] - kTileCap : 0u;
         }
-        uint32_t inc = sum;
+        uint32_t inc = sum, oinc = osum;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
             const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
+            const uint32_t yo = __shfl_up_sync(0xffffffffu, oinc, o);
+            if (lane >= o) {
+                inc += y;
+                oinc += yo;
+            }
         }
-        if (lane == 31) s_w[warp] = inc;
+        if (lane == 31) {
+            s_w[warp] = inc;
+            s_wo[warp] = oinc;
+        }
         __syncthreads();
         if (warp == 0) {
-            uint32_t w = s_w[lane];
+            uint32_t w = s_w[lane], wo = s_wo[lane];
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= o) w += y;
+                const uint32_t yo = __shfl_up_sync(0xffffffffu, wo, o);
+                if (lane >= o) {
+                    w += y;
+                    wo += yo;
+                }
             }
             s_w[lane] = w;
+            s_wo[lane] = wo;
         }
         __syncthreads();
         uint32_t excl = carry + (warp ? s_w[warp - 1] : 0u) + inc - sum;
+        uint32_t oexcl = ocarry + (warp ? s_wo[warp - 1] : 0u) + oinc - osum;
 #pragma unroll
-        for (int k = 0; k < kScanPer; k++) {  // tile starts replace the counts (all were read above)
+        for (int k = 0; k < kScanPer; k++) {  // starts replace the counts (all were read above)
             const int idx = tid * kScanPer + k;
-            if (idx < m) s_c[idx] = excl;
+            if (idx < m) {
+                s_c[idx] = excl;
+                s_o[idx] = oexcl;
+            }
             excl += v[k];
+            oexcl += v[k] > kTileCap ? v[k] - kTileCap : 0u;
         }
         const uint32_t carry_next = carry + s_w[kScanT / 32 - 1];
+        const uint32_t ocarry_next = ocarry + s_wo[kScanT / 32 - 1];
         __syncthreads();
         const unsigned lt = (1u << lane) - 1u;
-        for (int i0 = 0; i0 < m; i0 += kScanT) {  // coalesced (start, end) stores + list appends
+        for (int i0 = 0; i0 < m; i0 += kScanT) {  // coalesced stores + list appends
             const int i = i0 + tid;
-            uint32_t c = 0, st = 0;
+            uint32_t c = 0;
             if (i < m) {
-                st = s_c[i];
+                const uint32_t st = s_c[i];
                 c = (i + 1 < m ? s_c[i + 1] : carry_next) - st;
-                reinterpret_cast<uint2*>(ranges)[r0 + i] = c ? make_uint2(st, st + c) : make_uint2(0u, 0u);
+                // clamped to the pair capacity (only after an overflow, which the stats report)
+                const uint32_t a = min(st, cap), b = min(st + c, cap);
+                reinterpret_cast<uint2*>(ranges)[r0 + i] = c ? make_uint2(a, b) : make_uint2(0u, 0u);
+                ovf_off[r0 + i] = s_o[i];
+                c = b - a;
             }
             const uint32_t t = (uint32_t)(r0 + i);
             const unsigned mb = __ballot_sync(0xffffffffu, c > small_max);
@@ -212,43 +239,38 @@ __global__ void __launch_bounds__(kScanT) k_tile_scan(uint32_t* __restrict__ cnt
             if ((ms >> lane) & 1u) list[list_cap - 1 - (bs + __popc(ms & lt))] = t;  // small ones from the back
         }
         carry = carry_next;
+        ocarry = ocarry_next;
         __syncthreads();
     }
     if (tid == 0) {
         list_n[0] = s_nb;
         list_n[1] = s_ns;
         list_n[2] = 0u;  // k_tile_sort's small-tile work counter
+        *total = carry;
     }
 }
 
-__global__ void __launch_bounds__(256) k_bucket(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ vals,
-                                                const uint32_t* __restrict__ rank, const uint32_t* __restrict__ n_dev,
-                                                int64_t cap, const uint32_t* __restrict__ ranges,
-                                                uint64_t* __restrict__ bucket) {
-    const int64_t n = min((int64_t)*n_dev, cap);
-    constexpr int U = 4;  // independent items per thread (latency hiding)
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i0 < n; i0 += stride * U) {
-        uint64_t k[U];
-        uint32_t r[U], v[U], b[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            const int64_t i = i0 + u * stride;
-            k[u] = i < n ? keys[i] : 0ull;
-            r[u] = i < n ? rank[i] : 0u;
-            v[u] = i < n ? vals[i] : 0u;
-        }
-#pragma unroll
-        for (int u = 0; u < U; u++) b[u] = (i0 + u * stride < n) ? ranges[2 * (size_t)(uint32_t)(k[u] >> 32)] : 0u;
-#pragma unroll
-        for (int u = 0; u < U; u++)
-            if (i0 + u * stride < n) bucket[b[u] + r[u]] = (k[u] << 32) | v[u];
+// Overflow pairs (rank >= kTileCap) into their tile's overflow slots.
+__global__ void __launch_bounds__(256) k_ovf_bucket(const uint64_t* __restrict__ okeys,
+                                                    const uint32_t* __restrict__ ovals,
+                                                    const uint32_t* __restrict__ orank,
+                                                    const uint32_t* __restrict__ n_dev, uint32_t cap,
+                                                    const uint32_t* __restrict__ ovf_off,
+                                                    uint64_t* __restrict__ obucket) {
+    const uint32_t n = min(*n_dev, cap);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint64_t k = okeys[i];
+        const uint32_t pos = ovf_off[(uint32_t)(k >> 32)] + orank[i] - kTileCap;
+        if (pos < cap) obucket[pos] = (k << 32) | ovals[i];
     }
 }
 
 __global__ void __launch_bounds__(kBinT, 4) k_tile_sort(const uint32_t* __restrict__ list,
                                                      const uint32_t* __restrict__ list_n, int64_t list_cap,
-                                                     const uint32_t* __restrict__ ranges, uint64_t* bucket,
+                                                     const uint32_t* __restrict__ ranges,
+                                                     const uint64_t* __restrict__ tbucket,
+                                                     const uint32_t* __restrict__ ovf_off,
+                                                     const uint64_t* __restrict__ obucket, uint64_t* scratch,
                                                      uint64_t* keys, uint32_t* __restrict__ vals, uint32_t cap_smem,
                                                      uint32_t* work) {
     extern __shared__ __align__(16) uint64_t s_k[];
@@ -259,13 +281,18 @@ __global__ void __launch_bounds__(kBinT, 4) k_tile_sort(const uint32_t* __restri
         const uint32_t t = list[w];
         const uint32_t off = ranges[2 * (size_t)t], n = ranges[2 * (size_t)t + 1] - off;
         const uint64_t tk = (uint64_t)t << 32;
-        uint64_t* bk = bucket + off;
+        const uint64_t* tb = tbucket + (size_t)t * kTileCap;
+        const uint64_t* ob = obucket + ovf_off[t];  // element i >= kTileCap is ob[i - kTileCap]
+        uint64_t* bk = scratch + off;
         for (uint32_t c0 = 0; c0 < n; c0 += cap_smem) {
             const uint32_t m = min(cap_smem, n - c0);
             uint32_t P = 64;
             while (P < m) P <<= 1;
             __syncthreads();  // the previous tile/chunk is done with s_k
-            for (uint32_t i = tid; i < P; i += kBinT) s_k[i] = i < m ? bk[c0 + i] : ~0ull;
+            for (uint32_t i = tid; i < P; i += kBinT) {
+                const uint32_t e = c0 + i;
+                s_k[i] = i < m ? (e < kTileCap ? tb[e] : ob[e - kTileCap]) : ~0ull;
+            }
             __syncthreads();
             bitonic_sort_smem<kBinT>(s_k, P);
             if (n <= cap_smem) {
@@ -278,7 +305,7 @@ __global__ void __launch_bounds__(kBinT, 4) k_tile_sort(const uint32_t* __restri
                 for (uint32_t i = tid; i < m; i += kBinT) bk[c0 + i] = s_k[i];
             }
         }
-        if (n > cap_smem) {  // merge the sorted chunks: bucket <-> keys ping-pong over this tile's range
+        if (n > cap_smem) {  // merge the sorted chunks: scratch <-> keys ping-pong over this tile's range
             uint64_t* src = bk;
             uint64_t* dst = keys + off;
             for (uint32_t L = cap_smem; L < n; L <<= 1) {
@@ -311,9 +338,10 @@ __global__ void __launch_bounds__(kBinT, 4) k_tile_sort(const uint32_t* __restri
         const uint32_t t = list[list_cap - 1 - w];
         const uint32_t off = ranges[2 * (size_t)t], n = ranges[2 * (size_t)t + 1] - off;
         const uint64_t tk = (uint64_t)t << 32;
-        if (n <= 64) warp_sort_tile<2>(bucket + off, n, tk, keys + off, vals + off, sw, lane);
-        else if (n <= 128) warp_sort_tile<4>(bucket + off, n, tk, keys + off, vals + off, sw, lane);
-        else warp_sort_tile<8>(bucket + off, n, tk, keys + off, vals + off, sw, lane);
+        const uint64_t* tb = tbucket + (size_t)t * kTileCap;  // n <= 256 <= kTileCap: all direct slots
+        if (n <= 64) warp_sort_tile<2>(tb, n, tk, keys + off, vals + off, sw, lane);
+        else if (n <= 128) warp_sort_tile<4>(tb, n, tk, keys + off, vals + off, sw, lane);
+        else warp_sort_tile<8>(tb, n, tk, keys + off, vals + off, sw, lane);
     }
 }
 
@@ -329,14 +357,19 @@ static int sms_now() {
 }
 
 void launch_binsort(FrameBufs fb, int64_t cap, int64_t n_tiles, BinScratch b, cudaStream_t st) {
-    if (n_tiles <= 0) return;
+    if (n_tiles <= 0) {
+        cudaMemsetAsync(fb.total, 0, 4, st);
+        return;
+    }
     cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kBinCap * 8));
     const int sms = sms_now();
-    k_tile_scan<<<1, kScanT, 0, st>>>(b.tile_cnt, n_tiles, fb.ranges, b.list, b.list_n, b.max_tiles,
-                                      min(b.cap_smem, (uint32_t)kWarpSortMax));
-    k_bucket<<<sms * 8, 256, 0, st>>>(fb.keys, fb.vals, b.rank, fb.total, cap, fb.ranges, fb.keys_alt);
-    k_tile_sort<<<sms * 4, kBinT, kBinCap * 8, st>>>(b.list, b.list_n, b.max_tiles, fb.ranges, fb.keys_alt, fb.keys,
-                                                     fb.vals, b.cap_smem, b.list_n + 2);
+    k_tile_scan<<<1, kScanT, 0, st>>>(b.tile_cnt, n_tiles, fb.ranges, b.ovf_off, fb.total, (uint32_t)cap, b.list,
+                                      b.list_n, b.max_tiles, min(b.cap_smem, (uint32_t)kWarpSortMax));
+    k_ovf_bucket<<<sms * 2, 256, 0, st>>>(fb.keys_alt, fb.vals_alt, b.rank, b.ovf_count, (uint32_t)cap, b.ovf_off,
+                                          b.obucket);
+    k_tile_sort<<<sms * 4, kBinT, kBinCap * 8, st>>>(b.list, b.list_n, b.max_tiles, fb.ranges, b.tbucket, b.ovf_off,
+                                                     b.obucket, fb.keys_alt, fb.keys, fb.vals, b.cap_smem,
+                                                     b.list_n + 2);
 }
 
 }  // namespace vrs

@@ -696,9 +696,49 @@ __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const Fram
     return true;
 }
 
+// Frame path: every kept pair takes its arrival rank in its tile's counter
+// and goes straight into the tile's bucket slot (tile * kTileCap + rank), or,
+// past kTileCap, onto the overflow list (k_ovf_bucket places those once the
+// tile offsets are known).  No compaction, no block synchronisation.
+__global__ void __launch_bounds__(kTT, VRS_TT_MINB) k_tiletest_direct(FrameParams fp, FrameBufs fb, int64_t test_cap,
+                                                                      BinScratch bs) {
+    const int64_t total = min((int64_t)*fb.total_tests, test_cap);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < total; t0 += stride * kTTItems) {
+        uint64_t key[kTTItems];
+        uint32_t gv[kTTItems];
+        bool keep[kTTItems];
+#pragma unroll
+        for (int it = 0; it < kTTItems; it++) {
+            const int64_t t = t0 + it * stride;
+            keep[it] = false;
+            key[it] = 0;
+            gv[it] = 0;
+            if (t < total) keep[it] = test_candidate(fp, fb, fb.sidk[t], key[it], gv[it]);
+        }
+#pragma unroll
+        for (int it = 0; it < kTTItems; it++) {
+            if (!keep[it]) continue;
+            const uint32_t tl = (uint32_t)(key[it] >> 32);
+            const uint32_t r = atomicAdd(&bs.tile_cnt[tl], 1u);
+            if (r < kTileCap) {
+                bs.tbucket[(size_t)tl * kTileCap + r] = (key[it] << 32) | gv[it];
+            } else {
+                const uint32_t o = atomicAdd(bs.ovf_count, 1u);
+                if (o < fp.pair_cap) {
+                    fb.keys_alt[o] = key[it];
+                    fb.vals_alt[o] = gv[it];
+                    bs.rank[o] = r;
+                }
+            }
+        }
+    }
+}
+
+// Parity hook path (vrs_debug_pairs sorted=0): the kept pairs compacted into
+// (keys, vals) by one atomic per 512-candidate block tile.
 __global__ void __launch_bounds__(kTT, VRS_TT_MINB) k_tiletest(FrameParams fp, FrameBufs fb, int64_t test_cap, uint64_t* keys,
-                                                  uint32_t* vals, uint32_t* tile_cnt, uint32_t* rank,
-                                                  uint32_t* counter) {
+                                                  uint32_t* vals, uint32_t* counter) {
     __shared__ uint32_t s_wc[kTT / 32 * kTTItems];
     __shared__ uint32_t s_tile, s_base;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -721,7 +761,6 @@ __global__ void __launch_bounds__(kTT, VRS_TT_MINB) k_tiletest(FrameParams fp, F
             gv[it] = 0;
             if (t < total) keep[it] = test_candidate(fp, fb, fb.sidk[t], key[it], gv[it]);
         }
-        // block-local positions, one global atomic per block tile for the base
         uint32_t wbits[kTTItems];
 #pragma unroll
         for (int it = 0; it < kTTItems; it++) {
@@ -751,7 +790,6 @@ __global__ void __launch_bounds__(kTT, VRS_TT_MINB) k_tiletest(FrameParams fp, F
                 if (pos < fp.pair_cap) {
                     keys[pos] = key[it];
                     vals[pos] = gv[it];
-                    if (tile_cnt) rank[pos] = atomicAdd(&tile_cnt[(uint32_t)(key[it] >> 32)], 1u);
                 }
             }
         }
@@ -908,11 +946,18 @@ static int sm_count() {
 }
 
 void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, uint64_t* keys, uint32_t* vals,
-                     uint32_t* tile_cnt, uint32_t* rank, uint32_t* counter, cudaStream_t st) {
+                     uint32_t* counter, cudaStream_t st) {
     cudaMemsetAsync(fb.total, 0, 4, st);  // pair total: block atomics below
     if ((int64_t)fp.n_views * fp.N == 0) return;
     cudaMemsetAsync(counter, 0, 4, st);
-    k_tiletest<<<sm_count() * 8, kTT, 0, st>>>(fp, fb, test_cap, keys, vals, tile_cnt, rank, counter);
+    k_tiletest<<<sm_count() * 8, kTT, 0, st>>>(fp, fb, test_cap, keys, vals, counter);
+}
+
+void launch_tiletest_direct(const FrameParams& fp, FrameBufs fb, int64_t test_cap, const BinScratch& bs,
+                            cudaStream_t st) {
+    cudaMemsetAsync(bs.ovf_count, 0, 4, st);
+    if ((int64_t)fp.n_views * fp.N == 0) return;
+    k_tiletest_direct<<<sm_count() * 8, kTT, 0, st>>>(fp, fb, test_cap, bs);
 }
 
 void launch_counts(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {

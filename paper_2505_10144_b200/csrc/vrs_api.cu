@@ -121,7 +121,7 @@ static void free_all(vrs_context* c) {
                     c->d_sidk,
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
-                    c->bin.tile_cnt, c->bin.rank, c->bin.list, c->bin.list_n,
+                    c->bin.tile_cnt, c->bin.rank, c->bin.list, c->bin.list_n, c->bin.tbucket, c->bin.ovf_off, c->bin.obucket,
                     c->d_sat, c->d_cls, c->d_items, c->d_nitems, c->d_out_rgba, c->d_out_depth};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -170,7 +170,7 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     A(dalloc(&ctx->d_vis_list, (size_t)V * N));
     ctx->test_cap = 4 * P;
     A(dalloc(&ctx->d_sidk, (size_t)ctx->test_cap));
-    A(dalloc(&ctx->d_misc, 8));
+    A(dalloc(&ctx->d_misc, 8));  // pairs, overflow, tests, candidates, visible, tile overflow, primitive n, -
     A(dalloc(&ctx->d_keys, (size_t)P));
     A(dalloc(&ctx->d_keys_alt, (size_t)P));
     A(dalloc(&ctx->d_vals, (size_t)P));
@@ -189,6 +189,9 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     ctx->bin.cap_smem = kBinCap;
     A(dalloc(&ctx->bin.tile_cnt, (size_t)ctx->bin.max_tiles));
     A(dalloc(&ctx->bin.rank, (size_t)P));
+    A(dalloc(&ctx->bin.tbucket, (size_t)ctx->bin.max_tiles * kTileCap));
+    A(dalloc(&ctx->bin.ovf_off, (size_t)ctx->bin.max_tiles));
+    A(dalloc(&ctx->bin.obucket, (size_t)P));
     A(dalloc(&ctx->bin.list, (size_t)ctx->bin.max_tiles));
     A(dalloc(&ctx->bin.list_n, 4));
     A(dalloc(&ctx->d_vis, (size_t)V * ctx->max_tiles_view));
@@ -203,6 +206,7 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
         return (e == cudaErrorMemoryAllocation) ? VRS_E_OOM : VRS_E_CUDA;
     }
     cudaMemset(ctx->d_misc, 0, 32);
+    ctx->bin.ovf_count = ctx->d_misc + 5;
     cudaMemset(ctx->bin.tile_cnt, 0, sizeof(uint32_t) * ctx->bin.max_tiles);  // k_tile_scan re-zeroes per frame
     *out = ctx;
     return VRS_OK;
@@ -528,8 +532,7 @@ static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* ca
     launch_preprocess(sc, fp, fb, ctx->test_cap, st);  // (the candidate scan is fused into it: "scan" stage ~ 0)
     if (tm) CK(cudaEventRecord(ctx->ev[1], st));
     if (tm) CK(cudaEventRecord(ctx->ev[2], st));
-    launch_tiletest(fp, fb, ctx->test_cap, fb.keys, fb.vals, ctx->bin.tile_cnt, ctx->bin.rank,
-                    ctx->sort.counters + 7, st);
+    launch_tiletest_direct(fp, fb, ctx->test_cap, ctx->bin, st);
     if (tm) CK(cudaEventRecord(ctx->ev[3], st));
     // binned per-tile sort; its tile-count scan also writes the ranges ("ranges" stage ~ 0)
     launch_binsort(fb, fp.pair_cap, ctx->last_tiles, ctx->bin, st);
@@ -777,8 +780,8 @@ vrs_status vrs_debug_pairs(vrs_context* ctx, int32_t sorted, uint64_t* keys, uin
     } else {
         // re-run the fused tests + compaction (emission order) into the alternate buffers
         FrameBufs fb = frame_bufs(ctx);
-        launch_tiletest(ctx->fp, fb, ctx->test_cap, ctx->d_keys_alt, ctx->d_vals_alt, nullptr, nullptr,
-                        ctx->sort.counters + 7, st);  // (re-derives the same pair total)
+        launch_tiletest(ctx->fp, fb, ctx->test_cap, ctx->d_keys_alt, ctx->d_vals_alt, ctx->sort.counters + 7,
+                        st);  // (re-derives the same pair total)
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(st));
         CK(cudaMemcpy(keys, ctx->d_keys_alt, 8 * n, cudaMemcpyDeviceToHost));
@@ -839,7 +842,7 @@ vrs_status vrs_sort_pairs(vrs_context* ctx, uint64_t* keys, uint32_t* vals, int6
     CK(cudaSetDevice(ctx->cfg.device));
     cudaStream_t st = (cudaStream_t)stream;
     uint32_t nn = (uint32_t)n;
-    uint32_t* d_n = ctx->d_misc + 4;
+    uint32_t* d_n = ctx->d_misc + 6;
     CK(cudaMemcpyAsync(d_n, &nn, 4, cudaMemcpyHostToDevice, st));
     CK(cudaStreamSynchronize(st));
     launch_sort(keys, vals, ctx->d_keys_alt, ctx->d_vals_alt, d_n, n, key_bits, ctx->sort, st, false);

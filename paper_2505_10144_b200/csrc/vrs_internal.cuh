@@ -103,10 +103,31 @@ void launch_scan(const uint32_t* in, uint32_t* out, uint32_t* total, const uint3
                  uint32_t* scratch, cudaStream_t st, unsigned long long* expand = nullptr,
                  int64_t expand_cap = 0);
 size_t scan_scratch_words(int64_t n);
-// Fused Eq.4 tests + keys + stream compaction; with tile_cnt != null every
-// written pair also gets rank[pos] = its arrival rank in tile_cnt[tile].
+// Binned per-tile sort (k_binsort.cu): tile test -> per-tile buckets (direct
+// slots up to kTileCap, overflow list beyond), one-block tile-count scan ->
+// ranges (+ overflow offsets, pair total), overflow placement, per-tile sort
+// of (depth bits, g) -> sorted (keys, vals).  cap_smem: largest tile sorted in
+// shared memory (power of two <= kBinCap); bigger tiles merge in global memory.
+constexpr uint32_t kBinCap = 4096;   // shared-memory sort capacity (32 KB of u64 keys)
+constexpr uint32_t kTileCap = 1024;  // direct bucket slots per tile
+struct BinScratch {
+    uint32_t* tile_cnt;      // [max tiles] per-tile pair counters (kept zero between frames)
+    uint64_t* tbucket;       // [max tiles][kTileCap] (depth bits << 32 | g) in arrival order
+    uint32_t* ovf_off;       // [max tiles] exclusive scan of max(0, count - kTileCap)
+    uint64_t* obucket;       // [cap] overflow pairs placed per tile
+    uint32_t* ovf_count;     // [1] overflow list length (list in keys_alt / vals_alt / rank)
+    uint32_t* rank;          // [cap] overflow entry's rank inside its tile
+    uint32_t* list;          // [max tiles] non-empty tiles: big ones from the front, small from the back
+    uint32_t* list_n;        // [3] (big, small, small-tile work counter)
+    int64_t max_tiles;
+    uint32_t cap_smem;
+};
+// Fused Eq.4 tests + keys: frame path into the per-tile buckets ...
+void launch_tiletest_direct(const FrameParams& fp, FrameBufs fb, int64_t test_cap, const BinScratch& bs,
+                            cudaStream_t st);
+// ... or (parity hook) compacted into (keys, vals) in arbitrary block order.
 void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, uint64_t* keys, uint32_t* vals,
-                     uint32_t* tile_cnt, uint32_t* rank, uint32_t* counter, cudaStream_t st);
+                     uint32_t* counter, cudaStream_t st);
 void launch_counts(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st);
 struct SortScratch {
     uint32_t* hist;          // [8][256] digit histograms (may be filled by k_compact)
@@ -119,19 +140,6 @@ size_t sort_status_words(int64_t cap);
 // Sort n_dev (device count, capped at cap) pairs by key bits [0, key_bits); result in (keys, vals).
 void launch_sort(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, const uint32_t* n_dev,
                  int64_t cap, int key_bits, SortScratch s, cudaStream_t st, bool hist_ready);
-// Binned per-tile sort (k_binsort.cu): tile_cnt (zeroed again on the way)
-// -> ranges; pairs (keys, vals, rank) -> bucket (keys_alt) -> per-tile sort of
-// (depth bits, g) -> sorted (keys, vals).  cap_smem: largest tile sorted in
-// shared memory (power of two <= kBinCap); bigger tiles merge in global memory.
-constexpr uint32_t kBinCap = 4096;  // shared-memory sort capacity (32 KB of u64 keys)
-struct BinScratch {
-    uint32_t* tile_cnt;      // [max tiles] per-tile pair counters (kept zero between frames)
-    uint32_t* rank;          // [cap] pair rank inside its tile
-    uint32_t* list;          // [max tiles] non-empty tiles: big ones from the front, small from the back
-    uint32_t* list_n;        // [3] (big, small, small-tile work counter)
-    int64_t max_tiles;
-    uint32_t cap_smem;
-};
 void launch_binsort(FrameBufs fb, int64_t cap, int64_t n_tiles, BinScratch b, cudaStream_t st);
 void launch_ranges(const uint64_t* keys, const uint32_t* n_dev, int64_t cap, uint32_t* ranges, int64_t n_tiles,
                    cudaStream_t st);

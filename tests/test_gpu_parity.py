@@ -435,3 +435,32 @@ def test_two_pass_baseline_parity(vrs, oracle_mod, W, H, seed):
     # the second render reuses the cached half masks and per-eye setup
     rgba2, depth2 = r.render_two_pass(cams, fov)
     assert torch.equal(rgba, rgba2) and torch.equal(depth, depth2)
+
+
+@pytest.mark.parametrize("cap", [4096, 128])
+def test_binned_sort_tile_overflow_parity(vrs, oracle_mod, cap):
+    """Binned sort with tiles holding more pairs than their direct bucket
+    (kTileCap = 1024 slots): the overflow pairs take the overflow list and are
+    merged back per tile -- sorted pairs, ranges and images equal the oracle's
+    (also with the merge path forced by a small shared-memory capacity)."""
+    rng = np.random.default_rng(21)
+    n = 5000
+    means = np.column_stack([rng.normal(0, 0.05, n), rng.normal(0, 0.05, n), rng.uniform(2.0, 4.0, n)])
+    scene = scene_from(means, np.exp(rng.uniform(np.log(0.01), np.log(0.05), (n, 3))),
+                       opacities=rng.uniform(0.05, 0.6, n), dc=rng.normal(0, 0.5, (n, 3)))
+    cam = identity_camera(96, 64, 200.0)
+    r = vrs.Renderer(max_gaussians=scene.n, max_views=1, max_pairs=1 << 20, max_width=96, max_height=64,
+                     assign_tile=16)
+    r.upload(scene)
+    r.vrs_debug_set_sort_smem_cap(cap)
+    rgba, depth = r.render([cam])
+    torch.cuda.synchronize()
+    o = oracle_mod.Oracle(scene).prepare([cam], assign_tile=16)
+    rng_o = o.ranges()
+    assert (rng_o[:, 1] - rng_o[:, 0]).max() > 2048, "test needs tiles past the direct bucket capacity"
+    k, v = r.vrs_debug_pairs(True)
+    ok, ov = o.pairs(True)
+    assert np.array_equal(k, ok) and np.array_equal(v, ov)
+    assert np.array_equal(r.vrs_debug_ranges(), rng_o)
+    g = vrs.vrs.split_views(rgba.cpu().numpy(), depth.cpu().numpy(), [cam])
+    assert_images_close(g, o.render())
