@@ -167,19 +167,24 @@ static inline float alpha_of_x(float x, float sigma) {
     float a = sigma * e;
     return a < 0.99f ? a : 0.99f;
 }
-static inline SampleAT sample_alpha_tau(float num, float ss, float den, float dtb, float sigma) {
-    float r = 1.0f / (ss * den);
+/* r = 1/v in IEEE binary32 with v clamped to [2^-100, 2^100] (R9; the clamp
+ * never binds for a visible splat and lets the GPU skip rcp.rn's slow path). */
+static inline float rcp_clamped(float v) {
+    return 1.0f / std::fmin(std::fmax(v, 0x1p-100f), 0x1p100f);
+}
+static inline SampleAT sample_alpha_tau(float num, float ss, float den, float dtb, float sigma, float near_plane) {
+    float r = rcp_clamped(ss * den);
     float x = std::fmax((num * -0.72134752f) * (den * r), -64.0f);  // NaN/-inf guard
     SampleAT o;
     o.alpha = alpha_of_x(x, sigma);
-    o.tau = std::fmax(dtb * (ss * r), -1e30f) + 0.0f;  // canonical: NaN/-inf -> -1e30, -0 -> +0 (R4)
+    o.tau = std::fmax(dtb * (ss * r), near_plane);  // clamped >= near like the tile key (O8, R4); NaN -> near
     return o;
 }
 /* EWA baseline per sample (q directly in pixels; one IEEE division for tau). */
-static inline SampleAT sample_alpha_tau_ewa(float q, float den, float dtb, float sigma) {
+static inline SampleAT sample_alpha_tau_ewa(float q, float den, float dtb, float sigma, float near_plane) {
     SampleAT o;
     o.alpha = alpha_of_x(std::fmax(q * -0.72134752f, -64.0f), sigma);
-    o.tau = std::fmax(dtb / den, -1e30f) + 0.0f;
+    o.tau = std::fmax(dtb / den, near_plane);
     return o;
 }
 static inline float ewa_q(const float* C, float dx, float dy) {
@@ -686,7 +691,8 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
             float q = ewa_q(sp.Cp, xs - sp.m2[0], ys - sp.m2[1]);
             if (!(q <= sp.qcut)) continue;
             at = sample_alpha_tau_ewa(q, quad3(sp.A, x, y, 1.0f),
-                                      std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2])), sp.sigma);
+                                      std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2])), sp.sigma,
+                                      O.p.near_plane);
         } else {
             float s = std::fmaf(sp.u[0], x, std::fmaf(sp.u[1], y, sp.u[2]));
             if (!(s > 0.0f)) continue;
@@ -695,7 +701,7 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
             if (!(num <= sp.qcut * ss)) continue;  // alpha < 1/255, division-free (R3)
             float den = quad3(sp.A, x, y, 1.0f);
             float dtb = std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2]));
-            at = sample_alpha_tau(num, ss, den, dtb, sp.sigma);  // P:254, L10, R9
+            at = sample_alpha_tau(num, ss, den, dtb, sp.sigma, O.p.near_plane);  // P:254, L10, R9
         }
         float alpha = at.alpha;
         float tau = at.tau;  // depth of max density along this pixel's ray (O10)
@@ -1141,14 +1147,14 @@ int orc_render_bruteforce(void* h, int view, float* rgba, float* depth) {
                 if (O.p.projection == 1) {
                     float q = ewa_q(sp.Cp, ((float)i + 0.5f) - sp.m2[0], ((float)j + 0.5f) - sp.m2[1]);
                     if (!(q <= sp.qcut)) continue;
-                    at = sample_alpha_tau_ewa(q, den, dtb, sp.sigma);
+                    at = sample_alpha_tau_ewa(q, den, dtb, sp.sigma, O.p.near_plane);
                 } else {
                     float s = std::fmaf(sp.u[0], x, std::fmaf(sp.u[1], y, sp.u[2]));
                     if (!(s > 0.0f)) continue;
                     float dray[3] = {x, y, 1.0f};
                     float num = chart_num(sp.e1, sp.e2, sp.C, dray);
                     if (!(num <= sp.qcut * (s * s))) continue;
-                    at = sample_alpha_tau(num, s * s, den, dtb, sp.sigma);
+                    at = sample_alpha_tau(num, s * s, den, dtb, sp.sigma, O.p.near_plane);
                 }
                 all.push_back(WEnt{at.tau, (uint32_t)g, at.alpha});
             }
@@ -1234,7 +1240,7 @@ float orc_sample_depth(void* h, int view, int64_t g, float xs, float ys) {
     float dtb = std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2]));
     float s = std::fmaf(sp.u[0], x, std::fmaf(sp.u[1], y, sp.u[2]));
     float d[3] = {x, y, 1.0f};
-    return sample_alpha_tau(chart_num(sp.e1, sp.e2, sp.C, d), s * s, den, dtb, sp.sigma).tau;
+    return sample_alpha_tau(chart_num(sp.e1, sp.e2, sp.C, d), s * s, den, dtb, sp.sigma, O.p.near_plane).tau;
 }
 
 }  // extern "C"

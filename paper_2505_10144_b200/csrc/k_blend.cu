@@ -75,16 +75,14 @@ constexpr uint32_t kSlotBytes = kBT * 8;                   // one ring slot of k
 constexpr uint32_t kRingMask = (kWindow - 1) * kSlotBytes;    // byte-offset ring mask
 static_assert((kWindow & (kWindow - 1)) == 0, "ring needs a power-of-two window");
 
-// Canonical tau (DESIGN R4: max(tau, -1e30) maps NaN/-inf to -1e30, +0.0 maps
-// -0 to +0), then (tau, g) -> u64 whose unsigned order is the (tau, g)
-// lexicographic order.
-__device__ __forceinline__ unsigned long long order_key(float tau, uint32_t g) {
-    const uint32_t b = __float_as_uint(fmaxf(tau, -1e30f) + 0.0f);
-    const uint32_t k = b ^ ((uint32_t)((int32_t)b >> 31) | 0x80000000u);
-    return ((unsigned long long)k << 32) | g;
+// Per-sample depth clamped below at the near plane (DESIGN R4, like the tile
+// key of O8): tau >= near > 0, so its IEEE bits order as unsigned integers
+// and (tau, g) packs into one order-preserving u64 with no transform.
+__device__ __forceinline__ unsigned long long order_key(float tau, uint32_t g, float near) {
+    return ((unsigned long long)__float_as_uint(fmaxf(tau, near)) << 32) | g;
 }
-// sentinel: tau = -2e30 (finite, below every canonical tau), g = 0, alpha = 0
-constexpr unsigned long long kSentinelKey = (unsigned long long)(~0xf1c9f2cau) << 32;
+// sentinel: tau = +0 (below every clamped tau), g = 0, alpha = 0
+constexpr unsigned long long kSentinelKey = 0ull;
 __device__ __forceinline__ float fast_rcp(float x) {
     float r;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -113,15 +111,26 @@ __device__ __forceinline__ float alpha_of_x(float x, float sigma) {
     const float a = sigma * e;
     return a < kAlphaMax ? a : kAlphaMax;
 }
+// IEEE round-to-nearest reciprocal of v clamped to [2^-100, 2^100] (DESIGN
+// R9): inside that range the MUFU estimate + one Newton step is correctly
+// rounded (the fast path of rcp.rn, checked exhaustively by tools/rcp_check.cu),
+// so no slow-path branch is needed.
+__device__ __forceinline__ float rcp_clamped(float v) {
+    v = fminf(fmaxf(v, 0x1p-100f), 0x1p100f);
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
+    const float e = fmaf(-v, r, 1.0f);
+    return fmaf(r, e, r);
+}
 __device__ __forceinline__ float alpha_tau(float num, float ss, float den, float dtb, float sigma, float& tau) {
-    const float r = __frcp_rn(ss * den);
+    const float r = rcp_clamped(ss * den);
     const float x = fmaxf((num * -0.72134752f) * (den * r), -64.0f);  // NaN/-inf guard
     tau = dtb * (ss * r);
     return alpha_of_x(x, sigma);
 }
 __device__ __forceinline__ float key_tau(unsigned long long key) {
     const uint32_t k = (uint32_t)(key >> 32);
-    return __uint_as_float(k ^ (((int32_t)k < 0) ? 0x80000000u : 0xffffffffu));
+    return __uint_as_float(k);
 }
 
 }  // namespace
@@ -273,7 +282,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
             const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, a5.x));
             alpha = alpha_tau(num, ss, den, dtb, a5.y, tau);
         }
-        contribute(order_key(tau, g), alpha, pos);
+        contribute(order_key(tau, g, fp.near_plane), alpha, pos);
     };
 
     for (uint32_t base = rb; base < re; base += kBatch) {
@@ -302,6 +311,45 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
             if (__all_sync(0xffffffffu, done)) break;
             const bool rel = (c + lane < nb) && ((S.mask[c + lane] >> warp) & 1u);
             unsigned bits = __ballot_sync(0xffffffffu, rel);
+            if (!kEwa) {
+                // two list entries per iteration: both memberships first (independent
+                // chains), then the contributions in stream order
+                auto member = [&](const int j, float& num, float& ss) {
+                    const float4 a0 = S.r0[j], a1 = S.r1[j], a2 = S.r2[j];
+                    const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
+                    const float ex = fmaf(a1.x, x, a1.y);
+                    const float ey = fmaf(a1.z, x, fmaf(a1.w, y, a2.x));
+                    const float cx = fmaf(a2.y, ex, a2.z * ey), cy = fmaf(a2.z, ex, a2.w * ey);
+                    num = fmaf(ex, cx, ey * cy);
+                    ss = s * s;
+                    return (s > 0.0f) && (num <= a0.w * ss);
+                };
+                auto contrib = [&](const int j, const float num, const float ss) {
+                    const float4 a3 = S.r3[j], a4 = S.r4[j], t = S.r5[j];
+                    const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
+                    const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, t.x));
+                    float tau;
+                    const float alpha = alpha_tau(num, ss, den, dtb, t.y, tau);
+                    contribute(order_key(tau, __float_as_uint(t.z), fp.near_plane), alpha, base + j);
+                };
+                while (bits) {
+                    const int j = c + __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    float n1, s1;
+                    const bool m1 = member(j, n1, s1) && !done;
+                    if (bits) {
+                        const int j2 = c + __ffs(bits) - 1;
+                        bits &= bits - 1;
+                        float n2, s2;
+                        const bool m2 = member(j2, n2, s2);
+                        if (m1) contrib(j, n1, s1);
+                        if (m2 && !done) contrib(j2, n2, s2);
+                    } else if (m1) {
+                        contrib(j, n1, s1);
+                    }
+                }
+                continue;
+            }
             while (bits) {
                 const int j = c + __ffs(bits) - 1;
                 bits &= bits - 1;
