@@ -730,6 +730,194 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
     return out;
 }
 
+/* SURVEY N2 / DESIGN "N2 hierarchical resort": StopThePop's hierarchy
+ * ("hierarchical per-pixel resorting") with a block level ahead
+ * of the per-sample window.  The 16 samples of one 4x4 sample block (4x4
+ * pixels of a full-rate item, 4x4 2x2-group samples of a LowRes item) stream
+ * their tile's list in key order together:
+ *   1. entry g is ADMITTED to the block iff at least one not-yet-terminated
+ *      in-image sample of the block passes the per-sample membership test
+ *      (R3, exactly as O10); the set of such samples is kept with it;
+ *   2. admitted entries wait in a block queue Q sorted by (tau_B, g), tau_B =
+ *      max(dtb/den, near) on the ray through the block centre (the R4/R6
+ *      forms, one IEEE division);  when |Q| > K_B the minimum is RELEASED;
+ *   3. a release gives every sample of its set that has not terminated the
+ *      entry's per-sample alpha and tau (R9) and inserts it into that
+ *      sample's window (K_P = window_k entries, ordered by (tau, g)); window
+ *      overflow pops and blends the minimum exactly as O10-O11;
+ *   4. at stream end Q releases in order, then every window drains (O11).
+ * K_B = 0 releases every entry at admission, i.e. the flat per-sample mode
+ * with K = K_P (pin H1); K_B, K_P >= list length gives the full per-sample
+ * sort (pin H2).  Evaluations count list entries visited before the sample's
+ * termination (the entry whose processing released the terminating blend). */
+struct HEnt { float tauB; uint32_t g; uint32_t mask; uint32_t idx; };
+
+/* Block-level list entry with everything its samples need (computed by
+ * render_block_hier from the geometry, or given directly to the pin H3). */
+struct HIn {
+    float tauB;           // block-centre depth (R4 form)
+    uint32_t g;           // Gaussian index (tie-break, R4)
+    uint32_t member;      // bit s: sample s passes the membership test (R3)
+    float tau[16], alpha[16];  // per-sample depth and alpha (R9), where member
+    float rgb[3];         // colour (O5)
+};
+
+/* The two-level queue mechanics of N2 on one block's stream (steps 1-4
+ * above); valid[s] = sample s is in the image; dn[s] = |d| of its ray. */
+static void hier_core(const std::vector<HIn>& in, int KB, int KP, const bool* valid, const double* dn,
+                      const float* bg, Px* out, SampleStats* st) {
+    const uint32_t n = (uint32_t)in.size();
+    float T[16];
+    double C[16][3], D[16];
+    bool done[16], ovf[16];
+    uint32_t stop[16];
+    std::vector<WEnt> win[16];
+    for (int s = 0; s < 16; s++) {
+        T[s] = 1.0f;
+        C[s][0] = C[s][1] = C[s][2] = 0.0;
+        D[s] = 0.0;
+        done[s] = !valid[s];
+        ovf[s] = false;
+        stop[s] = n ? n - 1 : 0;
+    }
+    std::vector<uint32_t> colour_of;  // WEnt.g holds the entry index; colours by index
+    auto blend = [&](int s, const WEnt& w, uint32_t pos) {
+        const HIn& h = in[w.g];
+        double wt = (double)w.alpha * (double)T[s];
+        for (int c = 0; c < 3; c++) C[s][c] += (double)h.rgb[c] * wt;
+        D[s] += (double)w.tau * dn[s] * wt;
+        T[s] = T[s] * (1.0f - w.alpha);
+        if (T[s] < 1e-4f) { done[s] = true; stop[s] = pos; }
+    };
+    auto release = [&](const HEnt& e, uint32_t pos) {
+        const HIn& h = in[e.idx];
+        for (int s = 0; s < 16; s++) {
+            if (!((e.mask >> s) & 1u) || done[s]) continue;
+            st[s].contribs++;
+            WEnt ent{h.tau[s], e.idx, h.alpha[s]};  // .g = entry index; order by (tau, Gaussian g)
+            auto it = std::upper_bound(win[s].begin(), win[s].end(), ent, [&](const WEnt& a, const WEnt& c) {
+                return a.tau < c.tau || (a.tau == c.tau && in[a.g].g < in[c.g].g);
+            });
+            win[s].insert(it, ent);
+            if ((int)win[s].size() > KP) {
+                ovf[s] = true;
+                WEnt m = win[s].front();
+                win[s].erase(win[s].begin());
+                blend(s, m, pos);
+            }
+        }
+    };
+    std::vector<HEnt> Q;
+    for (uint32_t i = 0; i < n; i++) {
+        bool all = true;
+        for (int s = 0; s < 16; s++) all = all && done[s];
+        if (all) break;
+        uint32_t mask = 0;
+        for (int s = 0; s < 16; s++)
+            if (!done[s] && ((in[i].member >> s) & 1u)) mask |= 1u << s;
+        if (!mask) continue;
+        HEnt h{in[i].tauB, in[i].g, mask, i};
+        auto it = std::upper_bound(Q.begin(), Q.end(), h, [](const HEnt& a, const HEnt& c) {
+            return a.tauB < c.tauB || (a.tauB == c.tauB && a.g < c.g);
+        });
+        Q.insert(it, h);
+        if ((int)Q.size() > KB) {
+            HEnt m = Q.front();
+            Q.erase(Q.begin());
+            release(m, i);
+        }
+    }
+    for (const HEnt& h : Q) release(h, n ? n - 1 : 0);
+    for (int s = 0; s < 16; s++) {
+        for (size_t k = 0; k < win[s].size() && !done[s]; k++) blend(s, win[s][k], n ? n - 1 : 0);
+        if (valid[s]) {
+            st[s].evals += n ? (int64_t)stop[s] + 1 : 0;
+            if (ovf[s]) st[s].overflow++;
+            if (done[s]) st[s].term++;
+        }
+        out[s].r = C[s][0] + (double)T[s] * bg[0];
+        out[s].g = C[s][1] + (double)T[s] * bg[1];
+        out[s].b = C[s][2] + (double)T[s] * bg[2];
+        out[s].a = 1.0 - (double)T[s];
+        out[s].d = D[s];
+    }
+}
+
+static void render_block_hier(const Oracle& O, int view, int64_t gtile, const float* xs, const float* ys,
+                              const bool* valid, float xc, float yc, Px* out, SampleStats* st) {
+    const ViewState& vs = O.views[view];
+    const orc_view& v = vs.v;
+    const uint32_t b = O.ranges[2 * gtile], e = O.ranges[2 * gtile + 1];
+    float x[16], y[16];
+    double dn[16];
+    for (int s = 0; s < 16; s++) {
+        x[s] = (xs[s] - v.cx) / v.fx;
+        y[s] = (ys[s] - v.cy) / v.fy;
+        dn[s] = std::sqrt((double)x[s] * x[s] + (double)y[s] * y[s] + 1.0);
+    }
+    const float xB = (xc - v.cx) / v.fx, yB = (yc - v.cy) / v.fy;  // block-centre ray (R6 sample form)
+    std::vector<HIn> in(e - b);
+    for (uint32_t i = b; i < e; i++) {
+        HIn& h = in[i - b];
+        h.g = O.vals[i];
+        const Splat& sp = vs.splats[h.g];
+        float den = quad3(sp.A, xB, yB, 1.0f);
+        float dtb = std::fmaf(sp.bv[0], xB, std::fmaf(sp.bv[1], yB, sp.bv[2]));
+        h.tauB = std::fmax(dtb / den, O.p.near_plane);  // tau_B (R4 form; NaN -> near)
+        h.member = 0;
+        for (int c = 0; c < 3; c++) h.rgb[c] = sp.rgb[c];
+        for (int s = 0; s < 16; s++) {
+            h.tau[s] = h.alpha[s] = 0.0f;
+            float sv = std::fmaf(sp.u[0], x[s], std::fmaf(sp.u[1], y[s], sp.u[2]));
+            if (!(sv > 0.0f)) continue;
+            float dray[3] = {x[s], y[s], 1.0f};
+            float num = chart_num(sp.e1, sp.e2, sp.C, dray);
+            float ss = sv * sv;
+            if (!(num <= sp.qcut * ss)) continue;  // alpha < 1/255 (R3)
+            h.member |= 1u << s;
+            float dens = quad3(sp.A, x[s], y[s], 1.0f);
+            float dtbs = std::fmaf(sp.bv[0], x[s], std::fmaf(sp.bv[1], y[s], sp.bv[2]));
+            SampleAT at = sample_alpha_tau(num, ss, dens, dtbs, sp.sigma, O.p.near_plane);
+            h.tau[s] = at.tau;
+            h.alpha[s] = at.alpha;
+        }
+    }
+    hier_core(in, O.p.block_queue, O.p.window_k, valid, dn, O.p.background, out, st);
+}
+
+/* The 4x4 sample block containing full-rate sample (i, j) or LowRes group
+ * (i, j) (pixel of the group origin) of coarse tile (tx, ty): sample points,
+ * in-image flags and the block centre (mean of its 16 sample points). */
+static void hier_block(const ViewState& vs, int T, bool low, int i, int j, int* bx0, int* by0, float* xs,
+                       float* ys, bool* valid, float* xc, float* yc) {
+    const int W = vs.v.width, H = vs.v.height;
+    if (low) {  // blocks of 4x4 groups = 8x8 pixels, aligned inside the tile
+        int x0 = (i / T) * T, y0 = (j / T) * T;
+        int gx0 = ((i - x0) / 2) & ~3, gy0 = ((j - y0) / 2) & ~3;
+        *bx0 = x0 + 2 * gx0;
+        *by0 = y0 + 2 * gy0;
+        for (int k = 0; k < 16; k++) {
+            int px = *bx0 + 2 * (k & 3), py = *by0 + 2 * (k >> 2);
+            xs[k] = (float)(px + 1);
+            ys[k] = (float)(py + 1);
+            valid[k] = px < W && py < H;
+        }
+        *xc = (float)(*bx0 + 4);
+        *yc = (float)(*by0 + 4);
+    } else {
+        *bx0 = i & ~3;
+        *by0 = j & ~3;
+        for (int k = 0; k < 16; k++) {
+            int px = *bx0 + (k & 3), py = *by0 + (k >> 2);
+            xs[k] = (float)px + 0.5f;
+            ys[k] = (float)py + 0.5f;
+            valid[k] = px < W && py < H;
+        }
+        *xc = (float)(*bx0 + 2);
+        *yc = (float)(*by0 + 2);
+    }
+}
+
 struct FrameCtx {
     const Oracle* O;
     int view;
@@ -767,6 +955,21 @@ static Px pixel_sample(FrameCtx& F, int i, int j, bool low) {
     }
     auto it = F.memo.find(key);
     if (it != F.memo.end()) return it->second;
+    if (F.O->p.resort == 1) {  // the whole 4x4 block renders together (N2)
+        int bx0, by0;
+        float bxs[16], bys[16], xc, yc;
+        bool valid[16];
+        hier_block(vs, T, low, i, j, &bx0, &by0, bxs, bys, valid, &xc, &yc);
+        Px outs[16];
+        SampleStats sts[16];
+        render_block_hier(*F.O, F.view, gt, bxs, bys, valid, xc, yc, outs, sts);
+        for (int k = 0; k < 16; k++) {
+            uint64_t kk = low ? ((1ull << 62) | ((uint64_t)(by0 + 2 * (k >> 2)) << 31) | (uint64_t)(bx0 + 2 * (k & 3)))
+                              : (((uint64_t)(by0 + (k >> 2)) << 31) | (uint64_t)(bx0 + (k & 3)));
+            F.memo[kk] = outs[k];
+        }
+        return F.memo[key];
+    }
     Px p = render_sample(*F.O, F.view, gt, xs, ys, F.st);
     F.memo[key] = p;
     return p;
@@ -1033,7 +1236,7 @@ int orc_render(void* h, float* rgba, float* depth) {
         const ViewState& vs = O.views[v];
         const int W = vs.v.width, H = vs.v.height, T = O.p.assign_tile;
         const int We = W + (W & 1), He = H + (H & 1);  // even extents: 2x2 groups at odd borders
-        std::vector<Px> full((size_t)We * He), low((size_t)(We / 2) * (He / 2));
+        std::vector<Px> full((size_t)We * He), low_((size_t)(We / 2) * (He / 2));
         int nt = nthreads(O);
         std::atomic<int64_t> next(0);
         std::vector<SampleStats> sts(nt);
@@ -1050,12 +1253,39 @@ int orc_render(void* h, float* rgba, float* depth) {
                     if (c == CLS_INVIS) continue;
                     int64_t gt = vs.tile_base + tt;
                     int x0 = tx * T, y0 = ty * T;
+                    if (O.p.resort == 1) {  // N2: 4x4 sample blocks render together
+                        const bool low = c == CLS_LOW;
+                        const int span = low ? 8 : 4;
+                        for (int by = y0; by < std::min(y0 + T, He); by += span)
+                            for (int bx = x0; bx < std::min(x0 + T, We); bx += span) {
+                                int bx0, by0;
+                                float bxs[16], bys[16], xc, yc;
+                                bool valid[16];
+                                hier_block(vs, T, low, bx, by, &bx0, &by0, bxs, bys, valid, &xc, &yc);
+                                Px outs[16];
+                                SampleStats bst[16];
+                                render_block_hier(O, v, gt, bxs, bys, valid, xc, yc, outs, bst);
+                                for (int k = 0; k < 16; k++) {
+                                    int px = low ? bx0 + 2 * (k & 3) : bx0 + (k & 3);
+                                    int py = low ? by0 + 2 * (k >> 2) : by0 + (k >> 2);
+                                    if (px >= We || py >= He) continue;
+                                    if (low) low_[(size_t)(py / 2) * (We / 2) + px / 2] = outs[k];
+                                    else full[(size_t)py * We + px] = outs[k];
+                                    if (valid[k]) {
+                                        nsamp[t]++;
+                                        sts[t].evals += bst[k].evals; sts[t].contribs += bst[k].contribs;
+                                        sts[t].overflow += bst[k].overflow; sts[t].term += bst[k].term;
+                                    }
+                                }
+                            }
+                        continue;
+                    }
                     if (c == CLS_LOW) {
                         for (int gy = 0; 2 * gy < std::min(T, He - y0); gy++)
                             for (int gx = 0; 2 * gx < std::min(T, We - x0); gx++) {
                                 bool in = x0 + 2 * gx < W && y0 + 2 * gy < H;
                                 SampleStats dummy;
-                                low[(size_t)(y0 / 2 + gy) * (We / 2) + x0 / 2 + gx] =
+                                low_[(size_t)(y0 / 2 + gy) * (We / 2) + x0 / 2 + gx] =
                                     render_sample(O, v, gt, (float)(x0 + 2 * gx + 1), (float)(y0 + 2 * gy + 1),
                                                   in ? sts[t] : dummy);
                                 nsamp[t] += in;
@@ -1081,7 +1311,7 @@ int orc_render(void* h, float* rgba, float* depth) {
         std::atomic<int> nextrow(0);
         for (int t = 0; t < nt; t++)
             th.emplace_back([&]() {
-                FrameCtx F{&O, v, {}, {}, &full, &low, We};
+                FrameCtx F{&O, v, {}, {}, &full, &low_, We};
                 for (;;) {
                     int j = nextrow.fetch_add(1);
                     if (j >= H) break;
@@ -1227,6 +1457,38 @@ float orc_eq4_edge(const float* C, const float* p, const float* d, float* xhat) 
     xhat[1] = std::fmaf(t, d[1], p[1]);
     float cX = std::fmaf(C[0], xhat[0], C[1] * xhat[1]), cY = std::fmaf(C[1], xhat[0], C[2] * xhat[1]);
     return std::fmaf(xhat[0], cX, xhat[1] * cY);
+}
+
+/* Pin H3 hook: the N2 queue mechanics on a given stream of n block entries
+ * (tauB[n], g[n], member[n], tau[n*16], alpha[n*16], rgb[n*3]); all 16
+ * samples in the image, |d| = 1; out = 16 x (r, g, b, a, depth). */
+int orc_hier_core(int64_t n, int kb, int kp, const float* tauB, const uint32_t* g, const uint32_t* member,
+                  const float* tau, const float* alpha, const float* rgb, double* out, int64_t* stats) {
+    std::vector<HIn> in((size_t)n);
+    for (int64_t i = 0; i < n; i++) {
+        in[i].tauB = tauB[i];
+        in[i].g = g[i];
+        in[i].member = member[i];
+        for (int s = 0; s < 16; s++) {
+            in[i].tau[s] = tau[16 * i + s];
+            in[i].alpha[s] = alpha[16 * i + s];
+        }
+        for (int c = 0; c < 3; c++) in[i].rgb[c] = rgb[3 * i + c];
+    }
+    bool valid[16];
+    double dn[16];
+    for (int s = 0; s < 16; s++) { valid[s] = true; dn[s] = 1.0; }
+    const float bg[3] = {0.0f, 0.0f, 0.0f};
+    Px px[16];
+    SampleStats st[16];
+    hier_core(in, kb, kp, valid, dn, bg, px, st);
+    for (int s = 0; s < 16; s++) {
+        out[5 * s + 0] = px[s].r; out[5 * s + 1] = px[s].g; out[5 * s + 2] = px[s].b;
+        out[5 * s + 3] = px[s].a; out[5 * s + 4] = px[s].d;
+        stats[4 * s + 0] = st[s].evals; stats[4 * s + 1] = st[s].contribs;
+        stats[4 * s + 2] = st[s].overflow; stats[4 * s + 3] = st[s].term;
+    }
+    return 0;
 }
 
 /* Per-sample depth tau (O10) of Gaussian g at image point (x, y) (pixel

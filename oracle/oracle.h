@@ -41,7 +41,11 @@ typedef struct {
     float near_plane;      /* 0.2 */
     float background[3];   /* black */
     int32_t threads;       /* worker threads over tiles; 0 = hardware concurrency */
-    int32_t projection;    /* 0 = Optimal Projection (only mode in round 1) */
+    int32_t projection;    /* 0 = Optimal Projection, 1 = EWA baseline (config C5) */
+    int32_t resort;        /* 0 = per-sample window of window_k; 1 = hierarchical
+                              (DESIGN "N2"): a block queue of block_queue entries per
+                              4x4 sample block ahead of a per-sample window of window_k */
+    int32_t block_queue;   /* K_B >= 0 (hierarchical mode only) */
 } orc_params;
 
 #define ORC_SPLAT_FLOATS 48
@@ -75,6 +79,8 @@ void orc_sat(int tw, int th, const uint8_t* bits, uint32_t* sat);
 int64_t orc_sat_count(int tw, const uint32_t* sat, int x0, int y0, int x1, int y1);
 float orc_eq4_edge(const float* C, const float* p, const float* d, float* xhat);
 float orc_sample_depth(void* h, int view, int64_t g, float x, float y);
+int orc_hier_core(int64_t n, int kb, int kp, const float* tauB, const uint32_t* g, const uint32_t* member,
+                  const float* tau, const float* alpha, const float* rgb, double* out, int64_t* stats);
 
 #ifdef __cplusplus
 }
