@@ -54,6 +54,9 @@ CONFIGS = {
     "c7": dict(n=500_000, scale_mul=1.0, sh=3, fovea=False, T=16, masks=False, seed=2,
                desc="large-FOV protocol (App. D) on the C2 scene: per eye, crop [W,2W)x[H,2H) of the 3W x 3H "
                     "render at the same pixel focal length vs the W x H render, Optimal Projection vs EWA"),
+    "c8": dict(n=500_000, scale_mul=1.0, sh=3, fovea=True, T=32, masks=True, seed=2, resort=1,
+               desc="C2 workload with the hierarchical resort mode (SURVEY N2): K_B = 8 block queue per 4x4 "
+                    "sample block ahead of a K_P = 8 per-sample window; vs_flat compares with the K = 16 frame"),
     "c6": dict(n=500_000, scale_mul=1.0, sh=3, fovea=True, T=32, masks=True, seed=2, two_pass=True,
                desc="C2 workload rendered with the paper's two-pass foveated baseline (App. A): full-res "
                     "centre crop + half-res masked periphery, bilinear upsample + blend (SURVEY N1)"),
@@ -352,6 +355,8 @@ def main():
                  max_pairs=16 << 20 if cfg["n"] > 1e6 or two_pass else 8 << 20,
                  max_width=W, max_height=H, assign_tile=cfg["T"], device=local, projection=args.projection)
     render = r.render_two_pass if two_pass else r.render
+    if cfg.get("resort"):
+        r.vrs_set_resort_mode(cfg["resort"])
     r.upload(scene)
     for k, m in masks.items():
         r.set_mask(k, m)
@@ -517,11 +522,45 @@ def main():
             "context": {"paper_rtx4090_ms_per_stereo_frame_0.5M_scenes": [9.89, 12.19],
                         "paper_headline": "72+ FPS on RTX 4090 at 2x2064x2272 (P:91, P:107)"},
         }
-        if not args.no_cpu_baseline and world == 1 and not two_pass:
+        if cfg.get("resort"):
+            line["vs_flat"] = compare_flat(r, render, cams, fov, rgba, depth, stream, counters)
+        if not args.no_cpu_baseline and world == 1 and not two_pass and not cfg.get("resort"):
             line["cpu_baseline"] = cpu_baseline(scene, cams, fov, masks, cfg["T"])
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def compare_flat(r, render, cams, fov, rgba, depth, stream, counters):
+    """Hierarchical frame vs the flat K = 16 frame of the same cameras: PSNR of
+    RGB, max |dRGBA|, and both modes' window-overflow counters (approximation
+    events) and blend times."""
+    import torch
+    with torch.cuda.stream(stream):
+        render(cams, fov, rgba, depth, stream=stream)
+    torch.cuda.synchronize()
+    hier = rgba.clone()
+    r.vrs_set_resort_mode(0)
+    r.vrs_set_instrumentation(counters=1, timing=1)
+    with torch.cuda.stream(stream):
+        render(cams, fov, rgba, depth, stream=stream)
+    flat_counters = r.stats()
+    blend_flat = []
+    r.vrs_set_instrumentation(counters=0, timing=1)
+    for _ in range(10):
+        with torch.cuda.stream(stream):
+            render(cams, fov, rgba, depth, stream=stream)
+        blend_flat.append(r.stats()["stage_ms"][5])
+    torch.cuda.synchronize()
+    d = (hier[:, :3] - rgba[:, :3]).double()
+    mse = float((d * d).mean())
+    out = {"psnr_rgb_db": 10.0 * np.log10(1.0 / mse) if mse > 0 else float("inf"),
+           "max_abs_rgba": float((hier - rgba).abs().max()),
+           "overflow_samples": {"hier": counters["overflow_samples"], "flat": flat_counters["overflow_samples"]},
+           "contributions": {"hier": counters["contributions"], "flat": flat_counters["contributions"]},
+           "flat_blend_ms": float(np.mean(blend_flat))}
+    r.vrs_set_resort_mode(1)
+    return out
 
 
 def make_cams_only(cfg_name):

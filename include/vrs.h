@@ -174,6 +174,16 @@ VRS_API vrs_status vrs_render_views_two_pass(vrs_context* ctx, int32_t n_views, 
 
 /* Detailed counters (evaluations, contributions, overflow) cost atomics;
  * stage timing costs events.  Both off by default. */
+/* Resort mode of the blend (DESIGN "N2 hierarchical resort").
+ * mode 0 (default): StopThePop per-sample window, K = 16;
+ * mode 1: hierarchical -- per 4x4 sample block a queue of block_queue = 8
+ * entries ordered by the block-centre depth (entries admitted when a sample
+ * of the block passes the membership test) ahead of a per-sample window of
+ * pixel_window = 8 ("hierarchical per-pixel resorting").
+ * 0 for a size selects the compiled value.  Takes effect from the next render.
+ * Errors: VRS_E_INVALID_ARG (unknown mode, sizes other than the compiled ones,
+ * mode 1 with the EWA projection). */
+VRS_API vrs_status vrs_set_resort_mode(vrs_context* ctx, int32_t mode, int32_t block_queue, int32_t pixel_window);
 VRS_API vrs_status vrs_set_instrumentation(vrs_context* ctx, int32_t counters, int32_t timing);
 
 /* Synchronises the last frame's stream and returns its statistics.

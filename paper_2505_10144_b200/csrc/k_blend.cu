@@ -16,7 +16,7 @@
 // blending front to back (Eq.2 with product transmittance), terminating once
 // T < 1e-4 (checked after blending).  Hybrid pixels blend their value with
 // the 2x2 group average via warp shuffles.
-#include "vrs_internal.cuh"
+#include "k_blend_common.cuh"
 
 namespace vrs {
 
@@ -74,64 +74,6 @@ struct BlendSmem {
 constexpr uint32_t kSlotBytes = kBT * 8;                   // one ring slot of keys
 constexpr uint32_t kRingMask = (kWindow - 1) * kSlotBytes;    // byte-offset ring mask
 static_assert((kWindow & (kWindow - 1)) == 0, "ring needs a power-of-two window");
-
-// Per-sample depth clamped below at the near plane (DESIGN R4, like the tile
-// key of O8): tau >= near > 0, so its IEEE bits order as unsigned integers
-// and (tau, g) packs into one order-preserving u64 with no transform.
-__device__ __forceinline__ unsigned long long order_key(float tau, uint32_t g, float near) {
-    return ((unsigned long long)__float_as_uint(fmaxf(tau, near)) << 32) | g;
-}
-// sentinel: tau = +0 (below every clamped tau), g = 0, alpha = 0
-constexpr unsigned long long kSentinelKey = 0ull;
-__device__ __forceinline__ float fast_rcp(float x) {
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-__device__ __forceinline__ float fast_ex2(float x) {
-    float r;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
-    return r;
-}
-// Per-sample alpha and depth (DESIGN R9): one IEEE reciprocal of s^2*den
-// serves x = -q/2 log2 e and tau = dtb/den; alpha = min(0.99, sigma 2^x) with
-// the contract's deterministic binary32 exp2 -- the oracle evaluates the
-// identical operations, so transmittance and the T < 1e-4 stop are exact.
-__device__ __forceinline__ float alpha_of_x(float x, float sigma) {
-    const float fl = floorf(x);
-    const int n = (int)fl;
-    const float f = x - fl;
-    float p = 0.00187757565f;
-    p = fmaf(p, f, 0.00898934249f);
-    p = fmaf(p, f, 0.0558263175f);
-    p = fmaf(p, f, 0.240153611f);
-    p = fmaf(p, f, 0.693153083f);
-    p = fmaf(p, f, 0.99999994f);
-    const float e = __int_as_float(__float_as_int(p) + (n << 23));  // p * 2^n, exact (normal range)
-    const float a = sigma * e;
-    return a < kAlphaMax ? a : kAlphaMax;
-}
-// IEEE round-to-nearest reciprocal of v clamped to [2^-100, 2^100] (DESIGN
-// R9): inside that range the MUFU estimate + one Newton step is correctly
-// rounded (the fast path of rcp.rn, checked exhaustively by tools/rcp_check.cu),
-// so no slow-path branch is needed.
-__device__ __forceinline__ float rcp_clamped(float v) {
-    v = fminf(fmaxf(v, 0x1p-100f), 0x1p100f);
-    float r;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(v));
-    const float e = fmaf(-v, r, 1.0f);
-    return fmaf(r, e, r);
-}
-__device__ __forceinline__ float alpha_tau(float num, float ss, float den, float dtb, float sigma, float& tau) {
-    const float r = rcp_clamped(ss * den);
-    const float x = fmaxf((num * -0.72134752f) * (den * r), -64.0f);  // NaN/-inf guard
-    tau = dtb * (ss * r);
-    return alpha_of_x(x, sigma);
-}
-__device__ __forceinline__ float key_tau(unsigned long long key) {
-    const uint32_t k = (uint32_t)(key >> 32);
-    return __uint_as_float(k);
-}
 
 }  // namespace
 
@@ -441,6 +383,10 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
 void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
                   cudaStream_t st) {
     if (total_items <= 0) return;
+    if (fp.resort == 1) {
+        launch_blend_hier(fp, fb, total_items, rgba, depth, st);
+        return;
+    }
     const size_t smem = sizeof(BlendSmem);
     const unsigned grid = (unsigned)total_items * kSplit;
     static bool attr_set = false;

@@ -94,6 +94,7 @@ struct vrs_context {
     size_t out_px_cap = 0;
     // instrumentation
     int counters = 0, timing = 0, no_cull = 0;
+    int resort = 0;  // 0 = per-sample window (K = 16); 1 = hierarchical
     cudaEvent_t ev[8] = {};
     bool ev_created = false;
 };
@@ -400,6 +401,7 @@ static vrs_status prepare_frame(vrs_context* ctx, int nv, const vrs_camera* cams
     fp.sh_coeffs = (ctx->deg + 1) * (ctx->deg + 1);
     fp.counters = ctx->counters;
     fp.no_cull = ctx->no_cull;
+    fp.resort = ctx->resort;
     fp.ewa = ctx->cfg.projection;
     fp.N = ctx->N;
     fp.pair_cap = ctx->cfg.max_pairs;
@@ -752,6 +754,23 @@ vrs_status vrs_debug_counts(vrs_context* ctx, uint32_t* counts, int64_t capacity
     launch_counts(ctx->fp, frame_bufs(ctx), ctx->test_cap, ctx->last_stream);
     CK(cudaStreamSynchronize(ctx->last_stream));
     if (n) CK(cudaMemcpy(counts, ctx->d_counts, 4 * n, cudaMemcpyDeviceToHost));
+    return VRS_OK;
+}
+
+vrs_status vrs_set_resort_mode(vrs_context* ctx, int32_t mode, int32_t block_queue, int32_t pixel_window) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    if (mode == 0) {
+        if (pixel_window != 0 && pixel_window != kWindow)
+            return fail(ctx, VRS_E_INVALID_ARG, "per-sample mode: only K = 16 is compiled");
+    } else if (mode == 1) {
+        if ((block_queue != 0 && block_queue != kHierQueue) || (pixel_window != 0 && pixel_window != kHierWindow))
+            return fail(ctx, VRS_E_INVALID_ARG, "hierarchical mode: only K_B = 8, K_P = 8 are compiled");
+        if (ctx->cfg.projection != 0)
+            return fail(ctx, VRS_E_INVALID_ARG, "hierarchical mode needs the Optimal Projection");
+    } else {
+        return fail(ctx, VRS_E_INVALID_ARG, "resort mode must be 0 or 1");
+    }
+    ctx->resort = mode;
     return VRS_OK;
 }
 

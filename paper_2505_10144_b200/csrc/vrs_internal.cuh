@@ -16,6 +16,8 @@ namespace vrs {
 
 constexpr int kBlend = 256;        // threads per blend block
 constexpr int kWindow = 16;        // StopThePop per-sample resort window K
+constexpr int kHierQueue = 8;      // N2 hierarchical mode: block queue K_B per 4x4 sample block
+constexpr int kHierWindow = 8;     // N2 hierarchical mode: per-sample window K_P
 constexpr int kRecF4 = 8;          // float4 per projected-splat record (128 B)
 constexpr float kO7Margin = 1.001f;  // O7 keep threshold factor (DESIGN R7)
 constexpr float kTmin = 1e-4f;     // early termination (L11)
@@ -54,6 +56,7 @@ struct FrameParams {
     int32_t counters;        // instrumentation on
     int32_t no_cull;         // test hook: disable the warp-block footprint skip (P12)
     int32_t ewa;             // projection: 0 = Optimal Projection, 1 = EWA baseline (config C5)
+    int32_t resort;          // 0 = per-sample window K = 16; 1 = hierarchical
     int64_t N;
     int64_t pair_cap;
     float near_plane;
@@ -160,6 +163,8 @@ void launch_two_pass_combine(const TwoPassParams& tp, const float4* prgba, const
                              float* depth, int64_t total, cudaStream_t st);
 void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
                   cudaStream_t st);
+void launch_blend_hier(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
+                       cudaStream_t st);
 void launch_compose(const FrameParams& fp, FrameBufs fb, float* rgba, float* depth, cudaStream_t st);
 void launch_debug_splats(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int view, float* out,
                          cudaStream_t st);
