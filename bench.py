@@ -412,68 +412,76 @@ def main():
     # call (render + D2H + stream sync per frame).
     e2e = None
     if not args.no_e2e:
-        px = sum(c.width * c.height for c in cams)
-        hr = [torch.empty((px, 4), dtype=torch.float32).pin_memory() for _ in range(2)]
-        hd = [torch.empty(px, dtype=torch.float32).pin_memory() for _ in range(2)]
-        dr = [rgba, torch.empty_like(rgba)]
-        dd = [depth, torch.empty_like(depth)]
-        cstream = torch.cuda.Stream(device=local)
-        rendered = [torch.cuda.Event() for _ in range(2)]
-        copied = [torch.cuda.Event() for _ in range(2)]
-        n_e2e = min(args.steps, 20)
-
-        def pipelined(n):
-            for s in range(n):
-                b = s & 1
-                cs = step_cams(args.config, cams, s, rank, world)
-                if s >= 2:
-                    stream.wait_event(copied[b])
-                with torch.cuda.stream(stream):
-                    render(cs, fov, dr[b], dd[b], stream=stream)
-                    rendered[b].record(stream)
-                cstream.wait_event(rendered[b])
-                with torch.cuda.stream(cstream):
-                    hr[b].copy_(dr[b], non_blocking=True)
-                    hd[b].copy_(dd[b], non_blocking=True)
-                    copied[b].record(cstream)
-            cstream.synchronize()
-
-        def sync_call():
-            if two_pass:  # public Python API: device render, then D2H into pinned memory on the same stream
-                with torch.cuda.stream(stream):
-                    render(cams, fov, rgba, depth, stream=stream)
-                    hr[0].copy_(rgba, non_blocking=True)
-                    hd[0].copy_(depth, non_blocking=True)
-                stream.synchronize()
-            else:
-                r.render_host(cams, fov, hr[0], hd[0], stream=stream)
-
-        def timed(fn):
-            if world > 1:
-                dist.barrier()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            fn()
-            t = time.perf_counter() - t0
-            e_t = torch.tensor([t], dtype=torch.float64, device="cuda")
-            if world > 1:
-                dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
-            return float(e_t.item())
-
-        pipelined(4)
-        for _ in range(2):
-            sync_call()
-        pipe_s = timed(lambda: pipelined(n_e2e)) / n_e2e
-        sync_s = timed(lambda: [sync_call() for _ in range(n_e2e)]) / n_e2e
-        cam_bytes = len(cams) * (72 + 24)
         unit = "stereo frames/s" if len(cams) == 2 else "frames/s"
-        e2e = {"value": world / pipe_s, "unit": unit,
-               "h2d_bytes_per_step": cam_bytes, "d2h_bytes_per_step": int(px * 20),
-               "sync_value": world / sync_s,
-               "note": ("render_two_pass" if two_pass else "render") + " into device buffers with the D2H of RGBA "
-                       "f32 + depth f32 into pinned host memory on a copy stream, two frames in flight (value); "
-                       "sync_value = " + ("render_two_pass + D2H + sync" if two_pass else "vrs_render_views_host")
-                       + " per frame; host wall clock; camera/fovea structs travel as kernel parameters"}
+        cam_bytes = len(cams) * (72 + 24)
+
+        def measure_e2e(fmt):
+            r.vrs_set_output_format(fmt)
+            h = [r.alloc_outputs(cams, pinned_host=True) for _ in range(2)]
+            d = [r.alloc_outputs(cams) for _ in range(2)]
+            cstream = torch.cuda.Stream(device=local)
+            rendered = [torch.cuda.Event() for _ in range(2)]
+            copied = [torch.cuda.Event() for _ in range(2)]
+            n_e2e = min(args.steps, 20)
+
+            def pipelined(n):
+                for s in range(n):
+                    b = s & 1
+                    cs = step_cams(args.config, cams, s, rank, world)
+                    if s >= 2:
+                        stream.wait_event(copied[b])
+                    with torch.cuda.stream(stream):
+                        render(cs, fov, d[b][0], d[b][1], stream=stream)
+                        rendered[b].record(stream)
+                    cstream.wait_event(rendered[b])
+                    with torch.cuda.stream(cstream):
+                        h[b][0].copy_(d[b][0], non_blocking=True)
+                        h[b][1].copy_(d[b][1], non_blocking=True)
+                        copied[b].record(cstream)
+                cstream.synchronize()
+
+            def sync_call():
+                if two_pass:  # public Python API: device render, then D2H into pinned memory on the same stream
+                    with torch.cuda.stream(stream):
+                        render(cams, fov, d[0][0], d[0][1], stream=stream)
+                        h[0][0].copy_(d[0][0], non_blocking=True)
+                        h[0][1].copy_(d[0][1], non_blocking=True)
+                    stream.synchronize()
+                else:
+                    r.render_host(cams, fov, h[0][0], h[0][1], stream=stream)
+
+            def timed(fn):
+                if world > 1:
+                    dist.barrier()
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                fn()
+                t = time.perf_counter() - t0
+                e_t = torch.tensor([t], dtype=torch.float64, device="cuda")
+                if world > 1:
+                    dist.all_reduce(e_t, op=dist.ReduceOp.MAX)
+                return float(e_t.item())
+
+            pipelined(4)
+            for _ in range(2):
+                sync_call()
+            pipe_s = timed(lambda: pipelined(n_e2e)) / n_e2e
+            sync_s = timed(lambda: [sync_call() for _ in range(n_e2e)]) / n_e2e
+            r.vrs_set_output_format(0)
+            nbytes = int(h[0][0].numel() * h[0][0].element_size() + h[0][1].numel() * h[0][1].element_size())
+            return world / pipe_s, world / sync_s, nbytes
+
+        v8, s8, b8 = measure_e2e(1)
+        v32, s32, b32 = measure_e2e(0)
+        what = "render_two_pass" if two_pass else "render"
+        e2e = {"value": v8, "unit": unit, "h2d_bytes_per_step": cam_bytes, "d2h_bytes_per_step": b8,
+               "sync_value": s8, "format": "VRS_OUT_RGBA8_D16F (RGBA unorm8 + depth binary16, the HMD display format)",
+               "f32": {"value": v32, "sync_value": s32, "d2h_bytes_per_step": b32,
+                       "format": "VRS_OUT_F32 (RGBA float32 + depth float32)"},
+               "note": what + " into device buffers with the D2H of the frame into pinned host memory on a copy "
+                       "stream, two frames in flight (value); sync_value = " +
+                       ("render_two_pass + D2H + sync" if two_pass else "vrs_render_views_host") +
+                       " per frame; host wall clock; camera/fovea structs travel as kernel parameters"}
 
     if rank == 0:
         peaks, src = measured_peaks()

@@ -48,6 +48,10 @@ extern "C" {
 #define VRS_MAX_VIEWS 8          /* views per vrs_render_views call */
 #define VRS_MAX_MASK_SLOTS 8
 
+/* Output pixel formats (vrs_set_output_format). */
+#define VRS_OUT_F32 0            /* rgba: float[4] per pixel, depth: float per pixel (default) */
+#define VRS_OUT_RGBA8_D16F 1     /* rgba: uint8[4] unorm = round(clamp(v,0,1)*255), depth: IEEE binary16 */
+
 typedef enum {
     VRS_OK = 0,
     VRS_E_INVALID_ARG = 1, /* bad argument / camera (non-orthonormal R, bad sizes, ...) */
@@ -134,6 +138,17 @@ VRS_API vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_
 /* Visibility mask for a slot (HOST pointer, w*h bytes, row-major, >0 =
  * visible).  mask == NULL clears the slot (all visible). */
 VRS_API vrs_status vrs_set_visibility_mask(vrs_context* ctx, int32_t slot, int32_t w, int32_t h, const uint8_t* mask);
+
+/* Output format of the final pixels written by vrs_render_views,
+ * vrs_render_views_host and vrs_render_views_two_pass (default VRS_OUT_F32).
+ * VRS_OUT_RGBA8_D16F is the display format of an HMD compositor: 4 bytes of
+ * RGBA (round-to-nearest of clamp(v, 0, 1) * 255 of the same float values)
+ * and 2 bytes of depth (binary16, round to nearest) per pixel, 6 B instead of
+ * 20 B — what bounds the host path is the device->host copy.  The output
+ * pointers keep their float* type in the signatures; with VRS_OUT_RGBA8_D16F
+ * they must point to buffers of n_px*4 bytes (rgba) and n_px uint16 (depth),
+ * cast to float*.  Errors: VRS_E_INVALID_ARG (unknown format). */
+VRS_API vrs_status vrs_set_output_format(vrs_context* ctx, int32_t format);
 
 /* Render n_views views (one frame: all views share one sort and one blend
  * launch).  cams: HOST array of n_views cameras; fovea: HOST array of n_views

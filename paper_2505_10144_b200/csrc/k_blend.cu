@@ -339,14 +339,12 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         }
         if (px < v.W && py < v.H) {
             const size_t pi = (size_t)v.pix_off + (size_t)py * v.W + px;
-            reinterpret_cast<float4*>(rgba)[pi] = make_float4(outv[0], outv[1], outv[2], outv[3]);
-            depth[pi] = outv[4];
+            store_pixel(fp.out_fmt, rgba, depth, pi, make_float4(outv[0], outv[1], outv[2], outv[3]), outv[4]);
         }
     } else {
         if (px < v.W && py < v.H) {
             const size_t pi = (size_t)v.pix_off + (size_t)py * v.W + px;
-            reinterpret_cast<float4*>(rgba)[pi] = make_float4(oR, oG, oB, oA);
-            depth[pi] = Dd;
+            store_pixel(fp.out_fmt, rgba, depth, pi, make_float4(oR, oG, oB, oA), Dd);
         }
     }
     if (kCounters) {
@@ -492,15 +490,8 @@ __global__ void k_compose(FrameParams fp, FrameBufs fb, float* __restrict__ rgba
         const int j = j0 + b;
         if (j >= v.H) continue;
         const size_t row = (size_t)v.pix_off + (size_t)j * v.W;
-        if (i0 + 1 < v.W) {
-            reinterpret_cast<float4*>(rgba)[row + i0] = outc[b][0];
-            reinterpret_cast<float4*>(rgba)[row + i0 + 1] = outc[b][1];
-            depth[row + i0] = outd[b][0];
-            depth[row + i0 + 1] = outd[b][1];
-        } else {
-            reinterpret_cast<float4*>(rgba)[row + i0] = outc[b][0];
-            depth[row + i0] = outd[b][0];
-        }
+        store_pixel(fp.out_fmt, rgba, depth, row + i0, outc[b][0], outd[b][0]);
+        if (i0 + 1 < v.W) store_pixel(fp.out_fmt, rgba, depth, row + i0 + 1, outc[b][1], outd[b][1]);
     }
 }
 

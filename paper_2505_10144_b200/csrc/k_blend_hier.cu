@@ -318,13 +318,11 @@ __global__ void __launch_bounds__(kHT, VRS_HIER_MINB) k_blend_hier(FrameParams f
         }
         if (in_img) {
             const size_t pi = (size_t)v.pix_off + (size_t)py * v.W + px;
-            reinterpret_cast<float4*>(rgba)[pi] = make_float4(outv[0], outv[1], outv[2], outv[3]);
-            depth[pi] = outv[4];
+            store_pixel(fp.out_fmt, rgba, depth, pi, make_float4(outv[0], outv[1], outv[2], outv[3]), outv[4]);
         }
     } else if (in_img) {
         const size_t pi = (size_t)v.pix_off + (size_t)py * v.W + px;
-        reinterpret_cast<float4*>(rgba)[pi] = make_float4(oR, oG, oB, oA);
-        depth[pi] = Dd;
+        store_pixel(fp.out_fmt, rgba, depth, pi, make_float4(oR, oG, oB, oA), Dd);
     }
     if (kCounters) {
         const unsigned long long ev = in_img ? (unsigned long long)(stop_pos - rb + 1) : 0ull;

@@ -32,7 +32,7 @@ __global__ void k_mask_half(const uint8_t* __restrict__ src, int W, int H, uint8
 }
 
 __global__ void k_two_pass_combine(TwoPassParams tp, const float4* __restrict__ prgba, const float* __restrict__ pdepth,
-                                   float4* __restrict__ rgba, float* __restrict__ depth, int64_t total) {
+                                   float* __restrict__ rgba, float* __restrict__ depth, int64_t total) {
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < total; k += (int64_t)gridDim.x * blockDim.x) {
         int vi = 0;
         while (vi + 1 < tp.n && k >= tp.v[vi + 1].out_off) vi++;
@@ -69,8 +69,7 @@ __global__ void k_two_pass_combine(TwoPassParams tp, const float4* __restrict__ 
                 d = wf * ad + wb * d;
             }
         }
-        rgba[k] = c;
-        depth[k] = d;
+        store_pixel(tp.out_fmt, rgba, depth, (size_t)k, c, d);
     }
 }
 
@@ -87,8 +86,7 @@ void launch_two_pass_combine(const TwoPassParams& tp, const float4* prgba, const
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sms * 16);
-    k_two_pass_combine<<<(unsigned)blocks, 256, 0, st>>>(tp, prgba, pdepth, reinterpret_cast<float4*>(rgba), depth,
-                                                         total);
+    k_two_pass_combine<<<(unsigned)blocks, 256, 0, st>>>(tp, prgba, pdepth, rgba, depth, total);
 }
 
 }  // namespace vrs

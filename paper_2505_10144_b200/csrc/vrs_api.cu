@@ -95,6 +95,7 @@ struct vrs_context {
     // instrumentation
     int counters = 0, timing = 0, no_cull = 0;
     int resort = 0;  // 0 = per-sample window (K = 16); 1 = hierarchical
+    int out_fmt = VRS_OUT_F32;  // vrs_set_output_format
     cudaEvent_t ev[8] = {};
     bool ev_created = false;
 };
@@ -508,7 +509,7 @@ static FrameBufs frame_bufs(vrs_context* ctx) {
 }
 
 static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* cams, const vrs_fovea* fov, float* rgba,
-                              float* depth, cudaStream_t st) {
+                              float* depth, cudaStream_t st, int out_fmt) {
     if (!ctx) return VRS_E_INVALID_ARG;
     if (ctx->sticky != VRS_OK) return ctx->sticky;
     if (!ctx->uploaded) return fail(ctx, VRS_E_STATE, "render before vrs_upload_gaussians");
@@ -525,6 +526,7 @@ static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* ca
         vrs_status s = prepare_frame(ctx, nv, cams, fov, st, fp, total_items);
         if (s != VRS_OK) return s;
     }
+    fp.out_fmt = out_fmt;
     SceneDev sc{ctx->d_mu, ctx->d_cov, ctx->d_icov, ctx->d_sh, ctx->sh_chunks};
     FrameBufs fb = frame_bufs(ctx);
     const bool tm = ctx->timing && ctx->ev_created;
@@ -554,7 +556,8 @@ static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* ca
 
 vrs_status vrs_render_views(vrs_context* ctx, int32_t n_views, const vrs_camera* cams, const vrs_fovea* fovea,
                             float* rgba, float* depth, void* stream) {
-    return render_impl(ctx, n_views, cams, fovea, rgba, depth, (cudaStream_t)stream);
+    if (!ctx) return VRS_E_INVALID_ARG;
+    return render_impl(ctx, n_views, cams, fovea, rgba, depth, (cudaStream_t)stream, ctx->out_fmt);
 }
 
 vrs_status vrs_render_views_host(vrs_context* ctx, int32_t n_views, const vrs_camera* cams, const vrs_fovea* fovea,
@@ -573,10 +576,11 @@ vrs_status vrs_render_views_host(vrs_context* ctx, int32_t n_views, const vrs_ca
         ctx->out_px_cap = px;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    vrs_status s = render_impl(ctx, n_views, cams, fovea, ctx->d_out_rgba, ctx->d_out_depth, st);
+    vrs_status s = render_impl(ctx, n_views, cams, fovea, ctx->d_out_rgba, ctx->d_out_depth, st, ctx->out_fmt);
     if (s != VRS_OK) return s;
-    CK(cudaMemcpyAsync(rgba_host, ctx->d_out_rgba, sizeof(float) * 4 * px, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(depth_host, ctx->d_out_depth, sizeof(float) * px, cudaMemcpyDeviceToHost, st));
+    const bool f32 = ctx->out_fmt == VRS_OUT_F32;
+    CK(cudaMemcpyAsync(rgba_host, ctx->d_out_rgba, (f32 ? sizeof(float) : 1) * 4 * px, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(depth_host, ctx->d_out_depth, (f32 ? sizeof(float) : 2) * px, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return VRS_OK;
 }
@@ -682,9 +686,10 @@ vrs_status vrs_render_views_two_pass(vrs_context* ctx, int32_t n_views, const vr
     }
     ctx->internal_masks = true;
     vrs_status s = render_impl(ctx, 2 * n_views, pc, nullptr, reinterpret_cast<float*>(ctx->d_tp_rgba),
-                               ctx->d_tp_depth, st);
+                               ctx->d_tp_depth, st, VRS_OUT_F32);
     ctx->internal_masks = false;
     if (s != VRS_OK) return s;
+    tp.out_fmt = ctx->out_fmt;
     launch_two_pass_combine(tp, ctx->d_tp_rgba, ctx->d_tp_depth, rgba, depth, out_off, st);
     CK(cudaGetLastError());
     return VRS_OK;
@@ -754,6 +759,14 @@ vrs_status vrs_debug_counts(vrs_context* ctx, uint32_t* counts, int64_t capacity
     launch_counts(ctx->fp, frame_bufs(ctx), ctx->test_cap, ctx->last_stream);
     CK(cudaStreamSynchronize(ctx->last_stream));
     if (n) CK(cudaMemcpy(counts, ctx->d_counts, 4 * n, cudaMemcpyDeviceToHost));
+    return VRS_OK;
+}
+
+vrs_status vrs_set_output_format(vrs_context* ctx, int32_t format) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    if (format != VRS_OUT_F32 && format != VRS_OUT_RGBA8_D16F)
+        return fail(ctx, VRS_E_INVALID_ARG, "output format must be VRS_OUT_F32 or VRS_OUT_RGBA8_D16F");
+    ctx->out_fmt = format;
     return VRS_OK;
 }
 

@@ -8,6 +8,7 @@
 // "Numerics contract".
 #pragma once
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "../../include/vrs.h"
@@ -57,6 +58,7 @@ struct FrameParams {
     int32_t no_cull;         // test hook: disable the warp-block footprint skip (P12)
     int32_t ewa;             // projection: 0 = Optimal Projection, 1 = EWA baseline (config C5)
     int32_t resort;          // 0 = per-sample window K = 16; 1 = hierarchical
+    int32_t out_fmt;         // VRS_OUT_F32 or VRS_OUT_RGBA8_D16F (final output pixels)
     int64_t N;
     int64_t pair_cap;
     float near_plane;
@@ -156,11 +158,12 @@ struct TwoPassView {
 };
 struct TwoPassParams {
     int32_t n;
+    int32_t out_fmt;
     TwoPassView v[VRS_MAX_VIEWS];
 };
 void launch_mask_half(const uint8_t* src, int W, int H, uint8_t* dst, int W2, int H2, cudaStream_t st);
 void launch_two_pass_combine(const TwoPassParams& tp, const float4* prgba, const float* pdepth, float* rgba,
-                             float* depth, int64_t total, cudaStream_t st);
+                             float* depth, int64_t total, cudaStream_t st);  // writes tp.out_fmt
 void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
                   cudaStream_t st);
 void launch_blend_hier(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
@@ -181,6 +184,23 @@ __device__ __forceinline__ float quad3(float a, float b, float c, float p, float
 // z = 1 specialisation (bit-identical: p*1, e*1, f*1*1 are exact)
 __device__ __forceinline__ float quad3z1(float a, float b, float c, float p, float e, float f, float x, float y) {
     return fmaf(fmaf(a, x, fmaf(b, y, p)), x, fmaf(fmaf(c, y, e), y, f));
+}
+
+// Final output pixel i in the context's output format (vrs_set_output_format):
+// VRS_OUT_F32 = float4 RGBA + float depth; VRS_OUT_RGBA8_D16F = RGBA unorm8
+// (round to nearest of clamp(v, 0, 1) * 255) + depth IEEE binary16 (round to
+// nearest).  rgba / depth point to the caller's buffers of that format.
+__device__ __forceinline__ unsigned char unorm8(float v) {
+    return (unsigned char)__float2uint_rn(fminf(fmaxf(v, 0.0f), 1.0f) * 255.0f);
+}
+__device__ __forceinline__ void store_pixel(int fmt, float* rgba, float* depth, size_t i, float4 c, float d) {
+    if (fmt == VRS_OUT_F32) {
+        reinterpret_cast<float4*>(rgba)[i] = c;
+        depth[i] = d;
+    } else {
+        reinterpret_cast<uchar4*>(rgba)[i] = make_uchar4(unorm8(c.x), unorm8(c.y), unorm8(c.z), unorm8(c.w));
+        reinterpret_cast<__half*>(depth)[i] = __float2half_rn(d);
+    }
 }
 
 // Blend weight of the fovea ramp at a pixel centre (P:461

@@ -19,7 +19,7 @@ VRS_OK, VRS_E_INVALID_ARG, VRS_E_INGEST, VRS_E_CUDA, VRS_E_OOM, VRS_E_CAPACITY, 
 VRS_MAX_VIEWS = 8
 EXPORTS = ["vrs_abi_version", "vrs_create", "vrs_destroy", "vrs_last_error", "vrs_upload_gaussians",
            "vrs_set_visibility_mask", "vrs_render_views", "vrs_render_views_host", "vrs_set_instrumentation",
-           "vrs_set_resort_mode",
+           "vrs_set_resort_mode", "vrs_set_output_format",
            "vrs_render_views_two_pass", "vrs_get_frame_stats", "vrs_debug_counts", "vrs_debug_pairs", "vrs_debug_ranges", "vrs_debug_splats",
            "vrs_debug_tile_info", "vrs_debug_set_sort_smem_cap", "vrs_sort_pairs", "vrs_exclusive_scan"]
 
@@ -83,6 +83,7 @@ def lib():
             "vrs_render_views_two_pass": (i32, [vp, i32, vp, vp, vp, vp, vp]),
             "vrs_set_instrumentation": (i32, [vp, i32, i32]),
             "vrs_set_resort_mode": (i32, [vp, i32, i32, i32]),
+            "vrs_set_output_format": (i32, [vp, i32]),
             "vrs_get_frame_stats": (i32, [vp, C.POINTER(vrs_frame_stats)]),
             "vrs_debug_counts": (i32, [vp, vp, i64, C.POINTER(C.c_int64)]),
             "vrs_debug_pairs": (i32, [vp, i32, vp, vp, i64, C.POINTER(C.c_int64)]),
@@ -182,6 +183,11 @@ class Renderer:
 
     set_mask = vrs_set_visibility_mask
 
+    def vrs_set_output_format(self, fmt):
+        """VRS_OUT_F32 (0): float RGBA + float depth; VRS_OUT_RGBA8_D16F (1): uint8 RGBA + binary16 depth."""
+        self._check(lib().vrs_set_output_format(self.h, int(fmt)))
+        self.out_fmt = int(fmt)
+
     def vrs_set_resort_mode(self, mode, block_queue=0, pixel_window=0):
         """0 = per-sample window K = 16; 1 = hierarchical (K_B = 8 block queue, K_P = 8 window)."""
         self._check(lib().vrs_set_resort_mode(self.h, int(mode), int(block_queue), int(pixel_window)))
@@ -196,11 +202,17 @@ class Renderer:
             farr = (vrs_fovea * len(cams))(*[make_fovea(f) for f in foveas])
         return carr, farr
 
-    def alloc_outputs(self, cams):
+    def alloc_outputs(self, cams, pinned_host=False):
+        """Output tensors for the context's format: (px, 4) float32 + (px,) float32, or
+        (px, 4) uint8 + (px,) float16 for VRS_OUT_RGBA8_D16F; on the device, or pinned host."""
         import torch
         px = sum(c.width * c.height for c in cams)
+        packed = getattr(self, "out_fmt", 0) == 1
+        rt, dt = (torch.uint8, torch.float16) if packed else (torch.float32, torch.float32)
+        if pinned_host:
+            return (torch.empty((px, 4), dtype=rt).pin_memory(), torch.empty(px, dtype=dt).pin_memory())
         dev = torch.device("cuda", self.device)
-        return torch.empty((px, 4), dtype=torch.float32, device=dev), torch.empty(px, dtype=torch.float32, device=dev)
+        return torch.empty((px, 4), dtype=rt, device=dev), torch.empty(px, dtype=dt, device=dev)
 
     def vrs_render_views(self, cams, foveas=None, rgba=None, depth=None, stream=None):
         """Render into DEVICE torch tensors (allocated if None) on `stream`
@@ -243,8 +255,9 @@ class Renderer:
         """End-to-end path: outputs land in HOST buffers (numpy or pinned torch tensors)."""
         px = sum(c.width * c.height for c in cams)
         if rgba_host is None:
-            rgba_host = np.empty((px, 4), np.float32)
-            depth_host = np.empty(px, np.float32)
+            packed = getattr(self, "out_fmt", 0) == 1
+            rgba_host = np.empty((px, 4), np.uint8 if packed else np.float32)
+            depth_host = np.empty(px, np.float16 if packed else np.float32)
         rp = rgba_host.data_ptr() if hasattr(rgba_host, "data_ptr") else rgba_host.ctypes.data
         dp = depth_host.data_ptr() if hasattr(depth_host, "data_ptr") else depth_host.ctypes.data
         carr, farr = self._views_structs(cams, foveas)

@@ -464,3 +464,48 @@ def test_binned_sort_tile_overflow_parity(vrs, oracle_mod, cap):
     assert np.array_equal(r.vrs_debug_ranges(), rng_o)
     g = vrs.vrs.split_views(rgba.cpu().numpy(), depth.cpu().numpy(), [cam])
     assert_images_close(g, o.render())
+
+
+# --------------------------------------------------------------------- packed display output format
+
+def _pack_ref(rgba, depth):
+    q = np.rint(np.clip(rgba, 0.0, 1.0).astype(np.float32) * np.float32(255.0)).astype(np.uint8)
+    return q, depth.astype(np.float16)
+
+
+@pytest.mark.parametrize("mode", ["single", "two_pass", "hier", "host"])
+def test_packed_output_is_the_quantised_f32_frame(vrs, mode):
+    """VRS_OUT_RGBA8_D16F writes round(clamp(v,0,1)*255) and binary16 of the
+    very float values the F32 format writes (bit-exact), on every path."""
+    W, H = 320, 256
+    scene = sg.vr_room(7, 20000, sh_degree=3)
+    f = sg.focal_for_hfov(W, 110.0)
+    cams = [sg.look_camera((x, 0, 0), 0.3, 0.1, 0.0, f=f, width=W, height=H, mask_slot=e)
+            for e, x in enumerate((-0.0315, 0.0315))]
+    fov = [sg.Fovea((W / 2, H / 2), (W / 4, H / 4), 0.10)] * 2
+    r = vrs.Renderer(max_gaussians=scene.n, max_views=4, max_pairs=1 << 22, max_width=W, max_height=H,
+                     assign_tile=32)
+    r.upload(scene)
+    for e in range(2):
+        r.set_mask(e, sg.ellipse_mask(W, H))
+    if mode == "hier":
+        r.vrs_set_resort_mode(1)
+    fn = r.render_two_pass if mode == "two_pass" else r.render
+
+    def run():
+        if mode == "host":
+            a, d = r.vrs_render_views_host(cams, fov)
+            return np.asarray(a).copy(), np.asarray(d).copy()
+        a, d = fn(cams, fov)
+        torch.cuda.synchronize()
+        return a.cpu().numpy(), d.cpu().numpy()
+
+    a32, d32 = run()
+    r.vrs_set_output_format(1)
+    a8, d16 = run()
+    assert a8.dtype == np.uint8 and d16.dtype == np.float16
+    qa, qd = _pack_ref(a32, d32)
+    assert np.array_equal(a8, qa)
+    assert np.array_equal(d16.view(np.uint16), qd.view(np.uint16))
+    with pytest.raises(vrs.vrs.VrsError):
+        r.vrs_set_output_format(7)
