@@ -330,9 +330,17 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: VRS_BENCH_ONE_GPU=1 runs every rank on cuda:0 over gloo (checks the multi-rank
+    # logic on a one-GPU box; NCCL refuses two ranks on one device)
+    one_gpu = os.environ.get("VRS_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = CONFIGS[args.config]
 
     # ---- scene: rank 0 generates, NCCL broadcast of the raw arrays (only data-path collective)
