@@ -377,7 +377,7 @@ def main():
     with torch.cuda.stream(stream):
         render(cams, fov, rgba, depth, stream=stream)
     counters = r.stats()
-    r.vrs_set_instrumentation(counters=0, timing=1)
+    r.vrs_set_instrumentation(counters=0, timing=0)  # the timed frames run the bare product path
 
     for w in range(args.warmup):
         with torch.cuda.stream(stream):
@@ -398,13 +398,20 @@ def main():
                 ev0[s].record(stream)
                 render(cs, fov, rgba, depth, stream=stream)
                 ev1[s].record(stream)
-            st = r.stats()  # syncs the stream; outside the event pair
-            stage.append(st["stage_ms"])
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     step_ms = [ev0[s].elapsed_time(ev1[s]) for s in range(args.steps)]
+    # per-stage times: the same frames again with the library's stage events on (outside the timed steps)
+    r.vrs_set_instrumentation(counters=0, timing=1)
+    for s in range(args.steps):
+        with torch.cuda.stream(stream):
+            if not args.no_flush:
+                flush.fill_(s & 0xff)
+            render(step_cams(args.config, cams, s, rank, world), fov, rgba, depth, stream=stream)
+        stage.append(r.stats()["stage_ms"])  # also raises VRS_E_CAPACITY if a frame overflowed
+    r.vrs_set_instrumentation(counters=0, timing=0)
     ms = float(np.mean(step_ms))
     ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -479,6 +486,7 @@ def main():
             nbytes = int(h[0][0].numel() * h[0][0].element_size() + h[0][1].numel() * h[0][1].element_size())
             return world / pipe_s, world / sync_s, nbytes
 
+        r.vrs_set_instrumentation(counters=0, timing=0)  # no per-stage events on the end-to-end path
         v8, s8, b8 = measure_e2e(1)
         v32, s32, b32 = measure_e2e(0)
         what = "render_two_pass" if two_pass else "render"

@@ -51,3 +51,5 @@ run(5)
 for n in (20, 50, 100):
     print(f"pipelined n={n}: {run(n)[0]:.3f} ms/frame, host submit {run(n)[1]:.3f} ms/frame")
 print(f"render only n=100: {run(100, copy=False)[0]:.3f} ms/frame")
+r.vrs_set_instrumentation(counters=0, timing=1)
+print(f"with stage timing events: pipelined n=20: {run(20)[0]:.3f} ms/frame")
