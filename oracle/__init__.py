@@ -87,6 +87,8 @@ def lib():
         L.orc_sample_depth.restype = C.c_float
         L.orc_sample_depth.argtypes = [vp, i32, i64, C.c_float, C.c_float]
         L.orc_hier_core.argtypes = [i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_blend_orders.restype = i64
+        L.orc_blend_orders.argtypes = [vp, i32, vp, vp, i64]
         _lib = L
     return _lib
 
@@ -229,6 +231,18 @@ class Oracle:
         out = np.zeros(6, np.float32)
         lib().orc_tile_test(self.h, view, g, x0, y0, x1, y1, _p(out))
         return dict(keep=out[0], qmin=out[1], t=out[2], dhat=out[3:6].copy())
+
+    def blend_orders(self, view):
+        """Per pixel of a non-foveated view: the Gaussians it blended, front to back (O10-O11).
+        Returns (counts (H, W) int32, seq uint32) with seq the concatenated per-pixel lists (row-major)."""
+        c = self.views[view]
+        counts = np.zeros(c.width * c.height, np.int32)
+        tot = lib().orc_blend_orders(self.h, view, _p(counts), None, 0)
+        if tot < 0:
+            raise ValueError("blend orders need a non-foveated view")
+        seq = np.zeros(max(tot, 1), np.uint32)
+        lib().orc_blend_orders(self.h, view, _p(counts), _p(seq), tot)
+        return counts.reshape(c.height, c.width), seq[:tot]
 
     def sample_depth(self, view, g, x, y):
         return lib().orc_sample_depth(self.h, view, g, x, y)

@@ -662,7 +662,8 @@ struct SampleStats { int64_t evals = 0, contribs = 0, overflow = 0, term = 0; };
  * checked after blending (L11); drain at stream end. */
 struct WEnt { float tau; uint32_t g; float alpha; };
 
-static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, float ys, SampleStats& st) {
+static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, float ys, SampleStats& st,
+                        std::vector<uint32_t>* order = nullptr) {
     const ViewState& vs = O.views[view];
     const orc_view& v = vs.v;
     const float x = (xs - v.cx) / v.fx, y = (ys - v.cy) / v.fy;
@@ -676,6 +677,7 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
     bool done = false, overflowed = false;
     auto blend = [&](const WEnt& w) {
         const Splat& sp = vs.splats[w.g];
+        if (order) order->push_back(w.g);
         double wt = (double)w.alpha * (double)T;
         for (int c = 0; c < 3; c++) C[c] += (double)sp.rgb[c] * wt;
         D += (double)w.tau * dn * wt;
@@ -1457,6 +1459,35 @@ float orc_eq4_edge(const float* C, const float* p, const float* d, float* xhat) 
     xhat[1] = std::fmaf(t, d[1], p[1]);
     float cX = std::fmaf(C[0], xhat[0], C[1] * xhat[1]), cY = std::fmaf(C[1], xhat[0], C[2] * xhat[1]);
     return std::fmaf(xhat[0], cX, xhat[1] * cY);
+}
+
+/* N4 hook (test infrastructure): the blend order of every pixel of a
+ * full-rate (non-foveated) view -- the Gaussians each pixel blended, front to
+ * back, as O10-O11 decide them.  counts[W*H]; seq gets the concatenated lists
+ * (up to cap entries); returns the total length (or -1 for a foveated view). */
+int64_t orc_blend_orders(void* h, int view, int32_t* counts, uint32_t* seq, int64_t cap) {
+    Oracle& O = *(Oracle*)h;
+    const ViewState& vs = O.views[view];
+    if (vs.v.fovea_enabled) return -1;
+    const int W = vs.v.width, H = vs.v.height, T = O.p.assign_tile;
+    int64_t tot = 0;
+    for (int j = 0; j < H; j++)
+        for (int i = 0; i < W; i++) {
+            if (vs.cls[(size_t)(j / T) * vs.tw + (i / T)] == CLS_INVIS) {
+                counts[(size_t)j * W + i] = 0;
+                continue;
+            }
+            const int64_t gt = vs.tile_base + (int64_t)(j / T) * vs.tw + (i / T);
+            std::vector<uint32_t> order;
+            SampleStats st;
+            render_sample(O, view, gt, (float)i + 0.5f, (float)j + 0.5f, st, &order);
+            counts[(size_t)j * W + i] = (int32_t)order.size();
+            for (uint32_t g : order) {
+                if (tot < cap) seq[tot] = g;
+                tot++;
+            }
+        }
+    return tot;
 }
 
 /* Pin H3 hook: the N2 queue mechanics on a given stream of n block entries

@@ -79,6 +79,7 @@ void orc_sat(int tw, int th, const uint8_t* bits, uint32_t* sat);
 int64_t orc_sat_count(int tw, const uint32_t* sat, int x0, int y0, int x1, int y1);
 float orc_eq4_edge(const float* C, const float* p, const float* d, float* xhat);
 float orc_sample_depth(void* h, int view, int64_t g, float x, float y);
+int64_t orc_blend_orders(void* h, int view, int32_t* counts, uint32_t* seq, int64_t cap);
 int orc_hier_core(int64_t n, int kb, int kp, const float* tauB, const uint32_t* g, const uint32_t* member,
                   const float* tau, const float* alpha, const float* rgb, double* out, int64_t* stats);
 
