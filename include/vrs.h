@@ -139,6 +139,23 @@ VRS_API vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_
  * visible).  mask == NULL clears the slot (all visible). */
 VRS_API vrs_status vrs_set_visibility_mask(vrs_context* ctx, int32_t slot, int32_t w, int32_t h, const uint8_t* mask);
 
+/* Backward pass of the last frame (the paper fine-tunes with a
+ * differentiable StopThePop + Optimal Projection rasterizer).
+ * For L = sum over pixels of grad_rgba . RGBA + grad_depth * Depth, writes
+ * dL/d(raw parameters) of the uploaded Gaussians (kept records, upload order):
+ * grad_means n*3, grad_quats n*4 (w,x,y,z, through the normalisation),
+ * grad_log_scales n*3, grad_logits n, grad_sh n*(deg+1)^2*3 (coefficient-major
+ * RGB, like the upload).  rgba/depth: the frame's own F32 outputs (DEVICE);
+ * grad_rgba n_px*4, grad_depth n_px (DEVICE, the frame's layout); outputs are
+ * DEVICE buffers, overwritten.  The blend order and the blended set are those
+ * of the frame; clamps (alpha <= 0.99, tau >= near, colour >= 0) pass no
+ * gradient.  Requires the last call to be vrs_render_views of non-foveated
+ * views with the Optimal Projection, resort mode 0 and VRS_OUT_F32 (else
+ * VRS_E_STATE), and the frame's buffers untouched since.  Enqueued on stream. */
+VRS_API vrs_status vrs_backward(vrs_context* ctx, const float* rgba, const float* depth, const float* grad_rgba,
+                                const float* grad_depth, float* grad_means, float* grad_quats,
+                                float* grad_log_scales, float* grad_logits, float* grad_sh, void* stream);
+
 /* Output format of the final pixels written by vrs_render_views,
  * vrs_render_views_host and vrs_render_views_two_pass (default VRS_OUT_F32).
  * VRS_OUT_RGBA8_D16F is the display format of an HMD compositor: 4 bytes of

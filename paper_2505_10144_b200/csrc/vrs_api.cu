@@ -42,6 +42,8 @@ struct vrs_context {
     int deg = 0;
     bool uploaded = false;
     float4 *d_mu = nullptr, *d_cov = nullptr, *d_icov = nullptr, *d_sh = nullptr;
+    float4* d_raw = nullptr;   // [N][2] raw quaternion (w,x,y,z) and (log-scales, logit): N4 backward
+    float* d_gbuf = nullptr;   // [max_views][max_gaussians][24] per-(view, Gaussian) gradient records
     int sh_chunks = 0;
     // frame buffers
     float4* d_rec = nullptr;
@@ -119,7 +121,7 @@ static vrs_status cuda_check(vrs_context* c, cudaError_t e, const char* where) {
     } while (0)
 
 static void free_all(vrs_context* c) {
-    void* ptrs[] = {c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_col, c->d_cand, c->d_counts, c->d_misc, c->d_vis_list,
+    void* ptrs[] = {c->d_raw, c->d_gbuf, c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_col, c->d_cand, c->d_counts, c->d_misc, c->d_vis_list,
                     c->d_sidk,
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
@@ -244,7 +246,8 @@ vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_degree, 
     icov.reserve(2 * n);
     std::vector<int64_t> keep;
     keep.reserve(n);
-    std::vector<float4> cov_hi, icov_hi;
+    std::vector<float4> cov_hi, icov_hi, rawv;
+    rawv.reserve(2 * n);
     for (int64_t i = 0; i < n; i++) {
         const float* m = means + 3 * i;
         const float* q = quats + 4 * i;
@@ -286,6 +289,8 @@ vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_degree, 
         cov_hi.push_back(make_float4(c6[4], c6[5], sg, (float)(smax * (1.0 + 1e-6))));
         icov.push_back(make_float4(i6[0], i6[1], i6[2], i6[3]));
         icov_hi.push_back(make_float4(i6[4], i6[5], 0.0f, 0.0f));
+        rawv.push_back(make_float4(q[0], q[1], q[2], q[3]));
+        rawv.push_back(make_float4(ls[0], ls[1], ls[2], logits[i]));
         keep.push_back(i);
     }
     const int64_t nk = (int64_t)keep.size();
@@ -303,18 +308,20 @@ vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_degree, 
         }
     }
     // (re)allocate scene buffers
-    for (float4** p : {&ctx->d_mu, &ctx->d_cov, &ctx->d_icov, &ctx->d_sh})
+    for (float4** p : {&ctx->d_mu, &ctx->d_cov, &ctx->d_icov, &ctx->d_sh, &ctx->d_raw})
         if (*p) { cudaFree(*p); *p = nullptr; }
     const size_t NN = std::max<int64_t>(nk, 1);
     CK(dalloc(&ctx->d_mu, NN));
     CK(dalloc(&ctx->d_cov, 2 * NN));
     CK(dalloc(&ctx->d_icov, 2 * NN));
     CK(dalloc(&ctx->d_sh, (size_t)chunks * NN));
+    CK(dalloc(&ctx->d_raw, 2 * NN));
     if (nk > 0) {
         CK(cudaMemcpy(ctx->d_mu, mu.data(), sizeof(float4) * nk, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->d_cov, cov.data(), sizeof(float4) * 2 * nk, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->d_icov, icov.data(), sizeof(float4) * 2 * nk, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->d_sh, shd.data(), sizeof(float4) * chunks * nk, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_raw, rawv.data(), sizeof(float4) * 2 * nk, cudaMemcpyHostToDevice));
     }
     ctx->N = nk;
     ctx->deg = sh_degree;
@@ -759,6 +766,40 @@ vrs_status vrs_debug_counts(vrs_context* ctx, uint32_t* counts, int64_t capacity
     launch_counts(ctx->fp, frame_bufs(ctx), ctx->test_cap, ctx->last_stream);
     CK(cudaStreamSynchronize(ctx->last_stream));
     if (n) CK(cudaMemcpy(counts, ctx->d_counts, 4 * n, cudaMemcpyDeviceToHost));
+    return VRS_OK;
+}
+
+/* backward of the last frame (training mode). */
+vrs_status vrs_backward(vrs_context* ctx, const float* rgba, const float* depth, const float* grad_rgba,
+                        const float* grad_depth, float* grad_means, float* grad_quats, float* grad_log_scales,
+                        float* grad_logits, float* grad_sh, void* stream) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    if (ctx->sticky != VRS_OK) return ctx->sticky;
+    if (!ctx->have_frame) return fail(ctx, VRS_E_STATE, "backward needs a rendered frame");
+    if (!rgba || !depth || !grad_rgba || !grad_depth || !grad_means || !grad_quats || !grad_log_scales ||
+        !grad_logits || !grad_sh)
+        return fail(ctx, VRS_E_INVALID_ARG, "null pointer");
+    const FrameParams& fp = ctx->fp;
+    if (fp.ewa || fp.resort != 0 || fp.out_fmt != VRS_OUT_F32 || ctx->internal_masks)
+        return fail(ctx, VRS_E_STATE, "backward needs a frame rendered with the Optimal Projection, the K = 16 "
+                                      "window and F32 outputs by vrs_render_views");
+    for (int i = 0; i < fp.n_views; i++)
+        if (fp.v[i].fovea) return fail(ctx, VRS_E_STATE, "backward needs a non-foveated frame");
+    CK(cudaSetDevice(ctx->cfg.device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const size_t gcount = (size_t)ctx->cfg.max_views * (size_t)std::max<int64_t>(ctx->cfg.max_gaussians, 1) * 24;
+    if (!ctx->d_gbuf) CK(dalloc(&ctx->d_gbuf, gcount));
+    const size_t N = (size_t)ctx->N;
+    CK(cudaMemsetAsync(ctx->d_gbuf, 0, sizeof(float) * (size_t)fp.n_views * N * 24, st));
+    CK(cudaMemsetAsync(grad_means, 0, sizeof(float) * 3 * N, st));
+    CK(cudaMemsetAsync(grad_quats, 0, sizeof(float) * 4 * N, st));
+    CK(cudaMemsetAsync(grad_log_scales, 0, sizeof(float) * 3 * N, st));
+    CK(cudaMemsetAsync(grad_logits, 0, sizeof(float) * N, st));
+    CK(cudaMemsetAsync(grad_sh, 0, sizeof(float) * 3 * (size_t)fp.sh_coeffs * N, st));
+    launch_backward(fp, frame_bufs(ctx), ctx->last_items, ctx->d_mu, ctx->d_raw,
+                    reinterpret_cast<const float*>(ctx->d_sh), 4 * ctx->sh_chunks, rgba, depth, grad_rgba,
+                    grad_depth, ctx->d_gbuf, grad_means, grad_quats, grad_log_scales, grad_logits, grad_sh, st);
+    CK(cudaGetLastError());
     return VRS_OK;
 }
 

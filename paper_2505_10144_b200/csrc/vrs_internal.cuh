@@ -168,6 +168,11 @@ void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* r
                   cudaStream_t st);
 void launch_blend_hier(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
                        cudaStream_t st);
+// N4 backward (k_backward.cu): gbuf [V][N][24] must be zero, outputs zeroed by the caller.
+void launch_backward(const FrameParams& fp, FrameBufs fb, int total_items, const float4* mu4, const float4* raw,
+                     const float* sh, int sh_stride, const float* f_rgba, const float* f_depth,
+                     const float* g_rgba, const float* g_depth, float* gbuf, float* g_means, float* g_quats,
+                     float* g_ls, float* g_logits, float* g_sh, cudaStream_t st);
 void launch_compose(const FrameParams& fp, FrameBufs fb, float* rgba, float* depth, cudaStream_t st);
 void launch_debug_splats(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int view, float* out,
                          cudaStream_t st);

@@ -19,7 +19,7 @@ VRS_OK, VRS_E_INVALID_ARG, VRS_E_INGEST, VRS_E_CUDA, VRS_E_OOM, VRS_E_CAPACITY, 
 VRS_MAX_VIEWS = 8
 EXPORTS = ["vrs_abi_version", "vrs_create", "vrs_destroy", "vrs_last_error", "vrs_upload_gaussians",
            "vrs_set_visibility_mask", "vrs_render_views", "vrs_render_views_host", "vrs_set_instrumentation",
-           "vrs_set_resort_mode", "vrs_set_output_format",
+           "vrs_set_resort_mode", "vrs_set_output_format", "vrs_backward",
            "vrs_render_views_two_pass", "vrs_get_frame_stats", "vrs_debug_counts", "vrs_debug_pairs", "vrs_debug_ranges", "vrs_debug_splats",
            "vrs_debug_tile_info", "vrs_debug_set_sort_smem_cap", "vrs_sort_pairs", "vrs_exclusive_scan"]
 
@@ -84,6 +84,7 @@ def lib():
             "vrs_set_instrumentation": (i32, [vp, i32, i32]),
             "vrs_set_resort_mode": (i32, [vp, i32, i32, i32]),
             "vrs_set_output_format": (i32, [vp, i32]),
+            "vrs_backward": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
             "vrs_get_frame_stats": (i32, [vp, C.POINTER(vrs_frame_stats)]),
             "vrs_debug_counts": (i32, [vp, vp, i64, C.POINTER(C.c_int64)]),
             "vrs_debug_pairs": (i32, [vp, i32, vp, vp, i64, C.POINTER(C.c_int64)]),
@@ -170,6 +171,7 @@ class Renderer:
         self._check(lib().vrs_upload_gaussians(self.h, scene.n, scene.sh_degree, *[_np_ptr(a) for a in arrs],
                                                C.byref(rej)))
         self.n = scene.n - rej.value
+        self.sh_degree = scene.sh_degree
         return rej.value
 
     upload = vrs_upload_gaussians
@@ -182,6 +184,28 @@ class Renderer:
             self._check(lib().vrs_set_visibility_mask(self.h, slot, m.shape[1], m.shape[0], _np_ptr(m)))
 
     set_mask = vrs_set_visibility_mask
+
+    def vrs_backward(self, rgba, depth, grad_rgba, grad_depth, stream=None):
+        """N4: gradients of L = sum grad_rgba . RGBA + grad_depth . Depth of the last (non-foveated)
+        frame w.r.t. the uploaded raw parameters.  All tensors on the device; returns a dict of
+        float32 device tensors means (n,3), quats (n,4), log_scales (n,3), logits (n,), sh (n,k,3)."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        n, k = self.n, (self.sh_degree + 1) ** 2
+        out = {"means": torch.empty((n, 3), device=dev), "quats": torch.empty((n, 4), device=dev),
+               "log_scales": torch.empty((n, 3), device=dev), "logits": torch.empty((max(n, 1),), device=dev)[:n],
+               "sh": torch.empty((n, k, 3), device=dev)}
+        for t in (rgba, depth, grad_rgba, grad_depth):
+            if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+                raise ValueError("backward tensors must be contiguous float32 CUDA tensors")
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+        self._check(lib().vrs_backward(self.h, *[C.c_void_p(t.data_ptr()) for t in (rgba, depth, grad_rgba, grad_depth)],
+                                       *[C.c_void_p(out[f].data_ptr()) for f in ("means", "quats", "log_scales",
+                                                                                  "logits", "sh")],
+                                       C.c_void_p(sp)))
+        return out
 
     def vrs_set_output_format(self, fmt):
         """VRS_OUT_F32 (0): float RGBA + float depth; VRS_OUT_RGBA8_D16F (1): uint8 RGBA + binary16 depth."""
