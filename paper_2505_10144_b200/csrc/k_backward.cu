@@ -114,10 +114,13 @@ __global__ void __launch_bounds__(256) k_blend_bwd(FrameParams fp, FrameBufs fb,
             const float4* rp = recv + (size_t)g * kRecF4;
             const float4 a0 = __ldg(rp + 0), a1 = __ldg(rp + 1), a2 = __ldg(rp + 2), a3 = __ldg(rp + 3),
                          a4 = __ldg(rp + 4), a5 = __ldg(rp + 5);
-            float* gr = gview + (size_t)g * 24;
-            atomicAdd(gr + kGRgb + 0, go.x * wgt);
-            atomicAdd(gr + kGRgb + 1, go.y * wgt);
-            atomicAdd(gr + kGRgb + 2, go.z * wgt);
+            // the 24 gradient components of this blend, added with six vector reductions
+            float gv[24];
+#pragma unroll
+            for (int k = 0; k < 24; k++) gv[k] = 0.0f;
+            gv[kGRgb + 0] = go.x * wgt;
+            gv[kGRgb + 1] = go.y * wgt;
+            gv[kGRgb + 2] = go.z * wgt;
             if (a < kAlphaMax) {  // alpha = sigma exp(-q/2) unclamped
                 const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
                 const float ex = fmaf(a1.x, x, a1.y);
@@ -126,37 +129,43 @@ __global__ void __launch_bounds__(256) k_blend_bwd(FrameParams fp, FrameBufs fb,
                 const float is = 1.0f / s;
                 const float q = num * is * is;
                 const float sigma = a5.y;
-                atomicAdd(gr + kGSigma, ga * (a / sigma));
+                gv[kGSigma] = ga * (a / sigma);
                 const float gq = -0.5f * ga * a;
                 const float gnum = gq * is * is, gs = -2.0f * gq * q * is;
-                atomicAdd(gr + kGC + 0, gnum * ex * ex);
-                atomicAdd(gr + kGC + 1, gnum * 2.0f * ex * ey);
-                atomicAdd(gr + kGC + 2, gnum * ey * ey);
+                gv[kGC + 0] = gnum * ex * ex;
+                gv[kGC + 1] = gnum * 2.0f * ex * ey;
+                gv[kGC + 2] = gnum * ey * ey;
                 const float gex = 2.0f * gnum * fmaf(a2.y, ex, a2.z * ey);
                 const float gey = 2.0f * gnum * fmaf(a2.z, ex, a2.w * ey);
-                atomicAdd(gr + kGE1x, gex * x);
-                atomicAdd(gr + kGE1z, gex);
-                atomicAdd(gr + kGE2 + 0, gey * x);
-                atomicAdd(gr + kGE2 + 1, gey * y);
-                atomicAdd(gr + kGE2 + 2, gey);
-                atomicAdd(gr + kGU + 0, gs * x);
-                atomicAdd(gr + kGU + 1, gs * y);
-                atomicAdd(gr + kGU + 2, gs);
+                gv[kGE1x] = gex * x;
+                gv[kGE1z] = gex;
+                gv[kGE2 + 0] = gey * x;
+                gv[kGE2 + 1] = gey * y;
+                gv[kGE2 + 2] = gey;
+                gv[kGU + 0] = gs * x;
+                gv[kGU + 1] = gs * y;
+                gv[kGU + 2] = gs;
             }
             if (tau > fp.near_plane) {  // tau = dtb / den unclamped
                 const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
                 const float gt = gd * dn * wgt;
                 const float gdtb = gt / den, gden = -gt * tau / den;
-                atomicAdd(gr + kGB3 + 0, gdtb * x);
-                atomicAdd(gr + kGB3 + 1, gdtb * y);
-                atomicAdd(gr + kGB3 + 2, gdtb);
-                atomicAdd(gr + kGA + 0, gden * x * x);
-                atomicAdd(gr + kGA + 1, gden * 2.0f * x * y);
-                atomicAdd(gr + kGA + 2, gden * 2.0f * x);
-                atomicAdd(gr + kGA + 3, gden * y * y);
-                atomicAdd(gr + kGA + 4, gden * 2.0f * y);
-                atomicAdd(gr + kGA + 5, gden);
+                gv[kGB3 + 0] = gdtb * x;
+                gv[kGB3 + 1] = gdtb * y;
+                gv[kGB3 + 2] = gdtb;
+                gv[kGA + 0] = gden * x * x;
+                gv[kGA + 1] = gden * 2.0f * x * y;
+                gv[kGA + 2] = gden * 2.0f * x;
+                gv[kGA + 3] = gden * y * y;
+                gv[kGA + 4] = gden * 2.0f * y;
+                gv[kGA + 5] = gden;
             }
+            float* gr = gview + (size_t)g * 24;
+#pragma unroll
+            for (int k = 0; k < 24; k += 4)
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(gr + k), "f"(gv[k]),
+                             "f"(gv[k + 1]), "f"(gv[k + 2]), "f"(gv[k + 3])
+                             : "memory");
         }
         Tr = Tr * (1.0f - a);
         done = Tr < kTmin;
