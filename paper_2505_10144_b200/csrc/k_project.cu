@@ -920,6 +920,13 @@ __global__ void __launch_bounds__(256) k_color(SceneDev sc, FrameParams fp, Fram
     }
 }
 
+static int sm_count_pp() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms > 0 ? sms : 148;
+}
+
 void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {
     cudaMemsetAsync(fb.total_tests, 0, 4, st);
     cudaMemsetAsync(fb.vis_count, 0, 4, st);
@@ -931,7 +938,11 @@ void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     k_preprocess<<<sms * 6, B, 0, st>>>(sc, fp, fb, test_cap);
-    k_color<<<sms * 8, B, 0, st>>>(sc, fp, fb);
+}
+
+void launch_color(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, cudaStream_t st) {
+    if (fp.N == 0) return;
+    k_color<<<sm_count_pp() * 8, 256, 0, st>>>(sc, fp, fb);
 }
 
 static int sm_count() {

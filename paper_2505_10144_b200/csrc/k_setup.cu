@@ -62,10 +62,13 @@ __global__ void k_sat_items(ViewParams v, int T, const int32_t* __restrict__ vis
             sat[(size_t)(y + 1) * S + x + 1] = col;
         }
     }
-    // work items in tile row-major order
+    // work items in tile row-major order, all LowRes items first (pass 0), then
+    // the full-rate ones (pass 1): the frame blends them in two launches so the
+    // periphery compose can start while the full-rate items are still blending
     if (threadIdx.x == 0) s_carry = 0;
     __syncthreads();
     const int ntile = tw * th;
+    for (int pass = 0; pass < 2; pass++)
     for (int base = 0; base < ntile; base += blockDim.x) {
         int t = base + threadIdx.x;
         uint32_t cnt = 0;
@@ -74,8 +77,8 @@ __global__ void k_sat_items(ViewParams v, int T, const int32_t* __restrict__ vis
             c = cls[t];
             tx = t % tw;
             ty = t / tw;
-            if (c == kLow) cnt = 1;
-            else if (c != kInvisible) {
+            if (c == kLow) cnt = pass == 0 ? 1u : 0u;
+            else if (c != kInvisible && pass == 1) {
                 if (T == 16) cnt = 1;
                 else
                     for (int sub = 0; sub < 4; sub++)
@@ -92,7 +95,7 @@ __global__ void k_sat_items(ViewParams v, int T, const int32_t* __restrict__ vis
         }
         uint32_t pos = s_carry + s_scan[threadIdx.x] - cnt;
         if (t < ntile && cnt) {
-            if (c == kLow) {
+            if (pass == 0) {
                 items[pos] = (uint32_t)t | (kItemLow << 22);
             } else {
                 uint32_t kind = (c == kHybrid) ? kItemHybrid : kItemFull;
@@ -108,8 +111,9 @@ __global__ void k_sat_items(ViewParams v, int T, const int32_t* __restrict__ vis
         __syncthreads();
         if (threadIdx.x == blockDim.x - 1) s_carry += s_scan[threadIdx.x];
         __syncthreads();
+        if (pass == 0 && base + (int)blockDim.x >= ntile && threadIdx.x == 0) n_items[1] = (int32_t)s_carry;
     }
-    if (threadIdx.x == 0) *n_items = (int32_t)s_carry;
+    if (threadIdx.x == 0) n_items[0] = (int32_t)s_carry;
 }
 
 void launch_setup_view(const uint8_t* mask, int mask_w, ViewParams vp, int T, int32_t* vis, uint32_t* sat,

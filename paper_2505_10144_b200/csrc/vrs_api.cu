@@ -20,7 +20,7 @@ struct ViewSetup {
     int W = 0, H = 0, mask_slot = -1, T = 0, fovea = 0;
     uint64_t mask_gen = 0;
     float gx = 0, gy = 0, rx = 0, ry = 0, ramp = 0;
-    int32_t n_items = 0;
+    int32_t n_items = 0, n_low = 0;
     int32_t cls_count[4] = {0, 0, 0, 0};
 };
 
@@ -100,6 +100,10 @@ struct vrs_context {
     int out_fmt = VRS_OUT_F32;  // vrs_set_output_format
     cudaEvent_t ev[8] = {};
     bool ev_created = false;
+    // side stream of the frame: SH colour runs beside the tile tests and sort,
+    // the periphery compose beside the full-rate blend launch
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork_ev[4] = {};  // after preprocess, colour done, LowRes blend done, compose done
 };
 
 static vrs_status fail(vrs_context* c, vrs_status s, const std::string& msg) {
@@ -135,6 +139,9 @@ static void free_all(vrs_context* c) {
     if (c->d_tp_depth) cudaFree(c->d_tp_depth);
     if (c->ev_created)
         for (auto& e : c->ev) cudaEventDestroy(e);
+    for (auto& e : c->fork_ev)
+        if (e) cudaEventDestroy(e);
+    if (c->side) cudaStreamDestroy(c->side);
 }
 
 extern "C" {
@@ -202,7 +209,7 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     A(dalloc(&ctx->d_cls, (size_t)V * ctx->max_tiles_view));
     A(dalloc(&ctx->d_sat, (size_t)V * ctx->max_sat_view));
     A(dalloc(&ctx->d_items, (size_t)V * ctx->max_items_view));
-    A(dalloc(&ctx->d_nitems, (size_t)V));
+    A(dalloc(&ctx->d_nitems, (size_t)2 * V));
     if (e != cudaSuccess) {
         free_all(ctx);
         delete ctx;
@@ -464,23 +471,25 @@ static vrs_status prepare_frame(vrs_context* ctx, int nv, const vrs_camera* cams
             launch_setup_view(ms >= 0 ? ctx->d_mask[ms] : nullptr, v.W, v, T, ctx->d_vis + (size_t)vi * ctx->max_tiles_view,
                               ctx->d_sat + (size_t)vi * ctx->max_sat_view,
                               ctx->d_cls + (size_t)vi * ctx->max_tiles_view,
-                              ctx->d_items + (size_t)vi * ctx->max_items_view, ctx->d_nitems + vi, st);
+                              ctx->d_items + (size_t)vi * ctx->max_items_view, ctx->d_nitems + 2 * vi, st);
             CK(cudaGetLastError());
-            int32_t ni = 0;
+            int32_t ni[2] = {0, 0};
             std::vector<int32_t> cls((size_t)v.tw * v.th);
-            CK(cudaMemcpyAsync(&ni, ctx->d_nitems + vi, 4, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(ni, ctx->d_nitems + 2 * vi, 8, cudaMemcpyDeviceToHost, st));
             CK(cudaMemcpyAsync(cls.data(), ctx->d_cls + (size_t)vi * ctx->max_tiles_view, 4 * cls.size(),
                                cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
             s.valid = true;
             s.W = v.W; s.H = v.H; s.mask_slot = ms; s.mask_gen = mg; s.T = T; s.fovea = v.fovea;
             s.gx = v.gx; s.gy = v.gy; s.rx = v.rx; s.ry = v.ry; s.ramp = v.ramp;
-            s.n_items = ni;
+            s.n_items = ni[0];
+            s.n_low = ni[1];
             for (int k = 0; k < 4; k++) s.cls_count[k] = 0;
             for (int32_t cc : cls) s.cls_count[cc & 3]++;
         }
         for (int k = 0; k < 4; k++) ctx->last_cls[k] += s.cls_count[k];
         v.n_items = s.n_items;
+        v.n_low = s.n_low;
         v.item_off = total_items;
         total_items += s.n_items;
         tile_base += (int64_t)v.tw * v.th;
@@ -540,18 +549,47 @@ static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* ca
     if (tm) CK(cudaEventRecord(ctx->ev[0], st));
     CK(cudaMemsetAsync(ctx->d_misc + 1, 0, 4, st));
     if (ctx->counters) CK(cudaMemsetAsync(ctx->d_stats, 0, 8 * sizeof(unsigned long long), st));
+    if (!ctx->side) {
+        CK(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+        for (auto& e : ctx->fork_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
     launch_preprocess(sc, fp, fb, ctx->test_cap, st);  // (the candidate scan is fused into it: "scan" stage ~ 0)
     if (tm) CK(cudaEventRecord(ctx->ev[1], st));
+    // SH colour (needed by the blend only) beside the tile tests and the sort
+    CK(cudaEventRecord(ctx->fork_ev[0], st));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev[0], 0));
+    launch_color(sc, fp, fb, ctx->side);
+    CK(cudaEventRecord(ctx->fork_ev[1], ctx->side));
     if (tm) CK(cudaEventRecord(ctx->ev[2], st));
     launch_tiletest_direct(fp, fb, ctx->test_cap, ctx->bin, st);
     if (tm) CK(cudaEventRecord(ctx->ev[3], st));
     // binned per-tile sort; its tile-count scan also writes the ranges ("ranges" stage ~ 0)
     launch_binsort(fb, fp.pair_cap, ctx->last_tiles, ctx->bin, st);
     if (tm) CK(cudaEventRecord(ctx->ev[4], st));
+    CK(cudaStreamWaitEvent(st, ctx->fork_ev[1], 0));
     if (tm) CK(cudaEventRecord(ctx->ev[5], st));
-    launch_blend(fp, fb, total_items, rgba, depth, st);
-    if (tm) CK(cudaEventRecord(ctx->ev[6], st));
+    // blend in two launches: the LowRes items (listed first per view), then the
+    // full-rate ones; the periphery compose (which needs every LowRes sample and
+    // writes only LowRes / invisible pixels) runs on the side stream meanwhile
+    FrameParams fl = fp, ff = fp;
+    int n_low = 0, n_full = 0;
+    for (int i = 0; i < nv; i++) {
+        fl.v[i].item_off = n_low;
+        fl.v[i].n_items = fp.v[i].n_low;
+        ff.v[i].items = fp.v[i].items + fp.v[i].n_low;
+        ff.v[i].item_off = n_full;
+        ff.v[i].n_items = fp.v[i].n_items - fp.v[i].n_low;
+        n_low += fl.v[i].n_items;
+        n_full += ff.v[i].n_items;
+    }
+    CK(cudaEventRecord(ctx->fork_ev[2], st));
+    CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev[2], 0));
+    launch_blend(ff, fb, n_full, rgba, depth, ctx->side);   // full-rate items beside ...
+    CK(cudaEventRecord(ctx->fork_ev[3], ctx->side));
+    launch_blend(fl, fb, n_low, rgba, depth, st);           // ... the LowRes items, then the compose
     launch_compose(fp, fb, rgba, depth, st);
+    CK(cudaStreamWaitEvent(st, ctx->fork_ev[3], 0));
+    if (tm) CK(cudaEventRecord(ctx->ev[6], st));
     if (tm) CK(cudaEventRecord(ctx->ev[7], st));
     CK(cudaGetLastError());
     ctx->fp = fp;

@@ -43,6 +43,7 @@ struct ViewParams {
     int64_t low_off;         // offset of this view in the low-res sample planes
     int32_t low_w;           // low-res plane width ((W+1)/2)
     int32_t n_items;         // blend work items of this view
+    int32_t n_low;           // of which LowRes (they come first in items)
     int32_t item_off;        // first item of this view in the launch
     const int32_t* vis;      // [th*tw] visibility bits
     const uint32_t* sat;     // [(th+1)*(tw+1)] summed-area table
@@ -97,10 +98,13 @@ struct FrameBufs {
 };
 
 // ----------------------------------------------------------------- launchers
+// n_items_dev[0] = items, n_items_dev[1] = LowRes items (listed first)
 void launch_setup_view(const uint8_t* mask, int mask_w, ViewParams vp, int T, int32_t* vis, uint32_t* sat,
                        int32_t* cls, uint32_t* items, int32_t* n_items_dev, cudaStream_t st);
 // Cull + preprocess + candidate expansion into fb.sidk (total in fb.total_tests).
 void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st);
+// SH colour of the visible list (after launch_preprocess; needed by the blend only)
+void launch_color(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, cudaStream_t st);
 // Exclusive scan of n = min(*n_dev, cap) u32 (n_dev may be null: n = cap); *total = sum.
 // out may be null.  expand (optional): for element e with count c at offset o,
 // expand[o + j] = e | (j << 32) for j < c (and o + j < expand_cap).
