@@ -517,9 +517,9 @@ def main():
             except Exception:
                 traffic = None
         n_views = len(cams)
-        # k_cull, k_preprocess, k_color, k_tiletest, k_tile_scan, k_bucket, k_tile_sort, k_blend, k_compose
-        # (+ k_two_pass_combine for the two-pass baseline)
-        launches_per_step = 9 + (1 if two_pass else 0)
+        # k_cull, k_preprocess, k_color, k_tiletest_direct, k_tile_scan, k_ovf_bucket, k_tile_sort,
+        # k_blend x 2 (LowRes items, full-rate items), k_compose (+ k_two_pass_combine for the two-pass baseline)
+        launches_per_step = 10 + (1 if two_pass else 0)
         line = {
             "metric": METRIC if args.config == "c2" else METRIC + f" [{args.config}]",
             "value": world * 1000.0 / ms_max,
