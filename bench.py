@@ -509,11 +509,12 @@ def main():
         alg_ops = 11.0 * counters["evaluations"] + 65.0 * counters["contributions"]
         peak_ops = 148 * 4 * 32 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
         achieved = alg_ops / (blend_ms * 1e-3) if blend_ms > 0 else 0.0
-        traffic = None
+        traffic, winst = None, None
         tp = os.path.join(ROOT, "profiles", "blend_traffic.json")
         if os.path.exists(tp):
             try:
-                traffic = json.load(open(tp)).get(args.config)
+                tj = json.load(open(tp))
+                traffic, winst = tj.get(args.config), tj.get(args.config + "_warp_instructions")
             except Exception:
                 traffic = None
         n_views = len(cams)
@@ -539,7 +540,11 @@ def main():
             "roofline": {"kernel": "k_blend", "bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
                          "unit": "T lane-instr/s", "frac": achieved / peak_ops, "traffic": traffic,
                          "peak_source": f"148 SM x 4 schedulers x 32 lanes x sm_max_mhz ({src} MEASURED_PEAKS)",
-                         "algorithmic_ops_per_launch": alg_ops},
+                         "algorithmic_ops_per_launch": alg_ops,
+                         # executed warp instructions of the launch (ncu, profiles/) over the live blend time
+                         # against the issue peak (148 SM x 4 schedulers x clock): how full the issue slots are
+                         "issue_frac": (winst / (blend_ms * 1e-3 * 148 * 4 * float(peaks.get("sm_max_mhz", 1965.0))
+                                                 * 1e6)) if winst and blend_ms > 0 else None},
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "e2e": e2e,
