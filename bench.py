@@ -57,6 +57,9 @@ CONFIGS = {
     "c8": dict(n=500_000, scale_mul=1.0, sh=3, fovea=True, T=32, masks=True, seed=2, resort=1,
                desc="C2 workload with the hierarchical resort mode (SURVEY N2): K_B = 8 block queue per 4x4 "
                     "sample block ahead of a K_P = 8 per-sample window; vs_flat compares with the K = 16 frame"),
+    "c9": dict(n=500_000, scale_mul=1.0, sh=3, fovea=False, T=16, masks=False, seed=2,
+               desc="training step (SURVEY N4): C2 scene, stereo 2x2064x2208 non-foveated (T_a = 16), forward "
+                    "render + vrs_backward of synthetic gradient images to all raw parameters"),
     "c6": dict(n=500_000, scale_mul=1.0, sh=3, fovea=True, T=32, masks=True, seed=2, two_pass=True,
                desc="C2 workload rendered with the paper's two-pass foveated baseline (App. A): full-res "
                     "centre crop + half-res masked periphery, bilinear upsample + blend (SURVEY N1)"),
@@ -274,6 +277,62 @@ def run_c7(args):
     print(json.dumps(line), flush=True)
 
 
+def run_c9(args):
+    """Config C9: one training step = forward render of a
+    non-foveated stereo frame + vrs_backward of fixed synthetic gradient
+    images (a stand-in loss; the paper's datasets are out of scope), timed
+    with CUDA events on the stream; per-part times reported."""
+    import torch
+    from paper_2505_10144_b200 import Renderer
+    cfg = CONFIGS["c9"]
+    scene = sg.vr_room(cfg["seed"], cfg["n"], scale_mul=cfg["scale_mul"], sh_degree=cfg["sh"])
+    cams = sg.stereo_pair(masks=False)
+    r = Renderer(max_gaussians=scene.n, max_views=2, max_pairs=16 << 20, max_width=cams[0].width,
+                 max_height=cams[0].height, assign_tile=cfg["T"])
+    r.upload(scene)
+    stream = torch.cuda.Stream()
+    rgba, depth = r.alloc_outputs(cams)
+    gen = torch.Generator(device="cuda").manual_seed(0)
+    g_rgba = torch.randn(rgba.shape, device="cuda", generator=gen)
+    g_depth = torch.randn(depth.shape, device="cuda", generator=gen) * 0.1
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def step():
+        r.render(cams, None, rgba, depth, stream=stream)
+        mid.record(stream)
+        return r.vrs_backward(rgba, depth, g_rgba, g_depth, stream=stream)
+
+    mid = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+    torch.cuda.synchronize()
+    fw, bw, tot = [], [], []
+    with ClockSampler(0) as clk:
+        for s_ in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            mid = torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                flush.fill_(s_ & 0xff)
+                e0.record(stream)
+                out = step()
+                e1.record(stream)
+            torch.cuda.synchronize()
+            fw.append(e0.elapsed_time(mid))
+            bw.append(mid.elapsed_time(e1))
+            tot.append(e0.elapsed_time(e1))
+    ms = float(np.mean(tot))
+    line = {"metric": "training steps/s (forward + backward, stereo 2x2064x2208 non-foveated) [c9]",
+            "value": 1000.0 / ms, "unit": "steps/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": {"workload": "c9", "desc": cfg["desc"], "gaussians": scene.n,
+                                            "l2": "flushed between steps (outside the event pair)"},
+            "stage_ms": {"forward": float(np.mean(fw)), "backward": float(np.mean(bw))},
+            "grad_abs_max": {k: float(v.abs().max()) for k, v in out.items()},
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
 def run_c5(args):
     """Config C5: FoV sweep 90-160 deg on the C2 scene, Optimal Projection vs the
     EWA baseline: pairs per eye, blend ms and frame ms per FoV (one GPU)."""
@@ -324,6 +383,8 @@ def main():
         return run_c5(args)
     if args.config == "c7":
         return run_c7(args)
+    if args.config == "c9":
+        return run_c9(args)
     import torch
     import torch.distributed as dist
 

@@ -26,7 +26,10 @@ namespace vrs {
 
 namespace {
 constexpr int kScanT = 1024;
-constexpr int kScanPer = 4;
+#ifndef VRS_SCAN_PER
+#define VRS_SCAN_PER 12
+#endif
+constexpr int kScanPer = VRS_SCAN_PER;
 constexpr int kScanRound = kScanT * kScanPer;
 constexpr int kBinT = 256;
 constexpr int kWarpSortMax = 256;  // tiles up to this size: one warp, keys in registers (E <= 8)
@@ -145,8 +148,9 @@ __global__ void __launch_bounds__(kScanT) k_tile_scan(uint32_t* __restrict__ cnt
                                                       uint32_t* __restrict__ total, uint32_t cap,
                                                       uint32_t* __restrict__ list, uint32_t* __restrict__ list_n,
                                                       int64_t list_cap, uint32_t small_max) {
-    __shared__ uint32_t s_c[kScanRound];  // counts, then tile starts
-    __shared__ uint32_t s_o[kScanRound];  // overflow starts
+    extern __shared__ uint32_t s_dyn[];
+    uint32_t* const s_c = s_dyn;               // [kScanRound] counts, then tile starts
+    uint32_t* const s_o = s_dyn + kScanRound;  // [kScanRound] overflow starts
     __shared__ uint32_t s_w[kScanT / 32], s_wo[kScanT / 32];
     __shared__ uint32_t s_nb, s_ns;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -363,7 +367,8 @@ void launch_binsort(FrameBufs fb, int64_t cap, int64_t n_tiles, BinScratch b, cu
     }
     cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kBinCap * 8));
     const int sms = sms_now();
-    k_tile_scan<<<1, kScanT, 0, st>>>(b.tile_cnt, n_tiles, fb.ranges, b.ovf_off, fb.total, (uint32_t)cap, b.list,
+    cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kScanRound * 4));
+    k_tile_scan<<<1, kScanT, 2 * kScanRound * 4, st>>>(b.tile_cnt, n_tiles, fb.ranges, b.ovf_off, fb.total, (uint32_t)cap, b.list,
                                       b.list_n, b.max_tiles, min(b.cap_smem, (uint32_t)kWarpSortMax));
     k_ovf_bucket<<<sms * 2, 256, 0, st>>>(fb.keys_alt, fb.vals_alt, b.rank, b.ovf_count, (uint32_t)cap, b.ovf_off,
                                           b.obucket);
