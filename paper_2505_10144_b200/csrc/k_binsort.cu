@@ -80,6 +80,58 @@ __device__ __forceinline__ void merge_block(const uint64_t* a, uint32_t na, cons
         out[d] = ta ? a[i++] : b[j++];
     }
 }
+// One warp sorts the 256-key run r[0, 256) in shared memory in place, in
+// registers (blocked layout through the warp's padded scratch sw, the same
+// network as warp_sort_tile).
+__device__ __forceinline__ void warp_sort_run256(uint64_t* r, uint64_t* sw, int lane) {
+    constexpr int E = 8;
+    uint64_t x[E];
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint32_t idx = (uint32_t)(e * 32 + lane);
+        sw[(idx / E) * (E + 1) + idx % E] = r[idx];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; e++) x[e] = sw[lane * (E + 1) + e];
+#pragma unroll
+    for (int k = 2; k <= 32 * E; k <<= 1) {
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            if (j < E) {
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    if ((e & j) == 0) {
+                        const bool asc = ((lane * E + e) & k) == 0;
+                        const uint64_t a = x[e], b = x[e | j];
+                        const bool sw_ = (a > b) == asc;
+                        x[e] = sw_ ? b : a;
+                        x[e | j] = sw_ ? a : b;
+                    }
+                }
+            } else {
+                const int jl = j / E;
+                const bool keep_min = ((lane & jl) == 0) == (((lane * E) & k) == 0);
+#pragma unroll
+                for (int e = 0; e < E; e++) {
+                    const uint64_t y = __shfl_xor_sync(0xffffffffu, x[e], jl);
+                    x[e] = keep_min ? (x[e] < y ? x[e] : y) : (x[e] < y ? y : x[e]);
+                }
+            }
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; e++) sw[lane * (E + 1) + e] = x[e];
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+        const uint32_t idx = (uint32_t)(e * 32 + lane);
+        r[idx] = sw[(idx / E) * (E + 1) + idx % E];
+    }
+    __syncwarp();
+}
+
 // One warp sorts one tile of n <= 32*E keys held in registers (blocked
 // layout: lane l holds elements l*E .. l*E+E-1; padding ~0 sorts last):
 // bitonic stages with distance j < E are register compare-exchanges, the
@@ -298,15 +350,35 @@ __global__ void __launch_bounds__(kBinT, 4) k_tile_sort(const uint32_t* __restri
                 s_k[i] = i < m ? (e < kTileCap ? tb[e] : ob[e - kTileCap]) : ~0ull;
             }
             __syncthreads();
-            bitonic_sort_smem<kBinT>(s_k, P);
+            const uint64_t* sorted = s_k;
+            if (P >= 512 && P <= kBinCap / 2) {
+                // runs of 256 sorted by the 8 warps in registers, then merged pairwise in
+                // shared memory (ping-pong with the upper half of s_k; the warps' transpose
+                // scratch sits past it)
+                uint64_t* sw = s_k + kBinCap + (tid >> 5) * (32 * 9);
+                for (uint32_t r = tid >> 5; r < P / 256; r += kBinT / 32) warp_sort_run256(s_k + r * 256, sw, (int)(tid & 31u));
+                uint64_t* src = s_k;
+                uint64_t* dst = s_k + kBinCap / 2;
+                for (uint32_t L = 256; L < P; L <<= 1) {
+                    __syncthreads();
+                    for (uint32_t s0 = 0; s0 < P; s0 += 2 * L) merge_block(src + s0, L, src + s0 + L, L, dst + s0);
+                    uint64_t* tmp = src;
+                    src = dst;
+                    dst = tmp;
+                }
+                __syncthreads();
+                sorted = src;
+            } else {
+                bitonic_sort_smem<kBinT>(s_k, P);
+            }
             if (n <= cap_smem) {
                 for (uint32_t i = tid; i < m; i += kBinT) {
-                    const uint64_t k = s_k[i];
+                    const uint64_t k = sorted[i];
                     keys[off + i] = tk | (k >> 32);
                     vals[off + i] = (uint32_t)k;
                 }
             } else {
-                for (uint32_t i = tid; i < m; i += kBinT) bk[c0 + i] = s_k[i];
+                for (uint32_t i = tid; i < m; i += kBinT) bk[c0 + i] = sorted[i];
             }
         }
         if (n > cap_smem) {  // merge the sorted chunks: scratch <-> keys ping-pong over this tile's range
@@ -365,14 +437,15 @@ void launch_binsort(FrameBufs fb, int64_t cap, int64_t n_tiles, BinScratch b, cu
         cudaMemsetAsync(fb.total, 0, 4, st);
         return;
     }
-    cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kBinCap * 8));
+    const int sort_smem = (int)(kBinCap * 8 + (kBinT / 32) * 32 * 9 * 8);
+    cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, sort_smem);
     const int sms = sms_now();
     cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kScanRound * 4));
     k_tile_scan<<<1, kScanT, 2 * kScanRound * 4, st>>>(b.tile_cnt, n_tiles, fb.ranges, b.ovf_off, fb.total, (uint32_t)cap, b.list,
                                       b.list_n, b.max_tiles, min(b.cap_smem, (uint32_t)kWarpSortMax));
     k_ovf_bucket<<<sms * 2, 256, 0, st>>>(fb.keys_alt, fb.vals_alt, b.rank, b.ovf_count, (uint32_t)cap, b.ovf_off,
                                           b.obucket);
-    k_tile_sort<<<sms * 4, kBinT, kBinCap * 8, st>>>(b.list, b.list_n, b.max_tiles, fb.ranges, b.tbucket, b.ovf_off,
+    k_tile_sort<<<sms * 4, kBinT, sort_smem, st>>>(b.list, b.list_n, b.max_tiles, fb.ranges, b.tbucket, b.ovf_off,
                                                      b.obucket, fb.keys_alt, fb.keys, fb.vals, b.cap_smem,
                                                      b.list_n + 2);
 }

@@ -197,7 +197,7 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     ctx->sort.max_tiles = (P + 4095) / 4096;
     ctx->sort.epoch = &ctx->sort_epoch;
     ctx->bin.max_tiles = V * ctx->max_tiles_view;
-    ctx->bin.cap_smem = kBinCap;
+    ctx->bin.cap_smem = kBinCap / 2;  // chunks sorted as 256-key runs + shared-memory merges
     A(dalloc(&ctx->bin.tile_cnt, (size_t)ctx->bin.max_tiles));
     A(dalloc(&ctx->bin.rank, (size_t)P));
     A(dalloc(&ctx->bin.tbucket, (size_t)ctx->bin.max_tiles * kTileCap));

@@ -572,3 +572,29 @@ def test_maximum_views_in_one_call(vrs, oracle_mod):
     assert_lists_equal(r, o)
     assert_images_close(g, oi)
     assert r.stats()["work_items"] > 0
+
+
+@pytest.mark.parametrize("cap", [512, 1024, 2048])
+def test_binned_sort_run_merge_parity(vrs, oracle_mod, cap):
+    """Big tiles: chunks of up to `cap` keys are sorted as 256-key register runs
+    merged in shared memory (2048 = the default), larger tiles additionally
+    merged in global memory -- sorted pairs and ranges equal the oracle's."""
+    scene = sg.vr_room(12, 400_000, scale_mul=1.5, sh_degree=0)
+    W, H = 256, 192
+    cams = sg.stereo_pair(width=W, height=H, masks=False)
+    r = vrs.Renderer(max_gaussians=scene.n, max_views=2, max_pairs=1 << 23, max_width=W, max_height=H,
+                     assign_tile=32)
+    r.upload(scene)
+    if cap != 2048:
+        r.vrs_debug_set_sort_smem_cap(cap)
+    rgba, depth = r.render(cams, None)
+    torch.cuda.synchronize()
+    o = oracle_mod.Oracle(scene)
+    o.prepare(cams, None, assign_tile=32)
+    rng = o.ranges()
+    sizes = rng[:, 1] - rng[:, 0]
+    assert sizes.max() > 2 * cap and (sizes > 256).sum() > 10, "test needs big tiles"
+    k, v = r.vrs_debug_pairs(True)
+    ok, ov = o.pairs(True)
+    assert np.array_equal(k, ok) and np.array_equal(v, ov)
+    assert np.array_equal(r.vrs_debug_ranges(), rng)
