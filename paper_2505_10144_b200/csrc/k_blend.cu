@@ -249,6 +249,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         }
         if (__syncthreads_count(!done) == 0) break;
         const int nb = min((int)(re - base), kBatch);
+#define POS_OF(j) (base + (uint32_t)(j))
         for (int c = 0; c < nb; c += 32) {
             if (__all_sync(0xffffffffu, done)) break;
             const bool rel = (c + lane < nb) && ((S.mask[c + lane] >> warp) & 1u);
@@ -272,7 +273,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
                     const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, t.x));
                     float tau;
                     const float alpha = alpha_tau(num, ss, den, dtb, t.y, tau);
-                    contribute(order_key(tau, __float_as_uint(t.z), fp.near_plane), alpha, base + j);
+                    contribute(order_key(tau, __float_as_uint(t.z), fp.near_plane), alpha, POS_OF(j));
                 };
                 while (bits) {
                     const int j = c + __ffs(bits) - 1;
@@ -295,7 +296,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
             while (bits) {
                 const int j = c + __ffs(bits) - 1;
                 bits &= bits - 1;
-                evaluate(base + j, __float_as_uint(S.r5[j].z), S.r0[j], S.r1[j], kEwa ? S.r1[j] : S.r2[j],
+                evaluate(POS_OF(j), __float_as_uint(S.r5[j].z), S.r0[j], S.r1[j], kEwa ? S.r1[j] : S.r2[j],
                          [&](float4& a3, float4& a4, float2& a5) {
                              a3 = S.r3[j];
                              a4 = S.r4[j];
@@ -305,6 +306,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
             }
         }
     }
+#undef POS_OF
     // drain the window in order (sentinels pop as no-ops)
 #pragma unroll 1
     for (int k = 0; k < kWindow && !done; k++) {
@@ -361,6 +363,8 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
             c2 += __shfl_xor_sync(0xffffffffu, c2, o);
             c3 += __shfl_xor_sync(0xffffffffu, c3, o);
         }
+        __syncthreads();
+        if (tid < 4) S.cnt[tid] = 0ull;  // (the staging may have used cnt as scratch)
         __syncthreads();
         if (lane == 0) {
             atomicAdd(&S.cnt[0], c0);
