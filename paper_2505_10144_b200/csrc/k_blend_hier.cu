@@ -282,6 +282,7 @@ __global__ void __launch_bounds__(kHT, VRS_HIER_MINB) k_blend_hier(FrameParams f
                 __syncwarp();
                 const bool pop = admit && qn > kHB;
                 if (__any_sync(0xffffffffu, pop)) pop_release(pop, base + (uint32_t)j);
+                __syncwarp();  // the released slot's cache reads precede its reuse (memory order, not just execution)
             }
         }
     }
