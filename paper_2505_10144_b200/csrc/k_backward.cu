@@ -36,6 +36,8 @@ enum : int { kGRgb = 0, kGSigma = 3, kGU = 4, kGE1x = 7, kGE1z = 8, kGE2 = 9, kG
 
 struct BwdSmem {
     float4 r0[kGB], r1[kGB], r2[kGB], r3[kGB], r4[kGB], r5[kGB];
+    uint32_t mask[kGB];
+    float4 wblock[8];
     unsigned long long w_key[kWindow][256];
     float w_a[kWindow][256];
 };
@@ -82,6 +84,11 @@ __global__ void __launch_bounds__(256) k_blend_bwd(FrameParams fp, FrameBufs fb,
         gd = g_depth[pi];
     }
     const float Tfin = 1.0f - fo.w;
+    if (tid < 8) {  // per-warp sample extent (the forward's conservative footprint skip)
+        const int wwx = (tid & 1) * 8, wwy = (tid >> 1) * 4;
+        S.wblock[tid] = make_float4((float)(ox + wwx) + 0.5f, (float)(ox + wwx + 7) + 0.5f, (float)(oy + wwy) + 0.5f,
+                                    (float)(oy + wwy + 3) + 0.5f);
+    }
     char* const wkb = reinterpret_cast<char*>(&S.w_key[0][tid]);
     char* const wab = reinterpret_cast<char*>(&S.w_a[0][tid]);
 #define WK(off) (*reinterpret_cast<unsigned long long*>(wkb + (off)))
@@ -161,11 +168,32 @@ __global__ void __launch_bounds__(256) k_blend_bwd(FrameParams fp, FrameBufs fb,
                 gv[kGA + 5] = gden;
             }
             float* gr = gview + (size_t)g * 24;
+#ifndef VRS_BWD_NO_AGG
+            // lanes blending the same Gaussian at this instant sum their records first
+            // (tree over the group's ranks by shuffles); one lane per group adds it
+            const unsigned act = __activemask();
+            const unsigned peers = __match_any_sync(act, g);
+            const int n = __popc(peers);
+            const int nmax = (int)__reduce_max_sync(act, (unsigned)n);
+            const int rk = __popc(peers & ((1u << lane) - 1u));
+            for (int st = 1; st < nmax; st <<= 1) {
+                const int sr = rk + st;
+                const int src = (sr < n) ? (int)__fns(peers, 0, sr + 1) : lane;
+                const bool take = ((rk & (2 * st - 1)) == 0) && sr < n;
+#pragma unroll
+                for (int k = 0; k < 24; k++) {
+                    const float o = __shfl_sync(act, gv[k], src);
+                    gv[k] += take ? o : 0.0f;
+                }
+            }
+            if (rk == 0)
+#endif
 #pragma unroll
             for (int k = 0; k < 24; k += 4)
-                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(gr + k), "f"(gv[k]),
-                             "f"(gv[k + 1]), "f"(gv[k + 2]), "f"(gv[k + 3])
-                             : "memory");
+                if (gv[k] != 0.0f || gv[k + 1] != 0.0f || gv[k + 2] != 0.0f || gv[k + 3] != 0.0f)
+                    asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(gr + k), "f"(gv[k]),
+                                 "f"(gv[k + 1]), "f"(gv[k + 2]), "f"(gv[k + 3])
+                                 : "memory");
         }
         Tr = Tr * (1.0f - a);
         done = Tr < kTmin;
@@ -206,12 +234,24 @@ __global__ void __launch_bounds__(256) k_blend_bwd(FrameParams fp, FrameBufs fb,
             S.r2[tid] = __ldg(rp + 2);
             S.r3[tid] = __ldg(rp + 3);
             S.r4[tid] = __ldg(rp + 4);
-            const float4 a5 = __ldg(rp + 5);
+            const float4 a5 = __ldg(rp + 5), a7 = __ldg(rp + 7);
             S.r5[tid] = make_float4(a5.x, a5.y, __uint_as_float(g), 0.0f);
+            uint32_t m = 0;
+#pragma unroll
+            for (int w = 0; w < 8; w++) {
+                const float4 b = S.wblock[w];
+                m |= !(a7.y < b.x || a7.x > b.y || a7.w < b.z || a7.z > b.w) ? (1u << w) : 0u;
+            }
+            S.mask[tid] = m;
         }
         if (__syncthreads_count(!done) == 0) break;
         const int nb = min((int)(re - base), kGB);
-        for (int j = 0; j < nb; j++) {
+        for (int c = 0; c < nb; c += 32) {
+          if (__all_sync(0xffffffffu, done)) break;
+          unsigned bits = __ballot_sync(0xffffffffu, (c + lane < nb) && ((S.mask[c + lane] >> warp) & 1u));
+          while (bits) {
+            const int j = c + __ffs(bits) - 1;
+            bits &= bits - 1;
             if (done) continue;
             const float4 a0 = S.r0[j], a1 = S.r1[j], a2 = S.r2[j];
             const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
@@ -227,6 +267,7 @@ __global__ void __launch_bounds__(256) k_blend_bwd(FrameParams fp, FrameBufs fb,
             float tau;
             const float alpha = alpha_tau(num, ss, den, dtb, t.y, tau);
             contribute(order_key(tau, __float_as_uint(t.z), fp.near_plane), alpha);
+          }
         }
     }
 #pragma unroll 1
