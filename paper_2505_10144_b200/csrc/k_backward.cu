@@ -535,11 +535,7 @@ void launch_backward(const FrameParams& fp, FrameBufs fb, int total_items, const
                      float* g_logits, float* g_sh, cudaStream_t st) {
     if (total_items > 0) {
         const size_t smem = sizeof(BwdSmem);
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(k_blend_bwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-            attr = true;
-        }
+        ensure_smem_attr((const void*)k_blend_bwd, (int)smem);
         k_blend_bwd<<<(unsigned)total_items, 256, smem, st>>>(fp, fb, f_rgba, f_depth, g_rgba, g_depth, gbuf);
     }
     const int64_t total = (int64_t)fp.n_views * fp.N;

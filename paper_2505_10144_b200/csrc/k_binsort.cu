@@ -422,14 +422,7 @@ __global__ void __launch_bounds__(kBinT, 4) k_tile_sort(const uint32_t* __restri
 }
 
 static int sms_now() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
+    return device_sms();
 }
 
 void launch_binsort(FrameBufs fb, int64_t cap, int64_t n_tiles, BinScratch b, cudaStream_t st) {
@@ -438,9 +431,9 @@ void launch_binsort(FrameBufs fb, int64_t cap, int64_t n_tiles, BinScratch b, cu
         return;
     }
     const int sort_smem = (int)(kBinCap * 8 + (kBinT / 32) * 32 * 9 * 8);
-    cudaFuncSetAttribute(k_tile_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, sort_smem);
+    ensure_smem_attr((const void*)k_tile_sort, sort_smem);
     const int sms = sms_now();
-    cudaFuncSetAttribute(k_tile_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kScanRound * 4));
+    ensure_smem_attr((const void*)k_tile_scan, (int)(2 * kScanRound * 4));
     k_tile_scan<<<1, kScanT, 2 * kScanRound * 4, st>>>(b.tile_cnt, n_tiles, fb.ranges, b.ovf_off, fb.total, (uint32_t)cap, b.list,
                                       b.list_n, b.max_tiles, min(b.cap_smem, (uint32_t)kWarpSortMax));
     k_ovf_bucket<<<sms * 2, 256, 0, st>>>(fb.keys_alt, fb.vals_alt, b.rank, b.ovf_count, (uint32_t)cap, b.ovf_off,

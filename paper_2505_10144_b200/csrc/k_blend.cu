@@ -34,9 +34,7 @@ __global__ void k_ranges(const uint64_t* __restrict__ keys, const uint32_t* __re
 void launch_ranges(const uint64_t* keys, const uint32_t* n_dev, int64_t cap, uint32_t* ranges, int64_t n_tiles,
                    cudaStream_t st) {
     cudaMemsetAsync(ranges, 0, sizeof(uint32_t) * 2 * (size_t)n_tiles, st);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_sms();
     k_ranges<<<sms * 16, 256, 0, st>>>(keys, n_dev, cap, ranges, n_tiles);
 }
 
@@ -391,14 +389,10 @@ void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* r
     }
     const size_t smem = sizeof(BlendSmem);
     const unsigned grid = (unsigned)total_items * kSplit;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_blend<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_blend<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_blend<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_blend<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
-    }
+    ensure_smem_attr((const void*)k_blend<true, false>, (int)smem);
+    ensure_smem_attr((const void*)k_blend<false, false>, (int)smem);
+    ensure_smem_attr((const void*)k_blend<true, true>, (int)smem);
+    ensure_smem_attr((const void*)k_blend<false, true>, (int)smem);
     if (fp.ewa) {
         if (fp.counters) k_blend<true, true><<<grid, kBT, smem, st>>>(fp, fb, rgba, depth);
         else k_blend<false, true><<<grid, kBT, smem, st>>>(fp, fb, rgba, depth);

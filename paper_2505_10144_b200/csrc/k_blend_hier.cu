@@ -358,12 +358,8 @@ void launch_blend_hier(const FrameParams& fp, FrameBufs fb, int total_items, flo
                        cudaStream_t st) {
     if (total_items <= 0) return;
     const size_t smem = sizeof(HierSmem);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_blend_hier<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(k_blend_hier<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr_set = true;
-    }
+    ensure_smem_attr((const void*)k_blend_hier<true>, (int)smem);
+    ensure_smem_attr((const void*)k_blend_hier<false>, (int)smem);
     if (fp.counters) k_blend_hier<true><<<(unsigned)total_items, kHT, smem, st>>>(fp, fb, rgba, depth);
     else k_blend_hier<false><<<(unsigned)total_items, kHT, smem, st>>>(fp, fb, rgba, depth);
 }

@@ -920,12 +920,6 @@ __global__ void __launch_bounds__(256) k_color(SceneDev sc, FrameParams fp, Fram
     }
 }
 
-static int sm_count_pp() {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    return sms > 0 ? sms : 148;
-}
 
 void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {
     cudaMemsetAsync(fb.total_tests, 0, 4, st);
@@ -934,26 +928,17 @@ void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, 
     const int B = 256;
     cudaMemsetAsync(fb.cand_count, 0, 4, st);
     k_cull<<<(unsigned)((fp.N + B - 1) / B), B, 0, st>>>(sc, fp, fb);
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_sms();
     k_preprocess<<<sms * 6, B, 0, st>>>(sc, fp, fb, test_cap);
 }
 
 void launch_color(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, cudaStream_t st) {
     if (fp.N == 0) return;
-    k_color<<<sm_count_pp() * 8, 256, 0, st>>>(sc, fp, fb);
+    k_color<<<device_sms() * 8, 256, 0, st>>>(sc, fp, fb);
 }
 
 static int sm_count() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
+    return device_sms();
 }
 
 void launch_tiletest(const FrameParams& fp, FrameBufs fb, int64_t test_cap, uint64_t* keys, uint32_t* vals,

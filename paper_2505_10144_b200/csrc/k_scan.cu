@@ -152,13 +152,7 @@ void launch_scan(const uint32_t* in, uint32_t* out, uint32_t* total, const uint3
         cudaMemsetAsync(total, 0, 4, st);
         return;
     }
-    static int sms = 0;
-    if (!sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+    const int sms = device_sms();
     const int64_t tiles = (cap + kScanTile - 1) / kScanTile;
     cudaMemsetAsync(scratch, 0, (size_t)(tiles + 1) * 8, st);
     const int64_t grid = std::min<int64_t>(tiles, (int64_t)sms * 4);

@@ -258,16 +258,7 @@ __global__ void k_copy_pairs(const uint64_t* __restrict__ ks, const uint32_t* __
 
 size_t sort_status_words(int64_t cap) { return 2 * ((size_t)((cap + kSortTile - 1) / kSortTile + 1) * kRadix); }
 
-static int g_num_sms = 0;
-static int num_sms() {
-    if (!g_num_sms) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    }
-    return g_num_sms;
-}
+static int num_sms() { return device_sms(); }
 
 void launch_sort(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* vals_alt, const uint32_t* n_dev,
                  int64_t cap, int key_bits, SortScratch s, cudaStream_t st, bool hist_ready) {
@@ -280,11 +271,7 @@ void launch_sort(uint64_t* keys, uint32_t* vals, uint64_t* keys_alt, uint32_t* v
         cudaMemsetAsync(s.hist, 0, sizeof(uint32_t) * 8 * kRadix, st);
         k_sort_hist<<<sms * 2, kSortThreads, 0, st>>>(keys, n_dev, cap, passes, s.hist);
     }
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_onesweep, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(OnesweepSmem));
-        attr = true;
-    }
+    ensure_smem_attr((const void*)k_onesweep, (int)sizeof(OnesweepSmem));
     const unsigned grid = (unsigned)std::min<int64_t>(max_tiles, (int64_t)sms * 3);
     uint64_t *ka = keys, *kb = keys_alt;
     uint32_t *va = vals, *vb = vals_alt;

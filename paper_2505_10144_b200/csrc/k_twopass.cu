@@ -82,9 +82,7 @@ void launch_mask_half(const uint8_t* src, int W, int H, uint8_t* dst, int W2, in
 void launch_two_pass_combine(const TwoPassParams& tp, const float4* prgba, const float* pdepth, float* rgba,
                              float* depth, int64_t total, cudaStream_t st) {
     if (total == 0) return;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int sms = device_sms();
     const int64_t blocks = std::min<int64_t>((total + 255) / 256, (int64_t)sms * 16);
     k_two_pass_combine<<<(unsigned)blocks, 256, 0, st>>>(tp, prgba, pdepth, rgba, depth, total);
 }

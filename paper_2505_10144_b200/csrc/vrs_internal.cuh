@@ -11,6 +11,10 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <mutex>
+#include <set>
+#include <tuple>
+
 #include "../../include/vrs.h"
 
 namespace vrs {
@@ -96,6 +100,32 @@ struct FrameBufs {
     float* low_depth;        // low-res samples depth
     unsigned long long* stats;  // [8] device counters
 };
+
+// ----------------------------------------------------------------- device helpers (host side)
+// Dynamic shared-memory limit of a kernel, set once per (kernel, device, size):
+// the attribute is per device, and contexts on several devices may share a process.
+inline void ensure_smem_attr(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::set<std::tuple<const void*, int, int>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    if (done.insert(std::make_tuple(func, dev, bytes)).second)
+        cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+// SM count of the current device (cached per device).
+inline int device_sms() {
+    static int cache[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = n > 0 ? n : 148;
+    }
+    return cache[dev];
+}
 
 // ----------------------------------------------------------------- launchers
 // n_items_dev[0] = items, n_items_dev[1] = LowRes items (listed first)
