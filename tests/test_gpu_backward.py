@@ -78,3 +78,54 @@ def test_backward_rejects_foveated_frames(vrs):
     z = torch.zeros_like(rgba), torch.zeros_like(depth)
     with pytest.raises(vrs.vrs.VrsError):
         r.vrs_backward(rgba, depth, *z)
+
+
+@pytest.mark.parametrize("which", ["rgb_only", "alpha_only", "depth_only"])
+def test_backward_single_output_losses(vrs, oracle_mod, which):
+    """Each output channel group on its own (the colour, transmittance and
+    depth chains are separate code paths of k_blend_bwd)."""
+    scene = sg.random_scene(7, n=300, sh_degree=1)
+    cam = sg.look_camera((0, 0, 0), f=40.0, width=64, height=48)
+    r = vrs.Renderer(max_gaussians=scene.n, max_views=1, max_pairs=1 << 20, max_width=64, max_height=48,
+                     assign_tile=16)
+    r.upload(scene)
+    rgba, depth = r.render([cam])
+    rng = np.random.default_rng(11)
+    gr = rng.normal(size=(48, 64, 4))
+    gd = rng.normal(size=(48, 64)) * 0.1
+    if which == "rgb_only":
+        gr[..., 3] = 0.0
+        gd[:] = 0.0
+    elif which == "alpha_only":
+        gr[..., :3] = 0.0
+        gd[:] = 0.0
+    else:
+        gr[:] = 0.0
+    out = r.vrs_backward(rgba, depth, torch.tensor(gr.reshape(-1, 4), dtype=torch.float32, device="cuda"),
+                         torch.tensor(gd.reshape(-1), dtype=torch.float32, device="cuda"))
+    torch.cuda.synchronize()
+    o = oracle_mod.Oracle(scene).prepare([cam], assign_tile=16)
+    ref, _ = grad.gradients(scene, [cam], [o.blend_orders(0)], [gr], [gd])
+    for k in ("means", "quats", "log_scales", "logits", "sh"):
+        a = out[k].cpu().numpy().astype(np.float64).reshape(ref[k].shape)
+        scale = np.abs(ref[k]).max()
+        assert np.abs(a - ref[k]).max() <= REL * scale + 1e-7, (which, k)
+
+
+def test_backward_rejects_other_modes(vrs):
+    W, H = 64, 64
+    scene = sg.vr_room(9, 500, sh_degree=0)
+    cam = sg.look_camera((0, 0, 0), f=40.0, width=W, height=H)
+    for setup in ("ewa", "hier", "packed"):
+        r = vrs.Renderer(max_gaussians=scene.n, max_views=1, max_pairs=1 << 20, max_width=W, max_height=H,
+                         assign_tile=16, projection=1 if setup == "ewa" else 0)
+        r.upload(scene)
+        if setup == "hier":
+            r.vrs_set_resort_mode(1)
+        if setup == "packed":
+            r.vrs_set_output_format(1)
+        rgba, depth = r.render([cam])
+        f32 = (torch.zeros((W * H, 4), device="cuda"), torch.zeros(W * H, device="cuda"))
+        with pytest.raises(vrs.vrs.VrsError):
+            r.vrs_backward(*f32, *f32)
+        r.close()
