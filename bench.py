@@ -55,8 +55,9 @@ CONFIGS = {
                desc="large-FOV protocol (App. D) on the C2 scene: per eye, crop [W,2W)x[H,2H) of the 3W x 3H "
                     "render at the same pixel focal length vs the W x H render, Optimal Projection vs EWA"),
     "c8": dict(n=500_000, scale_mul=1.0, sh=3, fovea=True, T=32, masks=True, seed=2, resort=1,
-               desc="C2 workload with the hierarchical resort mode (SURVEY N2): K_B = 8 block queue per 4x4 "
-                    "sample block ahead of a K_P = 8 per-sample window; vs_flat compares with the K = 16 frame"),
+               desc="C2 workload with the hierarchical resort mode (SURVEY N2): K_B = 8 queue per 4x4 sample "
+                    "block, K_G = 4 queue per 2x2 group, K_P = 8 per-sample window; vs_flat compares with the "
+                    "K = 16 frame"),
     "c9": dict(n=500_000, scale_mul=1.0, sh=3, fovea=False, T=16, masks=False, seed=2,
                desc="training step (SURVEY N4): C2 scene, stereo 2x2064x2208 non-foveated (T_a = 16), forward "
                     "render + vrs_backward of synthetic gradient images to all raw parameters"),

@@ -210,8 +210,9 @@ VRS_API vrs_status vrs_render_views_two_pass(vrs_context* ctx, int32_t n_views, 
  * mode 0 (default): StopThePop per-sample window, K = 16;
  * mode 1: hierarchical -- per 4x4 sample block a queue of block_queue = 8
  * entries ordered by the block-centre depth (entries admitted when a sample
- * of the block passes the membership test) ahead of a per-sample window of
- * pixel_window = 8 ("hierarchical per-pixel resorting").
+ * of the block passes the membership test), then per 2x2 sample group a queue
+ * of 4 entries ordered by the group-centre depth, ahead of a per-sample window
+ * of pixel_window = 8 ("hierarchical per-pixel resorting").
  * 0 for a size selects the compiled value.  Takes effect from the next render.
  * Errors: VRS_E_INVALID_ARG (unknown mode, sizes other than the compiled ones,
  * mode 1 with the EWA projection). */

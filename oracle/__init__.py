@@ -45,7 +45,7 @@ class _View(C.Structure):
 class _Params(C.Structure):
     _fields_ = [("assign_tile", C.c_int32), ("window_k", C.c_int32), ("near_plane", C.c_float),
                 ("background", C.c_float * 3), ("threads", C.c_int32), ("projection", C.c_int32),
-                ("resort", C.c_int32), ("block_queue", C.c_int32)]
+                ("resort", C.c_int32), ("block_queue", C.c_int32), ("group_queue", C.c_int32)]
 
 
 _lib = None
@@ -86,7 +86,7 @@ def lib():
         L.orc_eq4_edge.argtypes = [vp, vp, vp, vp]
         L.orc_sample_depth.restype = C.c_float
         L.orc_sample_depth.argtypes = [vp, i32, i64, C.c_float, C.c_float]
-        L.orc_hier_core.argtypes = [i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_hier_core.argtypes = [i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]
         L.orc_blend_orders.restype = i64
         L.orc_blend_orders.argtypes = [vp, i32, vp, vp, i64]
         _lib = L
@@ -149,7 +149,7 @@ class Oracle:
             lib().orc_set_mask(self.h, slot, m.shape[1], m.shape[0], _p(m))
 
     def prepare(self, cams, foveas=None, assign_tile=16, window_k=16, near=0.2, background=(0, 0, 0),
-                threads=0, projection=0, resort=0, block_queue=8):
+                threads=0, projection=0, resort=0, block_queue=8, group_queue=0):
         foveas = foveas if foveas is not None else [None] * len(cams)
         arr = (_View * len(cams))(*[make_view(c, f) for c, f in zip(cams, foveas)])
         p = _Params()
@@ -157,7 +157,7 @@ class Oracle:
         p.background[:] = list(background)
         p.threads = threads
         p.projection = projection
-        p.resort, p.block_queue = resort, block_queue
+        p.resort, p.block_queue, p.group_queue = resort, block_queue, group_queue
         rc = lib().orc_prepare(self.h, len(cams), C.cast(arr, C.c_void_p), C.cast(C.pointer(p), C.c_void_p))
         if rc != 0:
             raise ValueError(f"orc_prepare rc={rc}")
@@ -268,13 +268,16 @@ def eq4_edge(Cc, p, d):
     return q, xh
 
 
-def hier_core(tau_b, g, member, tau, alpha, rgb, kb, kp):
-    """Pin H3 hook: the N2 two-level queue on a given block stream (n entries;
-    tau/alpha are n x 16).  Returns (out 16 x (r, g, b, a, depth), stats 16 x
-    (evals, contribs, overflow, term))."""
+def hier_core(tau_b, g, member, tau, alpha, rgb, kb, kp, kg=0, tau_g=None):
+    """Pin H3 hook: the N2 queue cascade on a given block stream (n entries;
+    tau/alpha are n x 16, tau_g n x 4 (default: tau_b for every group)).
+    Returns (out 16 x (r, g, b, a, depth), stats 16 x (evals, contribs, overflow, term))."""
     n = len(tau_b)
-    a = [np.ascontiguousarray(x, t) for x, t in ((tau_b, np.float32), (g, np.uint32), (member, np.uint32),
-                                                 (tau, np.float32), (alpha, np.float32), (rgb, np.float32))]
+    if tau_g is None:
+        tau_g = np.repeat(np.asarray(tau_b, np.float32)[:, None], 4, 1)
+    a = [np.ascontiguousarray(x, t) for x, t in ((tau_b, np.float32), (tau_g, np.float32), (g, np.uint32),
+                                                 (member, np.uint32), (tau, np.float32), (alpha, np.float32),
+                                                 (rgb, np.float32))]
     out, st = np.zeros((16, 5), np.float64), np.zeros((16, 4), np.int64)
-    lib().orc_hier_core(n, kb, kp, *[_p(x) for x in a], _p(out), _p(st))
+    lib().orc_hier_core(n, kb, kg, kp, *[_p(x) for x in a], _p(out), _p(st))
     return out, st

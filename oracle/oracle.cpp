@@ -758,6 +758,7 @@ struct HEnt { float tauB; uint32_t g; uint32_t mask; uint32_t idx; };
  * render_block_hier from the geometry, or given directly to the pin H3). */
 struct HIn {
     float tauB;           // block-centre depth (R4 form)
+    float tauG[4];        // 2x2-group-centre depths (R4 form), group q = (row / 2) * 2 + col / 2
     uint32_t g;           // Gaussian index (tie-break, R4)
     uint32_t member;      // bit s: sample s passes the membership test (R3)
     float tau[16], alpha[16];  // per-sample depth and alpha (R9), where member
@@ -766,7 +767,7 @@ struct HIn {
 
 /* The two-level queue mechanics of N2 on one block's stream (steps 1-4
  * above); valid[s] = sample s is in the image; dn[s] = |d| of its ray. */
-static void hier_core(const std::vector<HIn>& in, int KB, int KP, const bool* valid, const double* dn,
+static void hier_core(const std::vector<HIn>& in, int KB, int KG, int KP, const bool* valid, const double* dn,
                       const float* bg, Px* out, SampleStats* st) {
     const uint32_t n = (uint32_t)in.size();
     float T[16];
@@ -791,7 +792,7 @@ static void hier_core(const std::vector<HIn>& in, int KB, int KP, const bool* va
         T[s] = T[s] * (1.0f - w.alpha);
         if (T[s] < 1e-4f) { done[s] = true; stop[s] = pos; }
     };
-    auto release = [&](const HEnt& e, uint32_t pos) {
+    auto release_samples = [&](const HEnt& e, uint32_t pos) {
         const HIn& h = in[e.idx];
         for (int s = 0; s < 16; s++) {
             if (!((e.mask >> s) & 1u) || done[s]) continue;
@@ -806,6 +807,30 @@ static void hier_core(const std::vector<HIn>& in, int KB, int KP, const bool* va
                 WEnt m = win[s].front();
                 win[s].erase(win[s].begin());
                 blend(s, m, pos);
+            }
+        }
+    };
+    // 2x2 group level: a block release enters the queue of every group holding a
+    // not-terminated member sample (members restricted to the group), ordered by
+    // the group-centre depth; group overflow releases the minimum to its samples
+    std::vector<HEnt> QG[4];
+    auto release = [&](const HEnt& e, uint32_t pos) {
+        for (int q = 0; q < 4; q++) {
+            uint32_t gm = 0;
+            for (int s = 0; s < 16; s++) {
+                const int row = s >> 2, col = s & 3;
+                if (((row >> 1) * 2 + (col >> 1)) == q && ((e.mask >> s) & 1u) && !done[s]) gm |= 1u << s;
+            }
+            if (!gm) continue;
+            HEnt h{in[e.idx].tauG[q], e.g, gm, e.idx};
+            auto it = std::upper_bound(QG[q].begin(), QG[q].end(), h, [](const HEnt& a, const HEnt& c) {
+                return a.tauB < c.tauB || (a.tauB == c.tauB && a.g < c.g);
+            });
+            QG[q].insert(it, h);
+            if ((int)QG[q].size() > KG) {
+                HEnt m = QG[q].front();
+                QG[q].erase(QG[q].begin());
+                release_samples(m, pos);
             }
         }
     };
@@ -830,6 +855,8 @@ static void hier_core(const std::vector<HIn>& in, int KB, int KP, const bool* va
         }
     }
     for (const HEnt& h : Q) release(h, n ? n - 1 : 0);
+    for (int q = 0; q < 4; q++)
+        for (const HEnt& h : QG[q]) release_samples(h, n ? n - 1 : 0);
     for (int s = 0; s < 16; s++) {
         for (size_t k = 0; k < win[s].size() && !done[s]; k++) blend(s, win[s][k], n ? n - 1 : 0);
         if (valid[s]) {
@@ -846,7 +873,8 @@ static void hier_core(const std::vector<HIn>& in, int KB, int KP, const bool* va
 }
 
 static void render_block_hier(const Oracle& O, int view, int64_t gtile, const float* xs, const float* ys,
-                              const bool* valid, float xc, float yc, Px* out, SampleStats* st) {
+                              const bool* valid, float xc, float yc, const float* xgc, const float* ygc, Px* out,
+                              SampleStats* st) {
     const ViewState& vs = O.views[view];
     const orc_view& v = vs.v;
     const uint32_t b = O.ranges[2 * gtile], e = O.ranges[2 * gtile + 1];
@@ -866,6 +894,12 @@ static void render_block_hier(const Oracle& O, int view, int64_t gtile, const fl
         float den = quad3(sp.A, xB, yB, 1.0f);
         float dtb = std::fmaf(sp.bv[0], xB, std::fmaf(sp.bv[1], yB, sp.bv[2]));
         h.tauB = std::fmax(dtb / den, O.p.near_plane);  // tau_B (R4 form; NaN -> near)
+        for (int q = 0; q < 4; q++) {  // tau_G on the group-centre rays (same forms)
+            const float xq = (xgc[q] - v.cx) / v.fx, yq = (ygc[q] - v.cy) / v.fy;
+            const float dq = quad3(sp.A, xq, yq, 1.0f);
+            const float tq = std::fmaf(sp.bv[0], xq, std::fmaf(sp.bv[1], yq, sp.bv[2]));
+            h.tauG[q] = std::fmax(tq / dq, O.p.near_plane);
+        }
         h.member = 0;
         for (int c = 0; c < 3; c++) h.rgb[c] = sp.rgb[c];
         for (int s = 0; s < 16; s++) {
@@ -884,14 +918,14 @@ static void render_block_hier(const Oracle& O, int view, int64_t gtile, const fl
             h.alpha[s] = at.alpha;
         }
     }
-    hier_core(in, O.p.block_queue, O.p.window_k, valid, dn, O.p.background, out, st);
+    hier_core(in, O.p.block_queue, O.p.group_queue, O.p.window_k, valid, dn, O.p.background, out, st);
 }
 
 /* The 4x4 sample block containing full-rate sample (i, j) or LowRes group
  * (i, j) (pixel of the group origin) of coarse tile (tx, ty): sample points,
  * in-image flags and the block centre (mean of its 16 sample points). */
 static void hier_block(const ViewState& vs, int T, bool low, int i, int j, int* bx0, int* by0, float* xs,
-                       float* ys, bool* valid, float* xc, float* yc) {
+                       float* ys, bool* valid, float* xc, float* yc, float* xgc, float* ygc) {
     const int W = vs.v.width, H = vs.v.height;
     if (low) {  // blocks of 4x4 groups = 8x8 pixels, aligned inside the tile
         int x0 = (i / T) * T, y0 = (j / T) * T;
@@ -906,6 +940,10 @@ static void hier_block(const ViewState& vs, int T, bool low, int i, int j, int* 
         }
         *xc = (float)(*bx0 + 4);
         *yc = (float)(*by0 + 4);
+        for (int q = 0; q < 4; q++) {  // group q: samples (2(q&1).., 2(q>>1)..) -> centre 4 px further per step
+            xgc[q] = (float)(*bx0 + 4 * (q & 1) + 2);
+            ygc[q] = (float)(*by0 + 4 * (q >> 1) + 2);
+        }
     } else {
         *bx0 = i & ~3;
         *by0 = j & ~3;
@@ -917,6 +955,10 @@ static void hier_block(const ViewState& vs, int T, bool low, int i, int j, int* 
         }
         *xc = (float)(*bx0 + 2);
         *yc = (float)(*by0 + 2);
+        for (int q = 0; q < 4; q++) {
+            xgc[q] = (float)(*bx0 + 2 * (q & 1) + 1);
+            ygc[q] = (float)(*by0 + 2 * (q >> 1) + 1);
+        }
     }
 }
 
@@ -959,12 +1001,12 @@ static Px pixel_sample(FrameCtx& F, int i, int j, bool low) {
     if (it != F.memo.end()) return it->second;
     if (F.O->p.resort == 1) {  // the whole 4x4 block renders together (N2)
         int bx0, by0;
-        float bxs[16], bys[16], xc, yc;
+        float bxs[16], bys[16], xc, yc, xgc[4], ygc[4];
         bool valid[16];
-        hier_block(vs, T, low, i, j, &bx0, &by0, bxs, bys, valid, &xc, &yc);
+        hier_block(vs, T, low, i, j, &bx0, &by0, bxs, bys, valid, &xc, &yc, xgc, ygc);
         Px outs[16];
         SampleStats sts[16];
-        render_block_hier(*F.O, F.view, gt, bxs, bys, valid, xc, yc, outs, sts);
+        render_block_hier(*F.O, F.view, gt, bxs, bys, valid, xc, yc, xgc, ygc, outs, sts);
         for (int k = 0; k < 16; k++) {
             uint64_t kk = low ? ((1ull << 62) | ((uint64_t)(by0 + 2 * (k >> 2)) << 31) | (uint64_t)(bx0 + 2 * (k & 3)))
                               : (((uint64_t)(by0 + (k >> 2)) << 31) | (uint64_t)(bx0 + (k & 3)));
@@ -1261,12 +1303,12 @@ int orc_render(void* h, float* rgba, float* depth) {
                         for (int by = y0; by < std::min(y0 + T, He); by += span)
                             for (int bx = x0; bx < std::min(x0 + T, We); bx += span) {
                                 int bx0, by0;
-                                float bxs[16], bys[16], xc, yc;
+                                float bxs[16], bys[16], xc, yc, xgc[4], ygc[4];
                                 bool valid[16];
-                                hier_block(vs, T, low, bx, by, &bx0, &by0, bxs, bys, valid, &xc, &yc);
+                                hier_block(vs, T, low, bx, by, &bx0, &by0, bxs, bys, valid, &xc, &yc, xgc, ygc);
                                 Px outs[16];
                                 SampleStats bst[16];
-                                render_block_hier(O, v, gt, bxs, bys, valid, xc, yc, outs, bst);
+                                render_block_hier(O, v, gt, bxs, bys, valid, xc, yc, xgc, ygc, outs, bst);
                                 for (int k = 0; k < 16; k++) {
                                     int px = low ? bx0 + 2 * (k & 3) : bx0 + (k & 3);
                                     int py = low ? by0 + 2 * (k >> 2) : by0 + (k >> 2);
@@ -1491,13 +1533,15 @@ int64_t orc_blend_orders(void* h, int view, int32_t* counts, uint32_t* seq, int6
 }
 
 /* Pin H3 hook: the N2 queue mechanics on a given stream of n block entries
- * (tauB[n], g[n], member[n], tau[n*16], alpha[n*16], rgb[n*3]); all 16
+ * (tauB[n], tauG[n*4], g[n], member[n], tau[n*16], alpha[n*16], rgb[n*3]); all 16
  * samples in the image, |d| = 1; out = 16 x (r, g, b, a, depth). */
-int orc_hier_core(int64_t n, int kb, int kp, const float* tauB, const uint32_t* g, const uint32_t* member,
-                  const float* tau, const float* alpha, const float* rgb, double* out, int64_t* stats) {
+int orc_hier_core(int64_t n, int kb, int kg, int kp, const float* tauB, const float* tauG, const uint32_t* g,
+                  const uint32_t* member, const float* tau, const float* alpha, const float* rgb, double* out,
+                  int64_t* stats) {
     std::vector<HIn> in((size_t)n);
     for (int64_t i = 0; i < n; i++) {
         in[i].tauB = tauB[i];
+        for (int q = 0; q < 4; q++) in[i].tauG[q] = tauG[4 * i + q];
         in[i].g = g[i];
         in[i].member = member[i];
         for (int s = 0; s < 16; s++) {
@@ -1512,7 +1556,7 @@ int orc_hier_core(int64_t n, int kb, int kp, const float* tauB, const uint32_t* 
     const float bg[3] = {0.0f, 0.0f, 0.0f};
     Px px[16];
     SampleStats st[16];
-    hier_core(in, kb, kp, valid, dn, bg, px, st);
+    hier_core(in, kb, kg, kp, valid, dn, bg, px, st);
     for (int s = 0; s < 16; s++) {
         out[5 * s + 0] = px[s].r; out[5 * s + 1] = px[s].g; out[5 * s + 2] = px[s].b;
         out[5 * s + 3] = px[s].a; out[5 * s + 4] = px[s].d;

@@ -46,6 +46,7 @@ typedef struct {
                               (DESIGN "N2"): a block queue of block_queue entries per
                               4x4 sample block ahead of a per-sample window of window_k */
     int32_t block_queue;   /* K_B >= 0 (hierarchical mode only) */
+    int32_t group_queue;   /* K_G >= 0: per-2x2-group queue between the block queue and the windows */
 } orc_params;
 
 #define ORC_SPLAT_FLOATS 48
@@ -80,8 +81,9 @@ int64_t orc_sat_count(int tw, const uint32_t* sat, int x0, int y0, int x1, int y
 float orc_eq4_edge(const float* C, const float* p, const float* d, float* xhat);
 float orc_sample_depth(void* h, int view, int64_t g, float x, float y);
 int64_t orc_blend_orders(void* h, int view, int32_t* counts, uint32_t* seq, int64_t cap);
-int orc_hier_core(int64_t n, int kb, int kp, const float* tauB, const uint32_t* g, const uint32_t* member,
-                  const float* tau, const float* alpha, const float* rgb, double* out, int64_t* stats);
+int orc_hier_core(int64_t n, int kb, int kg, int kp, const float* tauB, const float* tauG, const uint32_t* g,
+                  const uint32_t* member, const float* tau, const float* alpha, const float* rgb, double* out,
+                  int64_t* stats);
 
 #ifdef __cplusplus
 }

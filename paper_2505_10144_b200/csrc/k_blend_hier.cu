@@ -33,6 +33,8 @@ constexpr int kHW = kHT / 32;
 constexpr int kHBatch = 80;       // staged records per batch
 constexpr int kHP = kHierWindow;  // per-sample window K_P
 constexpr int kHB = kHierQueue;   // block queue K_B (+1 slot for the incoming entry)
+constexpr int kHG = kHierGroup;   // 2x2 group queue K_G (the 4 lanes of a group hold one entry each)
+static_assert(kHG <= 4, "the group queue lives in the 4 lanes of a 2x2 group");
 static_assert(kHB + 1 <= 16, "the block queue lives in the 16 lanes of a half-warp");
 static_assert((kHP & (kHP - 1)) == 0, "ring needs a power-of-two window");
 
@@ -96,6 +98,18 @@ __global__ void __launch_bounds__(kHT, VRS_HIER_MINB) k_blend_hier(FrameParams f
         yc = (float)(oy + wy + 2);
     }
     const bool in_img = px < v.W && py < v.H;
+    // 2x2 group of this lane (lanes l0, l0|1, l0|8, l0|9), its rank inside it and its centre
+    const int grk = ((lane >> 3) & 1) * 2 + (lane & 1);
+    const unsigned glanes = 0x303u << (lane & ~9);
+    auto lane_of_g = [&](int r) { return (lane & ~9) | (r & 1) | ((r >> 1) << 3); };
+    float xgc, ygc;
+    if (low) {
+        xgc = (float)(x0 + 2 * (wx + 4 * hb) + 4 * ((lane & 3) >> 1) + 2);
+        ygc = (float)(y0 + 2 * wy + 4 * (ly >> 1) + 2);
+    } else {
+        xgc = (float)(ox + wx + 4 * hb + 2 * ((lane & 3) >> 1) + 1);
+        ygc = (float)(oy + wy + 2 * (ly >> 1) + 1);
+    }
     if (tid < kHW) {
         const int wwx = (tid & 1) * 8, wwy = (tid >> 1) * 4;
         float4 b;
@@ -112,6 +126,8 @@ __global__ void __launch_bounds__(kHT, VRS_HIER_MINB) k_blend_hier(FrameParams f
     const float y = (ys - v.cy) / v.fy;
     const float xB = (xc - v.cx) / v.fx;
     const float yB = (yc - v.cy) / v.fy;
+    const float xG = (xgc - v.cx) / v.fx;
+    const float yG = (ygc - v.cy) / v.fy;
     const float dn = sqrtf(fmaf(x, x, fmaf(y, y, 1.0f)));
     const uint32_t rb = fb.ranges[2 * (size_t)(v.tile_base + tile)];
     const uint32_t re = fb.ranges[2 * (size_t)(v.tile_base + tile) + 1];
@@ -134,6 +150,10 @@ __global__ void __launch_bounds__(kHT, VRS_HIER_MINB) k_blend_hier(FrameParams f
     unsigned long long qkey = ~0ull;
     uint32_t qmask = 0, qslot = 0;
     int qn = 0, fslot = 0;
+    // group queue: this lane's entry grk (valid when grk < gn), count (uniform per group)
+    unsigned long long gkey = ~0ull;
+    uint32_t gmask = 0;
+    int gn = 0;
 
     auto blend_one = [&](unsigned long long key, float a) {
         const float4* cp;
@@ -190,6 +210,78 @@ __global__ void __launch_bounds__(kHT, VRS_HIER_MINB) k_blend_hier(FrameParams f
         const float alpha = alpha_tau(num, ss, den, dtb, t5.y, tau);
         contribute(order_key(tau, __float_as_uint(t5.z), fp.near_plane), alpha, pos);
     };
+    // release of entry g to this lane's sample with the record read from global memory
+    // (a group-queue entry outlives its block-queue cache slot)
+    auto release_global = [&](const uint32_t g, const uint32_t pos) {
+        const float4* rp = recv + (size_t)g * kRecF4;
+        const float4 a0 = __ldg(rp + 0), a1 = __ldg(rp + 1), a2 = __ldg(rp + 2);
+        const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
+        const float ex = fmaf(a1.x, x, a1.y);
+        const float ey = fmaf(a1.z, x, fmaf(a1.w, y, a2.x));
+        const float cx = fmaf(a2.y, ex, a2.z * ey), cy = fmaf(a2.z, ex, a2.w * ey);
+        const float num = fmaf(ex, cx, ey * cy);
+        const float ss = s * s;
+        const float4 a3 = __ldg(rp + 3), a4 = __ldg(rp + 4), t5 = __ldg(rp + 5);
+        const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
+        const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, t5.x));
+        float tau;
+        const float alpha = alpha_tau(num, ss, den, dtb, t5.y, tau);
+        contribute(order_key(tau, g, fp.near_plane), alpha, pos);
+    };
+    // the 2x2 group level: a block release (key ek, member lanes em, cache slot es; valid per
+    // half) enters the queue of every group with a not-terminated member, ordered by the
+    // group-centre depth; a full group queue releases its minimum (possibly the new entry)
+    auto group_stage = [&](const bool valid, const unsigned long long ek, const uint32_t em, const int es,
+                           const uint32_t pos) {
+        const unsigned notdone = __ballot_sync(0xffffffffu, !done);
+        const uint32_t gm = valid ? (em & glanes & notdone) : 0u;
+        const bool ins = gm != 0u;
+        if (!__any_sync(0xffffffffu, ins)) return;
+        unsigned long long kg = ~0ull;
+        if (ins) {  // tau_G (R4 form, one IEEE division) from the entry's cached record
+            const float4* rc = S.cache[blk][es];
+            const float4 a3 = rc[3], a4 = rc[4], t5 = rc[5];
+            const float denG = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, xG, yG);
+            const float dtbG = fmaf(a4.z, xG, fmaf(a4.w, yG, t5.x));
+            const float tauG = fmaxf(__fdiv_rn(dtbG, denG), fp.near_plane);
+            kg = ((unsigned long long)__float_as_uint(tauG) << 32) | (uint32_t)ek;
+        }
+        const int pg = __popc(__ballot_sync(0xffffffffu, grk < gn && gkey < kg) & glanes);
+        const int su = lane_of_g(grk > 0 ? grk - 1 : 0), sd = lane_of_g(grk < 3 ? grk + 1 : 3);
+        const unsigned long long ku = __shfl_sync(0xffffffffu, gkey, su), kd = __shfl_sync(0xffffffffu, gkey, sd),
+                                 k0 = __shfl_sync(0xffffffffu, gkey, lane_of_g(0));
+        const uint32_t mu = __shfl_sync(0xffffffffu, gmask, su), md = __shfl_sync(0xffffffffu, gmask, sd),
+                       m0 = __shfl_sync(0xffffffffu, gmask, lane_of_g(0));
+        unsigned long long rk = 0;
+        uint32_t rm = 0;
+        if (ins) {
+            if (gn < kHG) {  // room: insert at pg
+                if (grk > pg) {
+                    gkey = ku;
+                    gmask = mu;
+                } else if (grk == pg) {
+                    gkey = kg;
+                    gmask = gm;
+                }
+                gn++;
+            } else if (pg == 0) {  // full, the new entry is the minimum: released at once
+                rk = kg;
+                rm = gm;
+            } else {  // full: release the minimum, the new entry takes rank pg - 1
+                rk = k0;
+                rm = m0;
+                if (grk < pg - 1) {
+                    gkey = kd;
+                    gmask = md;
+                } else if (grk == pg - 1) {
+                    gkey = kg;
+                    gmask = gm;
+                }
+            }
+        }
+        if (((rm >> lane) & 1u) && !done) release_global((uint32_t)rk, pos);
+        __syncwarp();
+    };
     // pop the minimum of each half whose flag is set; release it to its samples
     auto pop_release = [&](const bool pop, const uint32_t pos) {
         const unsigned long long ek = __shfl_sync(0xffffffffu, qkey, lane_of(0));
@@ -205,8 +297,11 @@ __global__ void __launch_bounds__(kHT, VRS_HIER_MINB) k_blend_hier(FrameParams f
             qslot = ns;
             qn--;
             fslot = es;
-            (void)ek;
-            if (((em >> lane) & 1u) && !done) release(es, pos);
+        }
+        if (kHG == 0) {
+            if (pop && ((em >> lane) & 1u) && !done) release(es, pos);
+        } else {
+            group_stage(pop, ek, em, es, pos);
         }
     };
 
@@ -288,6 +383,22 @@ __global__ void __launch_bounds__(kHT, VRS_HIER_MINB) k_blend_hier(FrameParams f
     }
     // stream end: the queues release in order, then the windows drain
     while (__any_sync(0xffffffffu, qn > 0)) pop_release(qn > 0, re - 1);
+    // then the group queues release in order
+    while (__any_sync(0xffffffffu, gn > 0)) {
+        const bool has = gn > 0;
+        const unsigned long long k0 = __shfl_sync(0xffffffffu, gkey, lane_of_g(0));
+        const uint32_t m0 = __shfl_sync(0xffffffffu, gmask, lane_of_g(0));
+        const int sd = lane_of_g(grk < 3 ? grk + 1 : 3);
+        const unsigned long long kd = __shfl_sync(0xffffffffu, gkey, sd);
+        const uint32_t md = __shfl_sync(0xffffffffu, gmask, sd);
+        if (has) {
+            gkey = (grk + 1 < gn) ? kd : ~0ull;
+            gmask = md;
+            gn--;
+            if (((m0 >> lane) & 1u) && !done) release_global((uint32_t)k0, re - 1);
+        }
+        __syncwarp();
+    }
 #pragma unroll 1
     for (int k = 0; k < kHP && !done; k++) {
         blend_one(WK(hk), WA(hk));

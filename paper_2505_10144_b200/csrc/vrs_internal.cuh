@@ -23,6 +23,7 @@ constexpr int kBlend = 256;        // threads per blend block
 constexpr int kWindow = 16;        // StopThePop per-sample resort window K
 constexpr int kHierQueue = 8;      // N2 hierarchical mode: block queue K_B per 4x4 sample block
 constexpr int kHierWindow = 8;     // N2 hierarchical mode: per-sample window K_P
+constexpr int kHierGroup = 4;      // N2 hierarchical mode: queue K_G per 2x2 sample group
 constexpr int kRecF4 = 8;          // float4 per projected-splat record (128 B)
 constexpr float kO7Margin = 1.001f;  // O7 keep threshold factor (DESIGN R7)
 constexpr float kTmin = 1e-4f;     // early termination (L11)

@@ -1,5 +1,6 @@
 """GPU parity of the N2 hierarchical resort mode (vrs_set_resort_mode(1):
-K_B = 8 block queue per 4x4 sample block, K_P = 8 per-sample window) against
+K_B = 8 block queue per 4x4 sample block, K_G = 4 queue per 2x2 group,
+K_P = 8 per-sample window) against
 the oracle's resort=1 mode (pinned by tests/test_hier_pins.py).  Bars as in
 test_gpu_parity.py: pair lists bit-exact (unchanged by the mode), RGB/A
 within 2e-3, depth within 1e-4 relative, workload counters equal (they count
@@ -17,6 +18,7 @@ pytestmark = pytest.mark.gpu
 RGB_TOL = 2e-3
 DEPTH_REL = 1e-4
 KB = KP = 8
+KG = 4
 COUNTERS = ("pairs", "samples", "evaluations", "contributions", "overflow_samples", "terminated_samples")
 
 
@@ -45,7 +47,7 @@ def _render(vrs, oracle_mod, scene, cams, fov=None, T=16, masks=None, max_pairs=
     rgba, depth = r.render(cams, fov)
     torch.cuda.synchronize()
     g = vrs.vrs.split_views(rgba.cpu().numpy(), depth.cpu().numpy(), cams)
-    o.prepare(cams, fov, assign_tile=T, window_k=KP, resort=1, block_queue=KB)
+    o.prepare(cams, fov, assign_tile=T, window_k=KP, resort=1, block_queue=KB, group_queue=KG)
     oi = o.render() if oracle_full else None
     return r, o, g, oi
 

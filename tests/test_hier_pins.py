@@ -135,3 +135,73 @@ def test_h4_invariants_and_determinism(oracle_mod):
         assert (da >= 0).all()
     st = o.stats()
     assert st["contributions"] > 0 and st["samples"] > 0
+
+
+# --------------------------------------------------------------------- the 2x2 group level (K_G > 0)
+
+def test_h3_hand_derived_group_level(oracle_mod):
+    """The H3 stream with a group queue of one between the block queue and the
+    windows: block releases e1, e2, e0 (tau_B = 3, 1, 2) enter every group's
+    queue ordered by tau_G = (2, 3, 1): e1 waits; e2 arrives -> e2 released;
+    e0 arrives -> e0 released; drain -> e1.  Samples (K_P = 1, tau = 1, 2, 3,
+    alpha 1/2) receive e2, e0, e1: e0 arrives -> blend e0 (T 1 -> 1/2); e1 ->
+    blend e1 (T -> 1/4); drain e2 (T -> 1/8): RGB = (1/2, 1/4, 1/8), A = 7/8,
+    depth = 1/2 + 2/4 + 3/8 = 11/8."""
+    n = 3
+    tau_b = np.array([3, 1, 2], np.float32)
+    tau_g = np.repeat(np.array([2, 3, 1], np.float32)[:, None], 4, 1)
+    g = np.array([10, 11, 12], np.uint32)
+    member = np.full(n, 0xFFFF, np.uint32)
+    tau = np.repeat(np.array([1, 2, 3], np.float32)[:, None], 16, 1)
+    alpha = np.full((n, 16), 0.5, np.float32)
+    rgb = np.eye(3, dtype=np.float32)
+    out, st = oracle_mod.hier_core(tau_b, g, member, tau, alpha, rgb, kb=3, kp=1, kg=1, tau_g=tau_g)
+    np.testing.assert_array_equal(out, np.tile([0.5, 0.25, 0.125, 0.875, 1.375], (16, 1)))
+    # a group whose samples are not members never sees the entry
+    member2 = member.copy()
+    member2[0] = 0xFFFF & ~np.uint32(0x0033)  # e0 misses group 0 (samples 0, 1, 4, 5)
+    out2, _ = oracle_mod.hier_core(tau_b, g, member2, tau, alpha, rgb, kb=3, kp=1, kg=1, tau_g=tau_g)
+    np.testing.assert_array_equal(out2[15], out[15])
+    assert not np.array_equal(out2[0], out[0])
+
+
+@pytest.mark.parametrize("seed", range(6))
+@pytest.mark.parametrize("kb,kg,kp", [(1, 1, 1), (2, 3, 4), (8, 4, 8), (0, 5, 3)])
+def test_h3_three_level_cascade_equals_one_queue(oracle_mod, seed, kb, kg, kp):
+    rng = np.random.default_rng(100 + seed)
+    n = 60
+    t = rng.permutation(np.arange(1, n + 1)).astype(np.float32) * 0.25
+    t[rng.integers(0, n, 5)] = t[0]
+    g = rng.permutation(1000)[:n].astype(np.uint32)
+    member = np.full(n, 0xFFFF, np.uint32)
+    tau = np.repeat(t[:, None], 16, 1)
+    alpha = rng.uniform(0.01, 0.3, (n, 16)).astype(np.float32)
+    rgb = rng.uniform(0, 1, (n, 3)).astype(np.float32)
+    a, sa = oracle_mod.hier_core(t, g, member, tau, alpha, rgb, kb=kb, kp=kp, kg=kg)
+    b, sb = oracle_mod.hier_core(t, g, member, tau, alpha, rgb, kb=0, kp=kb + kg + kp, kg=0)
+    np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.parametrize("seed", [0, 3])
+def test_h2_three_levels_unbounded_are_the_full_sort(oracle_mod, seed):
+    scene, cam = _c1(seed)
+    o = oracle_mod.Oracle(scene)
+    o.prepare([cam], assign_tile=16, window_k=1 << 20, resort=1, block_queue=1 << 20, group_queue=1 << 20)
+    (a, da), = o.render()
+    bf, bfd = o.bruteforce(0)
+    assert np.array_equal(a, bf) and np.array_equal(da, bfd)
+
+
+def test_h4_three_levels_foveated_invariants(oracle_mod):
+    W, H = 160, 128
+    scene = sg.vr_room(6, 20000, scale_mul=1.0, sh_degree=2)
+    cams = _stereo(W, H)
+    fov = [sg.Fovea((W / 2, H / 2), (W / 4, H / 4), 0.1)] * 2
+    o = oracle_mod.Oracle(scene)
+    outs = []
+    for threads in (1, 4):
+        o.prepare(cams, fov, assign_tile=32, window_k=8, resort=1, block_queue=8, group_queue=4, threads=threads)
+        outs.append(o.render())
+    for (a, da), (b, db) in zip(*outs):
+        assert np.array_equal(a, b) and np.array_equal(da, db)
+        assert (a[..., :3] >= 0).all() and (a[..., 3] >= 0).all() and (a[..., 3] <= 1).all()
