@@ -166,12 +166,23 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
 
 
-def cpu_baseline(scene, cams, fov, masks, T, budget_s=15.0):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def cpu_baseline(scene, cams, fov, masks, T, budget_s=15.0, threads=0):
     """The oracle as it stands on the host cores, on a bounded sample:
     full per-Gaussian stage + instantiation + sort + ranges for both eyes, then
-    a random sample of output pixels; frames/s extrapolated to the full frame."""
+    a random sample of output pixels; frames/s extrapolated to the full frame.
+    threads = 0: all cores."""
     import oracle
-    ncores = os.cpu_count() or 1
+    ncores = threads or os.cpu_count() or 1
     o = oracle.Oracle(scene)
     for k, m in masks.items():
         o.set_mask(k, m)
@@ -193,7 +204,7 @@ def cpu_baseline(scene, cams, fov, masks, T, budget_s=15.0):
         n = min(n * 2, 65536)
     frame_s = t_prep + t_pix * (total_px / done)
     return {"value": 1.0 / frame_s, "unit": "stereo frames/s" if len(cams) == 2 else "frames/s", "cores": ncores,
-            "kind": "oracle", "prep_s": t_prep,
+            "kind": "oracle", "prep_s": t_prep, "cpu_model": cpu_model(),
             "sample": f"full preprocess+pairs+sort+ranges of the frame ({t_prep:.2f}s) + {done} random output "
                       f"pixels ({t_pix:.2f}s) of {total_px}, extrapolated per pixel"}
 
@@ -620,7 +631,9 @@ def main():
         if cfg.get("resort"):
             line["vs_flat"] = compare_flat(r, render, cams, fov, rgba, depth, stream, counters)
         if not args.no_cpu_baseline and world == 1 and not two_pass and not cfg.get("resort"):
-            line["cpu_baseline"] = cpu_baseline(scene, cams, fov, masks, cfg["T"])
+            line["cpu_baseline"] = cpu_baseline(scene, cams, fov, masks, cfg["T"], budget_s=12.0)
+            one = cpu_baseline(scene, cams, fov, masks, cfg["T"], budget_s=8.0, threads=1)
+            line["cpu_baseline"]["single_thread"] = {k: one[k] for k in ("value", "cores", "sample")}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
