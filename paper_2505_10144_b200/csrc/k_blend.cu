@@ -1,21 +1,25 @@
-// Steps 5-7: per-tile ranges, the single foveated blend launch
+// Steps 5-7: per-tile ranges, the single-pass foveated blend
 // and the periphery compose.
 //
-// Blend: ONE launch whose 256-thread blocks
+// Blend: one kernel whose 256-thread blocks
 // are either 16x16 full-rate items (HighRes / Hybrid subtiles of a
 // 32x32 coarse tile, or 16x16 tiles when assigning at 16), or 32x32 LowRes
 // tiles where every thread renders one 2x2 pixel group sampled at the group
-// centre.  All items stream their coarse tile's sorted list in key
-// order.  Batches of 256 splat records are staged in shared memory;
-// each warp covers an 8x4 block of samples and skips, warp-uniformly, every
-// splat whose conservative pixel footprint misses the block (the
-// hierarchical culling of P:431 — it never changes results, only work).  Each
-// sample runs the StopThePop per-pixel resort: a
-// K = 16 entry window ordered by (tau, g) kept in shared memory (a per-thread
-// ring buffer, bank-conflict free), popping the nearest entry on overflow and
-// blending front to back (Eq.2 with product transmittance), terminating once
-// T < 1e-4 (checked after blending).  Hybrid pixels blend their value with
-// the 2x2 group average via warp shuffles.
+// centre.  The frame launches it twice -- the full-rate items on a
+// side stream beside the LowRes items, so that the compose can follow the
+// LowRes launch (vrs_api.cu) -- but every item is the same code.  All items
+// stream their coarse tile's sorted list in key order.  Batches of 80
+// splat records are staged in shared memory; each warp covers an 8x4 block
+// of samples and skips, warp-uniformly, every splat whose conservative pixel
+// footprint misses the block (the hierarchical culling of P:431 -- it never
+// changes results, only work), evaluating two list entries' memberships per
+// iteration.  Each sample runs the StopThePop per-pixel resort (P:274-275,
+// P:306-309): a K = 16 entry window ordered by (tau, g) kept in shared memory
+// (a per-thread ring buffer, bank-conflict free), popping the nearest entry on
+// overflow and blending front to back (Eq.2 with product transmittance),
+// terminating once T < 1e-4 (checked after blending).  Hybrid pixels blend
+// their value with the 2x2 group average via warp shuffles.
+// Final pixels are written in the context's output format (store_pixel).
 #include "k_blend_common.cuh"
 
 namespace vrs {
