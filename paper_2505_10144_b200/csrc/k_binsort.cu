@@ -13,10 +13,11 @@
 //                 the counters zeroed for the next frame;
 //   k_ovf_bucket  overflow pairs -> their per-tile overflow slots;
 //   k_tile_sort   one warp per tile of <= 256 pairs (keys in registers,
-//                 bitonic by shuffles), one block per larger tile (shared-
-//                 memory bitonic; beyond the shared-memory capacity sorted
-//                 chunks merged along merge paths in global memory), written
-//                 back as (tile << 32 | depth, g) at the tile's range.
+//                 bitonic by shuffles), one block per larger tile (chunks of
+//                 <= 2048 keys sorted as 256-key register runs merged along
+//                 merge paths in shared memory; chunks merged along merge
+//                 paths in global memory), written back as
+//                 (tile << 32 | depth, g) at the tile's range.
 // (depth bits, g) is unique inside a tile, so the result does not depend on
 // the atomic arrival order and equals the stable (tile, depth) sort of the
 // (view, g, tile) emission order -- the oracle's order, bit for bit.

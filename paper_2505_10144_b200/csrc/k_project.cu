@@ -4,9 +4,13 @@
 // plane, StopThePop per-tile depth at the back-projected maximum
 // point and visibility-mask skipping through the SAT.
 //
-// One thread per Gaussian; the Gaussian's attributes are read once and
-// projected for every view of the frame (stereo fusion of the per-Gaussian
-// stage, the "fusion of stereo rendering passes" of P:735).
+// k_cull: one thread per Gaussian tests every view's frustum cone (the
+// Gaussian's attributes read once for all views: stereo fusion of the
+// per-Gaussian stage, the "fusion of stereo rendering passes" of P:735) and
+// appends the surviving (view, Gaussian) candidates; k_preprocess projects
+// them and expands their footprint tiles into the test list; k_color
+// evaluates the SH colour of the visible ones (on the side stream);
+// k_tiletest_direct runs one Eq.4 test per (Gaussian, tile) candidate.
 #include <algorithm>
 
 #include "vrs_internal.cuh"

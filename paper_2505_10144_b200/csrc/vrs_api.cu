@@ -1,7 +1,10 @@
 // C ABI of libvrs (include/vrs.h): context, scene upload (host activation),
 // visibility masks, per-eye static setup cache and the per-frame launch
-// sequence preprocess -> scan -> duplicate -> onesweep sort -> ranges ->
-// blend -> compose, all enqueued on the caller's stream with no host sync.
+// sequence cull -> preprocess (+ fused candidate scan) -> tile tests into
+// per-tile buckets -> binned sort (+ ranges) -> blend -> compose, enqueued on
+// the caller's stream (with a fork/join onto the context's side stream for
+// the SH colour and the full-rate blend items) with no host sync; the
+// two-pass baseline, the output formats, the resort modes and the backward.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
