@@ -27,6 +27,9 @@ namespace vrs {
 
 namespace {
 constexpr int kScanT = 1024;
+#ifndef VRS_TS_GRID
+#define VRS_TS_GRID 4
+#endif
 #ifndef VRS_SCAN_PER
 #define VRS_SCAN_PER 12
 #endif
@@ -439,7 +442,7 @@ void launch_binsort(FrameBufs fb, int64_t cap, int64_t n_tiles, BinScratch b, cu
                                       b.list_n, b.max_tiles, min(b.cap_smem, (uint32_t)kWarpSortMax));
     k_ovf_bucket<<<sms * 2, 256, 0, st>>>(fb.keys_alt, fb.vals_alt, b.rank, b.ovf_count, (uint32_t)cap, b.ovf_off,
                                           b.obucket);
-    k_tile_sort<<<sms * 4, kBinT, sort_smem, st>>>(b.list, b.list_n, b.max_tiles, fb.ranges, b.tbucket, b.ovf_off,
+    k_tile_sort<<<sms * VRS_TS_GRID, kBinT, sort_smem, st>>>(b.list, b.list_n, b.max_tiles, fb.ranges, b.tbucket, b.ovf_off,
                                                      b.obucket, fb.keys_alt, fb.keys, fb.vals, b.cap_smem,
                                                      b.list_n + 2);
 }

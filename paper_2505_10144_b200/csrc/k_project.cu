@@ -544,6 +544,12 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
 #ifndef VRS_PP_MINB
 #define VRS_PP_MINB 3
 #endif
+#ifndef VRS_PP_GRID
+#define VRS_PP_GRID 6
+#endif
+#ifndef VRS_TT_GRID
+#define VRS_TT_GRID 8
+#endif
 #ifndef VRS_TT_HOIST
 #define VRS_TT_HOIST 0
 #endif
@@ -933,7 +939,7 @@ void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, 
     cudaMemsetAsync(fb.cand_count, 0, 4, st);
     k_cull<<<(unsigned)((fp.N + B - 1) / B), B, 0, st>>>(sc, fp, fb);
     const int sms = device_sms();
-    k_preprocess<<<sms * 6, B, 0, st>>>(sc, fp, fb, test_cap);
+    k_preprocess<<<sms * VRS_PP_GRID, B, 0, st>>>(sc, fp, fb, test_cap);
 }
 
 void launch_color(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, cudaStream_t st) {
@@ -957,7 +963,7 @@ void launch_tiletest_direct(const FrameParams& fp, FrameBufs fb, int64_t test_ca
                             cudaStream_t st) {
     cudaMemsetAsync(bs.ovf_count, 0, 4, st);
     if ((int64_t)fp.n_views * fp.N == 0) return;
-    k_tiletest_direct<<<sm_count() * 8, kTT, 0, st>>>(fp, fb, test_cap, bs);
+    k_tiletest_direct<<<sm_count() * VRS_TT_GRID, kTT, 0, st>>>(fp, fb, test_cap, bs);
 }
 
 void launch_counts(const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {
