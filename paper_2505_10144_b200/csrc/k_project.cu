@@ -660,7 +660,10 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
 // preprocess wrote (sidk: splat | rect-local tile index << 32).
 namespace {
 constexpr int kTT = 256;           // threads per block
-constexpr int kTTItems = 2;        // candidates per thread (independent: ILP)
+#ifndef VRS_TT_ITEMS
+#define VRS_TT_ITEMS 2
+#endif
+constexpr int kTTItems = VRS_TT_ITEMS;  // candidates per thread (independent: ILP)
 constexpr int kTTTile = kTT * kTTItems;
 }  // namespace
 
