@@ -45,7 +45,8 @@ class _View(C.Structure):
 class _Params(C.Structure):
     _fields_ = [("assign_tile", C.c_int32), ("window_k", C.c_int32), ("near_plane", C.c_float),
                 ("background", C.c_float * 3), ("threads", C.c_int32), ("projection", C.c_int32),
-                ("resort", C.c_int32), ("block_queue", C.c_int32), ("group_queue", C.c_int32)]
+                ("resort", C.c_int32), ("block_queue", C.c_int32), ("group_queue", C.c_int32),
+                ("sort_mode", C.c_int32), ("tau_unclamped", C.c_int32)]
 
 
 _lib = None
@@ -87,6 +88,7 @@ def lib():
         L.orc_sample_depth.restype = C.c_float
         L.orc_sample_depth.argtypes = [vp, i32, i64, C.c_float, C.c_float]
         L.orc_hier_core.argtypes = [i64, i32, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_sample_alpha_tau.argtypes = [i64, vp, vp, vp, vp, vp, C.c_float, vp, vp]
         L.orc_blend_orders.restype = i64
         L.orc_blend_orders.argtypes = [vp, i32, vp, vp, i64]
         _lib = L
@@ -149,7 +151,7 @@ class Oracle:
             lib().orc_set_mask(self.h, slot, m.shape[1], m.shape[0], _p(m))
 
     def prepare(self, cams, foveas=None, assign_tile=16, window_k=16, near=0.2, background=(0, 0, 0),
-                threads=0, projection=0, resort=0, block_queue=8, group_queue=0):
+                threads=0, projection=0, resort=0, block_queue=8, group_queue=0, sort_mode=0, tau_unclamped=0):
         foveas = foveas if foveas is not None else [None] * len(cams)
         arr = (_View * len(cams))(*[make_view(c, f) for c, f in zip(cams, foveas)])
         p = _Params()
@@ -158,6 +160,7 @@ class Oracle:
         p.threads = threads
         p.projection = projection
         p.resort, p.block_queue, p.group_queue = resort, block_queue, group_queue
+        p.sort_mode, p.tau_unclamped = sort_mode, tau_unclamped
         rc = lib().orc_prepare(self.h, len(cams), C.cast(arr, C.c_void_p), C.cast(C.pointer(p), C.c_void_p))
         if rc != 0:
             raise ValueError(f"orc_prepare rc={rc}")
@@ -266,6 +269,16 @@ def eq4_edge(Cc, p, d):
     xh = np.zeros(2, np.float32)
     q = lib().orc_eq4_edge(_p(Cc), _p(p), _p(d), _p(xh))
     return q, xh
+
+
+def sample_alpha_tau(num, ss, den, dtb, sigma, near=0.2):
+    """Pin hook: the contract's per-sample alpha and tau (DESIGN R9) on float32 arrays."""
+    a = [np.ascontiguousarray(np.broadcast_to(np.asarray(x, np.float32), np.shape(num))) for x in
+         (num, ss, den, dtb, sigma)]
+    n = a[0].size
+    alpha, tau = np.zeros(n, np.float32), np.zeros(n, np.float32)
+    lib().orc_sample_alpha_tau(n, *[_p(x) for x in a], near, _p(alpha), _p(tau))
+    return alpha.reshape(np.shape(num)), tau.reshape(np.shape(num))
 
 
 def hier_core(tau_b, g, member, tau, alpha, rgb, kb, kp, kg=0, tau_g=None):

@@ -15,9 +15,10 @@
  * other, std::stable_sort for the global sort, plain loops for the rest;
  * threads only across independent output samples.
  *
- * Parity unpinned (contract choices): the off-axis value
- * of the pixel-mapped dilation (L5), the hybrid/periphery reconstruction
- * details (L12, L13, L17).
+ * Every function is pinned (tests/test_oracle_pins*.py):
+ * the readings of DESIGN.md (L5 dilation, L12/L13/L17 periphery, R4 tau
+ * clamp) are contract choices, and the oracle's implementation of each is
+ * checked against closed forms, limits or an independent reconstruction.
  */
 #include "oracle.h"
 
@@ -558,6 +559,16 @@ static float tile_depth(const Splat& sp, const float d[3], float near_plane) {
     return (t > near_plane) ? t : near_plane;
 }
 
+/* Global-sort baselines (N3): one depth per (view, Gaussian)
+ * for every tile -- Mini-Splatting (z): the view-space z of mu (the 3DGS sort
+ * order, "given by the z-coordinate of mu in view-space");
+ * Mini-Splatting (Dist): |mu - o| = sqrt(mu_c . mu_c).  Both
+ * exceed near (O1 culls mu_c.z <= near, and |mu_c| >= mu_c.z). */
+static float global_depth(const Splat& sp, int mode) {
+    if (mode == 1) return sp.muc[2];
+    return std::sqrt(dot3(sp.muc, sp.muc));
+}
+
 static inline uint32_t fbits(float f) {
     uint32_t u;
     std::memcpy(&u, &f, 4);
@@ -669,7 +680,12 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
     const float x = (xs - v.cx) / v.fx, y = (ys - v.cy) / v.fy;
     const float dray[3] = {x, y, 1.0f};
     const double dn = std::sqrt((double)x * x + (double)y * y + 1.0);
-    const int K = O.p.window_k;
+    // global-sort baselines (N3) have no per-sample window: every contribution
+    // is blended in list order (K = 0: insert, then pop the same entry)
+    const bool global = O.p.sort_mode != 0;
+    const int K = global ? 0 : O.p.window_k;
+    // tau clamp at near (R4) unless the pin hook asks for the unclamped reading
+    const float tau_floor = O.p.tau_unclamped ? -INFINITY : O.p.near_plane;
     uint32_t b = O.ranges[2 * gtile], e = O.ranges[2 * gtile + 1];
     std::vector<WEnt> win;
     float T = 1.0f;  // transmittance: binary32 product (exact decision, R9)
@@ -694,7 +710,7 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
             if (!(q <= sp.qcut)) continue;
             at = sample_alpha_tau_ewa(q, quad3(sp.A, x, y, 1.0f),
                                       std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2])), sp.sigma,
-                                      O.p.near_plane);
+                                      tau_floor);
         } else {
             float s = std::fmaf(sp.u[0], x, std::fmaf(sp.u[1], y, sp.u[2]));
             if (!(s > 0.0f)) continue;
@@ -703,7 +719,7 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
             if (!(num <= sp.qcut * ss)) continue;  // alpha < 1/255, division-free (R3)
             float den = quad3(sp.A, x, y, 1.0f);
             float dtb = std::fmaf(sp.bv[0], x, std::fmaf(sp.bv[1], y, sp.bv[2]));
-            at = sample_alpha_tau(num, ss, den, dtb, sp.sigma, O.p.near_plane);  // P:254, L10, R9
+            at = sample_alpha_tau(num, ss, den, dtb, sp.sigma, tau_floor);  // P:254, L10, R9
         }
         float alpha = at.alpha;
         float tau = at.tau;  // depth of max density along this pixel's ray (O10)
@@ -714,7 +730,7 @@ static Px render_sample(const Oracle& O, int view, int64_t gtile, float xs, floa
         });
         win.insert(pos, ent);
         if ((int)win.size() > K) {
-            overflowed = true;
+            overflowed = !global;
             WEnt m = win.front();
             win.erase(win.begin());
             blend(m);
@@ -1131,6 +1147,7 @@ int orc_prepare(void* h, int n_views, const orc_view* views, const orc_params* p
     O.p = *p;
     if (O.p.assign_tile != 16 && O.p.assign_tile != 32) return 1;
     if (O.p.projection != 0 && O.p.projection != 1) return 4;
+    if (O.p.sort_mode < 0 || O.p.sort_mode > 2 || (O.p.sort_mode != 0 && O.p.resort != 0)) return 5;
     O.views.assign(n_views, ViewState());
     O.ntiles = 0;
     for (int v = 0; v < n_views; v++) {
@@ -1175,7 +1192,8 @@ int orc_prepare(void* h, int n_views, const orc_view* views, const orc_params* p
         for (int64_t g = 0; g < N; g++) {
             for_kept_tiles(O, vs, vs.splats[g], [&](int tx, int ty, const float* dh) {
                 uint64_t tile = (uint64_t)(vs.tile_base + (int64_t)ty * vs.tw + tx);
-                float td = tile_depth(vs.splats[g], dh, O.p.near_plane);
+                float td = O.p.sort_mode == 0 ? tile_depth(vs.splats[g], dh, O.p.near_plane)
+                                              : global_depth(vs.splats[g], O.p.sort_mode);
                 O.keys_unsorted[off] = (tile << 32) | fbits(td);
                 O.vals_unsorted[off] = (uint32_t)g;
                 off++;
@@ -1432,9 +1450,17 @@ int orc_render_bruteforce(void* h, int view, float* rgba, float* depth) {
                 }
                 all.push_back(WEnt{at.tau, (uint32_t)g, at.alpha});
             }
-            std::stable_sort(all.begin(), all.end(), [](const WEnt& a, const WEnt& c) {
-                return a.tau < c.tau || (a.tau == c.tau && a.g < c.g);
-            });
+            if (O.p.sort_mode == 0) {
+                std::stable_sort(all.begin(), all.end(), [](const WEnt& a, const WEnt& c) {
+                    return a.tau < c.tau || (a.tau == c.tau && a.g < c.g);
+                });
+            } else {  // global-sort baselines: one depth per Gaussian, ties by g
+                std::stable_sort(all.begin(), all.end(), [&](const WEnt& a, const WEnt& c) {
+                    float ka = global_depth(vs.splats[a.g], O.p.sort_mode);
+                    float kc = global_depth(vs.splats[c.g], O.p.sort_mode);
+                    return ka < kc || (ka == kc && a.g < c.g);
+                });
+            }
             float T = 1.0f;
             double C[3] = {0, 0, 0}, D = 0.0;
             for (const WEnt& w : all) {
@@ -1568,6 +1594,16 @@ int orc_hier_core(int64_t n, int kb, int kg, int kp, const float* tauB, const fl
 
 /* Per-sample depth tau (O10) of Gaussian g at image point (x, y) (pixel
  * coordinates), for the ray-march pin P5. */
+/* Pin hook: the contract's per-sample alpha and tau (DESIGN R9) on given inputs. */
+void orc_sample_alpha_tau(int64_t n, const float* num, const float* ss, const float* den, const float* dtb,
+                          const float* sigma, float near_plane, float* alpha, float* tau) {
+    for (int64_t i = 0; i < n; i++) {
+        SampleAT at = sample_alpha_tau(num[i], ss[i], den[i], dtb[i], sigma[i], near_plane);
+        alpha[i] = at.alpha;
+        tau[i] = at.tau;
+    }
+}
+
 float orc_sample_depth(void* h, int view, int64_t g, float xs, float ys) {
     Oracle& O = *(Oracle*)h;
     const ViewState& vs = O.views[view];

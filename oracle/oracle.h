@@ -47,6 +47,12 @@ typedef struct {
                               4x4 sample block ahead of a per-sample window of window_k */
     int32_t block_queue;   /* K_B >= 0 (hierarchical mode only) */
     int32_t group_queue;   /* K_G >= 0: per-2x2-group queue between the block queue and the windows */
+    int32_t sort_mode;     /* 0 = StopThePop (per-tile key depth + per-sample window);
+                              1 = global sort by view-space z of mu, blended in list order
+                              (Mini-Splatting (z)); 2 = global sort by |mu - o|,
+                              blended in list order (Mini-Splatting (Dist)) */
+    int32_t tau_unclamped; /* pin hook (DESIGN R4): 1 = per-sample tau NOT clamped at the near plane
+                              (flat window mode only); 0 = the contract's clamp */
 } orc_params;
 
 #define ORC_SPLAT_FLOATS 48
@@ -81,6 +87,8 @@ int64_t orc_sat_count(int tw, const uint32_t* sat, int x0, int y0, int x1, int y
 float orc_eq4_edge(const float* C, const float* p, const float* d, float* xhat);
 float orc_sample_depth(void* h, int view, int64_t g, float x, float y);
 int64_t orc_blend_orders(void* h, int view, int32_t* counts, uint32_t* seq, int64_t cap);
+void orc_sample_alpha_tau(int64_t n, const float* num, const float* ss, const float* den, const float* dtb,
+                          const float* sigma, float near_plane, float* alpha, float* tau);
 int orc_hier_core(int64_t n, int kb, int kg, int kp, const float* tauB, const float* tauG, const uint32_t* g,
                   const uint32_t* member, const float* tau, const float* alpha, const float* rgb, double* out,
                   int64_t* stats);

@@ -212,10 +212,8 @@ def test_pair_counts_equal_bruteforce_enumeration(oracle_mod):
                 for tx in range(6):
                     if vis[ty, tx] and o.tile_test(0, g, tx * 16, ty * 16, min(tx * 16 + 16, 96), ty * 16 + 16)["keep"] == 1:
                         c += 1
-        else:
-            # culled splats: never contribute anywhere (dense check on the full image)
-            X = (np.arange(96)[None, :] + 0.5 - cam.cx) / cam.fx
-            Y = (np.arange(80)[:, None] + 0.5 - cam.cy) / cam.fy
+        # (culled splats: count 0; that they reach q <= q_cut nowhere in the image is
+        # test_oracle_pins_r2.py::test_cone_culled_splats_never_reach_qcut)
         assert counts[g] == c, g
     k, v = o.pairs()
     tiles = (k >> np.uint64(32)).astype(np.int64)
