@@ -241,7 +241,8 @@ VRS_API vrs_status vrs_debug_tile_info(vrs_context* ctx, int32_t view, int32_t* 
 
 /* Largest tile (in pairs) the binned sort sorts in shared memory; larger
  * tiles are sorted in chunks of that size and merged in global memory.  A
- * power of two in [64, 4096] (default 4096); lowering it only exercises the
+ * power of two in [64, 4096] (default 2048: 256-key register runs merged in
+ * shared memory; 4096 takes a one-block bitonic sort); lowering it only exercises the
  * merge path (results are identical).  Applies from the next frame. */
 VRS_API vrs_status vrs_debug_set_sort_smem_cap(vrs_context* ctx, int32_t cap);
 

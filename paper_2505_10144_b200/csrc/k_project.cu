@@ -665,6 +665,7 @@ constexpr int kTT = 256;           // threads per block
 #endif
 constexpr int kTTItems = VRS_TT_ITEMS;  // candidates per thread (independent: ILP)
 constexpr int kTTTile = kTT * kTTItems;
+static_assert(kTT / 32 * kTTItems <= 32, "k_tiletest's single-warp scan covers at most 32 warp-slots");
 }  // namespace
 
 __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const FrameBufs& fb, unsigned long long sk,
@@ -782,7 +783,7 @@ __global__ void __launch_bounds__(kTT, VRS_TT_MINB) k_tiletest(FrameParams fp, F
         }
         __syncthreads();
         if (warp == 0) {
-            constexpr int nw = kTT / 32 * kTTItems;  // 16 warp-slots
+            constexpr int nw = kTT / 32 * kTTItems;  // warp-slots (<= 32, static_assert above)
             const uint32_t c = (lane < nw) ? s_wc[lane] : 0u;
             uint32_t inc = c;
 #pragma unroll

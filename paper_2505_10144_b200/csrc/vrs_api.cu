@@ -91,6 +91,7 @@ struct vrs_context {
     // last frame
     FrameParams fp{};
     bool have_frame = false;
+    bool last_two_pass = false;                      // last frame = internal 2n-view two-pass frame
     cudaStream_t last_stream = nullptr;
     int64_t last_items = 0, last_tiles = 0;
     int32_t last_cls[4] = {0, 0, 0, 0};
@@ -334,6 +335,8 @@ vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_degree, 
         CK(cudaMemcpy(ctx->d_raw, rawv.data(), sizeof(float4) * 2 * nk, cudaMemcpyHostToDevice));
     }
     ctx->N = nk;
+    ctx->have_frame = false;  // the last frame's records refer to the old scene
+    ctx->last_items = 0;
     ctx->deg = sh_degree;
     ctx->sh_chunks = chunks;
     ctx->uploaded = true;
@@ -597,6 +600,7 @@ static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* ca
     CK(cudaGetLastError());
     ctx->fp = fp;
     ctx->have_frame = true;
+    ctx->last_two_pass = false;
     ctx->last_stream = st;
     ctx->last_items = total_items;
     return VRS_OK;
@@ -737,6 +741,7 @@ vrs_status vrs_render_views_two_pass(vrs_context* ctx, int32_t n_views, const vr
                                ctx->d_tp_depth, st, VRS_OUT_F32);
     ctx->internal_masks = false;
     if (s != VRS_OK) return s;
+    ctx->last_two_pass = true;  // the frame state is the internal 2n-view frame: no backward on it
     tp.out_fmt = ctx->out_fmt;
     launch_two_pass_combine(tp, ctx->d_tp_rgba, ctx->d_tp_depth, rgba, depth, out_off, st);
     CK(cudaGetLastError());
@@ -821,7 +826,7 @@ vrs_status vrs_backward(vrs_context* ctx, const float* rgba, const float* depth,
         !grad_logits || !grad_sh)
         return fail(ctx, VRS_E_INVALID_ARG, "null pointer");
     const FrameParams& fp = ctx->fp;
-    if (fp.ewa || fp.resort != 0 || fp.out_fmt != VRS_OUT_F32 || ctx->internal_masks)
+    if (fp.ewa || fp.resort != 0 || fp.out_fmt != VRS_OUT_F32 || ctx->last_two_pass)
         return fail(ctx, VRS_E_STATE, "backward needs a frame rendered with the Optimal Projection, the K = 16 "
                                       "window and F32 outputs by vrs_render_views");
     for (int i = 0; i < fp.n_views; i++)

@@ -198,6 +198,12 @@ class Renderer:
         for t in (rgba, depth, grad_rgba, grad_depth):
             if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
                 raise ValueError("backward tensors must be contiguous float32 CUDA tensors")
+            if t.device.index != self.device:
+                raise ValueError(f"backward tensors must live on cuda:{self.device}, got {t.device}")
+        if self._views is not None:  # (after a two-pass frame the C ABI rejects the call itself)
+            px = sum(c.width * c.height for c in self._views)
+            self._check_buffers(px, rgba, depth, fmt=0)
+            self._check_buffers(px, grad_rgba, grad_depth, fmt=0)
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
         sp = stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
@@ -218,6 +224,30 @@ class Renderer:
 
     def vrs_set_instrumentation(self, counters=0, timing=0, no_cull=0):
         self._check(lib().vrs_set_instrumentation(self.h, int(counters) | (int(no_cull) << 8), int(timing)))
+
+    def _check_buffers(self, px, rgba, depth, fmt=None, host=False):
+        """Validate caller buffers before they reach the C ABI: element counts for px
+        pixels, dtypes of the output format, contiguity, and (device buffers) the
+        context's device -- a mismatched buffer raises here instead of becoming an
+        out-of-bounds device access."""
+        import torch
+        fmt = getattr(self, "out_fmt", 0) if fmt is None else fmt
+        want_r, want_d = (torch.uint8, torch.float16) if fmt == 1 else (torch.float32, torch.float32)
+        np_r, np_d = (np.uint8, np.float16) if fmt == 1 else (np.float32, np.float32)
+        for t, n, wt, wn, name in ((rgba, 4 * px, want_r, np_r, "rgba"), (depth, px, want_d, np_d, "depth")):
+            if isinstance(t, np.ndarray):
+                if not host:
+                    raise ValueError(f"{name}: a device tensor is required")
+                if t.dtype != wn or t.size != n or not t.flags["C_CONTIGUOUS"]:
+                    raise ValueError(f"{name}: need {n} contiguous {np.dtype(wn).name}, got {t.size} {t.dtype}")
+                continue
+            if t.dtype != wt or t.numel() != n or not t.is_contiguous():
+                raise ValueError(f"{name}: need {n} contiguous {wt}, got {t.numel()} {t.dtype}")
+            if host:
+                if t.is_cuda:
+                    raise ValueError(f"{name}: a host buffer is required")
+            elif not t.is_cuda or t.device.index != self.device:
+                raise ValueError(f"{name}: must live on cuda:{self.device}, got {t.device}")
 
     def _views_structs(self, cams, foveas):
         carr = (vrs_camera * len(cams))(*[make_camera(c) for c in cams])
@@ -244,6 +274,7 @@ class Renderer:
         import torch
         if rgba is None or depth is None:
             rgba, depth = self.alloc_outputs(cams)
+        self._check_buffers(sum(c.width * c.height for c in cams), rgba, depth)
         carr, farr = self._views_structs(cams, foveas)
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
@@ -262,6 +293,7 @@ class Renderer:
         import torch
         if rgba is None or depth is None:
             rgba, depth = self.alloc_outputs(cams)
+        self._check_buffers(sum(c.width * c.height for c in cams), rgba, depth)
         carr, farr = self._views_structs(cams, foveas)
         if stream is None:
             stream = torch.cuda.current_stream(self.device)
@@ -282,6 +314,7 @@ class Renderer:
             packed = getattr(self, "out_fmt", 0) == 1
             rgba_host = np.empty((px, 4), np.uint8 if packed else np.float32)
             depth_host = np.empty(px, np.float16 if packed else np.float32)
+        self._check_buffers(px, rgba_host, depth_host, host=True)
         rp = rgba_host.data_ptr() if hasattr(rgba_host, "data_ptr") else rgba_host.ctypes.data
         dp = depth_host.data_ptr() if hasattr(depth_host, "data_ptr") else depth_host.ctypes.data
         carr, farr = self._views_structs(cams, foveas)

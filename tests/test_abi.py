@@ -101,3 +101,30 @@ def test_product_has_no_oracle_dependency():
             if f.endswith((".py", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "oracle.h" not in txt and "liboracle" not in txt, f
+
+
+def test_binding_validates_buffers_before_the_abi(vrsmod):
+    """the binding rejects mismatched output buffers (element count,
+    dtype of the output format, device) before calling into libvrs."""
+    import numpy as np
+    import torch
+
+    class Fake:
+        device = 0
+        out_fmt = 0
+
+    chk = vrsmod.Renderer._check_buffers
+    px = 16
+    # CPU tensors are not device buffers
+    with pytest.raises(ValueError, match="cuda"):
+        chk(Fake(), px, torch.zeros((px, 4)), torch.zeros(px))
+    # wrong element count / dtype (host path, where CPU buffers are right)
+    with pytest.raises(ValueError, match="need 64"):
+        chk(Fake(), px, torch.zeros((px - 1, 4)), torch.zeros(px), host=True)
+    with pytest.raises(ValueError, match="float16"):
+        f = Fake()
+        f.out_fmt = 1
+        chk(f, px, torch.zeros((px, 4), dtype=torch.uint8), torch.zeros(px), host=True)
+    chk(Fake(), px, np.zeros((px, 4), np.float32), np.zeros(px, np.float32), host=True)
+    with pytest.raises(ValueError, match="device tensor"):
+        chk(Fake(), px, np.zeros((px, 4), np.float32), np.zeros(px, np.float32))

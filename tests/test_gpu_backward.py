@@ -129,3 +129,21 @@ def test_backward_rejects_other_modes(vrs):
         with pytest.raises(vrs.vrs.VrsError):
             r.vrs_backward(*f32, *f32)
         r.close()
+    # the two-pass baseline's frame state is its internal 2n-view frame
+    r = vrs.Renderer(max_gaussians=scene.n, max_views=2, max_pairs=1 << 20, max_width=W, max_height=H,
+                     assign_tile=32)
+    r.upload(scene)
+    r.render_two_pass([cam], [sg.Fovea((32, 32), (16, 16), 0.1)])
+    f32 = (torch.zeros((W * H, 4), device="cuda"), torch.zeros(W * H, device="cuda"))
+    with pytest.raises(vrs.vrs.VrsError):
+        r.vrs_backward(*f32, *f32)
+    # a new upload invalidates the last frame (its records refer to the old scene)
+    r2 = vrs.Renderer(max_gaussians=scene.n, max_views=1, max_pairs=1 << 20, max_width=W, max_height=H,
+                      assign_tile=16)
+    r2.upload(scene)
+    rgba, depth = r2.render([cam])
+    r2.upload(sg.vr_room(10, 300, sh_degree=0))
+    with pytest.raises(vrs.vrs.VrsError):
+        r2.vrs_backward(rgba, depth, *f32)
+    r.close()
+    r2.close()
