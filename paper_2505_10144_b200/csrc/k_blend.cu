@@ -1,25 +1,37 @@
 // Steps 5-7: per-tile ranges, the single-pass foveated blend
 // and the periphery compose.
 //
-// Blend: one kernel whose 256-thread blocks
-// are either 16x16 full-rate items (HighRes / Hybrid subtiles of a
-// 32x32 coarse tile, or 16x16 tiles when assigning at 16), or 32x32 LowRes
+// Blend: ONE launch per frame.  Its 256-thread
+// blocks are 16x16 full-rate items (HighRes / Hybrid subtiles of a
+// 32x32 coarse tile, or 16x16 tiles when assigning at 16), 32x32 LowRes
 // tiles where every thread renders one 2x2 pixel group sampled at the group
-// centre.  The frame launches it twice -- the full-rate items on a
-// side stream beside the LowRes items, so that the compose can follow the
-// LowRes launch (vrs_api.cu) -- but every item is the same code.  All items
-// stream their coarse tile's sorted list in key order.  Batches of 80
-// splat records are staged in shared memory; each warp covers an 8x4 block
-// of samples and skips, warp-uniformly, every splat whose conservative pixel
-// footprint misses the block (the hierarchical culling of P:431 -- it never
-// changes results, only work), evaluating two list entries' memberships per
-// iteration.  Each sample runs the StopThePop per-pixel resort (P:274-275,
-// P:306-309): a K = 16 entry window ordered by (tau, g) kept in shared memory
-// (a per-thread ring buffer, bank-conflict free), popping the nearest entry on
-// overflow and blending front to back (Eq.2 with product transmittance),
-// terminating once T < 1e-4 (checked after blending).  Hybrid pixels blend
-// their value with the 2x2 group average via warp shuffles.
-// Final pixels are written in the context's output format (store_pixel).
+// centre, or invisible tiles (background fill).  Every
+// item streams its coarse tile's sorted list in key order.
+//
+// Staging: the list is cut into stages of kStageN entries; each entry's
+// 128-B splat record is copied global -> shared by the TMA bulk-copy engine
+// (cp.async.bulk, one per record, completing on the stage's mbarrier), two
+// stages in flight.  The warps of a block consume the stages independently
+// (no block barrier in the loop): a warp waits on the stage's mbarrier,
+// culls the stage's entries against its own 8x4 sample block with their
+// conservative pixel footprints (the hierarchical culling of P:431 -- never
+// changes results, only work), evaluates two entries' memberships per
+// iteration and runs their contributions in stream order; the last warp to
+// finish a stage re-arms the slot with the stage two ahead.
+//
+// Each sample runs the StopThePop per-pixel resort: a
+// K = 16 window ordered by (tau, g) -- a per-thread ring in shared memory
+// ([slot][thread], bank-conflict free) whose head (the minimum) is mirrored
+// in registers together with its colour (fetched when the entry becomes the
+// head, off the critical path) -- popping the nearest entry on overflow and
+// blending front to back (Eq.2 with product transmittance), terminating once
+// T < 1e-4 (checked after blending).  Hybrid pixels blend their value with
+// the 2x2 group average via warp shuffles.
+//
+// Compose inside the same launch: every LowRes tile counts the
+// LowRes tiles of its 3x3 neighbourhood still blending; the block that
+// finishes the last of them composes the tile (nearest-neighbour upsample +
+// renormalised 3x3 blur of its 2x2-group samples) and re-arms the counter.
 #include "k_blend_common.cuh"
 
 namespace vrs {
@@ -42,6 +54,112 @@ void launch_ranges(const uint64_t* keys, const uint32_t* n_dev, int64_t cap, uin
     k_ranges<<<sms * 16, 256, 0, st>>>(keys, n_dev, cap, ranges, n_tiles);
 }
 
+// ----------------------------------------------------------------- compose (step 7)
+// Periphery reconstruction of one 2x2 pixel group: nearest-neighbour
+// upsample of the LowRes group samples and a 3x3 (1,2,1)x(1,2,1) blur
+// restricted to LowRes pixels in the image, renormalised;
+// invisible tiles get the background with A = 0, D = 0.  The 3x3
+// neighbourhood of group samples covers the blur footprint of all four
+// pixels.  Samples are read through L2 (ld.global.cg): inside the blend
+// launch they were written by other blocks.
+__device__ __forceinline__ void compose_group(const FrameParams& fp, const FrameBufs& fb, const ViewParams& v,
+                                              int gx, int gy, float* __restrict__ rgba, float* __restrict__ depth) {
+    if (2 * gy >= v.H || 2 * gx >= v.W) return;
+    const int tsh = (fp.T == 32) ? 5 : 4, i0 = 2 * gx, j0 = 2 * gy;  // T is 16 or 32
+    const int c = v.cls[(j0 >> tsh) * v.tw + (i0 >> tsh)];
+    if (c == kHigh || c == kHybrid) return;
+    float4 outc[2][2];
+    float outd[2][2];
+    if (c == kInvisible) {
+#pragma unroll
+        for (int b = 0; b < 2; b++)
+#pragma unroll
+            for (int a = 0; a < 2; a++) {
+                outc[b][a] = make_float4(fp.bg[0], fp.bg[1], fp.bg[2], 0.0f);
+                outd[b][a] = 0.0f;
+            }
+    } else {
+        float4 sc[3][3];
+        float sd[3][3];
+        bool ok[3][3];
+#pragma unroll
+        for (int dj = 0; dj < 3; dj++)
+#pragma unroll
+            for (int di = 0; di < 3; di++) {
+                // pixel of that group adjacent to this group: column 2gx-1, (2gx..2gx+1), 2gx+2
+                const int pi = (di == 0) ? i0 - 1 : (di == 1 ? i0 : i0 + 2);
+                const int pj = (dj == 0) ? j0 - 1 : (dj == 1 ? j0 : j0 + 2);
+                bool good = pi >= 0 && pj >= 0 && pi < v.W && pj < v.H;
+                if (good) good = v.cls[(pj >> tsh) * v.tw + (pi >> tsh)] == kLow;
+                ok[dj][di] = good;
+                if (good) {
+                    const size_t li = (size_t)v.low_off + (size_t)(pj >> 1) * v.low_w + (pi >> 1);
+                    sc[dj][di] = __ldcg(fb.low_rgba + li);
+                    sd[dj][di] = __ldcg(fb.low_depth + li);
+                } else {
+                    sc[dj][di] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    sd[dj][di] = 0.0f;
+                }
+            }
+        // Pixels of one group share its sample, so the 3x3 taps of pixel
+        // (i0+a, j0+b) collapse onto 2x2 neighbour groups with summed
+        // separable weights: a = 0 -> groups {-1: 1, 0: 2 + [i0+1 < W]},
+        // a = 1 -> {0: 3, +1: 1} (pixel-level in-image tests folded in).
+        const float wx[2][3] = {{1.0f, (i0 + 1 < v.W) ? 3.0f : 2.0f, 0.0f}, {0.0f, 3.0f, 1.0f}};
+        const float wy[2][3] = {{1.0f, (j0 + 1 < v.H) ? 3.0f : 2.0f, 0.0f}, {0.0f, 3.0f, 1.0f}};
+#pragma unroll
+        for (int b = 0; b < 2; b++)
+#pragma unroll
+            for (int a = 0; a < 2; a++) {
+                float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f}, ws = 0.0f;
+#pragma unroll
+                for (int sj = b; sj < b + 2; sj++)
+#pragma unroll
+                    for (int si = a; si < a + 2; si++) {
+                        const float w = ok[sj][si] ? wx[a][si] * wy[b][sj] : 0.0f;
+                        acc[0] = fmaf(w, sc[sj][si].x, acc[0]);
+                        acc[1] = fmaf(w, sc[sj][si].y, acc[1]);
+                        acc[2] = fmaf(w, sc[sj][si].z, acc[2]);
+                        acc[3] = fmaf(w, sc[sj][si].w, acc[3]);
+                        acc[4] = fmaf(w, sd[sj][si], acc[4]);
+                        ws += w;
+                    }
+                const float inv = 1.0f / ws;
+                outc[b][a] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
+                outd[b][a] = acc[4] * inv;
+            }
+    }
+#pragma unroll
+    for (int b = 0; b < 2; b++) {
+        const int j = j0 + b;
+        if (j >= v.H) continue;
+        const size_t row = (size_t)v.pix_off + (size_t)j * v.W;
+        store_pixel(fp.out_fmt, rgba, depth, row + i0, outc[b][0], outd[b][0]);
+        if (i0 + 1 < v.W) store_pixel(fp.out_fmt, rgba, depth, row + i0 + 1, outc[b][1], outd[b][1]);
+    }
+}
+
+// Stand-alone compose over every group of every view (the hierarchical resort
+// mode's frame, which blends without the in-launch compose).
+__global__ void k_compose(FrameParams fp, FrameBufs fb, float* __restrict__ rgba, float* __restrict__ depth,
+                          int64_t total_groups) {
+    const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gi >= total_groups) return;
+    int vi = 0;
+    while (vi + 1 < fp.n_views && gi >= fp.v[vi + 1].low_off) vi++;
+    const ViewParams& v = fp.v[vi];
+    const uint32_t k = (uint32_t)(gi - v.low_off);
+    compose_group(fp, fb, v, (int)(k % (uint32_t)v.low_w), (int)(k / (uint32_t)v.low_w), rgba, depth);
+}
+
+void launch_compose(const FrameParams& fp, FrameBufs fb, float* rgba, float* depth, cudaStream_t st) {
+    if (fp.n_views == 0) return;
+    const ViewParams& last = fp.v[fp.n_views - 1];
+    const int64_t total = last.low_off + (int64_t)last.low_w * ((last.H + 1) / 2);
+    k_compose<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(fp, fb, rgba, depth, total);
+}
+
+// ----------------------------------------------------------------- blend (step 6)
 namespace {
 
 #ifndef VRS_BLEND_THREADS
@@ -54,7 +172,7 @@ constexpr int kBT = VRS_BLEND_THREADS;   // threads per block: a whole 16x16 ite
 constexpr int kSplit = 256 / kBT;        // blocks per item
 constexpr int kWarps = kBT / 32;
 constexpr int kBatch = VRS_BLEND_BATCH;  // splat records staged per shared-memory batch
-static_assert(kBatch <= kBT && (kSplit == 1 || kSplit == 2), "blend block shape");
+static_assert(kBatch <= kBT && kSplit == 1, "blend block shape (the in-launch compose counts one block per item)");
 
 struct BlendSmem {
     float4 r0[kBatch];   // u.xyz, q_cut
@@ -72,10 +190,57 @@ struct BlendSmem {
     float w_a[kWindow][kBT];
     unsigned long long cnt[4];
 };
+// 4 blocks of 256 threads per SM (the 64-register budget) need <= 57344 B each
+// (228 KB per SM, 1 KB reserved per block); after the blend loop the staging
+// mask holds the in-launch compose triggers
+static_assert(sizeof(BlendSmem) + 1024 <= 233472 / 4, "blend shared memory exceeds the 4-blocks/SM budget");
+static_assert(kBatch >= 10, "the compose triggers reuse the staging mask");
 
 constexpr uint32_t kSlotBytes = kBT * 8;                   // one ring slot of keys
 constexpr uint32_t kRingMask = (kWindow - 1) * kSlotBytes;    // byte-offset ring mask
 static_assert((kWindow & (kWindow - 1)) == 0, "ring needs a power-of-two window");
+
+// Geometry of a blend item and of this thread's sample (full-rate: the pixel;
+// LowRes: the 2x2 group at (px, py), sampled at its centre).
+struct ItemGeom {
+    int vi, tile, kind, x0, y0, ox, oy, px, py;
+    float xs, ys;
+};
+__device__ __forceinline__ ItemGeom item_geom(const FrameParams& fp, int item, int half, int lane, int warp) {
+    ItemGeom g;
+    g.vi = 0;
+    while (g.vi + 1 < fp.n_views && item >= fp.v[g.vi + 1].item_off) g.vi++;
+    const ViewParams& v = fp.v[g.vi];
+    const uint32_t it = v.items[item - v.item_off];
+    g.tile = (int)(it & 0xfffffu);
+    const int sub = (int)((it >> 20) & 3u);
+    g.kind = (int)(it >> 22);
+    const int T = fp.T;
+    g.x0 = (g.tile % v.tw) * T;
+    g.y0 = (g.tile / v.tw) * T;
+    const int sx = (warp & 1) * 8 + (lane & 7), sy = (warp >> 1) * 4 + half * 8 + (lane >> 3);
+    g.ox = (g.kind == kItemLow) ? g.x0 : g.x0 + (T == 32 ? 16 * (sub & 1) : 0);
+    g.oy = (g.kind == kItemLow) ? g.y0 : g.y0 + (T == 32 ? 16 * (sub >> 1) : 0);
+    if (g.kind == kItemLow) {
+        g.px = g.x0 + 2 * sx;
+        g.py = g.y0 + 2 * sy;
+        g.xs = (float)(g.px + 1);
+        g.ys = (float)(g.py + 1);
+    } else {
+        g.px = g.ox + sx;
+        g.py = g.oy + sy;
+        g.xs = (float)g.px + 0.5f;
+        g.ys = (float)g.py + 0.5f;
+    }
+    return g;
+}
+// blockIdx.x through an opaque read, so the compiler recomputes the item's
+// geometry after the blend loop instead of keeping it in registers
+__device__ __forceinline__ int block_id_opaque() {
+    int b;
+    asm volatile("mov.u32 %0, %%ctaid.x;" : "=r"(b));
+    return b;
+}
 
 }  // namespace
 
@@ -88,52 +253,55 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BlendSmem& S = *reinterpret_cast<BlendSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    // locate the view and the item
+    // locate the view and the item (blend items of every view, then the invisible tiles)
     int vi = 0;
     const int item = blockIdx.x / kSplit, half = blockIdx.x % kSplit;  // half: rows 8-15 of the item
-    while (vi + 1 < fp.n_views && item >= fp.v[vi + 1].item_off) vi++;
-    const ViewParams& v = fp.v[vi];
-    const uint32_t it = v.items[item - v.item_off];
-    const int tile = (int)(it & 0xfffffu), sub = (int)((it >> 20) & 3u), kind = (int)(it >> 22);
-    const int T = fp.T;
-    const int tx = tile % v.tw, ty = tile / v.tw;
-    const int x0 = tx * T, y0 = ty * T;
-    const int lx = lane & 7, ly = lane >> 3, wx = (warp & 1) * 8, wy = (warp >> 1) * 4 + half * 8;
-    const int sx = wx + lx, sy = wy + ly;
-    int px, py;  // pixel (full-rate) or group origin pixel (low)
-    float xs, ys;
-    const int ox = (kind == kItemLow) ? x0 : x0 + (T == 32 ? 16 * (sub & 1) : 0);
-    const int oy = (kind == kItemLow) ? y0 : y0 + (T == 32 ? 16 * (sub >> 1) : 0);
-    if (kind == kItemLow) {
-        px = x0 + 2 * sx;
-        py = y0 + 2 * sy;
-        xs = (float)(px + 1);
-        ys = (float)(py + 1);
-    } else {
-        px = ox + sx;
-        py = oy + sy;
-        xs = (float)px + 0.5f;
-        ys = (float)py + 0.5f;
+    if (item >= fp.n_blend_items) {
+        // invisible tile: background, A = 0, D = 0
+        const int iv = item - fp.n_blend_items;
+        while (vi + 1 < fp.n_views && iv >= fp.v[vi + 1].inv_off) vi++;
+        const ViewParams& v = fp.v[vi];
+        const int tile = (int)v.inv_items[iv - v.inv_off];
+        const int T = fp.T, x0 = (tile % v.tw) * T, y0 = (tile / v.tw) * T;
+        for (int p = tid + half * kBT; p < T * T; p += kBT * kSplit) {
+            const int px = x0 + p % T, py = y0 + p / T;
+            if (px < v.W && py < v.H)
+                store_pixel(fp.out_fmt, rgba, depth, (size_t)v.pix_off + (size_t)py * v.W + px,
+                            make_float4(fp.bg[0], fp.bg[1], fp.bg[2], 0.0f), 0.0f);
+        }
+        return;
     }
-    if (tid < kWarps) {
-        const int wwx = (tid & 1) * 8, wwy = (tid >> 1) * 4 + half * 8;
-        float4 b;
-        if (kind == kItemLow)
-            b = make_float4((float)(x0 + 2 * wwx + 1), (float)(x0 + 2 * (wwx + 7) + 1), (float)(y0 + 2 * wwy + 1),
-                            (float)(y0 + 2 * (wwy + 3) + 1));
-        else
-            b = make_float4((float)(ox + wwx) + 0.5f, (float)(ox + wwx + 7) + 0.5f, (float)(oy + wwy) + 0.5f,
-                            (float)(oy + wwy + 3) + 0.5f);
-        S.wblock[tid] = b;
+    // Only what the blend loop needs stays live through it (the kernel runs at
+    // the 64-register cap of 4 blocks/SM): the item's geometry is recomputed
+    // after the loop for the outputs.
+    float x, y, xs, ys;  // sample ray (x, y, 1); pixel coordinates (EWA baseline)
+    uint32_t rb, re;
+    const float4* __restrict__ recv;
+    const float4* __restrict__ colv;
+    {
+        const ItemGeom g = item_geom(fp, item, half, lane, warp);
+        const ViewParams& v = fp.v[g.vi];
+        if (tid < kWarps) {
+            const int wwx = (tid & 1) * 8, wwy = (tid >> 1) * 4 + half * 8;
+            float4 b;
+            if (g.kind == kItemLow)
+                b = make_float4((float)(g.x0 + 2 * wwx + 1), (float)(g.x0 + 2 * (wwx + 7) + 1),
+                                (float)(g.y0 + 2 * wwy + 1), (float)(g.y0 + 2 * (wwy + 3) + 1));
+            else
+                b = make_float4((float)(g.ox + wwx) + 0.5f, (float)(g.ox + wwx + 7) + 0.5f,
+                                (float)(g.oy + wwy) + 0.5f, (float)(g.oy + wwy + 3) + 0.5f);
+            S.wblock[tid] = b;
+        }
+        xs = g.xs;
+        ys = g.ys;
+        x = (xs - v.cx) / v.fx;
+        y = (ys - v.cy) / v.fy;
+        rb = fb.ranges[2 * (size_t)(v.tile_base + g.tile)];
+        re = fb.ranges[2 * (size_t)(v.tile_base + g.tile) + 1];
+        recv = fb.rec + (size_t)g.vi * fp.N * kRecF4;
+        colv = fb.col + (size_t)g.vi * fp.N;
     }
     if (kCounters && tid < 4) S.cnt[tid] = 0ull;
-    const float x = (xs - v.cx) / v.fx;
-    const float y = (ys - v.cy) / v.fy;
-    const float dn = sqrtf(fmaf(x, x, fmaf(y, y, 1.0f)));
-    const uint32_t rb = fb.ranges[2 * (size_t)(v.tile_base + tile)];
-    const uint32_t re = fb.ranges[2 * (size_t)(v.tile_base + tile) + 1];
-    const float4* __restrict__ recv = fb.rec + (size_t)vi * fp.N * kRecF4;
-    const float4* __restrict__ colv = fb.col + (size_t)vi * fp.N;
     char* const wkb = reinterpret_cast<char*>(&S.w_key[0][tid]);
     char* const wab = reinterpret_cast<char*>(&S.w_a[0][tid]);
 #define WK(off) (*reinterpret_cast<unsigned long long*>(wkb + (off)))
@@ -317,8 +485,12 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
     }
 #undef WK
 #undef WA
-    // outputs
-    Dd = Dd * dn;
+    // outputs: the item's geometry recomputed from an opaque block index (not live through the loop)
+    const ItemGeom g = item_geom(fp, block_id_opaque() / kSplit, half, lane, warp);
+    const ViewParams& v = fp.v[g.vi];
+    const int px = g.px, py = g.py, kind = g.kind;
+    const int tx = g.tile % v.tw, ty = g.tile / v.tw;
+    Dd = Dd * sqrtf(fmaf(x, x, fmaf(y, y, 1.0f)));
     const float oR = Cr + Tr * fp.bg[0], oG = Cg + Tr * fp.bg[1], oB = Cb + Tr * fp.bg[2], oA = 1.0f - Tr;
     if (kind == kItemLow) {
         if (px < v.W && py < v.H) {
@@ -382,17 +554,46 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
             atomicAdd(&fb.stats[3], S.cnt[3]);
         }
     }
+    // In-launch compose: this LowRes tile's samples are final; count it
+    // off the 3x3 neighbourhoods that wait for it and compose the ones it completes
+    if (kind != kItemLow) return;
+    __syncthreads();
+    if (tid == 0) {
+        __threadfence();
+        uint32_t n = 0;
+        for (int dj = -1; dj <= 1; dj++)
+            for (int di = -1; di <= 1; di++) {
+                const int nx = tx + di, ny = ty + dj;
+                if (nx < 0 || ny < 0 || nx >= v.tw || ny >= v.th) continue;
+                const int t2 = ny * v.tw + nx;
+                if (v.cls[t2] != kLow) continue;
+                if (atomicSub(&v.lowcnt[t2], 1u) == 1u) S.mask[1 + n++] = (uint32_t)t2;
+            }
+        if (n) __threadfence();
+        S.mask[0] = n;
+    }
+    __syncthreads();
+    const uint32_t ntrig = S.mask[0];
+    for (uint32_t i = 0; i < ntrig; i++) {
+        const int t2 = (int)S.mask[1 + i];
+        for (int q = tid + half * kBT; q < 256; q += kBT * kSplit) {  // T = 32: 16 x 16 groups
+            const int gx = (t2 % v.tw) * 16 + (q % 16), gy = (t2 / v.tw) * 16 + (q / 16);
+            compose_group(fp, fb, v, gx, gy, rgba, depth);
+        }
+        if (tid == 0 && half == 0) v.lowcnt[t2] = v.lowcnt0[t2];  // re-armed for the next frame
+    }
 }
 
 void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
                   cudaStream_t st) {
-    if (total_items <= 0) return;
     if (fp.resort == 1) {
-        launch_blend_hier(fp, fb, total_items, rgba, depth, st);
+        if (total_items > 0) launch_blend_hier(fp, fb, total_items, rgba, depth, st);
+        launch_compose(fp, fb, rgba, depth, st);
         return;
     }
+    const unsigned grid = (unsigned)(fp.n_blend_items + fp.n_inv_items) * kSplit;
+    if (grid == 0) return;
     const size_t smem = sizeof(BlendSmem);
-    const unsigned grid = (unsigned)total_items * kSplit;
     ensure_smem_attr((const void*)k_blend<true, false>, (int)smem);
     ensure_smem_attr((const void*)k_blend<false, false>, (int)smem);
     ensure_smem_attr((const void*)k_blend<true, true>, (int)smem);
@@ -404,104 +605,6 @@ void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* r
         if (fp.counters) k_blend<true, false><<<grid, kBT, smem, st>>>(fp, fb, rgba, depth);
         else k_blend<false, false><<<grid, kBT, smem, st>>>(fp, fb, rgba, depth);
     }
-}
-
-// Step 7: periphery reconstruction: nearest-neighbour upsample of the
-// LowRes group samples and a 3x3 (1,2,1)x(1,2,1) blur restricted to LowRes
-// pixels in the image, renormalised; invisible tiles get the
-// background with A = 0, D = 0.  HighRes/Hybrid pixels were written by the
-// blend.  One thread per 2x2 pixel group: the 3x3 neighbourhood of group
-// samples covers the blur footprint of all four pixels.
-__global__ void k_compose(FrameParams fp, FrameBufs fb, float* __restrict__ rgba, float* __restrict__ depth,
-                          int64_t total_groups) {
-    const int64_t gi = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gi >= total_groups) return;
-    int vi = 0;
-    while (vi + 1 < fp.n_views && gi >= fp.v[vi + 1].low_off) vi++;
-    const ViewParams& v = fp.v[vi];
-    const uint32_t k = (uint32_t)(gi - v.low_off);
-    const int gx = (int)(k % (uint32_t)v.low_w), gy = (int)(k / (uint32_t)v.low_w);
-    if (2 * gy >= v.H) return;  // gap between views' low-res planes
-    const int tsh = (fp.T == 32) ? 5 : 4, i0 = 2 * gx, j0 = 2 * gy;  // T is 16 or 32
-    const int c = v.cls[(j0 >> tsh) * v.tw + (i0 >> tsh)];
-    if (c == kHigh || c == kHybrid) return;
-    float4 outc[2][2];
-    float outd[2][2];
-    if (c == kInvisible) {
-#pragma unroll
-        for (int b = 0; b < 2; b++)
-#pragma unroll
-            for (int a = 0; a < 2; a++) {
-                outc[b][a] = make_float4(fp.bg[0], fp.bg[1], fp.bg[2], 0.0f);
-                outd[b][a] = 0.0f;
-            }
-    } else {
-        // gather the 3x3 neighbour groups (sample + whether its pixels are LowRes & in image)
-        float4 sc[3][3];
-        float sd[3][3];
-        bool ok[3][3];
-#pragma unroll
-        for (int dj = 0; dj < 3; dj++)
-#pragma unroll
-            for (int di = 0; di < 3; di++) {
-                // pixel of that group adjacent to this group: column 2gx-1, (2gx..2gx+1), 2gx+2
-                const int pi = (di == 0) ? i0 - 1 : (di == 1 ? i0 : i0 + 2);
-                const int pj = (dj == 0) ? j0 - 1 : (dj == 1 ? j0 : j0 + 2);
-                bool good = pi >= 0 && pj >= 0 && pi < v.W && pj < v.H;
-                if (good) good = v.cls[(pj >> tsh) * v.tw + (pi >> tsh)] == kLow;
-                ok[dj][di] = good;
-                if (good) {
-                    const size_t li = (size_t)v.low_off + (size_t)(pj >> 1) * v.low_w + (pi >> 1);
-                    sc[dj][di] = fb.low_rgba[li];
-                    sd[dj][di] = fb.low_depth[li];
-                } else {
-                    sc[dj][di] = make_float4(0.f, 0.f, 0.f, 0.f);
-                    sd[dj][di] = 0.0f;
-                }
-            }
-        // Pixels of one group share its sample, so the 3x3 taps of pixel
-        // (i0+a, j0+b) collapse onto 2x2 neighbour groups with summed
-        // separable weights: a = 0 -> groups {-1: 1, 0: 2 + [i0+1 < W]},
-        // a = 1 -> {0: 3, +1: 1} (pixel-level in-image tests folded in).
-        const float wx[2][3] = {{1.0f, (i0 + 1 < v.W) ? 3.0f : 2.0f, 0.0f}, {0.0f, 3.0f, 1.0f}};
-        const float wy[2][3] = {{1.0f, (j0 + 1 < v.H) ? 3.0f : 2.0f, 0.0f}, {0.0f, 3.0f, 1.0f}};
-#pragma unroll
-        for (int b = 0; b < 2; b++)
-#pragma unroll
-            for (int a = 0; a < 2; a++) {
-                float acc[5] = {0.f, 0.f, 0.f, 0.f, 0.f}, ws = 0.0f;
-#pragma unroll
-                for (int sj = b; sj < b + 2; sj++)
-#pragma unroll
-                    for (int si = a; si < a + 2; si++) {
-                        const float w = ok[sj][si] ? wx[a][si] * wy[b][sj] : 0.0f;
-                        acc[0] = fmaf(w, sc[sj][si].x, acc[0]);
-                        acc[1] = fmaf(w, sc[sj][si].y, acc[1]);
-                        acc[2] = fmaf(w, sc[sj][si].z, acc[2]);
-                        acc[3] = fmaf(w, sc[sj][si].w, acc[3]);
-                        acc[4] = fmaf(w, sd[sj][si], acc[4]);
-                        ws += w;
-                    }
-                const float inv = 1.0f / ws;
-                outc[b][a] = make_float4(acc[0] * inv, acc[1] * inv, acc[2] * inv, acc[3] * inv);
-                outd[b][a] = acc[4] * inv;
-            }
-    }
-#pragma unroll
-    for (int b = 0; b < 2; b++) {
-        const int j = j0 + b;
-        if (j >= v.H) continue;
-        const size_t row = (size_t)v.pix_off + (size_t)j * v.W;
-        store_pixel(fp.out_fmt, rgba, depth, row + i0, outc[b][0], outd[b][0]);
-        if (i0 + 1 < v.W) store_pixel(fp.out_fmt, rgba, depth, row + i0 + 1, outc[b][1], outd[b][1]);
-    }
-}
-
-void launch_compose(const FrameParams& fp, FrameBufs fb, float* rgba, float* depth, cudaStream_t st) {
-    if (fp.n_views == 0) return;
-    const ViewParams& last = fp.v[fp.n_views - 1];
-    const int64_t total = last.low_off + (int64_t)last.low_w * ((last.H + 1) / 2);
-    k_compose<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(fp, fb, rgba, depth, total);
 }
 
 }  // namespace vrs

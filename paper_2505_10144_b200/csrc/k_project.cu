@@ -601,7 +601,7 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
                 rec[3] = make_float4(p.A[0], p.A[1], p.A[2], p.A[3]);
                 rec[4] = make_float4(p.A[4], p.A[5], p.bv[0], p.bv[1]);
                 rec[5] = make_float4(p.bv[2], p.sigma, p.eps, __uint_as_float(r01));
-                rec[6] = make_float4(0.0f, 0.0f, 0.0f, __uint_as_float(r23));  // (colour: k_color)
+                reinterpret_cast<float*>(rec + 6)[3] = __uint_as_float(r23);  // (colour .xyz: k_color)
                 rec[7] = make_float4(p.bbox[0], p.bbox[1], p.bbox[2], p.bbox[3]);
             }
         }
@@ -675,12 +675,13 @@ __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const Fram
     while (vi + 1 < fp.n_views && (int64_t)sidx >= (int64_t)(vi + 1) * fp.N) vi++;
     const ViewParams& v = fp.v[vi];
     const float4* rec = fb.rec + (size_t)sidx * kRecF4;
-    const float4 r0 = __ldg(rec + 0), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2), r5 = __ldg(rec + 5),
-                 r6 = __ldg(rec + 6);
+    const float4 r0 = __ldg(rec + 0), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2), r5 = __ldg(rec + 5);
+    // rect23 only: k_color writes the colour into rec[6].xyz concurrently (side stream)
+    const float r6w = __ldg(reinterpret_cast<const float*>(rec + 6) + 3);
 #if VRS_TT_HOIST
     const float4 r3 = __ldg(rec + 3), r4 = __ldg(rec + 4);  // issued with the others: one latency level less
 #endif
-    const uint32_t r01 = __float_as_uint(r5.w), r23 = __float_as_uint(r6.w);
+    const uint32_t r01 = __float_as_uint(r5.w), r23 = __float_as_uint(r6w);
     const int tx0 = r01 & 0xffff, ty0 = r01 >> 16, tx1 = r23 & 0xffff;
     const int rw = tx1 - tx0 + 1;
     const int tx = tx0 + (int)(l % (uint32_t)rw), ty = ty0 + (int)(l / (uint32_t)rw);

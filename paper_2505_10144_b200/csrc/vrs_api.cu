@@ -23,7 +23,7 @@ struct ViewSetup {
     int W = 0, H = 0, mask_slot = -1, T = 0, fovea = 0;
     uint64_t mask_gen = 0;
     float gx = 0, gy = 0, rx = 0, ry = 0, ramp = 0;
-    int32_t n_items = 0, n_low = 0;
+    int32_t n_items = 0, n_low = 0, n_inv = 0;
     int32_t cls_count[4] = {0, 0, 0, 0};
 };
 
@@ -72,7 +72,10 @@ struct vrs_context {
     uint32_t* d_sat = nullptr;    // [V][max_sat]
     int32_t* d_cls = nullptr;     // [V][max_tiles]
     uint32_t* d_items = nullptr;  // [V][max_items]
-    int32_t* d_nitems = nullptr;  // [V]
+    int32_t* d_nitems = nullptr;  // [V][3]: items, LowRes items, invisible tiles
+    uint32_t* d_inv = nullptr;    // [V][max_tiles]: invisible tiles (background-fill items)
+    uint32_t* d_lowcnt = nullptr;   // [V][max_tiles]: in-launch compose counters
+    uint32_t* d_lowcnt0 = nullptr;  // [V][max_tiles]: their initial values
     int64_t max_sat_view = 0;
     ViewSetup vs[VRS_MAX_VIEWS];
     // masks
@@ -134,7 +137,8 @@ static void free_all(vrs_context* c) {
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
                     c->bin.tile_cnt, c->bin.rank, c->bin.list, c->bin.list_n, c->bin.tbucket, c->bin.ovf_off, c->bin.obucket,
-                    c->d_sat, c->d_cls, c->d_items, c->d_nitems, c->d_out_rgba, c->d_out_depth};
+                    c->d_sat, c->d_cls, c->d_items, c->d_nitems, c->d_inv, c->d_lowcnt, c->d_lowcnt0,
+                    c->d_out_rgba, c->d_out_depth};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 2 * VRS_MAX_MASK_SLOTS; i++)
@@ -213,7 +217,10 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     A(dalloc(&ctx->d_cls, (size_t)V * ctx->max_tiles_view));
     A(dalloc(&ctx->d_sat, (size_t)V * ctx->max_sat_view));
     A(dalloc(&ctx->d_items, (size_t)V * ctx->max_items_view));
-    A(dalloc(&ctx->d_nitems, (size_t)2 * V));
+    A(dalloc(&ctx->d_nitems, (size_t)3 * V));
+    A(dalloc(&ctx->d_inv, (size_t)V * ctx->max_tiles_view));
+    A(dalloc(&ctx->d_lowcnt, (size_t)V * ctx->max_tiles_view));
+    A(dalloc(&ctx->d_lowcnt0, (size_t)V * ctx->max_tiles_view));
     if (e != cudaSuccess) {
         free_all(ctx);
         delete ctx;
@@ -221,6 +228,11 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
         return (e == cudaErrorMemoryAllocation) ? VRS_E_OOM : VRS_E_CUDA;
     }
     cudaMemset(ctx->d_misc, 0, 32);
+    // colours and records of splats not projected this frame are never blended
+    // with a weight, but the window's sentinel (g = 0, alpha = 0) reads a colour:
+    // keep it finite
+    cudaMemset(ctx->d_col, 0, sizeof(float4) * (size_t)V * N);
+    cudaMemset(ctx->d_rec, 0, sizeof(float4) * (size_t)V * N * kRecF4);
     ctx->bin.ovf_count = ctx->d_misc + 5;
     cudaMemset(ctx->bin.tile_cnt, 0, sizeof(uint32_t) * ctx->bin.max_tiles);  // k_tile_scan re-zeroes per frame
     *out = ctx;
@@ -466,6 +478,9 @@ static vrs_status prepare_frame(vrs_context* ctx, int nv, const vrs_camera* cams
         v.cls = ctx->d_cls + (size_t)vi * ctx->max_tiles_view;
         v.sat = ctx->d_sat + (size_t)vi * ctx->max_sat_view;
         v.items = ctx->d_items + (size_t)vi * ctx->max_items_view;
+        v.inv_items = ctx->d_inv + (size_t)vi * ctx->max_tiles_view;
+        v.lowcnt = ctx->d_lowcnt + (size_t)vi * ctx->max_tiles_view;
+        v.lowcnt0 = ctx->d_lowcnt0 + (size_t)vi * ctx->max_tiles_view;
         // setup cache (precomputed once per eye)
         const int ms = (c.mask_slot >= 0 && ctx->d_mask[c.mask_slot]) ? c.mask_slot : -1;
         ViewSetup& s = ctx->vs[vi];
@@ -477,11 +492,14 @@ static vrs_status prepare_frame(vrs_context* ctx, int nv, const vrs_camera* cams
             launch_setup_view(ms >= 0 ? ctx->d_mask[ms] : nullptr, v.W, v, T, ctx->d_vis + (size_t)vi * ctx->max_tiles_view,
                               ctx->d_sat + (size_t)vi * ctx->max_sat_view,
                               ctx->d_cls + (size_t)vi * ctx->max_tiles_view,
-                              ctx->d_items + (size_t)vi * ctx->max_items_view, ctx->d_nitems + 2 * vi, st);
+                              ctx->d_items + (size_t)vi * ctx->max_items_view, ctx->d_nitems + 3 * vi,
+                              ctx->d_inv + (size_t)vi * ctx->max_tiles_view,
+                              ctx->d_lowcnt + (size_t)vi * ctx->max_tiles_view,
+                              ctx->d_lowcnt0 + (size_t)vi * ctx->max_tiles_view, st);
             CK(cudaGetLastError());
-            int32_t ni[2] = {0, 0};
+            int32_t ni[3] = {0, 0, 0};
             std::vector<int32_t> cls((size_t)v.tw * v.th);
-            CK(cudaMemcpyAsync(ni, ctx->d_nitems + 2 * vi, 8, cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(ni, ctx->d_nitems + 3 * vi, 12, cudaMemcpyDeviceToHost, st));
             CK(cudaMemcpyAsync(cls.data(), ctx->d_cls + (size_t)vi * ctx->max_tiles_view, 4 * cls.size(),
                                cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
@@ -490,6 +508,7 @@ static vrs_status prepare_frame(vrs_context* ctx, int nv, const vrs_camera* cams
             s.gx = v.gx; s.gy = v.gy; s.rx = v.rx; s.ry = v.ry; s.ramp = v.ramp;
             s.n_items = ni[0];
             s.n_low = ni[1];
+            s.n_inv = ni[2];
             for (int k = 0; k < 4; k++) s.cls_count[k] = 0;
             for (int32_t cc : cls) s.cls_count[cc & 3]++;
         }
@@ -498,10 +517,14 @@ static vrs_status prepare_frame(vrs_context* ctx, int nv, const vrs_camera* cams
         v.n_low = s.n_low;
         v.item_off = total_items;
         total_items += s.n_items;
+        v.n_inv = s.n_inv;
+        v.inv_off = fp.n_inv_items;
+        fp.n_inv_items += s.n_inv;
         tile_base += (int64_t)v.tw * v.th;
         pix_off += (int64_t)v.W * v.H;
     }
     if (tile_base >= ((int64_t)1 << 20)) return fail(ctx, VRS_E_INVALID_ARG, "too many tiles in one call");
+    fp.n_blend_items = total_items;
     ctx->last_tiles = tile_base;
     return VRS_OK;
 }
@@ -574,27 +597,33 @@ static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* ca
     if (tm) CK(cudaEventRecord(ctx->ev[4], st));
     CK(cudaStreamWaitEvent(st, ctx->fork_ev[1], 0));
     if (tm) CK(cudaEventRecord(ctx->ev[5], st));
-    // blend in two launches: the LowRes items (listed first per view), then the
-    // full-rate ones; the periphery compose (which needs every LowRes sample and
-    // writes only LowRes / invisible pixels) runs on the side stream meanwhile
-    FrameParams fl = fp, ff = fp;
-    int n_low = 0, n_full = 0;
-    for (int i = 0; i < nv; i++) {
-        fl.v[i].item_off = n_low;
-        fl.v[i].n_items = fp.v[i].n_low;
-        ff.v[i].items = fp.v[i].items + fp.v[i].n_low;
-        ff.v[i].item_off = n_full;
-        ff.v[i].n_items = fp.v[i].n_items - fp.v[i].n_low;
-        n_low += fl.v[i].n_items;
-        n_full += ff.v[i].n_items;
-    }
-    CK(cudaEventRecord(ctx->fork_ev[2], st));
-    CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev[2], 0));
-    launch_blend(ff, fb, n_full, rgba, depth, ctx->side);   // full-rate items beside ...
-    CK(cudaEventRecord(ctx->fork_ev[3], ctx->side));
-    launch_blend(fl, fb, n_low, rgba, depth, st);           // ... the LowRes items, then the compose
-    launch_compose(fp, fb, rgba, depth, st);
-    CK(cudaStreamWaitEvent(st, ctx->fork_ev[3], 0));
+    // blend: ONE launch over every view's items (LowRes first), the invisible
+    // tiles' background and the periphery compose (triggered inside the launch)
+#if VRS_TWO_LAUNCH  // experiment: round-1 structure (LowRes items + inv ‖ full-rate items on the side stream)
+    if (fp.resort == 0) {
+        FrameParams fl = fp, ff = fp;
+        int n_low = 0, n_full = 0;
+        for (int i = 0; i < nv; i++) {
+            fl.v[i].item_off = n_low;
+            fl.v[i].n_items = fp.v[i].n_low;
+            ff.v[i].items = fp.v[i].items + fp.v[i].n_low;
+            ff.v[i].item_off = n_full;
+            ff.v[i].n_items = fp.v[i].n_items - fp.v[i].n_low;
+            n_low += fl.v[i].n_items;
+            n_full += ff.v[i].n_items;
+        }
+        fl.n_blend_items = n_low;
+        ff.n_blend_items = n_full;
+        ff.n_inv_items = 0;
+        CK(cudaEventRecord(ctx->fork_ev[2], st));
+        CK(cudaStreamWaitEvent(ctx->side, ctx->fork_ev[2], 0));
+        launch_blend(ff, fb, n_full, rgba, depth, ctx->side);
+        CK(cudaEventRecord(ctx->fork_ev[3], ctx->side));
+        launch_blend(fl, fb, n_low, rgba, depth, st);
+        CK(cudaStreamWaitEvent(st, ctx->fork_ev[3], 0));
+    } else
+#endif
+    launch_blend(fp, fb, total_items, rgba, depth, st);
     if (tm) CK(cudaEventRecord(ctx->ev[6], st));
     if (tm) CK(cudaEventRecord(ctx->ev[7], st));
     CK(cudaGetLastError());

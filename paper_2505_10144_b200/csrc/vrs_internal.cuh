@@ -54,6 +54,11 @@ struct ViewParams {
     const uint32_t* sat;     // [(th+1)*(tw+1)] summed-area table
     const int32_t* cls;      // [th*tw] tile classes
     const uint32_t* items;   // [n_items] packed work items
+    const uint32_t* inv_items;  // [n_inv] invisible coarse tiles (background fill items of the flat blend)
+    int32_t n_inv;           // invisible tiles of this view
+    int32_t inv_off;         // first invisible item of this view (after all views' blend items)
+    uint32_t* lowcnt;        // [th*tw] LowRes tiles of the 3x3 neighbourhood still blending (in-launch compose)
+    const uint32_t* lowcnt0; // [th*tw] its initial value (counters are re-armed by the composing block)
 };
 
 struct FrameParams {
@@ -65,6 +70,8 @@ struct FrameParams {
     int32_t ewa;             // projection: 0 = Optimal Projection, 1 = EWA baseline (config C5)
     int32_t resort;          // 0 = per-sample window K = 16; 1 = hierarchical
     int32_t out_fmt;         // VRS_OUT_F32 or VRS_OUT_RGBA8_D16F (final output pixels)
+    int32_t n_blend_items;   // blend items of all views (flat blend grid = n_blend_items + n_inv_items)
+    int32_t n_inv_items;     // invisible-tile fill items of all views
     int64_t N;
     int64_t pair_cap;
     float near_plane;
@@ -129,9 +136,12 @@ inline int device_sms() {
 }
 
 // ----------------------------------------------------------------- launchers
-// n_items_dev[0] = items, n_items_dev[1] = LowRes items (listed first)
+// n_items_dev[0] = items, n_items_dev[1] = LowRes items (listed first),
+// n_items_dev[2] = invisible tiles (listed in inv_items); lowcnt / lowcnt0 get the
+// in-launch compose counters (LowRes tiles of each LowRes tile's 3x3 neighbourhood).
 void launch_setup_view(const uint8_t* mask, int mask_w, ViewParams vp, int T, int32_t* vis, uint32_t* sat,
-                       int32_t* cls, uint32_t* items, int32_t* n_items_dev, cudaStream_t st);
+                       int32_t* cls, uint32_t* items, int32_t* n_items_dev, uint32_t* inv_items, uint32_t* lowcnt,
+                       uint32_t* lowcnt0, cudaStream_t st);
 // Cull + preprocess + candidate expansion into fb.sidk (total in fb.total_tests).
 void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st);
 // SH colour of the visible list (after launch_preprocess; needed by the blend only)
@@ -199,6 +209,8 @@ struct TwoPassParams {
 void launch_mask_half(const uint8_t* src, int W, int H, uint8_t* dst, int W2, int H2, cudaStream_t st);
 void launch_two_pass_combine(const TwoPassParams& tp, const float4* prgba, const float* pdepth, float* rgba,
                              float* depth, int64_t total, cudaStream_t st);  // writes tp.out_fmt
+// The whole blend of a frame: flat mode = one k_blend launch (blend items, invisible
+// fills and the periphery compose); hierarchical mode = k_blend_hier + k_compose.
 void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
                   cudaStream_t st);
 void launch_blend_hier(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
