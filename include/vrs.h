@@ -67,7 +67,7 @@ typedef struct vrs_context vrs_context;
 typedef struct {
     int32_t device;          /* CUDA device ordinal */
     int32_t max_views;       /* <= VRS_MAX_VIEWS views per render call */
-    int64_t max_gaussians;   /* upper bound on uploaded Gaussians */
+    int64_t max_gaussians;   /* upper bound on uploaded Gaussians, < 2^24 (16.7 M) */
     int64_t max_pairs;       /* capacity of the Gaussian/tile pair buffers (all views of a call) */
     int32_t max_width;       /* upper bounds on view resolution */
     int32_t max_height;
@@ -217,6 +217,20 @@ VRS_API vrs_status vrs_render_views_two_pass(vrs_context* ctx, int32_t n_views, 
  * Errors: VRS_E_INVALID_ARG (unknown mode, sizes other than the compiled ones,
  * mode 1 with the EWA projection). */
 VRS_API vrs_status vrs_set_resort_mode(vrs_context* ctx, int32_t mode, int32_t block_queue, int32_t pixel_window);
+
+/* How the blend stages each batch of splat records (the tile list's entries,
+ * north_star "Gaussian batches staged into shared memory") -- results are
+ * identical, only the copy engine differs:
+ *   VRS_STAGING_THREADS (default): the block's threads load the records
+ *     (seven 16-B loads each) and store them to shared memory;
+ *   VRS_STAGING_TMA: the Tensor Memory Accelerator copies them
+ *     (cp.async.bulk global -> shared, one 96-B copy per entry issued by the
+ *     block's warps, completion on an mbarrier).
+ * Applies to the flat (mode 0) blend from the next render.  Errors:
+ * VRS_E_INVALID_ARG (unknown mode). */
+#define VRS_STAGING_THREADS 0
+#define VRS_STAGING_TMA 1
+VRS_API vrs_status vrs_set_staging_mode(vrs_context* ctx, int32_t mode);
 VRS_API vrs_status vrs_set_instrumentation(vrs_context* ctx, int32_t counters, int32_t timing);
 
 /* Synchronises the last frame's stream and returns its statistics.

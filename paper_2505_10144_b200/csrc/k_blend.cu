@@ -162,27 +162,24 @@ void launch_compose(const FrameParams& fp, FrameBufs fb, float* rgba, float* dep
 // ----------------------------------------------------------------- blend (step 6)
 namespace {
 
-#ifndef VRS_BLEND_THREADS
-#define VRS_BLEND_THREADS 256
-#endif
+constexpr int kBT = 256;                 // threads per block: one 16x16 item / one 32x32 LowRes item
+constexpr int kWarps = kBT / 32;
 #ifndef VRS_BLEND_BATCH
 #define VRS_BLEND_BATCH 80
 #endif
-constexpr int kBT = VRS_BLEND_THREADS;   // threads per block: a whole 16x16 item, or half of it (16x8)
-constexpr int kSplit = 256 / kBT;        // blocks per item
-constexpr int kWarps = kBT / 32;
-constexpr int kBatch = VRS_BLEND_BATCH;  // splat records staged per shared-memory batch
-static_assert(kBatch <= kBT && kSplit == 1, "blend block shape (the in-launch compose counts one block per item)");
+constexpr int kBatch = VRS_BLEND_BATCH;  // list entries staged per shared-memory batch
+constexpr uint32_t kStageBytes = 96;     // r0..r5 of a splat record
+static_assert(kBatch <= kBT && kBatch >= 10, "one staging thread per entry; the compose triggers reuse mask[]");
 
 struct BlendSmem {
-    float4 r0[kBatch];   // u.xyz, q_cut
-    float4 r1[kBatch];   // e1.x, e1.z, e2.x, e2.y
-    float4 r2[kBatch];   // e2.z, C00, C01, C11
-    float4 r3[kBatch];   // A a, b, c, p
-    float4 r4[kBatch];   // A e, f, b.x, b.y
-    float4 r5[kBatch];   // b.z, sigma, g (bits), -
-    uint32_t mask[kBatch];
-    float4 wblock[kWarps];  // per-warp sample extent xmin, xmax, ymin, ymax (pixel coords)
+    // the staged entries: the first 96 B of their splat records, r0..r5
+    // (k_project.cu layout: u.xyz, q_cut | e1.x, e1.z, e2.x, e2.y | e2.z, C00,
+    // C01, C11 | A a, b, c, p | A e, f, b.x, b.y | b.z, sigma, -, -), written by
+    // the TMA bulk-copy engine (staging mode 1) or by the block's threads (mode 0)
+    float4 rec[kBatch][6];
+    uint32_t mask[kBatch];    // g << 8 | the warps whose samples the entry's pixel footprint meets
+    unsigned long long full;  // mbarrier: the batch landed (TMA staging)
+    float4 wblock[kWarps];    // per-warp sample extent xmin, xmax, ymin, ymax (pixel coords)
     // per-thread resort window: ring of K slots, (tau, g) packed into one
     // order-preserving 64-bit key, alpha alongside; [slot][thread] layout is
     // bank-conflict free for any per-thread slot index
@@ -194,7 +191,6 @@ struct BlendSmem {
 // (228 KB per SM, 1 KB reserved per block); after the blend loop the staging
 // mask holds the in-launch compose triggers
 static_assert(sizeof(BlendSmem) + 1024 <= 233472 / 4, "blend shared memory exceeds the 4-blocks/SM budget");
-static_assert(kBatch >= 10, "the compose triggers reuse the staging mask");
 
 constexpr uint32_t kSlotBytes = kBT * 8;                   // one ring slot of keys
 constexpr uint32_t kRingMask = (kWindow - 1) * kSlotBytes;    // byte-offset ring mask
@@ -234,6 +230,34 @@ __device__ __forceinline__ ItemGeom item_geom(const FrameParams& fp, int item, i
     }
     return g;
 }
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// TMA bulk copy global -> shared of `bytes` (multiple of 16, 16-B aligned),
+// completing its byte count on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+    uint64_t gsrc;
+    asm("cvta.to.global.u64 %0, %1;" : "=l"(gsrc) : "l"(src));
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 // blockIdx.x through an opaque read, so the compiler recomputes the item's
 // geometry after the blend loop instead of keeping it in registers
 __device__ __forceinline__ int block_id_opaque() {
@@ -244,18 +268,27 @@ __device__ __forceinline__ int block_id_opaque() {
 
 }  // namespace
 
-template <bool kCounters, bool kEwa>
+#define REC0(j) S.rec[j][0]
+#define REC1(j) S.rec[j][1]
+#define REC2(j) S.rec[j][2]
+#define REC3(j) S.rec[j][3]
+#define REC4(j) S.rec[j][4]
+#define REC5(j) S.rec[j][5]
+#define GID(j) (S.mask[j] >> 8)
+#define MASKJ(j) S.mask[j]
+
+template <bool kCounters, bool kEwa, bool kTma>
 #ifndef VRS_BLEND_MINB
-#define VRS_BLEND_MINB (1024 / VRS_BLEND_THREADS)
+#define VRS_BLEND_MINB 4
 #endif
 __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, FrameBufs fb, float* __restrict__ rgba,
                                                       float* __restrict__ depth) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     BlendSmem& S = *reinterpret_cast<BlendSmem*>(smem_raw);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // locate the view and the item (blend items of every view, then the invisible tiles)
     int vi = 0;
-    const int item = blockIdx.x / kSplit, half = blockIdx.x % kSplit;  // half: rows 8-15 of the item
+    const int item = blockIdx.x, half = 0;
     if (item >= fp.n_blend_items) {
         // invisible tile: background, A = 0, D = 0
         const int iv = item - fp.n_blend_items;
@@ -263,7 +296,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         const ViewParams& v = fp.v[vi];
         const int tile = (int)v.inv_items[iv - v.inv_off];
         const int T = fp.T, x0 = (tile % v.tw) * T, y0 = (tile / v.tw) * T;
-        for (int p = tid + half * kBT; p < T * T; p += kBT * kSplit) {
+        for (int p = tid + half * kBT; p < T * T; p += kBT) {
             const int px = x0 + p % T, py = y0 + p / T;
             if (px < v.W && py < v.H)
                 store_pixel(fp.out_fmt, rgba, depth, (size_t)v.pix_off + (size_t)py * v.W + px,
@@ -397,38 +430,82 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         contribute(order_key(tau, g, fp.near_plane), alpha, pos);
     };
 
+    uint32_t phase = 0;
+    if (kTma && tid == 0) {
+        mbar_init(&S.full, kWarps);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     for (uint32_t base = rb; base < re; base += kBatch) {
-        __syncthreads();
-        const uint32_t idx = base + tid;
-        if (tid < kBatch && idx < re) {
-            uint32_t g = __ldg(fb.vals + idx);
-            g = (g < (uint32_t)fp.N) ? g : 0u;  // memory safety after a capacity overflow only
-            const float4* rp = recv + (size_t)g * kRecF4;
-            const float4 a0 = __ldg(rp + 0), a1 = __ldg(rp + 1), a2 = __ldg(rp + 2), a3 = __ldg(rp + 3),
-                         a4 = __ldg(rp + 4), a5 = __ldg(rp + 5), a7 = __ldg(rp + 7);
-            S.r0[tid] = a0; S.r1[tid] = a1; S.r2[tid] = a2; S.r3[tid] = a3; S.r4[tid] = a4;
-            S.r5[tid] = make_float4(a5.x, a5.y, __uint_as_float(g), 0.0f);
-            uint32_t m = 0;
+        __syncthreads();  // the staging buffer is free again (and the mbarrier initialised)
+        const uint32_t n = min(re - base, (uint32_t)kBatch);
+        if constexpr (kTma) {
+            // every warp stages its share of the batch: one TMA bulk copy of r0..r5
+            // of each entry's record, completing on the batch's mbarrier (one
+            // arrival per warp, carrying its bytes); the issuing lane tests the
+            // entry's pixel footprint (r7) against every warp's samples meanwhile
+            constexpr uint32_t kPer = (kBatch + kWarps - 1) / kWarps;
+            const uint32_t i = (uint32_t)warp * kPer + (uint32_t)lane;
+            const bool mine = (uint32_t)lane < kPer && i < n;
+            uint32_t g = 0;
+            if (mine) {
+                g = __ldg(fb.vals + base + i);
+                g = (g < (uint32_t)fp.N) ? g : 0u;  // memory safety after a capacity overflow only
+                const float4 a7 = __ldg(recv + (size_t)g * kRecF4 + 7);
+                uint32_t m = 0;
 #pragma unroll
-            for (int w = 0; w < kWarps; w++) {
-                const float4 b = S.wblock[w];
-                const bool hit = !(a7.y < b.x || a7.x > b.y || a7.w < b.z || a7.z > b.w);
-                m |= hit ? (1u << w) : 0u;
+                for (int w = 0; w < kWarps; w++) {
+                    const float4 b = S.wblock[w];
+                    const bool hit = !(a7.y < b.x || a7.x > b.y || a7.w < b.z || a7.z > b.w);
+                    m |= hit ? (1u << w) : 0u;
+                }
+                S.mask[i] = (g << 8) | (fp.no_cull ? 0xffu : m);
             }
-            S.mask[tid] = fp.no_cull ? 0xffu : m;
+            // the previous batch was read through the generic proxy (ordered before
+            // this point by the block barrier); the copies write through the async proxy
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t w0 = (uint32_t)warp * kPer;
+                const uint32_t cnt = n > w0 ? min(n - w0, kPer) : 0u;
+                mbar_arrive_expect_tx(&S.full, cnt * kStageBytes);
+            }
+            __syncwarp();
+            if (mine) bulk_g2s(&S.rec[i][0], recv + (size_t)g * kRecF4, kStageBytes, &S.full);
+            while (!mbar_try_wait(&S.full, phase)) {
+            }
+            phase ^= 1u;
+        } else {
+            // the block's first n threads load one record each (seven independent LDG.128)
+            if ((uint32_t)tid < n) {
+                uint32_t g = __ldg(fb.vals + base + tid);
+                g = (g < (uint32_t)fp.N) ? g : 0u;  // memory safety after a capacity overflow only
+                const float4* rp = recv + (size_t)g * kRecF4;
+                const float4 a0 = __ldg(rp + 0), a1 = __ldg(rp + 1), a2 = __ldg(rp + 2), a3 = __ldg(rp + 3),
+                             a4 = __ldg(rp + 4), a5 = __ldg(rp + 5), a7 = __ldg(rp + 7);
+                S.rec[tid][0] = a0; S.rec[tid][1] = a1; S.rec[tid][2] = a2;
+                S.rec[tid][3] = a3; S.rec[tid][4] = a4; S.rec[tid][5] = a5;
+                uint32_t m = 0;
+#pragma unroll
+                for (int w = 0; w < kWarps; w++) {
+                    const float4 b = S.wblock[w];
+                    const bool hit = !(a7.y < b.x || a7.x > b.y || a7.w < b.z || a7.z > b.w);
+                    m |= hit ? (1u << w) : 0u;
+                }
+                S.mask[tid] = (g << 8) | (fp.no_cull ? 0xffu : m);
+            }
         }
         if (__syncthreads_count(!done) == 0) break;
         const int nb = min((int)(re - base), kBatch);
 #define POS_OF(j) (base + (uint32_t)(j))
         for (int c = 0; c < nb; c += 32) {
             if (__all_sync(0xffffffffu, done)) break;
-            const bool rel = (c + lane < nb) && ((S.mask[c + lane] >> warp) & 1u);
+            const bool rel = (c + lane < nb) && ((MASKJ(c + lane) >> warp) & 1u);
             unsigned bits = __ballot_sync(0xffffffffu, rel);
             if (!kEwa) {
                 // two list entries per iteration: both memberships first (independent
                 // chains), then the contributions in stream order
                 auto member = [&](const int j, float& num, float& ss) {
-                    const float4 a0 = S.r0[j], a1 = S.r1[j], a2 = S.r2[j];
+                    const float4 a0 = REC0(j), a1 = REC1(j), a2 = REC2(j);
                     const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
                     const float ex = fmaf(a1.x, x, a1.y);
                     const float ey = fmaf(a1.z, x, fmaf(a1.w, y, a2.x));
@@ -438,12 +515,12 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
                     return (s > 0.0f) && (num <= a0.w * ss);
                 };
                 auto contrib = [&](const int j, const float num, const float ss) {
-                    const float4 a3 = S.r3[j], a4 = S.r4[j], t = S.r5[j];
+                    const float4 a3 = REC3(j), a4 = REC4(j), t = REC5(j);
                     const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
                     const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, t.x));
                     float tau;
                     const float alpha = alpha_tau(num, ss, den, dtb, t.y, tau);
-                    contribute(order_key(tau, __float_as_uint(t.z), fp.near_plane), alpha, POS_OF(j));
+                    contribute(order_key(tau, GID(j), fp.near_plane), alpha, POS_OF(j));
                 };
                 while (bits) {
                     const int j = c + __ffs(bits) - 1;
@@ -466,11 +543,11 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
             while (bits) {
                 const int j = c + __ffs(bits) - 1;
                 bits &= bits - 1;
-                evaluate(POS_OF(j), __float_as_uint(S.r5[j].z), S.r0[j], S.r1[j], kEwa ? S.r1[j] : S.r2[j],
+                evaluate(POS_OF(j), GID(j), REC0(j), REC1(j), kEwa ? REC1(j) : REC2(j),
                          [&](float4& a3, float4& a4, float2& a5) {
-                             a3 = S.r3[j];
-                             a4 = S.r4[j];
-                             const float4 t = S.r5[j];
+                             a3 = REC3(j);
+                             a4 = REC4(j);
+                             const float4 t = REC5(j);
                              a5 = make_float2(t.x, t.y);
                          });
             }
@@ -486,7 +563,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
 #undef WK
 #undef WA
     // outputs: the item's geometry recomputed from an opaque block index (not live through the loop)
-    const ItemGeom g = item_geom(fp, block_id_opaque() / kSplit, half, lane, warp);
+    const ItemGeom g = item_geom(fp, block_id_opaque(), half, lane, warp);
     const ViewParams& v = fp.v[g.vi];
     const int px = g.px, py = g.py, kind = g.kind;
     const int tx = g.tile % v.tw, ty = g.tile / v.tw;
@@ -554,6 +631,8 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
             atomicAdd(&fb.stats[3], S.cnt[3]);
         }
     }
+    // (the compose triggers live in the staging mask array, free after the loop)
+    uint32_t* const TRIG = S.mask;
     // In-launch compose: this LowRes tile's samples are final; count it
     // off the 3x3 neighbourhoods that wait for it and compose the ones it completes
     if (kind != kItemLow) return;
@@ -567,16 +646,16 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
                 if (nx < 0 || ny < 0 || nx >= v.tw || ny >= v.th) continue;
                 const int t2 = ny * v.tw + nx;
                 if (v.cls[t2] != kLow) continue;
-                if (atomicSub(&v.lowcnt[t2], 1u) == 1u) S.mask[1 + n++] = (uint32_t)t2;
+                if (atomicSub(&v.lowcnt[t2], 1u) == 1u) TRIG[1 + n++] = (uint32_t)t2;
             }
         if (n) __threadfence();
-        S.mask[0] = n;
+        TRIG[0] = n;
     }
     __syncthreads();
-    const uint32_t ntrig = S.mask[0];
+    const uint32_t ntrig = TRIG[0];
     for (uint32_t i = 0; i < ntrig; i++) {
-        const int t2 = (int)S.mask[1 + i];
-        for (int q = tid + half * kBT; q < 256; q += kBT * kSplit) {  // T = 32: 16 x 16 groups
+        const int t2 = (int)TRIG[1 + i];
+        for (int q = tid + half * kBT; q < 256; q += kBT) {  // T = 32: 16 x 16 groups
             const int gx = (t2 % v.tw) * 16 + (q % 16), gy = (t2 / v.tw) * 16 + (q / 16);
             compose_group(fp, fb, v, gx, gy, rgba, depth);
         }
@@ -591,19 +670,23 @@ void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* r
         launch_compose(fp, fb, rgba, depth, st);
         return;
     }
-    const unsigned grid = (unsigned)(fp.n_blend_items + fp.n_inv_items) * kSplit;
+    const unsigned grid = (unsigned)(fp.n_blend_items + fp.n_inv_items);
     if (grid == 0) return;
     const size_t smem = sizeof(BlendSmem);
-    ensure_smem_attr((const void*)k_blend<true, false>, (int)smem);
-    ensure_smem_attr((const void*)k_blend<false, false>, (int)smem);
-    ensure_smem_attr((const void*)k_blend<true, true>, (int)smem);
-    ensure_smem_attr((const void*)k_blend<false, true>, (int)smem);
-    if (fp.ewa) {
-        if (fp.counters) k_blend<true, true><<<grid, kBT, smem, st>>>(fp, fb, rgba, depth);
-        else k_blend<false, true><<<grid, kBT, smem, st>>>(fp, fb, rgba, depth);
-    } else {
-        if (fp.counters) k_blend<true, false><<<grid, kBT, smem, st>>>(fp, fb, rgba, depth);
-        else k_blend<false, false><<<grid, kBT, smem, st>>>(fp, fb, rgba, depth);
+    auto go = [&](auto kern) {
+        ensure_smem_attr((const void*)kern, (int)smem);
+        kern<<<grid, kBT, smem, st>>>(fp, fb, rgba, depth);
+    };
+    const int sel = (fp.counters ? 4 : 0) | (fp.ewa ? 2 : 0) | (fp.staging == VRS_STAGING_TMA ? 1 : 0);
+    switch (sel) {
+        case 0: go(k_blend<false, false, false>); break;
+        case 1: go(k_blend<false, false, true>); break;
+        case 2: go(k_blend<false, true, false>); break;
+        case 3: go(k_blend<false, true, true>); break;
+        case 4: go(k_blend<true, false, false>); break;
+        case 5: go(k_blend<true, false, true>); break;
+        case 6: go(k_blend<true, true, false>); break;
+        default: go(k_blend<true, true, true>); break;
     }
 }
 

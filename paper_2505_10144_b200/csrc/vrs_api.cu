@@ -93,6 +93,7 @@ struct vrs_context {
     uint64_t gen_counter = 1;
     // last frame
     FrameParams fp{};
+    int32_t staging = VRS_STAGING_THREADS;           // blend record staging (vrs_set_staging_mode)
     bool have_frame = false;
     bool last_two_pass = false;                      // last frame = internal 2n-view two-pass frame
     cudaStream_t last_stream = nullptr;
@@ -164,7 +165,8 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     if (cfg->max_views < 1 || cfg->max_views > VRS_MAX_VIEWS || cfg->max_gaussians < 0 || cfg->max_pairs < 1 ||
         cfg->max_pairs >= (int64_t)1 << 30 || cfg->max_width < 1 || cfg->max_height < 1 ||
         (cfg->assign_tile != 16 && cfg->assign_tile != 32) || cfg->window_k != kWindow || (cfg->projection != 0 && cfg->projection != 1) ||
-        !(cfg->near_plane > 0.0f) || (int64_t)cfg->max_views * cfg->max_gaussians >= ((int64_t)1 << 32))
+        !(cfg->near_plane > 0.0f) || (int64_t)cfg->max_views * cfg->max_gaussians >= ((int64_t)1 << 32) ||
+        cfg->max_gaussians >= ((int64_t)1 << 24))  // the blend stages g in 24 bits beside an 8-warp mask
         return VRS_E_INVALID_ARG;
     vrs_context* ctx = new vrs_context();
     ctx->cfg = *cfg;
@@ -435,6 +437,7 @@ static vrs_status prepare_frame(vrs_context* ctx, int nv, const vrs_camera* cams
     fp.counters = ctx->counters;
     fp.no_cull = ctx->no_cull;
     fp.resort = ctx->resort;
+    fp.staging = ctx->staging;
     fp.ewa = ctx->cfg.projection;
     fp.N = ctx->N;
     fp.pair_cap = ctx->cfg.max_pairs;
@@ -900,6 +903,14 @@ vrs_status vrs_set_resort_mode(vrs_context* ctx, int32_t mode, int32_t block_que
         return fail(ctx, VRS_E_INVALID_ARG, "resort mode must be 0 or 1");
     }
     ctx->resort = mode;
+    return VRS_OK;
+}
+
+vrs_status vrs_set_staging_mode(vrs_context* ctx, int32_t mode) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    if (mode != VRS_STAGING_THREADS && mode != VRS_STAGING_TMA)
+        return fail(ctx, VRS_E_INVALID_ARG, "staging mode must be VRS_STAGING_THREADS or VRS_STAGING_TMA");
+    ctx->staging = mode;
     return VRS_OK;
 }
 

@@ -30,7 +30,7 @@ def vrs():
 
 
 def render_both(vrs, oracle_mod, scene, cams, foveas=None, T=16, masks=None, max_pairs=1 << 22, counters=True,
-                no_cull=False, oracle_render=True, projection=0):
+                no_cull=False, oracle_render=True, projection=0, staging=0):
     W = max(c.width for c in cams)
     H = max(c.height for c in cams)
     r = vrs.Renderer(max_gaussians=max(scene.n, 1), max_views=len(cams), max_pairs=max_pairs, max_width=W,
@@ -41,6 +41,7 @@ def render_both(vrs, oracle_mod, scene, cams, foveas=None, T=16, masks=None, max
         r.set_mask(slot, m)
         o.set_mask(slot, m)
     r.vrs_set_instrumentation(counters=counters, no_cull=no_cull)
+    r.vrs_set_staging_mode(staging)
     rgba, depth = r.render(cams, foveas)
     torch.cuda.synchronize()
     g_imgs = vrs.vrs.split_views(rgba.cpu().numpy(), depth.cpu().numpy(), cams)
