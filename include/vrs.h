@@ -228,6 +228,21 @@ VRS_API vrs_status vrs_set_resort_mode(vrs_context* ctx, int32_t mode, int32_t b
  *     block's warps, completion on an mbarrier).
  * Applies to the flat (mode 0) blend from the next render.  Errors:
  * VRS_E_INVALID_ARG (unknown mode). */
+/* Sort order: VRS_SORT_STOPTHEPOP (default)
+ * = the method -- per-tile key depth at the tile's maximum point and
+ * the per-sample K = 16 resort window; VRS_SORT_Z = Mini-Splatting (z): one
+ * key depth per Gaussian, its view-space z, blended in list order (no
+ * per-sample resort, the 3DGS order that pops under rotation);
+ * VRS_SORT_DIST = Mini-Splatting (Dist): key depth |mu - o|, list order
+ * (pops under translation).  The per-sample alpha, depth output and
+ * termination are those of the method.  Takes effect from the next render.
+ * Errors: VRS_E_INVALID_ARG (unknown mode; a global sort with the
+ * hierarchical resort mode). */
+#define VRS_SORT_STOPTHEPOP 0
+#define VRS_SORT_Z 1
+#define VRS_SORT_DIST 2
+VRS_API vrs_status vrs_set_sort_mode(vrs_context* ctx, int32_t mode);
+
 #define VRS_STAGING_THREADS 0
 #define VRS_STAGING_TMA 1
 VRS_API vrs_status vrs_set_staging_mode(vrs_context* ctx, int32_t mode);

@@ -277,7 +277,7 @@ __device__ __forceinline__ int block_id_opaque() {
 #define GID(j) (S.mask[j] >> 8)
 #define MASKJ(j) S.mask[j]
 
-template <bool kCounters, bool kEwa, bool kTma>
+template <bool kCounters, bool kEwa, bool kTma, bool kGlobal>
 #ifndef VRS_BLEND_MINB
 #define VRS_BLEND_MINB 4
 #endif
@@ -370,6 +370,11 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
     // order key: insert into the window, pop the minimum
     auto contribute = [&](const unsigned long long key, const float alpha, const uint32_t pos) {
         if (kCounters) n_contrib++;
+        if constexpr (kGlobal) {  // global-sort baselines (N3): no window, list order
+            blend_one(key, alpha);
+            if (kCounters && done) stop_pos = pos;
+            return;
+        }
         const unsigned long long kh = WK(hk);
         const bool direct = key < kh;  // the new entry is the minimum
         const float ah = WA(hk);
@@ -556,7 +561,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
 #undef POS_OF
     // drain the window in order (sentinels pop as no-ops)
 #pragma unroll 1
-    for (int k = 0; k < kWindow && !done; k++) {
+    for (int k = 0; k < kWindow && !done && !kGlobal; k++) {
         blend_one(WK(hk), WA(hk));
         hk = (hk + kSlotBytes) & kRingMask;
     }
@@ -604,7 +609,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         // evaluations: list entries visited before termination
         const unsigned long long ev = done ? (unsigned long long)(stop_pos - rb + 1) : (unsigned long long)(re - rb);
         const bool in_img = (px < v.W && py < v.H);
-        const bool overflowed = n_contrib > (uint32_t)kWindow;
+        const bool overflowed = !kGlobal && n_contrib > (uint32_t)kWindow;
         unsigned long long c0 = in_img ? ev : 0ull, c1 = in_img ? n_contrib : 0u,
                            c2 = (in_img && overflowed) ? 1u : 0u, c3 = (in_img && done) ? 1u : 0u;
 #pragma unroll
@@ -677,16 +682,25 @@ void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* r
         ensure_smem_attr((const void*)kern, (int)smem);
         kern<<<grid, kBT, smem, st>>>(fp, fb, rgba, depth);
     };
-    const int sel = (fp.counters ? 4 : 0) | (fp.ewa ? 2 : 0) | (fp.staging == VRS_STAGING_TMA ? 1 : 0);
+    const int sel = (fp.counters ? 8 : 0) | (fp.ewa ? 4 : 0) | (fp.staging == VRS_STAGING_TMA ? 2 : 0) |
+                    (fp.sort_mode != VRS_SORT_STOPTHEPOP ? 1 : 0);
     switch (sel) {
-        case 0: go(k_blend<false, false, false>); break;
-        case 1: go(k_blend<false, false, true>); break;
-        case 2: go(k_blend<false, true, false>); break;
-        case 3: go(k_blend<false, true, true>); break;
-        case 4: go(k_blend<true, false, false>); break;
-        case 5: go(k_blend<true, false, true>); break;
-        case 6: go(k_blend<true, true, false>); break;
-        default: go(k_blend<true, true, true>); break;
+        case 0: go(k_blend<false, false, false, false>); break;
+        case 1: go(k_blend<false, false, false, true>); break;
+        case 2: go(k_blend<false, false, true, false>); break;
+        case 3: go(k_blend<false, false, true, true>); break;
+        case 4: go(k_blend<false, true, false, false>); break;
+        case 5: go(k_blend<false, true, false, true>); break;
+        case 6: go(k_blend<false, true, true, false>); break;
+        case 7: go(k_blend<false, true, true, true>); break;
+        case 8: go(k_blend<true, false, false, false>); break;
+        case 9: go(k_blend<true, false, false, true>); break;
+        case 10: go(k_blend<true, false, true, false>); break;
+        case 11: go(k_blend<true, false, true, true>); break;
+        case 12: go(k_blend<true, true, false, false>); break;
+        case 13: go(k_blend<true, true, false, true>); break;
+        case 14: go(k_blend<true, true, true, false>); break;
+        default: go(k_blend<true, true, true, true>); break;
     }
 }
 

@@ -601,7 +601,12 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
                 rec[3] = make_float4(p.A[0], p.A[1], p.A[2], p.A[3]);
                 rec[4] = make_float4(p.A[4], p.A[5], p.bv[0], p.bv[1]);
                 rec[5] = make_float4(p.bv[2], p.sigma, p.eps, __uint_as_float(r01));
-                reinterpret_cast<float*>(rec + 6)[3] = __uint_as_float(r23);  // (colour .xyz: k_color)
+                // rec[6] = (global-sort key depth (N3: view-space z or |mu - o|), -, -, rect23)
+                float* r6 = reinterpret_cast<float*>(rec + 6);
+                r6[0] = (fp.sort_mode == VRS_SORT_Z) ? p.muc[2]
+                                                     : sqrtf(dot3(p.muc[0], p.muc[1], p.muc[2], p.muc[0], p.muc[1],
+                                                                  p.muc[2]));
+                r6[3] = __uint_as_float(r23);
                 rec[7] = make_float4(p.bbox[0], p.bbox[1], p.bbox[2], p.bbox[3]);
             }
         }
@@ -704,7 +709,9 @@ __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const Fram
 #endif
     s.A[0] = r3.x; s.A[1] = r3.y; s.A[2] = r3.z; s.A[3] = r3.w;
     s.A[4] = r4.x; s.A[5] = r4.y; s.bx = r4.z; s.by = r4.w; s.bz = r5.x;
-    const float td = tile_depth(s, hx, hy, hz, fp.near_plane);
+    // StopThePop per-tile depth at x_hat (O8), or the global-sort baselines' per-Gaussian depth (N3)
+    const float td = (fp.sort_mode == VRS_SORT_STOPTHEPOP) ? tile_depth(s, hx, hy, hz, fp.near_plane)
+                                                            : __ldg(reinterpret_cast<const float*>(rec + 6));
     const uint64_t tile = (uint64_t)(v.tile_base + ty * v.tw + tx);
     key = (tile << 32) | (uint64_t)__float_as_uint(td);
     gout = (uint32_t)((int64_t)sidx - (int64_t)vi * fp.N);

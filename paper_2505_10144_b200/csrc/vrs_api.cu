@@ -94,6 +94,7 @@ struct vrs_context {
     // last frame
     FrameParams fp{};
     int32_t staging = VRS_STAGING_THREADS;           // blend record staging (vrs_set_staging_mode)
+    int32_t sort_mode = VRS_SORT_STOPTHEPOP;         // vrs_set_sort_mode (N3 baselines)
     bool have_frame = false;
     bool last_two_pass = false;                      // last frame = internal 2n-view two-pass frame
     cudaStream_t last_stream = nullptr;
@@ -438,6 +439,7 @@ static vrs_status prepare_frame(vrs_context* ctx, int nv, const vrs_camera* cams
     fp.no_cull = ctx->no_cull;
     fp.resort = ctx->resort;
     fp.staging = ctx->staging;
+    fp.sort_mode = ctx->sort_mode;
     fp.ewa = ctx->cfg.projection;
     fp.N = ctx->N;
     fp.pair_cap = ctx->cfg.max_pairs;
@@ -858,7 +860,8 @@ vrs_status vrs_backward(vrs_context* ctx, const float* rgba, const float* depth,
         !grad_logits || !grad_sh)
         return fail(ctx, VRS_E_INVALID_ARG, "null pointer");
     const FrameParams& fp = ctx->fp;
-    if (fp.ewa || fp.resort != 0 || fp.out_fmt != VRS_OUT_F32 || ctx->last_two_pass)
+    if (fp.ewa || fp.resort != 0 || fp.sort_mode != VRS_SORT_STOPTHEPOP || fp.out_fmt != VRS_OUT_F32 ||
+        ctx->last_two_pass)
         return fail(ctx, VRS_E_STATE, "backward needs a frame rendered with the Optimal Projection, the K = 16 "
                                       "window and F32 outputs by vrs_render_views");
     for (int i = 0; i < fp.n_views; i++)
@@ -899,10 +902,22 @@ vrs_status vrs_set_resort_mode(vrs_context* ctx, int32_t mode, int32_t block_que
             return fail(ctx, VRS_E_INVALID_ARG, "hierarchical mode: only K_B = 8, K_P = 8 are compiled");
         if (ctx->cfg.projection != 0)
             return fail(ctx, VRS_E_INVALID_ARG, "hierarchical mode needs the Optimal Projection");
+        if (ctx->sort_mode != VRS_SORT_STOPTHEPOP)
+            return fail(ctx, VRS_E_INVALID_ARG, "hierarchical mode needs the StopThePop sort");
     } else {
         return fail(ctx, VRS_E_INVALID_ARG, "resort mode must be 0 or 1");
     }
     ctx->resort = mode;
+    return VRS_OK;
+}
+
+vrs_status vrs_set_sort_mode(vrs_context* ctx, int32_t mode) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    if (mode != VRS_SORT_STOPTHEPOP && mode != VRS_SORT_Z && mode != VRS_SORT_DIST)
+        return fail(ctx, VRS_E_INVALID_ARG, "sort mode must be VRS_SORT_STOPTHEPOP, VRS_SORT_Z or VRS_SORT_DIST");
+    if (mode != VRS_SORT_STOPTHEPOP && ctx->resort != 0)
+        return fail(ctx, VRS_E_INVALID_ARG, "a global sort has no per-sample resort: set resort mode 0 first");
+    ctx->sort_mode = mode;
     return VRS_OK;
 }
 

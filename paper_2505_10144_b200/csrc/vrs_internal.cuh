@@ -71,6 +71,7 @@ struct FrameParams {
     int32_t resort;          // 0 = per-sample window K = 16; 1 = hierarchical
     int32_t out_fmt;         // VRS_OUT_F32 or VRS_OUT_RGBA8_D16F (final output pixels)
     int32_t staging;         // blend staging of the splat records: VRS_STAGING_THREADS or VRS_STAGING_TMA
+    int32_t sort_mode;       // VRS_SORT_STOPTHEPOP (per-tile key depth + window) or a global-sort baseline (N3)
     int32_t n_blend_items;   // blend items of all views (flat blend grid = n_blend_items + n_inv_items)
     int32_t n_inv_items;     // invisible-tile fill items of all views
     int64_t N;

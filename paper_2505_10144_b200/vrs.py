@@ -18,9 +18,10 @@ LIB_PATH = os.environ.get("VRS_LIB") or os.path.join(_HERE, "libvrs.so")  # VRS_
 VRS_OK, VRS_E_INVALID_ARG, VRS_E_INGEST, VRS_E_CUDA, VRS_E_OOM, VRS_E_CAPACITY, VRS_E_STATE = range(7)
 VRS_MAX_VIEWS = 8
 VRS_STAGING_THREADS, VRS_STAGING_TMA = 0, 1
+VRS_SORT_STOPTHEPOP, VRS_SORT_Z, VRS_SORT_DIST = 0, 1, 2
 EXPORTS = ["vrs_abi_version", "vrs_create", "vrs_destroy", "vrs_last_error", "vrs_upload_gaussians",
            "vrs_set_visibility_mask", "vrs_render_views", "vrs_render_views_host", "vrs_set_instrumentation",
-           "vrs_set_resort_mode", "vrs_set_staging_mode", "vrs_set_output_format", "vrs_backward",
+           "vrs_set_resort_mode", "vrs_set_sort_mode", "vrs_set_staging_mode", "vrs_set_output_format", "vrs_backward",
            "vrs_render_views_two_pass", "vrs_get_frame_stats", "vrs_debug_counts", "vrs_debug_pairs", "vrs_debug_ranges", "vrs_debug_splats",
            "vrs_debug_tile_info", "vrs_debug_set_sort_smem_cap", "vrs_sort_pairs", "vrs_exclusive_scan"]
 
@@ -85,6 +86,7 @@ def lib():
             "vrs_set_instrumentation": (i32, [vp, i32, i32]),
             "vrs_set_resort_mode": (i32, [vp, i32, i32, i32]),
             "vrs_set_staging_mode": (i32, [vp, i32]),
+            "vrs_set_sort_mode": (i32, [vp, i32]),
             "vrs_set_output_format": (i32, [vp, i32]),
             "vrs_backward": (i32, [vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp]),
             "vrs_get_frame_stats": (i32, [vp, C.POINTER(vrs_frame_stats)]),
@@ -223,6 +225,10 @@ class Renderer:
     def vrs_set_resort_mode(self, mode, block_queue=0, pixel_window=0):
         """0 = per-sample window K = 16; 1 = hierarchical (K_B = 8 block queue, K_P = 8 window)."""
         self._check(lib().vrs_set_resort_mode(self.h, int(mode), int(block_queue), int(pixel_window)))
+
+    def vrs_set_sort_mode(self, mode):
+        """VRS_SORT_STOPTHEPOP (0, default), VRS_SORT_Z (1) or VRS_SORT_DIST (2): the N3 global-sort baselines."""
+        self._check(lib().vrs_set_sort_mode(self.h, int(mode)))
 
     def vrs_set_staging_mode(self, mode):
         """VRS_STAGING_THREADS (0, default): thread loads; VRS_STAGING_TMA (1): TMA bulk copies."""
