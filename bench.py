@@ -61,6 +61,9 @@ CONFIGS = {
     "c9": dict(n=500_000, scale_mul=1.0, sh=3, fovea=False, T=16, masks=False, seed=2,
                desc="training step (SURVEY N4): C2 scene, stereo 2x2064x2208 non-foveated (T_a = 16), forward "
                     "render + vrs_backward of synthetic gradient images to all raw parameters"),
+    "c10": dict(n=500_000, scale_mul=1.0, sh=3, fovea=True, T=32, masks=True, seed=2,
+                desc="C2 workload with the paper's global-sort baselines (SURVEY N3, P:456): Mini-Splatting (z) "
+                     "and (Dist) orders blended in list order, vs OP + StopThePop; pairs and blend ms per order"),
     "c6": dict(n=500_000, scale_mul=1.0, sh=3, fovea=True, T=32, masks=True, seed=2, two_pass=True,
                desc="C2 workload rendered with the paper's two-pass foveated baseline (App. A): full-res "
                     "centre crop + half-res masked periphery, bilinear upsample + blend (SURVEY N1)"),
@@ -76,6 +79,8 @@ def parse():
     ap.add_argument("--impl", default="vrs", choices=["vrs", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--projection", type=int, default=0, help="0 = Optimal Projection, 1 = EWA baseline")
+    ap.add_argument("--staging", default="threads", choices=["threads", "tma"],
+                    help="blend record staging: block threads (default) or the TMA bulk-copy engine")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true")
@@ -210,31 +215,49 @@ def cpu_baseline(scene, cams, fov, masks, T, budget_s=15.0, threads=0):
 
 
 def run_reference(args):
+    """The oracle (the paper published no code) on the host cores.  Each step is a
+    bounded sample of the workload -- the whole per-Gaussian / pairs / sort /
+    ranges pass of the frame plus a random sample of output pixels -- sized so
+    the K + W steps end within ~2.5 minutes; ms_per_step is the measured time of
+    one such step, value the stereo frames/s extrapolated per pixel."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     cfg = CONFIGS[args.config]
     scene, cams, fov, masks = make_workload(args.config)
-    # each step: the whole per-Gaussian / pairs / sort / ranges pass of the frame plus a random pixel
-    # sample; the pixel budget shrinks with K + W so the whole run stays at ~2.5 minutes of CPU time
     n_runs = max(1, args.steps + args.warmup)
     t_prep = cpu_baseline(scene, cams, fov, masks, cfg["T"], budget_s=0.0)["prep_s"]
     budget = max(0.3, 150.0 / n_runs - t_prep) + t_prep
-    vals = []
+    vals, step_s = [], []
     for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
         r = cpu_baseline(scene, cams, fov, masks, cfg["T"], budget_s=budget)
+        dt = time.perf_counter() - t0
         if s >= args.warmup:
             vals.append(r)
+            step_s.append(dt)
     v = statistics.median([r["value"] for r in vals])
     line = {"metric": METRIC if args.config == "c2" else METRIC + f" [{args.config}]", "value": v,
             "unit": vals[0]["unit"], "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
-            "config": {"workload": args.config, "desc": cfg["desc"]},
+            "warmup": args.warmup, "ms_per_step": 1000.0 * float(np.mean(step_s)), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": workload_config(args.config, scene, cams),
+            "reference_step": "a bounded sample of the frame (see cpu_baseline.sample); value = full stereo "
+                              "frames/s extrapolated per pixel, ms_per_step = measured time of one sampled step",
             "cpu_baseline": {"value": v, "unit": vals[0]["unit"], "cores": vals[0]["cores"], "kind": "oracle",
                              "sample": vals[0]["sample"]},
             "e2e": {"value": v, "unit": vals[0]["unit"], "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def workload_config(name, scene, cams, world=1, extra=None):
+    """The bench line's config object (the same for both arms)."""
+    cfg = CONFIGS[name]
+    out = {"workload": name, "desc": cfg["desc"], "gaussians": int(scene.n), "views": len(cams),
+           "resolution": [cams[0].width, cams[0].height], "assign_tile": cfg["T"],
+           "foveated": bool(cfg["fovea"]), "parallelism": f"views x{world} (replicated scene, weak)"}
+    out.update(extra or {})
+    return out
 
 
 def run_c7(args):
@@ -391,6 +414,56 @@ def run_c5(args):
     print(json.dumps(line), flush=True)
 
 
+def run_c10(args):
+    """Config C10: the C2 frame rendered with the
+    paper's global-sort baselines -- Mini-Splatting (z) and (Dist): one depth per
+    Gaussian, tile lists blended in list order, no per-pixel resort -- next to the
+    method (OP + StopThePop K = 16): pairs per eye, contributions, blend and frame
+    ms, and the PSNR of each baseline frame against the method's frame."""
+    import torch
+    from paper_2505_10144_b200 import Renderer
+    cfg = CONFIGS["c10"]
+    scene, cams, fov, masks = make_workload("c10")
+    r = Renderer(max_gaussians=scene.n, max_views=2, max_pairs=8 << 20, max_width=sg.QUEST_W,
+                 max_height=sg.QUEST_H, assign_tile=32)
+    r.upload(scene)
+    for k, m in masks.items():
+        r.set_mask(k, m)
+    stream = torch.cuda.Stream()
+    rgba, depth = r.alloc_outputs(cams)
+    rows, frames = [], {}
+    for mode, name in ((0, "OP + StopThePop (K = 16)"), (1, "Mini-Splatting (z)"), (2, "Mini-Splatting (Dist)")):
+        r.vrs_set_sort_mode(mode)
+        r.vrs_set_instrumentation(counters=1, timing=0)
+        r.render(cams, fov, rgba, depth, stream=stream)
+        st = r.stats()
+        frames[mode] = rgba.clone()
+        r.vrs_set_instrumentation(counters=0, timing=1)
+        for _ in range(args.warmup):
+            r.render(cams, fov, rgba, depth, stream=stream)
+        ms, blend = [], []
+        for _ in range(args.steps):
+            r.render(cams, fov, rgba, depth, stream=stream)
+            t = r.stats()["stage_ms"]
+            ms.append(t[7])
+            blend.append(t[5])
+        row = {"order": name, "sort_mode": mode, "pairs_per_eye": st["pairs"] / 2,
+               "contributions": st["contributions"], "evaluations": st["evaluations"],
+               "frame_ms": float(np.median(ms)), "blend_ms": float(np.median(blend))}
+        if mode:
+            d = (frames[mode][:, :3] - frames[0][:, :3]).double()
+            mse = float((d * d).mean())
+            row["psnr_vs_method_db"] = 10.0 * math.log10(1.0 / mse) if mse > 0 else None
+        rows.append(row)
+    r.close()
+    line = {"metric": "C10 global-sort baselines (N3): stereo frames/s of Mini-Splatting (z) order at C2",
+            "value": 1000.0 / rows[1]["frame_ms"], "unit": "stereo frames/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": rows[1]["frame_ms"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config("c10", scene, cams), "orders": rows}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -401,6 +474,8 @@ def main():
         return run_c7(args)
     if args.config == "c9":
         return run_c9(args)
+    if args.config == "c10":
+        return run_c10(args)
     import torch
     import torch.distributed as dist
 
@@ -442,6 +517,7 @@ def main():
     render = r.render_two_pass if two_pass else r.render
     if cfg.get("resort"):
         r.vrs_set_resort_mode(cfg["resort"])
+    r.vrs_set_staging_mode(1 if args.staging == "tma" else 0)
     r.upload(scene)
     for k, m in masks.items():
         r.set_mask(k, m)
@@ -567,14 +643,20 @@ def main():
         v8, s8, b8 = measure_e2e(1)
         v32, s32, b32 = measure_e2e(0)
         what = "render_two_pass" if two_pass else "render"
-        e2e = {"value": v8, "unit": unit, "h2d_bytes_per_step": cam_bytes, "d2h_bytes_per_step": b8,
-               "sync_value": s8, "format": "VRS_OUT_RGBA8_D16F (RGBA unorm8 + depth binary16, the HMD display format)",
-               "f32": {"value": v32, "sync_value": s32, "d2h_bytes_per_step": b32,
-                       "format": "VRS_OUT_F32 (RGBA float32 + depth float32)"},
+        e2e = {"value": v32, "unit": unit, "h2d_bytes_per_step": cam_bytes, "d2h_bytes_per_step": b32,
+               "sync_value": s32, "format": "VRS_OUT_F32 (RGBA float32 + depth float32: the frame the parity "
+                                            "tolerances are stated on)",
+               "display_packed": {"value": v8, "sync_value": s8, "d2h_bytes_per_step": b8,
+                                  "format": "VRS_OUT_RGBA8_D16F (RGBA unorm8 + depth binary16, the HMD display "
+                                            "format; depth quantised to 2^-11 relative, outside the 1e-4 bar)"},
                "note": what + " into device buffers with the D2H of the frame into pinned host memory on a copy "
                        "stream, two frames in flight (value); sync_value = " +
                        ("render_two_pass + D2H + sync" if two_pass else "vrs_render_views_host") +
                        " per frame; host wall clock; camera/fovea structs travel as kernel parameters"}
+
+    # ---- multi-GPU end to end: every step's frames gathered to rank 0 (grouped NCCL send/recv on a
+    # side stream, overlapping the next step's render; SURVEY §8e "final frame gather")
+    gather = measure_gather(args, r, render, cams, fov, stream, rank, world, local, one_gpu) if world > 1 else None
 
     if rank == 0:
         peaks, src = measured_peaks()
@@ -595,9 +677,10 @@ def main():
             except Exception:
                 traffic = None
         n_views = len(cams)
-        # k_cull, k_preprocess, k_color, k_tiletest_direct, k_tile_scan, k_ovf_bucket, k_tile_sort,
-        # k_blend x 2 (LowRes items, full-rate items), k_compose (+ k_two_pass_combine for the two-pass baseline)
-        launches_per_step = 10 + (1 if two_pass else 0)
+        # k_cull, k_preprocess, k_color, k_tiletest_direct, k_tile_scan, k_ovf_bucket, k_tile_sort and ONE
+        # k_blend (blend items, invisible fills and the in-launch compose); the hierarchical mode blends with
+        # k_blend_hier + k_compose; the two-pass baseline adds k_two_pass_combine
+        launches_per_step = 8 + (1 if cfg.get("resort") else 0) + (1 if two_pass else 0)
         line = {
             "metric": METRIC if args.config == "c2" else METRIC + f" [{args.config}]",
             "value": world * 1000.0 / ms_max,
@@ -605,10 +688,9 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": {"workload": args.config, "desc": cfg["desc"], "gaussians": scene.n, "views": n_views,
-                       "resolution": [cams[0].width, cams[0].height], "assign_tile": cfg["T"],
-                       "l2": "flushed between steps (256 MB write, outside the event pair)" if not args.no_flush
-                       else "not flushed", "parallelism": f"views x{world} (replicated scene, weak)"},
+            "config": workload_config(args.config, scene, cams, world, {
+                "l2": "flushed between steps (256 MB write, outside the event pair)" if not args.no_flush
+                else "not flushed", "staging": args.staging}),
             "stage_ms": dict(zip(names, stage_ms)),
             "workload_counters": {k: counters[k] for k in ("pairs", "samples", "evaluations", "contributions",
                                                            "overflow_samples", "terminated_samples", "work_items",
@@ -625,6 +707,7 @@ def main():
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "e2e": e2e,
+            "gather": gather,
             "context": {"paper_rtx4090_ms_per_stereo_frame_0.5M_scenes": [9.89, 12.19],
                         "paper_headline": "72+ FPS on RTX 4090 at 2x2064x2272 (P:91, P:107)"},
         }
@@ -637,6 +720,72 @@ def main():
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
+
+
+def measure_gather(args, r, render, cams, fov, stream, rank, world, local, one_gpu):
+    """Render + gather per step: each rank renders its step's frame into one of two
+    device buffers; a side stream waits for it and runs the grouped send/recv of
+    the frame (RGBA f32 + depth f32) to rank 0, which receives every rank's frame
+    into its own double buffer; a buffer is re-rendered only after its send
+    finished.  Host wall clock over the steps, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    n = min(args.steps, 20)
+    cstream = torch.cuda.Stream(device=local)
+    d = [r.alloc_outputs(cams) for _ in range(2)]
+    sent = [torch.cuda.Event() for _ in range(2)]
+    rendered = [torch.cuda.Event() for _ in range(2)]
+    recv = None
+    if rank == 0:
+        recv = [[r.alloc_outputs(cams) for _ in range(world)] for _ in range(2)]
+    bytes_per_rank = int(d[0][0].numel() * 4 + d[0][1].numel() * 4)
+
+    def step(s):
+        b = s & 1
+        cs = step_cams(args.config, cams, s, rank, world)
+        if s >= 2:
+            stream.wait_event(sent[b])
+        with torch.cuda.stream(stream):
+            render(cs, fov, d[b][0], d[b][1], stream=stream)
+            rendered[b].record(stream)
+        cstream.wait_event(rendered[b])
+        with torch.cuda.stream(cstream):
+            if one_gpu:  # gloo test hook: host tensors
+                cstream.synchronize()
+                frames = [d[b][0].cpu(), d[b][1].cpu()]
+            else:
+                frames = [d[b][0], d[b][1]]
+            if rank == 0:
+                ops = []
+                for src in range(1, world):
+                    for k in range(2):
+                        buf = recv[b][src][k] if not one_gpu else torch.empty_like(frames[k])
+                        ops.append(dist.P2POp(dist.irecv, buf, src))
+            else:
+                ops = [dist.P2POp(dist.isend, t, 0) for t in frames]
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+            sent[b].record(cstream)
+
+    for s in range(2):
+        step(s)
+    torch.cuda.synchronize()
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for s in range(n):
+        step(s)
+    cstream.synchronize()
+    torch.cuda.synchronize()
+    t = time.perf_counter() - t0
+    tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t = float(tt.item())
+    unit = "stereo frames/s" if len(cams) == 2 else "frames/s"
+    return {"value": world * n / t, "unit": unit, "steps": n, "ms_per_step": 1000.0 * t / n,
+            "gathered_bytes_per_step": bytes_per_rank * (world - 1),
+            "note": "render + grouped send/recv of every rank's RGBA f32 + depth f32 frame to rank 0 on a side "
+                    "stream (double-buffered), host wall clock, max over ranks; `value` above is render-only"}
 
 
 def compare_flat(r, render, cams, fov, rgba, depth, stream, counters):
