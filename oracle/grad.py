@@ -71,13 +71,17 @@ def render_fixed_order(params, cams, orders, sh_degree, near=0.2, background=(0.
     mu, cov, icov, sig = activate(params["means"], params["quats"], params["log_scales"], params["logits"])
     bg = torch.tensor(background, dtype=torch.float64)
     outs = []
-    for cam, (counts, seq) in zip(cams, orders):
+    for cam, order in zip(cams, orders):
+        # order = (counts (H, W), seq) for a whole view, or (counts, seq, y0) for the row block
+        # [y0, y0 + H) of it (the gradient of a sum over pixels can be taken block by block)
+        counts, seq = order[0], order[1]
+        y0 = order[2] if len(order) > 2 else 0
         H, W = counts.shape
         Wm = torch.tensor(np.asarray(cam.R_wc, np.float64).reshape(3, 3))
         o = torch.tensor(np.asarray(cam.position, np.float64))
         g = torch.as_tensor(seq.astype(np.int64))
         pix = torch.as_tensor(np.repeat(np.arange(H * W), counts.reshape(-1)))
-        jj, ii = pix // W, pix % W
+        jj, ii = pix // W + y0, pix % W
         x = ((ii.double() + 0.5) - cam.cx) / cam.fx
         y = ((jj.double() + 0.5) - cam.cy) / cam.fy
         # O1-O5 for the blended Gaussians (per entry; the same Gaussian repeats)
@@ -136,6 +140,27 @@ def to_params(scene, requires_grad=True):
     p = {"means": scene.means, "quats": scene.quats, "log_scales": scene.log_scales, "logits": scene.logits,
          "sh": scene.sh}
     return {k: torch.tensor(np.asarray(v, np.float64), requires_grad=requires_grad) for k, v in p.items()}
+
+
+def gradients_blocked(scene, cams, orders, g_rgba, g_depth, rows=64, near=0.2):
+    """gradients() for large frames: L is a sum over pixels and every pixel's
+    blend order is contiguous in seq, so the autograd graph is built and
+    back-propagated one block of `rows` image rows at a time (leaf gradients
+    accumulate); returns the gradient dict only."""
+    p = to_params(scene)
+    for cam, (counts, seq), gr, gd in zip(cams, orders, g_rgba, g_depth):
+        H, W = counts.shape
+        off = np.concatenate([[0], np.cumsum(counts.reshape(-1))])
+        for y0 in range(0, H, rows):
+            y1 = min(H, y0 + rows)
+            if not (np.any(gr[y0:y1]) or np.any(gd[y0:y1])):
+                continue  # no loss on these rows: no gradient from them
+            sub = (counts[y0:y1], seq[off[y0 * W]:off[y1 * W]], y0)
+            (rgba, dep), = render_fixed_order(p, [cam], [sub], scene.sh_degree, near)
+            L = (rgba * torch.as_tensor(np.asarray(gr[y0:y1], np.float64))).sum() + \
+                (dep * torch.as_tensor(np.asarray(gd[y0:y1], np.float64))).sum()
+            L.backward()
+    return {k: v.grad.numpy() for k, v in p.items()}
 
 
 def gradients(scene, cams, orders, g_rgba, g_depth, near=0.2):

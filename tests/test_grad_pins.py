@@ -97,3 +97,20 @@ def test_g3_on_axis_closed_forms(oracle_mod):
     # dA/d log s_k summed over the three axes (isotropic): da/dq * dq/d(log s) with s^2 in den
     dq_dlogs = -q * (2 * f * f * s * s / (z * z)) / den
     assert abs(g["log_scales"][0].sum() - (-a / 2) * dq_dlogs) < 1e-6 * a
+
+
+def test_blocked_gradients_equal_whole_frame(oracle_mod):
+    """gradients_blocked (row blocks, for large frames) = gradients (one graph)."""
+    import scenegen as sg
+    from oracle import grad
+    scene = sg.random_scene(3, n=120, sh_degree=1)
+    cam = sg.look_camera((0, 0, 0), f=40.0, width=48, height=40)
+    o = oracle_mod.Oracle(scene).prepare([cam], assign_tile=16)
+    orders = [o.blend_orders(0)]
+    rng = np.random.default_rng(2)
+    gr = [rng.normal(size=(40, 48, 4))]
+    gd = [rng.normal(size=(40, 48)) * 0.1]
+    ref, _ = grad.gradients(scene, [cam], orders, gr, gd)
+    got = grad.gradients_blocked(scene, [cam], orders, gr, gd, rows=7)
+    for k in ref:
+        np.testing.assert_allclose(got[k], ref[k], rtol=1e-9, atol=1e-12)
