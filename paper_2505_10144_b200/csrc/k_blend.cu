@@ -167,6 +167,9 @@ constexpr int kWarps = kBT / 32;
 #ifndef VRS_BLEND_BATCH
 #define VRS_BLEND_BATCH 80
 #endif
+#ifndef VRS_SELMASK
+#define VRS_SELMASK 1
+#endif
 constexpr int kBatch = VRS_BLEND_BATCH;  // list entries staged per shared-memory batch
 constexpr uint32_t kStageBytes = 96;     // r0..r5 of a splat record
 static_assert(kBatch <= kBT && kBatch >= 10, "one staging thread per entry; the compose triggers reuse mask[]");
@@ -376,11 +379,31 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
             return;
         }
         const unsigned long long kh = WK(hk);
-        const bool direct = key < kh;  // the new entry is the minimum
         const float ah = WA(hk);
+#if VRS_SELMASK
+        // one 64-bit compare, then bitwise selects (the compiler otherwise re-derives the
+        // comparison for every use)
+        uint32_t dm;  // all ones iff the new entry is the minimum
+        asm("{\n .reg .pred p;\n setp.lo.u64 p, %1, %2;\n selp.u32 %0, 0xffffffff, 0, p;\n}"
+            : "=r"(dm)
+            : "l"(key), "l"(kh));
+        auto bsel = [](uint32_t a, uint32_t b, uint32_t m) {  // (a & m) | (b & ~m), opaque to the compiler
+            uint32_t r;
+            asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "r"(m));
+            return r;
+        };
+        const uint32_t klo = bsel((uint32_t)key, (uint32_t)kh, dm);
+        const uint32_t khi = bsel((uint32_t)(key >> 32), (uint32_t)(kh >> 32), dm);
+        const float asel = __uint_as_float(bsel(__float_as_uint(alpha), __float_as_uint(ah), dm));
+        blend_one(((unsigned long long)khi << 32) | klo, asel);
+        if (kCounters && done) stop_pos = pos;
+        if ((dm | (uint32_t)done) != 0u) return;
+#else
+        const bool direct = key < kh;  // the new entry is the minimum
         blend_one(direct ? key : kh, direct ? alpha : ah);
         if (kCounters && done) stop_pos = pos;
         if (direct || done) return;
+#endif
         hk = (hk + kSlotBytes) & kRingMask;
         // insertion from the tail (entries arrive nearly sorted); dst
         // is the hole, starting at the popped head's slot

@@ -34,10 +34,11 @@ __device__ __forceinline__ void set_rect(const ViewParams& v, int T, double xmin
     p.bbox[0] = (float)fmax(xmin, -2.0); p.bbox[1] = (float)fmin(xmax, W + 2.0);
     p.bbox[2] = (float)fmax(ymin, -2.0); p.bbox[3] = (float)fmin(ymax, H + 2.0);
     if (xmax < 0.0 || ymax < 0.0 || xmin > W || ymin > H) return;
-    p.rect[0] = max(0, (int)floor(fmax(xmin, 0.0) / T));
-    p.rect[1] = max(0, (int)floor(fmax(ymin, 0.0) / T));
-    p.rect[2] = min(v.tw - 1, (int)floor(fmin(xmax, W) / T));
-    p.rect[3] = min(v.th - 1, (int)floor(fmin(ymax, H) / T));
+    const double it = (T == 32) ? 0.03125 : 0.0625;  // 1/T, exact (T is 16 or 32)
+    p.rect[0] = max(0, (int)floor(fmax(xmin, 0.0) * it));
+    p.rect[1] = max(0, (int)floor(fmax(ymin, 0.0) * it));
+    p.rect[2] = min(v.tw - 1, (int)floor(fmin(xmax, W) * it));
+    p.rect[3] = min(v.th - 1, (int)floor(fmin(ymax, H) * it));
 }
 
 // Sigma_c = W Sigma W^T (T = W*Sigma, then T*W^T, each entry a dot3)
@@ -185,14 +186,11 @@ __device__ void project_splat(const ViewParams& v, float4 m4, float4 c0, float4 
     const double t2 = (double)p.qcut * lmax;
     const double sinb = sqrt(t2 / (1.0 + t2));
     const double ud0 = p.u[0], ud1 = p.u[1], ud2 = p.u[2];
-    {
-        const double xl = (0.0 - v.cx) / v.fx, xr = ((double)v.W - v.cx) / v.fx;
-        const double yt = (0.0 - v.cy) / v.fy, yb = ((double)v.H - v.cy) / v.fy;
-        const double N[4][3] = {{1.0, 0.0, -xl}, {-1.0, 0.0, xr}, {0.0, 1.0, -yt}, {0.0, -1.0, yb}};
+    {   // unit normals precomputed per view in double (the oracle divides by |n| here; a
+        // rounding apart, which the 1e-4 margin covers: the test only has to be conservative)
 #pragma unroll
         for (int k = 0; k < 4; k++) {
-            const double nn = sqrt(N[k][0] * N[k][0] + N[k][1] * N[k][1] + N[k][2] * N[k][2]);
-            const double nu = (N[k][0] * ud0 + N[k][1] * ud1 + N[k][2] * ud2) / nn;
+            const double nu = v.dplane[k][0] * ud0 + v.dplane[k][1] * ud1 + v.dplane[k][2] * ud2;
             if (nu < -(sinb + 1e-4)) return;
         }
     }
@@ -213,9 +211,7 @@ __device__ void project_splat(const ViewParams& v, float4 m4, float4 c0, float4 
                             (double)p.C[2] * e2d[i] * e2d[j];
                 G[i][j] = mf - (double)p.qcut * ud[i] * ud[j];
             }
-        const double Ki[3][3] = {{1.0 / v.fx, 0.0, -(double)v.cx / v.fx},
-                                 {0.0, 1.0 / v.fy, -(double)v.cy / v.fy},
-                                 {0.0, 0.0, 1.0}};
+        const double Ki[3][3] = {{v.kinv[0], 0.0, v.kinv[2]}, {0.0, v.kinv[1], v.kinv[3]}, {0.0, 0.0, 1.0}};
         double Tq[3][3], Q[3][3];
 #pragma unroll
         for (int i = 0; i < 3; i++)
@@ -242,9 +238,9 @@ __device__ void project_splat(const ViewParams& v, float4 m4, float4 c0, float4 
         const double a12 = Q[0][1] * Q[0][2] - Q[0][0] * Q[1][2];
         const double dx = a02 * a02 - a00 * a22, dy = a12 * a12 - a11 * a22;
         if (a22 != 0.0 && dx >= 0.0 && dy >= 0.0 && isfinite(dx) && isfinite(dy)) {
-            const double sx = sqrt(dx), sy = sqrt(dy);
-            const double xa = (a02 - sx) / a22, xb = (a02 + sx) / a22;
-            const double ya = (a12 - sy) / a22, yb = (a12 + sy) / a22;
+            const double sx = sqrt(dx), sy = sqrt(dy), ia = 1.0 / a22;
+            const double xa = (a02 - sx) * ia, xb = (a02 + sx) * ia;
+            const double ya = (a12 - sy) * ia, yb = (a12 + sy) * ia;
             xmin = fmin(xa, xb); xmax = fmax(xa, xb);
             ymin = fmin(ya, yb); ymax = fmax(ya, yb);
         } else {
@@ -465,10 +461,11 @@ __device__ void sh_color(const SceneDev& sc, int64_t g, int64_t N, int ncoef, fl
 __device__ __forceinline__ void load_gauss(const SceneDev& sc, int64_t g, int64_t N, float4& m4, float4& c0,
                                            float4& c1, float4& i0, float4& i1) {
     m4 = __ldg(&sc.mu[g]);
-    c0 = __ldg(&sc.cov[g]);
-    c1 = __ldg(&sc.cov[N + g]);
-    i0 = __ldg(&sc.icov[g]);
-    i1 = __ldg(&sc.icov[N + g]);
+    (void)N;
+    c0 = __ldg(&sc.geo[4 * g + 0]);
+    c1 = __ldg(&sc.geo[4 * g + 1]);
+    i0 = __ldg(&sc.geo[4 * g + 2]);
+    i1 = __ldg(&sc.geo[4 * g + 3]);
 }
 
 // Step 1a: cheap conservative cull over all Gaussians and views.  The
@@ -485,7 +482,7 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
     float smax = 0.0f;
     if (in) {
         m4 = __ldg(&sc.mu[g]);
-        smax = __ldg(&sc.cov[N + g]).w;
+        smax = __ldg(&sc.smax[g]);
     }
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ uint32_t s_wcnt[32];
@@ -556,6 +553,116 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
 #ifndef VRS_TT_MINB
 #define VRS_TT_MINB 4
 #endif
+#ifndef VRS_PP_WARP
+#define VRS_PP_WARP 1
+#endif
+#if VRS_PP_WARP
+// Warp-independent form: each warp takes 32 consecutive candidates per
+// iteration, scans their tile counts with shuffles, reserves its slice of the
+// test list (and of the visible-splat list) with one atomic per warp, and
+// writes the expansion itself (each output slot finds its owner lane by a
+// binary search over the warp's prefix sums, by shuffles) -- no block barrier,
+// so warps do not wait for each other.  The next iteration's Gaussian data is
+// prefetched into L2 while this one is projected.
+__global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb, int64_t test_cap) {
+    const int lane = threadIdx.x & 31;
+    const int64_t N = fp.N;
+    const uint32_t nc = *fb.cand_count;
+    const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+    const unsigned lt = (1u << lane) - 1u;
+    auto prefetch_l2 = [](const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); };
+    for (uint32_t b0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u; b0 < nc; b0 += nw * 32u) {
+        const uint32_t i = b0 + lane;
+        {
+            const uint32_t inext = i + nw * 32u;
+            if (inext < nc) {
+                const uint32_t sn = __ldg(fb.cand + inext);
+                int vn = 0;
+                while (vn + 1 < fp.n_views && (int64_t)sn >= (int64_t)(vn + 1) * N) vn++;
+                const int64_t gn = (int64_t)sn - (int64_t)vn * N;
+                prefetch_l2(sc.mu + gn);
+                prefetch_l2(sc.geo + 4 * gn);  // 64 B: one line (the array is 64-B aligned)
+            }
+        }
+        uint32_t cnt = 0, sidx = 0;
+        if (i < nc) {
+            sidx = fb.cand[i];
+            int vi = 0;  // view = number of view blocks of N below sidx (no 64-bit division)
+            while (vi + 1 < fp.n_views && (int64_t)sidx >= (int64_t)(vi + 1) * N) vi++;
+            const int64_t g = (int64_t)sidx - (int64_t)vi * N;
+            const ViewParams& v = fp.v[vi];
+            const float4 m4 = __ldg(&sc.mu[g]);
+            const float4 c0 = __ldg(&sc.geo[4 * g + 0]), c1 = __ldg(&sc.geo[4 * g + 1]);
+            const float4 i0 = __ldg(&sc.geo[4 * g + 2]), i1 = __ldg(&sc.geo[4 * g + 3]);
+            Proj p;
+            if (fp.ewa) project_splat_ewa(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
+            else project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
+            // number of (Gaussian, tile) candidates = rect area, 0 if the rect holds no
+            // visible tile (SAT); the exact Eq.4 tests run load-balanced in k_tiletest
+            if (p.valid && p.rect[0] <= p.rect[2] && p.rect[1] <= p.rect[3] &&
+                sat_count(v.sat, v.tw + 1, p.rect[0], p.rect[1], p.rect[2], p.rect[3]) > 0)
+                cnt = (uint32_t)((p.rect[2] - p.rect[0] + 1) * (p.rect[3] - p.rect[1] + 1));
+            if (cnt) {
+                float4* rec = fb.rec + (size_t)sidx * kRecF4;
+                const uint32_t r01 = (uint32_t)p.rect[0] | ((uint32_t)p.rect[1] << 16);
+                const uint32_t r23 = (uint32_t)p.rect[2] | ((uint32_t)p.rect[3] << 16);
+                if (fp.ewa) {
+                    rec[0] = make_float4(p.m2[0], p.m2[1], p.qcut, p.Cp[0]);
+                    rec[1] = make_float4(p.Cp[1], p.Cp[2], 0.0f, 0.0f);
+                    rec[2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                    p.eps = 0.0f;
+                } else {
+                    rec[0] = make_float4(p.u[0], p.u[1], p.u[2], p.qcut);
+                    rec[1] = make_float4(p.e1[0], p.e1[2], p.e2[0], p.e2[1]);
+                    rec[2] = make_float4(p.e2[2], p.C[0], p.C[1], p.C[2]);
+                }
+                rec[3] = make_float4(p.A[0], p.A[1], p.A[2], p.A[3]);
+                rec[4] = make_float4(p.A[4], p.A[5], p.bv[0], p.bv[1]);
+                rec[5] = make_float4(p.bv[2], p.sigma, p.eps, __uint_as_float(r01));
+                // rec[6] = (global-sort key depth (N3: view-space z or |mu - o|), -, -, rect23)
+                float* r6 = reinterpret_cast<float*>(rec + 6);
+                r6[0] = (fp.sort_mode == VRS_SORT_Z) ? p.muc[2]
+                                                     : sqrtf(dot3(p.muc[0], p.muc[1], p.muc[2], p.muc[0], p.muc[1],
+                                                                  p.muc[2]));
+                r6[3] = __uint_as_float(r23);
+                rec[7] = make_float4(p.bbox[0], p.bbox[1], p.bbox[2], p.bbox[3]);
+            }
+        }
+        // warp inclusive scan of the counts; visible splats (cnt > 0) listed alongside
+        uint32_t inc = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
+        const unsigned vb = __ballot_sync(0xffffffffu, cnt != 0u);
+        uint32_t base = 0, vbase = 0;
+        if (lane == 0) {
+            base = tot ? atomicAdd(fb.total_tests, tot) : 0u;
+            vbase = vb ? atomicAdd(fb.vis_count, (uint32_t)__popc(vb)) : 0u;
+        }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        vbase = __shfl_sync(0xffffffffu, vbase, 0);
+        if (cnt) fb.vis_list[vbase + __popc(vb & lt)] = sidx;
+        for (uint32_t o0 = 0; o0 < tot; o0 += 32u) {
+            const uint32_t o = o0 + (uint32_t)lane;
+            int lo = 0;  // owner: first lane e with inc_e > o
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, inc, lo + step - 1);
+                if (v <= o) lo += step;
+            }
+            const uint32_t e_inc = __shfl_sync(0xffffffffu, inc, lo);
+            const uint32_t e_cnt = __shfl_sync(0xffffffffu, cnt, lo);
+            const uint32_t e_sidx = __shfl_sync(0xffffffffu, sidx, lo);
+            const int64_t pos = (int64_t)base + o;
+            if (o < tot && pos < test_cap)
+                fb.sidk[pos] = (unsigned long long)e_sidx | ((unsigned long long)(o - (e_inc - e_cnt)) << 32);
+        }
+    }
+}
+#else
 __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb, int64_t test_cap) {
     __shared__ uint32_t s_inc[256];
     __shared__ uint32_t s_sidx[256];
@@ -574,8 +681,8 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
             const int64_t g = (int64_t)sidx - (int64_t)vi * N;
             const ViewParams& v = fp.v[vi];
             const float4 m4 = __ldg(&sc.mu[g]);
-            const float4 c0 = __ldg(&sc.cov[g]), c1 = __ldg(&sc.cov[N + g]);
-            const float4 i0 = __ldg(&sc.icov[g]), i1 = __ldg(&sc.icov[N + g]);
+            const float4 c0 = __ldg(&sc.geo[4 * g + 0]), c1 = __ldg(&sc.geo[4 * g + 1]);
+            const float4 i0 = __ldg(&sc.geo[4 * g + 2]), i1 = __ldg(&sc.geo[4 * g + 3]);
             Proj p;
             if (fp.ewa) project_splat_ewa(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
             else project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
@@ -654,6 +761,8 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
         __syncthreads();
     }
 }
+
+#endif  // VRS_PP_WARP
 
 // Step 3 (fused): one thread per (Gaussian, candidate tile): Eq.4 test (O7)
 // and key (O8), then stream compaction of the kept candidates (blocks take

@@ -44,7 +44,8 @@ struct vrs_context {
     int64_t N = 0;
     int deg = 0;
     bool uploaded = false;
-    float4 *d_mu = nullptr, *d_cov = nullptr, *d_icov = nullptr, *d_sh = nullptr;
+    float4 *d_mu = nullptr, *d_geo = nullptr, *d_sh = nullptr;
+    float* d_smax = nullptr;
     float4* d_raw = nullptr;   // [N][2] raw quaternion (w,x,y,z) and (log-scales, logit): N4 backward
     float* d_gbuf = nullptr;   // [max_views][max_gaussians][24] per-(view, Gaussian) gradient records
     int sh_chunks = 0;
@@ -134,7 +135,7 @@ static vrs_status cuda_check(vrs_context* c, cudaError_t e, const char* where) {
     } while (0)
 
 static void free_all(vrs_context* c) {
-    void* ptrs[] = {c->d_raw, c->d_gbuf, c->d_mu, c->d_cov, c->d_icov, c->d_sh, c->d_rec, c->d_col, c->d_cand, c->d_counts, c->d_misc, c->d_vis_list,
+    void* ptrs[] = {c->d_raw, c->d_gbuf, c->d_mu, c->d_geo, c->d_smax, c->d_sh, c->d_rec, c->d_col, c->d_cand, c->d_counts, c->d_misc, c->d_vis_list,
                     c->d_sidk,
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
@@ -265,14 +266,14 @@ vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_degree, 
     const int ncoef = (sh_degree + 1) * (sh_degree + 1);
     const int nfl = ncoef * 3;
     const int chunks = (nfl + 3) / 4;
-    std::vector<float4> mu, cov, icov;
-    std::vector<float> shh;
+    std::vector<float4> mu, geo;
+    std::vector<float> shh, smaxv;
     mu.reserve(n);
-    cov.reserve(2 * n);
-    icov.reserve(2 * n);
+    geo.reserve(4 * n);
+    smaxv.reserve(n);
     std::vector<int64_t> keep;
     keep.reserve(n);
-    std::vector<float4> cov_hi, icov_hi, rawv;
+    std::vector<float4> rawv;
     rawv.reserve(2 * n);
     for (int64_t i = 0; i < n; i++) {
         const float* m = means + 3 * i;
@@ -311,17 +312,17 @@ vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_degree, 
         const float sg = (float)(1.0 / (1.0 + std::exp(-(double)logits[i])));
         const float qc = (float)(2.0 * std::log(255.0 * (double)sg));
         mu.push_back(make_float4(m[0], m[1], m[2], qc));
-        cov.push_back(make_float4(c6[0], c6[1], c6[2], c6[3]));
-        cov_hi.push_back(make_float4(c6[4], c6[5], sg, (float)(smax * (1.0 + 1e-6))));
-        icov.push_back(make_float4(i6[0], i6[1], i6[2], i6[3]));
-        icov_hi.push_back(make_float4(i6[4], i6[5], 0.0f, 0.0f));
+        const float smf = (float)(smax * (1.0 + 1e-6));
+        geo.push_back(make_float4(c6[0], c6[1], c6[2], c6[3]));
+        geo.push_back(make_float4(c6[4], c6[5], sg, smf));
+        geo.push_back(make_float4(i6[0], i6[1], i6[2], i6[3]));
+        geo.push_back(make_float4(i6[4], i6[5], 0.0f, 0.0f));
+        smaxv.push_back(smf);
         rawv.push_back(make_float4(q[0], q[1], q[2], q[3]));
         rawv.push_back(make_float4(ls[0], ls[1], ls[2], logits[i]));
         keep.push_back(i);
     }
     const int64_t nk = (int64_t)keep.size();
-    cov.insert(cov.end(), cov_hi.begin(), cov_hi.end());
-    icov.insert(icov.end(), icov_hi.begin(), icov_hi.end());
     // SH: coefficient-major RGB flattened, [N][chunk] float4 (a visible Gaussian reads its own 48 floats)
     std::vector<float4> shd((size_t)chunks * std::max<int64_t>(nk, 1));
     for (int64_t r = 0; r < nk; r++) {
@@ -334,18 +335,19 @@ vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_degree, 
         }
     }
     // (re)allocate scene buffers
-    for (float4** p : {&ctx->d_mu, &ctx->d_cov, &ctx->d_icov, &ctx->d_sh, &ctx->d_raw})
+    for (float4** p : {&ctx->d_mu, &ctx->d_geo, &ctx->d_sh, &ctx->d_raw})
         if (*p) { cudaFree(*p); *p = nullptr; }
+    if (ctx->d_smax) { cudaFree(ctx->d_smax); ctx->d_smax = nullptr; }
     const size_t NN = std::max<int64_t>(nk, 1);
     CK(dalloc(&ctx->d_mu, NN));
-    CK(dalloc(&ctx->d_cov, 2 * NN));
-    CK(dalloc(&ctx->d_icov, 2 * NN));
+    CK(dalloc(&ctx->d_geo, 4 * NN));
+    CK(dalloc(&ctx->d_smax, NN));
     CK(dalloc(&ctx->d_sh, (size_t)chunks * NN));
     CK(dalloc(&ctx->d_raw, 2 * NN));
     if (nk > 0) {
         CK(cudaMemcpy(ctx->d_mu, mu.data(), sizeof(float4) * nk, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(ctx->d_cov, cov.data(), sizeof(float4) * 2 * nk, cudaMemcpyHostToDevice));
-        CK(cudaMemcpy(ctx->d_icov, icov.data(), sizeof(float4) * 2 * nk, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_geo, geo.data(), sizeof(float4) * 4 * nk, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(ctx->d_smax, smaxv.data(), sizeof(float) * nk, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->d_sh, shd.data(), sizeof(float4) * chunks * nk, cudaMemcpyHostToDevice));
         CK(cudaMemcpy(ctx->d_raw, rawv.data(), sizeof(float4) * 2 * nk, cudaMemcpyHostToDevice));
     }
@@ -471,8 +473,15 @@ static vrs_status prepare_frame(vrs_context* ctx, int nv, const vrs_camera* cams
             const double Nn[4][3] = {{1.0, 0.0, -xl}, {-1.0, 0.0, xr}, {0.0, 1.0, -yt}, {0.0, -1.0, yb}};
             for (int k = 0; k < 4; k++) {
                 const double nn = std::sqrt(Nn[k][0] * Nn[k][0] + Nn[k][1] * Nn[k][1] + Nn[k][2] * Nn[k][2]);
-                for (int i = 0; i < 3; i++) v.plane[k][i] = (float)(Nn[k][i] / nn);
+                for (int i = 0; i < 3; i++) {
+                    v.plane[k][i] = (float)(Nn[k][i] / nn);
+                    v.dplane[k][i] = Nn[k][i] / nn;
+                }
             }
+            v.kinv[0] = 1.0 / c.fx;
+            v.kinv[1] = 1.0 / c.fy;
+            v.kinv[2] = -(double)c.cx / c.fx;
+            v.kinv[3] = -(double)c.cy / c.fy;
             const double fmin = std::min(c.fx, c.fy);
             v.dil = (float)(0.3 / (fmin * fmin) * 1.01);
         }
@@ -577,7 +586,7 @@ static vrs_status render_impl(vrs_context* ctx, int32_t nv, const vrs_camera* ca
         if (s != VRS_OK) return s;
     }
     fp.out_fmt = out_fmt;
-    SceneDev sc{ctx->d_mu, ctx->d_cov, ctx->d_icov, ctx->d_sh, ctx->sh_chunks};
+    SceneDev sc{ctx->d_mu, ctx->d_geo, ctx->d_smax, ctx->d_sh, ctx->sh_chunks};
     FrameBufs fb = frame_bufs(ctx);
     const bool tm = ctx->timing && ctx->ev_created;
     if (tm) CK(cudaEventRecord(ctx->ev[0], st));
@@ -983,7 +992,7 @@ vrs_status vrs_debug_splats(vrs_context* ctx, int32_t view, float* out, int64_t 
     if (ctx->N == 0) return VRS_OK;
     float* d = nullptr;
     CK(dalloc(&d, 48 * (size_t)ctx->N));
-    SceneDev sc{ctx->d_mu, ctx->d_cov, ctx->d_icov, ctx->d_sh, ctx->sh_chunks};
+    SceneDev sc{ctx->d_mu, ctx->d_geo, ctx->d_smax, ctx->d_sh, ctx->sh_chunks};
     FrameBufs fb = frame_bufs(ctx);
     launch_counts(ctx->fp, fb, ctx->test_cap, st);
     launch_debug_splats(sc, ctx->fp, fb, view, d, st);

@@ -43,6 +43,8 @@ struct ViewParams {
     int32_t fovea;           // foveation on
     float gx, gy, rx, ry, ramp;
     float plane[4][3];       // inward unit normals of the 4 frustum side planes (camera frame)
+    double dplane[4][3];     // the same in double (preprocess cone test, O6a)
+    double kinv[4];          // 1/fx, 1/fy, -cx/fx, -cy/fy in double (preprocess conic bbox, O6b)
     float dil;               // 0.3 / min(fx, fy)^2: dilation bound for the conservative cull
     int64_t pix_off;         // pixel offset of this view in the output buffers
     int64_t low_off;         // offset of this view in the low-res sample planes
@@ -82,9 +84,10 @@ struct FrameParams {
 };
 
 struct SceneDev {
-    const float4* mu;        // [N] mu.xyz, q_cut
-    const float4* cov;       // [2][N] (xx,xy,xz,yy) (yz,zz,sigma,s_max)
-    const float4* icov;      // [2][N] (xx,xy,xz,yy) (yz,zz,0,0)
+    const float4* mu;        // [N] mu.xyz, q_cut (read for every Gaussian by the cull)
+    const float4* geo;       // [N][4] Sigma_w (xx,xy,xz,yy) (yz,zz,sigma,s_max), Sigma_w^-1 (xx,xy,xz,yy)
+                             // (yz,zz,0,0): the 64 B a candidate's projection reads, contiguous
+    const float* smax;       // [N] largest scale (the cull's cone bound)
     const float4* sh;        // [N][chunks]
     int32_t sh_chunks;
 };
