@@ -553,10 +553,6 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
 #ifndef VRS_TT_MINB
 #define VRS_TT_MINB 4
 #endif
-#ifndef VRS_PP_WARP
-#define VRS_PP_WARP 1
-#endif
-#if VRS_PP_WARP
 // Warp-independent form: each warp takes 32 consecutive candidates per
 // iteration, scans their tile counts with shuffles, reserves its slice of the
 // test list (and of the visible-splat list) with one atomic per warp, and
@@ -637,13 +633,12 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
         }
         const uint32_t tot = __shfl_sync(0xffffffffu, inc, 31);
         const unsigned vb = __ballot_sync(0xffffffffu, cnt != 0u);
-        uint32_t base = 0, vbase = 0;
-        if (lane == 0) {
-            base = tot ? atomicAdd(fb.total_tests, tot) : 0u;
-            vbase = vb ? atomicAdd(fb.vis_count, (uint32_t)__popc(vb)) : 0u;
-        }
-        base = __shfl_sync(0xffffffffu, base, 0);
-        vbase = __shfl_sync(0xffffffffu, vbase, 0);
+        // one 64-bit atomic reserves both slices: tests in bits 0-35, visible splats in 36-63
+        unsigned long long old = 0;
+        if (lane == 0 && (tot | vb))
+            old = atomicAdd(fb.tv, ((unsigned long long)__popc(vb) << kTvShift) | (unsigned long long)tot);
+        old = __shfl_sync(0xffffffffu, old, 0);
+        const uint32_t base = (uint32_t)min(old & kTvMask, 0xffffffffull), vbase = (uint32_t)(old >> kTvShift);
         if (cnt) fb.vis_list[vbase + __popc(vb & lt)] = sidx;
         for (uint32_t o0 = 0; o0 < tot; o0 += 32u) {
             const uint32_t o = o0 + (uint32_t)lane;
@@ -662,107 +657,7 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
         }
     }
 }
-#else
-__global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb, int64_t test_cap) {
-    __shared__ uint32_t s_inc[256];
-    __shared__ uint32_t s_sidx[256];
-    __shared__ uint32_t s_w[8], s_vw[8];
-    __shared__ uint32_t s_base, s_vbase;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t N = fp.N;
-    const uint32_t nc = *fb.cand_count;
-    for (uint32_t b0 = blockIdx.x * 256u; b0 < nc; b0 += gridDim.x * 256u) {
-        const uint32_t i = b0 + tid;
-        uint32_t cnt = 0, sidx = 0;
-        if (i < nc) {
-            sidx = fb.cand[i];
-            int vi = 0;  // view = number of view blocks of N below sidx (no 64-bit division)
-            while (vi + 1 < fp.n_views && (int64_t)sidx >= (int64_t)(vi + 1) * N) vi++;
-            const int64_t g = (int64_t)sidx - (int64_t)vi * N;
-            const ViewParams& v = fp.v[vi];
-            const float4 m4 = __ldg(&sc.mu[g]);
-            const float4 c0 = __ldg(&sc.geo[4 * g + 0]), c1 = __ldg(&sc.geo[4 * g + 1]);
-            const float4 i0 = __ldg(&sc.geo[4 * g + 2]), i1 = __ldg(&sc.geo[4 * g + 3]);
-            Proj p;
-            if (fp.ewa) project_splat_ewa(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
-            else project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
-            // number of (Gaussian, tile) candidates = rect area, 0 if the rect holds no
-            // visible tile (SAT); the exact Eq.4 tests run load-balanced in k_tiletest
-            if (p.valid && p.rect[0] <= p.rect[2] && p.rect[1] <= p.rect[3] &&
-                sat_count(v.sat, v.tw + 1, p.rect[0], p.rect[1], p.rect[2], p.rect[3]) > 0)
-                cnt = (uint32_t)((p.rect[2] - p.rect[0] + 1) * (p.rect[3] - p.rect[1] + 1));
-            if (cnt) {
-                float4* rec = fb.rec + (size_t)sidx * kRecF4;
-                const uint32_t r01 = (uint32_t)p.rect[0] | ((uint32_t)p.rect[1] << 16);
-                const uint32_t r23 = (uint32_t)p.rect[2] | ((uint32_t)p.rect[3] << 16);
-                if (fp.ewa) {
-                    rec[0] = make_float4(p.m2[0], p.m2[1], p.qcut, p.Cp[0]);
-                    rec[1] = make_float4(p.Cp[1], p.Cp[2], 0.0f, 0.0f);
-                    rec[2] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-                    p.eps = 0.0f;
-                } else {
-                    rec[0] = make_float4(p.u[0], p.u[1], p.u[2], p.qcut);
-                    rec[1] = make_float4(p.e1[0], p.e1[2], p.e2[0], p.e2[1]);
-                    rec[2] = make_float4(p.e2[2], p.C[0], p.C[1], p.C[2]);
-                }
-                rec[3] = make_float4(p.A[0], p.A[1], p.A[2], p.A[3]);
-                rec[4] = make_float4(p.A[4], p.A[5], p.bv[0], p.bv[1]);
-                rec[5] = make_float4(p.bv[2], p.sigma, p.eps, __uint_as_float(r01));
-                // rec[6] = (global-sort key depth (N3: view-space z or |mu - o|), -, -, rect23)
-                float* r6 = reinterpret_cast<float*>(rec + 6);
-                r6[0] = (fp.sort_mode == VRS_SORT_Z) ? p.muc[2]
-                                                     : sqrtf(dot3(p.muc[0], p.muc[1], p.muc[2], p.muc[0], p.muc[1],
-                                                                  p.muc[2]));
-                r6[3] = __uint_as_float(r23);
-                rec[7] = make_float4(p.bbox[0], p.bbox[1], p.bbox[2], p.bbox[3]);
-            }
-        }
-        // block inclusive scan of the counts; visible splats (cnt > 0) counted alongside
-        uint32_t inc = cnt;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += y;
-        }
-        const unsigned vb = __ballot_sync(0xffffffffu, cnt != 0u);
-        if (lane == 31) {
-            s_w[warp] = inc;
-            s_vw[warp] = (uint32_t)__popc(vb);
-        }
-        __syncthreads();
-        uint32_t wpre = 0, tot = 0, vpre = 0, vtot = 0;
-#pragma unroll
-        for (int w = 0; w < 8; w++) {
-            wpre += (w < warp) ? s_w[w] : 0u;
-            tot += s_w[w];
-            vpre += (w < warp) ? s_vw[w] : 0u;
-            vtot += s_vw[w];
-        }
-        s_inc[tid] = wpre + inc;
-        s_sidx[tid] = sidx;
-        if (tid == 0) {
-            s_base = tot ? atomicAdd(fb.total_tests, tot) : 0u;
-            s_vbase = vtot ? atomicAdd(fb.vis_count, vtot) : 0u;
-        }
-        __syncthreads();
-        const uint32_t base = s_base;
-        if (cnt) fb.vis_list[s_vbase + vpre + __popc(vb & ((1u << lane) - 1u))] = sidx;
-        for (uint32_t o = tid; o < tot; o += 256u) {
-            int lo = 0, hi = 255;  // owner: first e with s_inc[e] > o
-            while (lo < hi) {
-                const int mid = (lo + hi) >> 1;
-                if (s_inc[mid] > o) hi = mid;
-                else lo = mid + 1;
-            }
-            const uint32_t excl = lo ? s_inc[lo - 1] : 0u;
-            const int64_t pos = (int64_t)base + o;
-            if (pos < test_cap) fb.sidk[pos] = (unsigned long long)s_sidx[lo] | ((unsigned long long)(o - excl) << 32);
-        }
-        __syncthreads();
-    }
-}
 
-#endif  // VRS_PP_WARP
 
 // Step 3 (fused): one thread per (Gaussian, candidate tile): Eq.4 test (O7)
 // and key (O8), then stream compaction of the kept candidates (blocks take
@@ -833,7 +728,7 @@ __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const Fram
 // tile offsets are known).  No compaction, no block synchronisation.
 __global__ void __launch_bounds__(kTT, VRS_TT_MINB) k_tiletest_direct(FrameParams fp, FrameBufs fb, int64_t test_cap,
                                                                       BinScratch bs) {
-    const int64_t total = min((int64_t)*fb.total_tests, test_cap);
+    const int64_t total = min(fb_tests(fb), test_cap);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < total; t0 += stride * kTTItems) {
         uint64_t key[kTTItems];
@@ -874,7 +769,7 @@ __global__ void __launch_bounds__(kTT, VRS_TT_MINB) k_tiletest(FrameParams fp, F
     __shared__ uint32_t s_tile, s_base;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const unsigned lt = (1u << lane) - 1u;
-    const int64_t total = min((int64_t)*fb.total_tests, test_cap);
+    const int64_t total = min(fb_tests(fb), test_cap);
     const int64_t ntiles = (total + kTTTile - 1) / kTTTile;
     while (true) {
         if (tid == 0) s_tile = atomicAdd(counter, 1u);
@@ -932,7 +827,7 @@ __global__ void __launch_bounds__(kTT, VRS_TT_MINB) k_tiletest(FrameParams fp, F
 // number of emitted pairs whose candidate falls in its candidate range;
 // computed by a binary search of the splat range in the candidate->pair map.
 __global__ void k_counts(FrameParams fp, FrameBufs fb, int64_t test_cap) {
-    const int64_t total = min((int64_t)*fb.total_tests, test_cap);
+    const int64_t total = min(fb_tests(fb), test_cap);
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         uint64_t key;
         uint32_t g;
@@ -1030,7 +925,7 @@ __device__ __forceinline__ void sh_color_q(const float4 q4[12], int chunks, int 
 // does not wait on the 192 B SH fetches).
 __global__ void __launch_bounds__(256) k_color(SceneDev sc, FrameParams fp, FrameBufs fb) {
     const int64_t N = fp.N;
-    const uint32_t n = *fb.vis_count;
+    const uint32_t n = fb_visible(fb);
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
         const uint32_t sidx = fb.vis_list[i];
         int vi = 0;
@@ -1053,8 +948,7 @@ __global__ void __launch_bounds__(256) k_color(SceneDev sc, FrameParams fp, Fram
 
 
 void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {
-    cudaMemsetAsync(fb.total_tests, 0, 4, st);
-    cudaMemsetAsync(fb.vis_count, 0, 4, st);
+    cudaMemsetAsync(fb.tv, 0, 8, st);
     if (fp.N == 0) return;
     const int B = 256;
     cudaMemsetAsync(fb.cand_count, 0, 4, st);

@@ -53,7 +53,8 @@ struct vrs_context {
     float4* d_rec = nullptr;
     float4* d_col = nullptr;
     uint32_t* d_cand = nullptr;
-    uint32_t *d_counts = nullptr, *d_misc = nullptr;  // misc: pairs, overflow, tests, candidates, visible
+    uint32_t *d_counts = nullptr, *d_misc = nullptr;  // misc: pairs, overflow, -, candidates, -
+    unsigned long long* d_tv = nullptr;               // tile tests | visible splats << 36
     uint32_t* d_vis_list = nullptr;
     unsigned long long* d_sidk = nullptr;    // [test_cap] candidate map
     int64_t test_cap = 0;
@@ -135,7 +136,7 @@ static vrs_status cuda_check(vrs_context* c, cudaError_t e, const char* where) {
     } while (0)
 
 static void free_all(vrs_context* c) {
-    void* ptrs[] = {c->d_raw, c->d_gbuf, c->d_mu, c->d_geo, c->d_smax, c->d_sh, c->d_rec, c->d_col, c->d_cand, c->d_counts, c->d_misc, c->d_vis_list,
+    void* ptrs[] = {c->d_raw, c->d_gbuf, c->d_mu, c->d_geo, c->d_smax, c->d_sh, c->d_rec, c->d_col, c->d_cand, c->d_counts, c->d_misc, c->d_tv, c->d_vis_list,
                     c->d_sidk,
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
@@ -193,7 +194,8 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     A(dalloc(&ctx->d_vis_list, (size_t)V * N));
     ctx->test_cap = 4 * P;
     A(dalloc(&ctx->d_sidk, (size_t)ctx->test_cap));
-    A(dalloc(&ctx->d_misc, 8));  // pairs, overflow, tests, candidates, visible, tile overflow, primitive n, -
+    A(dalloc(&ctx->d_misc, 8));
+    A(dalloc(&ctx->d_tv, 1));  // pairs, overflow, tests, candidates, visible, tile overflow, primitive n, -
     A(dalloc(&ctx->d_keys, (size_t)P));
     A(dalloc(&ctx->d_keys_alt, (size_t)P));
     A(dalloc(&ctx->d_vals, (size_t)P));
@@ -550,8 +552,7 @@ static FrameBufs frame_bufs(vrs_context* ctx) {
     fb.cand = ctx->d_cand;
     fb.cand_count = ctx->d_misc + 3;
     fb.vis_list = ctx->d_vis_list;
-    fb.vis_count = ctx->d_misc + 4;
-    fb.total_tests = ctx->d_misc + 2;
+    fb.tv = ctx->d_tv;
     fb.sidk = ctx->d_sidk;
     fb.counts = ctx->d_counts;
     fb.total = ctx->d_misc;
@@ -799,7 +800,9 @@ vrs_status vrs_get_frame_stats(vrs_context* ctx, vrs_frame_stats* out) {
     CK(cudaStreamSynchronize(ctx->last_stream));
     std::memset(out, 0, sizeof(*out));
     uint32_t misc[3] = {0, 0, 0};
+    unsigned long long tv = 0;
     CK(cudaMemcpy(misc, ctx->d_misc, 12, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(&tv, ctx->d_tv, 8, cudaMemcpyDeviceToHost));
     out->pairs = misc[0];
     unsigned long long st[8] = {0};
     if (ctx->counters) CK(cudaMemcpy(st, ctx->d_stats, sizeof(st), cudaMemcpyDeviceToHost));
@@ -840,7 +843,7 @@ vrs_status vrs_get_frame_stats(vrs_context* ctx, vrs_frame_stats* out) {
         for (int k = 0; k < 7; k++) CK(cudaEventElapsedTime(&out->stage_ms[k], ctx->ev[k], ctx->ev[k + 1]));
         CK(cudaEventElapsedTime(&out->stage_ms[7], ctx->ev[0], ctx->ev[7]));
     }
-    if (misc[1] || (int64_t)misc[0] > ctx->cfg.max_pairs || (int64_t)misc[2] > ctx->test_cap)
+    if (misc[1] || (int64_t)misc[0] > ctx->cfg.max_pairs || (int64_t)(tv & ((1ull << 36) - 1ull)) > ctx->test_cap)
         return fail(ctx, VRS_E_CAPACITY, "pair buffer overflow (max_pairs too small)");
     return VRS_OK;
 }

@@ -96,10 +96,10 @@ struct FrameBufs {
     float4* rec;             // [V][N][8]
     uint32_t* cand;          // [V*N] (view*N + g) passing the conservative cull
     uint32_t* cand_count;    // [1]
-    uint32_t* total_tests;   // [1] (device)
+    unsigned long long* tv;  // [1] expanded tile tests (bits 0-35) | visible splats (bits 36-63), device
     unsigned long long* sidk;  // [test_cap] candidate -> (splat view*N+g) | (rect-local tile index << 32)
     uint32_t* vis_list;      // [V*N] (view*N + g) with >= 1 candidate tile (colour work list)
-    uint32_t* vis_count;     // [1]
+
     uint32_t* counts;        // [V*N] exact pair counts (parity hook only)
     uint32_t* total;         // [1] pair total (device)
     uint32_t* overflow;      // [1] capacity overflow flag
@@ -113,6 +113,11 @@ struct FrameBufs {
     float* low_depth;        // low-res samples depth
     unsigned long long* stats;  // [8] device counters
 };
+
+constexpr int kTvShift = 36;
+constexpr unsigned long long kTvMask = (1ull << kTvShift) - 1ull;
+__device__ __forceinline__ int64_t fb_tests(const FrameBufs& fb) { return (int64_t)(*fb.tv & kTvMask); }
+__device__ __forceinline__ uint32_t fb_visible(const FrameBufs& fb) { return (uint32_t)(*fb.tv >> kTvShift); }
 
 // ----------------------------------------------------------------- device helpers (host side)
 // Dynamic shared-memory limit of a kernel, set once per (kernel, device, size):
@@ -147,7 +152,7 @@ inline int device_sms() {
 void launch_setup_view(const uint8_t* mask, int mask_w, ViewParams vp, int T, int32_t* vis, uint32_t* sat,
                        int32_t* cls, uint32_t* items, int32_t* n_items_dev, uint32_t* inv_items, uint32_t* lowcnt,
                        uint32_t* lowcnt0, cudaStream_t st);
-// Cull + preprocess + candidate expansion into fb.sidk (total in fb.total_tests).
+// Cull + preprocess + candidate expansion into fb.sidk (total in fb.tv).
 void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st);
 // SH colour of the visible list (after launch_preprocess; needed by the blend only)
 void launch_color(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, cudaStream_t st);
