@@ -315,10 +315,9 @@ __device__ bool tile_test_ewa(const TileSplat& s, const ViewParams& v, int x0, i
 // O7: Eq.4 on the optimal-plane polygon of the tile, corner
 // rays clipped at s >= eps (DESIGN R8); returns keep and d_hat.
 // Fast path: all four corners in front (the common case) -> unrolled quad.
-__device__ bool tile_test(const TileSplat& s, const ViewParams& v, int x0, int y0, int x1, int y1, float& dhx,
-                          float& dhy, float& dhz) {
-    const float ax = ((float)x0 - v.cx) / v.fx, bx = ((float)x1 - v.cx) / v.fx;
-    const float ay = ((float)y0 - v.cy) / v.fy, by = ((float)y1 - v.cy) / v.fy;
+// ax, bx, ay, by: the tile's corner rays ((float)x0 - cx) / fx etc. (per-view tables, k_cull)
+__device__ bool tile_test(const TileSplat& s, float ax, float bx, float ay, float by, float& dhx, float& dhy,
+                          float& dhz) {
     float dx[4] = {ax, bx, bx, ax}, dy[4] = {ay, ay, by, by}, sv[4];
     int nin = 0;
 #pragma unroll
@@ -475,6 +474,17 @@ __device__ __forceinline__ void load_gauss(const SceneDev& sc, int64_t g, int64_
 // frustum misses that (inflated) cone is also culled by the exact O6(a) test:
 // culling here never changes results, it only compacts the work of step 1b.
 __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, FrameBufs fb) {
+    if (blockIdx.x == 0) {
+        // per-view tile-corner ray tables for the tile test: xr[k] = ((float)min(kT, W) - cx) / fx,
+        // yr[k] likewise (the O7 corner rays, the same operations as the oracle's)
+        for (int vi = 0; vi < fp.n_views; vi++) {
+            const ViewParams& v = fp.v[vi];
+            for (int k = threadIdx.x; k <= v.tw; k += blockDim.x)
+                v.xr[k] = ((float)min(k * fp.T, v.W) - v.cx) / v.fx;
+            for (int k = threadIdx.x; k <= v.th; k += blockDim.x)
+                v.yr[k] = ((float)min(k * fp.T, v.H) - v.cy) / v.fy;
+        }
+    }
     const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t N = fp.N;
     const bool in = g < N;
@@ -706,7 +716,8 @@ __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const Fram
         s.e1x = r1.x; s.e1z = r1.y; s.e2x = r1.z; s.e2y = r1.w;
         s.e2z = r2.x; s.C0 = r2.y; s.C1 = r2.z; s.C2 = r2.w;
         s.eps = r5.z;
-        if (!tile_test(s, v, x0, y0, min(x0 + T, v.W), min(y0 + T, v.H), hx, hy, hz)) return false;
+        if (!tile_test(s, __ldg(v.xr + tx), __ldg(v.xr + tx + 1), __ldg(v.yr + ty), __ldg(v.yr + ty + 1), hx, hy, hz))
+            return false;
     }
 #if !VRS_TT_HOIST
     const float4 r3 = __ldg(rec + 3), r4 = __ldg(rec + 4);

@@ -77,6 +77,8 @@ struct vrs_context {
     int32_t* d_nitems = nullptr;  // [V][3]: items, LowRes items, invisible tiles
     uint32_t* d_inv = nullptr;    // [V][max_tiles]: invisible tiles (background-fill items)
     uint32_t* d_lowcnt = nullptr;   // [V][max_tiles]: in-launch compose counters
+    float* d_rays = nullptr;        // [V][max_rays_view]: tile-corner ray tables (x then y)
+    int64_t max_rays_view = 0;
     uint32_t* d_lowcnt0 = nullptr;  // [V][max_tiles]: their initial values
     int64_t max_sat_view = 0;
     ViewSetup vs[VRS_MAX_VIEWS];
@@ -141,7 +143,7 @@ static void free_all(vrs_context* c) {
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
                     c->bin.tile_cnt, c->bin.rank, c->bin.list, c->bin.list_n, c->bin.tbucket, c->bin.ovf_off, c->bin.obucket,
-                    c->d_sat, c->d_cls, c->d_items, c->d_nitems, c->d_inv, c->d_lowcnt, c->d_lowcnt0,
+                    c->d_sat, c->d_cls, c->d_items, c->d_nitems, c->d_inv, c->d_lowcnt, c->d_lowcnt0, c->d_rays,
                     c->d_out_rgba, c->d_out_depth};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -227,6 +229,8 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     A(dalloc(&ctx->d_inv, (size_t)V * ctx->max_tiles_view));
     A(dalloc(&ctx->d_lowcnt, (size_t)V * ctx->max_tiles_view));
     A(dalloc(&ctx->d_lowcnt0, (size_t)V * ctx->max_tiles_view));
+    ctx->max_rays_view = (tw + 1) + (th + 1);
+    A(dalloc(&ctx->d_rays, (size_t)V * ctx->max_rays_view));
     if (e != cudaSuccess) {
         free_all(ctx);
         delete ctx;
@@ -496,6 +500,8 @@ static vrs_status prepare_frame(vrs_context* ctx, int nv, const vrs_camera* cams
         v.items = ctx->d_items + (size_t)vi * ctx->max_items_view;
         v.inv_items = ctx->d_inv + (size_t)vi * ctx->max_tiles_view;
         v.lowcnt = ctx->d_lowcnt + (size_t)vi * ctx->max_tiles_view;
+        v.xr = ctx->d_rays + (size_t)vi * ctx->max_rays_view;
+        v.yr = v.xr + v.tw + 1;
         v.lowcnt0 = ctx->d_lowcnt0 + (size_t)vi * ctx->max_tiles_view;
         // setup cache (precomputed once per eye)
         const int ms = (c.mask_slot >= 0 && ctx->d_mask[c.mask_slot]) ? c.mask_slot : -1;

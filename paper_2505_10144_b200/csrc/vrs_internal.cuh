@@ -59,6 +59,8 @@ struct ViewParams {
     const uint32_t* inv_items;  // [n_inv] invisible coarse tiles (background fill items of the flat blend)
     int32_t n_inv;           // invisible tiles of this view
     int32_t inv_off;         // first invisible item of this view (after all views' blend items)
+    float* xr;               // [tw+1] tile-corner rays ((float)min(kT, W) - cx) / fx (filled by k_cull)
+    float* yr;               // [th+1] likewise in y
     uint32_t* lowcnt;        // [th*tw] LowRes tiles of the 3x3 neighbourhood still blending (in-launch compose)
     const uint32_t* lowcnt0; // [th*tw] its initial value (counters are re-armed by the composing block)
 };
