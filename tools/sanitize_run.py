@@ -1,6 +1,7 @@
 """Small renders through every kernel family for compute-sanitizer runs:
-flat foveated stereo (T=32, masks), non-foveated T=16 + backward, hierarchical
-mode, EWA, two-pass, packed output."""
+flat foveated stereo (T=32, masks; thread and TMA staging; the in-launch
+compose), non-foveated T=16 + backward, hierarchical mode, EWA, two-pass,
+packed output, the global-sort baselines."""
 import os
 import sys
 
@@ -25,6 +26,12 @@ for proj in (0, 1):
         r.set_mask(e, sg.ellipse_mask(W, H))
     r.vrs_set_instrumentation(counters=1)
     r.render(cams, fov)
+    r.vrs_set_staging_mode(1)  # TMA staging
+    r.render(cams, fov)
+    r.vrs_set_staging_mode(0)
+    r.vrs_set_sort_mode(1)     # global-sort baseline
+    r.render(cams, fov)
+    r.vrs_set_sort_mode(0)
     if proj == 0:
         r.render_two_pass(cams, fov)
         r.vrs_set_resort_mode(1)
