@@ -253,7 +253,8 @@ def run_reference(args):
 def workload_config(name, scene, cams, world=1, extra=None):
     """The bench line's config object (the same for both arms)."""
     cfg = CONFIGS[name]
-    out = {"workload": name, "desc": cfg["desc"], "gaussians": int(scene.n), "views": len(cams),
+    out = {"workload": name, "desc": cfg["desc"], "gaussians": int(scene if isinstance(scene, int) else scene.n),
+           "views": len(cams),
            "resolution": [cams[0].width, cams[0].height], "assign_tile": cfg["T"],
            "foveated": bool(cfg["fovea"]), "parallelism": f"views x{world} (replicated scene, weak)"}
     out.update(extra or {})
@@ -495,30 +496,31 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = CONFIGS[args.config]
 
-    # ---- scene: rank 0 generates, NCCL broadcast of the raw arrays (only data-path collective)
+    # ---- scene: rank 0 generates and uploads (host activation once); with N > 1 the activated
+    # device buffers go to every rank as one blob by NCCL broadcast (the only data-path collective)
+    scene = None
     if rank == 0:
         scene, cams, fov, masks = make_workload(args.config)
     else:
-        _, cams, fov, masks = None, None, None, None
-        scene = None
-    if world > 1:
-        from paper_2505_10144_b200.parallel import broadcast_scene
-        scene = broadcast_scene(scene, cfg["n"], cfg["sh"], device=torch.device("cuda", local))
-        if rank != 0:
-            cams, fov, masks = make_cams_only(args.config)
+        cams, fov, masks = make_cams_only(args.config)
     from paper_2505_10144_b200 import Renderer
 
     W = max(c.width for c in cams)
     H = max(c.height for c in cams)
     two_pass = bool(cfg.get("two_pass"))
-    r = Renderer(max_gaussians=scene.n, max_views=len(cams) * (2 if two_pass else 1),
+    r = Renderer(max_gaussians=cfg["n"], max_views=len(cams) * (2 if two_pass else 1),
                  max_pairs=16 << 20 if cfg["n"] > 1e6 or two_pass else 8 << 20,
                  max_width=W, max_height=H, assign_tile=cfg["T"], device=local, projection=args.projection)
     render = r.render_two_pass if two_pass else r.render
     if cfg.get("resort"):
         r.vrs_set_resort_mode(cfg["resort"])
     r.vrs_set_staging_mode(1 if args.staging == "tma" else 0)
-    r.upload(scene)
+    if rank == 0:
+        r.upload(scene)
+    scene_bcast_bytes = None
+    if world > 1:
+        from paper_2505_10144_b200.parallel import broadcast_uploaded_scene
+        scene_bcast_bytes = broadcast_uploaded_scene(r, src=0)
     for k, m in masks.items():
         r.set_mask(k, m)
     stream = torch.cuda.Stream(device=local)
@@ -688,7 +690,7 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
-            "config": workload_config(args.config, scene, cams, world, {
+            "config": workload_config(args.config, r.n, cams, world, {
                 "l2": "flushed between steps (256 MB write, outside the event pair)" if not args.no_flush
                 else "not flushed", "staging": args.staging}),
             "stage_ms": dict(zip(names, stage_ms)),
@@ -708,6 +710,7 @@ def main():
             "gpu_launches": launches_per_step * args.steps,
             "e2e": e2e,
             "gather": gather,
+            "scene_broadcast_bytes": scene_bcast_bytes,
             "context": {"paper_rtx4090_ms_per_stereo_frame_0.5M_scenes": [9.89, 12.19],
                         "paper_headline": "72+ FPS on RTX 4090 at 2x2064x2272 (P:91, P:107)"},
         }

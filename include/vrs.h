@@ -135,6 +135,27 @@ VRS_API vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_
                                 const float* quats_wxyz, const float* log_scales, const float* opacity_logits,
                                 const float* sh, int64_t* n_rejected);
 
+/* The activated scene as one DEVICE blob, for the multi-GPU setup (SURVEY
+ * §8e): rank 0 uploads (host activation, above) and exports; the blob goes
+ * device to device to every other rank (an NCCL broadcast); they import it --
+ * no host round trip, no second activation.  The blob holds, for the n kept
+ * Gaussians: mu + q_cut (16 B), Sigma_w / sigma / s_max / Sigma_w^-1 (64 B),
+ * s_max (4 B), SH (16 B per 4 coefficient floats) and the raw parameters the
+ * backward needs (32 B), each array 256-B aligned.
+ * vrs_scene_blob_bytes: size of the blob of n Gaussians at degree sh_degree.
+ * vrs_export_scene: copies the context's scene into `blob` (DEVICE, `bytes`
+ * = vrs_scene_blob_bytes of its n and degree), enqueued on `stream`; *n_out
+ * and *deg_out (HOST, may be NULL) get n and the degree.
+ * vrs_import_scene: replaces the context's scene by a blob exported by a
+ * context of the same library (any device), enqueued on `stream`.
+ * Errors: VRS_E_STATE (export before any upload), VRS_E_INVALID_ARG (bytes
+ * not the blob size, n > max_gaussians, degree not in 0..3). */
+VRS_API int64_t vrs_scene_blob_bytes(int64_t n, int32_t sh_degree);
+VRS_API vrs_status vrs_export_scene(vrs_context* ctx, void* blob, int64_t bytes, int64_t* n_out, int32_t* deg_out,
+                                    void* stream);
+VRS_API vrs_status vrs_import_scene(vrs_context* ctx, int64_t n, int32_t sh_degree, const void* blob, int64_t bytes,
+                                    void* stream);
+
 /* Visibility mask for a slot (HOST pointer, w*h bytes, row-major, >0 =
  * visible).  mask == NULL clears the slot (all visible). */
 VRS_API vrs_status vrs_set_visibility_mask(vrs_context* ctx, int32_t slot, int32_t w, int32_t h, const uint8_t* mask);

@@ -367,6 +367,91 @@ vrs_status vrs_upload_gaussians(vrs_context* ctx, int64_t n, int32_t sh_degree, 
     return VRS_OK;
 }
 
+// ---------------------------------------------------------------- scene blob (multi-GPU)
+namespace {
+inline size_t align256(size_t b) { return (b + 255) & ~(size_t)255; }
+struct BlobLayout {
+    size_t mu, geo, smax, sh, raw, total;
+};
+BlobLayout blob_layout(int64_t n, int deg) {
+    const size_t N = (size_t)std::max<int64_t>(n, 1);
+    const int chunks = ((deg + 1) * (deg + 1) * 3 + 3) / 4;
+    BlobLayout L;
+    L.mu = 0;
+    L.geo = L.mu + align256(16 * N);
+    L.smax = L.geo + align256(64 * N);
+    L.sh = L.smax + align256(4 * N);
+    L.raw = L.sh + align256(16 * (size_t)chunks * N);
+    L.total = L.raw + align256(32 * N);
+    return L;
+}
+}  // namespace
+
+int64_t vrs_scene_blob_bytes(int64_t n, int32_t sh_degree) {
+    if (n < 0 || sh_degree < 0 || sh_degree > 3) return -1;
+    return (int64_t)blob_layout(n, sh_degree).total;
+}
+
+vrs_status vrs_export_scene(vrs_context* ctx, void* blob, int64_t bytes, int64_t* n_out, int32_t* deg_out,
+                            void* stream) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    if (ctx->sticky != VRS_OK) return ctx->sticky;
+    if (!ctx->uploaded) return fail(ctx, VRS_E_STATE, "export before vrs_upload_gaussians");
+    const BlobLayout L = blob_layout(ctx->N, ctx->deg);
+    if (!blob || bytes != (int64_t)L.total) return fail(ctx, VRS_E_INVALID_ARG, "blob size differs from vrs_scene_blob_bytes");
+    CK(cudaSetDevice(ctx->cfg.device));
+    cudaStream_t st = (cudaStream_t)stream;
+    char* b = static_cast<char*>(blob);
+    const size_t N = (size_t)ctx->N;
+    if (N > 0) {
+        CK(cudaMemcpyAsync(b + L.mu, ctx->d_mu, 16 * N, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(b + L.geo, ctx->d_geo, 64 * N, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(b + L.smax, ctx->d_smax, 4 * N, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(b + L.sh, ctx->d_sh, 16 * (size_t)ctx->sh_chunks * N, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(b + L.raw, ctx->d_raw, 32 * N, cudaMemcpyDeviceToDevice, st));
+    }
+    if (n_out) *n_out = ctx->N;
+    if (deg_out) *deg_out = ctx->deg;
+    return VRS_OK;
+}
+
+vrs_status vrs_import_scene(vrs_context* ctx, int64_t n, int32_t sh_degree, const void* blob, int64_t bytes,
+                            void* stream) {
+    if (!ctx) return VRS_E_INVALID_ARG;
+    if (ctx->sticky != VRS_OK) return ctx->sticky;
+    if (n < 0 || n > ctx->cfg.max_gaussians || sh_degree < 0 || sh_degree > 3)
+        return fail(ctx, VRS_E_INVALID_ARG, "n / sh_degree");
+    const BlobLayout L = blob_layout(n, sh_degree);
+    if (!blob || bytes != (int64_t)L.total) return fail(ctx, VRS_E_INVALID_ARG, "blob size differs from vrs_scene_blob_bytes");
+    CK(cudaSetDevice(ctx->cfg.device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const int chunks = ((sh_degree + 1) * (sh_degree + 1) * 3 + 3) / 4;
+    for (float4** p : {&ctx->d_mu, &ctx->d_geo, &ctx->d_sh, &ctx->d_raw})
+        if (*p) { cudaFree(*p); *p = nullptr; }
+    if (ctx->d_smax) { cudaFree(ctx->d_smax); ctx->d_smax = nullptr; }
+    const size_t NN = (size_t)std::max<int64_t>(n, 1);
+    CK(dalloc(&ctx->d_mu, NN));
+    CK(dalloc(&ctx->d_geo, 4 * NN));
+    CK(dalloc(&ctx->d_smax, NN));
+    CK(dalloc(&ctx->d_sh, (size_t)chunks * NN));
+    CK(dalloc(&ctx->d_raw, 2 * NN));
+    const char* b = static_cast<const char*>(blob);
+    if (n > 0) {
+        CK(cudaMemcpyAsync(ctx->d_mu, b + L.mu, 16 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(ctx->d_geo, b + L.geo, 64 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(ctx->d_smax, b + L.smax, 4 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(ctx->d_sh, b + L.sh, 16 * (size_t)chunks * n, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(ctx->d_raw, b + L.raw, 32 * (size_t)n, cudaMemcpyDeviceToDevice, st));
+    }
+    ctx->N = n;
+    ctx->have_frame = false;
+    ctx->last_items = 0;
+    ctx->deg = sh_degree;
+    ctx->sh_chunks = chunks;
+    ctx->uploaded = true;
+    return VRS_OK;
+}
+
 vrs_status vrs_set_visibility_mask(vrs_context* ctx, int32_t slot, int32_t w, int32_t h, const uint8_t* mask) {
     if (!ctx) return VRS_E_INVALID_ARG;
     if (ctx->sticky != VRS_OK) return ctx->sticky;

@@ -3,7 +3,8 @@
 Views (left/right eye, trajectory frames) are independent units, so every
 rank holds a replica of the scene and renders a contiguous block of stereo
 pairs; there is no exchange inside a frame.  Collectives are used only to
-broadcast the scene once (``broadcast_scene``) and to gather finished frames
+broadcast the scene once (``broadcast_uploaded_scene``: the activated device
+buffers, device to device; ``broadcast_scene``: the raw arrays) and to gather finished frames
 to rank 0 (``gather_frames``, grouped point-to-point sends, since NCCL has no
 gather collective).  Works with ``nccl`` (CUDA tensors) and ``gloo`` (CPU
 tensors, used by the tests).
@@ -52,6 +53,39 @@ def broadcast_scene(scene, n: int, sh_degree: int, device=None, src: int = 0):
         dist.broadcast(t, src)
         out[f] = t.cpu().numpy()
     return RawScene(out["means"], out["quats"], out["log_scales"], out["logits"], out["sh"], sh_degree)
+
+
+def broadcast_uploaded_scene(renderer, src: int = 0):
+    """Device-to-device scene replication: ``src`` has uploaded the
+    scene (host activation once); its activated buffers travel as one device
+    blob by ``dist.broadcast`` (NCCL over NVLink; gloo test hook: host copy) and
+    every other rank imports it -- no host round trip, no second activation.
+    Returns the blob's byte count."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank()
+    dev = torch.device("cuda", renderer.device)
+    gloo = dist.get_backend() == "gloo"
+    meta = torch.zeros(3, dtype=torch.int64, device="cpu" if gloo else dev)
+    blob = None
+    if rank == src:
+        blob, n, deg = renderer.vrs_export_scene()
+        meta[0], meta[1], meta[2] = n, deg, blob.numel()
+    dist.broadcast(meta, src)
+    n, deg, nbytes = (int(x) for x in meta.tolist())
+    if rank != src:
+        blob = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    if gloo:
+        torch.cuda.synchronize(dev)
+        hb = blob.cpu()
+        dist.broadcast(hb, src)
+        blob.copy_(hb)
+    else:
+        dist.broadcast(blob, src)
+    if rank != src:
+        renderer.vrs_import_scene(n, deg, blob)
+    torch.cuda.synchronize(dev)
+    return nbytes
 
 
 def gather_frames(local_frames, views_per_rank, dst: int = 0):

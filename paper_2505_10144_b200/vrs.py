@@ -20,6 +20,7 @@ VRS_MAX_VIEWS = 8
 VRS_STAGING_THREADS, VRS_STAGING_TMA = 0, 1
 VRS_SORT_STOPTHEPOP, VRS_SORT_Z, VRS_SORT_DIST = 0, 1, 2
 EXPORTS = ["vrs_abi_version", "vrs_create", "vrs_destroy", "vrs_last_error", "vrs_upload_gaussians",
+           "vrs_scene_blob_bytes", "vrs_export_scene", "vrs_import_scene",
            "vrs_set_visibility_mask", "vrs_render_views", "vrs_render_views_host", "vrs_set_instrumentation",
            "vrs_set_resort_mode", "vrs_set_sort_mode", "vrs_set_staging_mode", "vrs_set_output_format", "vrs_backward",
            "vrs_render_views_two_pass", "vrs_get_frame_stats", "vrs_debug_counts", "vrs_debug_pairs", "vrs_debug_ranges", "vrs_debug_splats",
@@ -79,6 +80,9 @@ def lib():
             "vrs_destroy": (None, [vp]),
             "vrs_last_error": (C.c_char_p, [vp]),
             "vrs_upload_gaussians": (i32, [vp, i64, i32, vp, vp, vp, vp, vp, C.POINTER(C.c_int64)]),
+            "vrs_scene_blob_bytes": (i64, [i64, i32]),
+            "vrs_export_scene": (i32, [vp, vp, i64, C.POINTER(C.c_int64), C.POINTER(C.c_int32), vp]),
+            "vrs_import_scene": (i32, [vp, i64, i32, vp, i64, vp]),
             "vrs_set_visibility_mask": (i32, [vp, i32, i32, i32, vp]),
             "vrs_render_views": (i32, [vp, i32, vp, vp, vp, vp, vp]),
             "vrs_render_views_host": (i32, [vp, i32, vp, vp, vp, vp, vp]),
@@ -179,6 +183,32 @@ class Renderer:
         return rej.value
 
     upload = vrs_upload_gaussians
+
+    def _stream_ptr(self, stream):
+        import torch
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+    def vrs_export_scene(self, stream=None):
+        """The activated scene as one DEVICE blob (uint8 tensor on this renderer's device),
+        enqueued on `stream` (default: torch's current stream).  Returns (blob, n, sh_degree)."""
+        import torch
+        n, deg = self.n, self.sh_degree
+        nbytes = lib().vrs_scene_blob_bytes(n, deg)
+        blob = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", self.device))
+        n_out, d_out = C.c_int64(0), C.c_int32(0)
+        self._check(lib().vrs_export_scene(self.h, C.c_void_p(blob.data_ptr()), nbytes, C.byref(n_out),
+                                           C.byref(d_out), C.c_void_p(self._stream_ptr(stream))))
+        return blob, n_out.value, d_out.value
+
+    def vrs_import_scene(self, n, sh_degree, blob, stream=None):
+        """Adopt a scene blob exported by another renderer (DEVICE uint8 tensor on this device)."""
+        if not blob.is_cuda or blob.device.index != self.device or blob.dtype.itemsize != 1:
+            raise ValueError(f"blob must be a byte tensor on cuda:{self.device}")
+        self._check(lib().vrs_import_scene(self.h, int(n), int(sh_degree), C.c_void_p(blob.data_ptr()), blob.numel(),
+                                           C.c_void_p(self._stream_ptr(stream))))
+        self.n, self.sh_degree = int(n), int(sh_degree)
 
     def vrs_set_visibility_mask(self, slot, mask):
         if mask is None:
