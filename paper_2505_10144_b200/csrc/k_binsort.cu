@@ -6,7 +6,7 @@
 // tile: it takes the pair's arrival rank from the tile's counter and writes
 // (depth bits << 32 | g) straight into the tile's bucket slot (tile *
 // kTileCap + rank), or onto an overflow list past kTileCap.  Then:
-//   k_tile_scan   one block: exclusive scans of the per-tile counts -> ranges
+//   k_tile_scan   decoupled look-back scan of the per-tile counts -> ranges
 //                 (empty tiles (0, 0), as the oracle reports them; clamped to
 //                 the pair capacity), of the overflow counts -> overflow
 //                 offsets, the pair total, the list of non-empty tiles, and
@@ -26,17 +26,20 @@
 namespace vrs {
 
 namespace {
-constexpr int kScanT = 1024;
+constexpr int kScanT = 256;
 #ifndef VRS_TS_GRID
 #define VRS_TS_GRID 4
 #endif
-#ifndef VRS_SCAN_PER
-#define VRS_SCAN_PER 12
-#endif
-constexpr int kScanPer = VRS_SCAN_PER;
-constexpr int kScanRound = kScanT * kScanPer;
+constexpr int kScanPer = 4;                     // tiles per thread (one 16-B load)
+constexpr int kScanChunk = kScanT * kScanPer;   // tiles per look-back chunk
 constexpr int kBinT = 256;
-constexpr int kWarpSortMax = 256;  // tiles up to this size: one warp, keys in registers (E <= 8)
+// Tiles up to small_max pairs are sorted by one warp, keys in registers (E <=
+// 16); small_max is 512 when the frame has enough tiles to keep every warp
+// busy (>= 128 per SM: C3's 35.6k tiles, sort 0.285 -> 0.261 ms), else 256
+// (C2's 9k tiles: a 512-key register sort is a long serial chain, and the
+// block path's eight warps per tile finish sooner: 0.063 vs 0.070 ms).
+constexpr int kWarpSortMax = 512;
+constexpr int kWarpSortTilesPerSm = 128;
 
 // Ascending bitonic sort of s[0, P), P a power of two >= 64, by a block of NT
 // threads.  Compare-exchange i of a stage with distance j <= 32 touches only
@@ -199,114 +202,144 @@ __device__ __forceinline__ void warp_sort_tile(const uint64_t* __restrict__ bk, 
 }
 }  // namespace
 
+// Status word of a chunk's look-back: flag (1 = chunk aggregate, 2 =
+// inclusive prefix) in bits 62-63, value in bits 0-31.  Relaxed GPU-scope
+// accesses: a word carries its own flag, so no acquire ordering is needed.
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+constexpr unsigned long long kStatAgg = 1ull << 62, kStatInc = 2ull << 62;
+
+// The per-tile counts -> tile ranges, overflow offsets, the pair total and
+// the big / small tile lists, as one decoupled look-back scan over chunks of
+// kScanChunk tiles (four scanned quantities: pairs, overflow pairs, big
+// tiles, small tiles).  Chunks are taken in launch order from a ticket; the
+// last block to finish re-arms the ticket and the status words, and every
+// block re-zeroes the counts it read, for the next frame.  List positions
+// come from the scan, so both lists are in tile order.
 __global__ void __launch_bounds__(kScanT) k_tile_scan(uint32_t* __restrict__ cnt, int64_t n_tiles,
                                                       uint32_t* __restrict__ ranges, uint32_t* __restrict__ ovf_off,
                                                       uint32_t* __restrict__ total, uint32_t cap,
                                                       uint32_t* __restrict__ list, uint32_t* __restrict__ list_n,
-                                                      int64_t list_cap, uint32_t small_max) {
-    extern __shared__ uint32_t s_dyn[];
-    uint32_t* const s_c = s_dyn;               // [kScanRound] counts, then tile starts
-    uint32_t* const s_o = s_dyn + kScanRound;  // [kScanRound] overflow starts
-    __shared__ uint32_t s_w[kScanT / 32], s_wo[kScanT / 32];
-    __shared__ uint32_t s_nb, s_ns;
+                                                      int64_t list_cap, uint32_t small_max,
+                                                      unsigned long long* __restrict__ stat, uint32_t* __restrict__ ctr) {
+    __shared__ uint32_t s_w[4][kScanT / 32];
+    __shared__ uint32_t s_pre[4];
+    __shared__ uint32_t s_chunk;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_nb = s_ns = 0;
-    uint32_t carry = 0, ocarry = 0;
-    for (int64_t r0 = 0; r0 < n_tiles; r0 += kScanRound) {
-        const int m = (int)min((int64_t)kScanRound, n_tiles - r0);
-        for (int i = tid; i < m; i += kScanT) {  // coalesced, and re-zero for the next frame
-            s_c[i] = cnt[r0 + i];
-            cnt[r0 + i] = 0u;
-        }
-        __syncthreads();
-        uint32_t v[kScanPer], sum = 0, osum = 0;
+    if (tid == 0) s_chunk = atomicAdd(&ctr[0], 1u);
+    __syncthreads();
+    const uint32_t chunk = s_chunk, n_chunks = (uint32_t)((n_tiles + kScanChunk - 1) / kScanChunk);
+    const int64_t t0 = (int64_t)chunk * kScanChunk + (int64_t)tid * kScanPer;
+    uint32_t v[kScanPer];
+    if (t0 + kScanPer <= n_tiles) {
+        const uint4 q = *reinterpret_cast<const uint4*>(cnt + t0);
+        v[0] = q.x; v[1] = q.y; v[2] = q.z; v[3] = q.w;
+        *reinterpret_cast<uint4*>(cnt + t0) = make_uint4(0u, 0u, 0u, 0u);
+    } else {
 #pragma unroll
         for (int k = 0; k < kScanPer; k++) {
-            const int idx = tid * kScanPer + k;
-            v[k] = idx < m ? s_c[idx] : 0u;
-            sum += v[k];
-            osum += v[k] > kTileCap ? v[k] - kTileCap : 0u;
+            v[k] = t0 + k < n_tiles ? cnt[t0 + k] : 0u;
+            if (t0 + k < n_tiles) cnt[t0 + k] = 0u;
         }
-        uint32_t inc = sum, oinc = osum;
+    }
+    // this thread's sums: pairs, overflow pairs, big tiles, small tiles (sizes as
+    // clamped below only differ after a capacity overflow, which the lists tolerate)
+    uint32_t q[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int k = 0; k < kScanPer; k++) {
+        q[0] += v[k];
+        q[1] += v[k] > kTileCap ? v[k] - kTileCap : 0u;
+        q[2] += v[k] > small_max ? 1u : 0u;
+        q[3] += (v[k] != 0u && v[k] <= small_max) ? 1u : 0u;
+    }
+    uint32_t inc[4];
+#pragma unroll
+    for (int c = 0; c < 4; c++) {
+        inc[c] = q[c];
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
-            const uint32_t yo = __shfl_up_sync(0xffffffffu, oinc, o);
-            if (lane >= o) {
-                inc += y;
-                oinc += yo;
-            }
+            const uint32_t y = __shfl_up_sync(0xffffffffu, inc[c], o);
+            if (lane >= o) inc[c] += y;
         }
-        if (lane == 31) {
-            s_w[warp] = inc;
-            s_wo[warp] = oinc;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t w = s_w[lane], wo = s_wo[lane];
+        if (lane == 31) s_w[c][warp] = inc[c];
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+        for (int c = 0; c < 4; c++) {
+            uint32_t w = lane < kScanT / 32 ? s_w[c][lane] : 0u;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                const uint32_t yo = __shfl_up_sync(0xffffffffu, wo, o);
-                if (lane >= o) {
-                    w += y;
-                    wo += yo;
+                if (lane >= o) w += y;
+            }
+            if (lane < kScanT / 32) s_w[c][lane] = w;  // inclusive over warps
+        }
+        // look-back: lane c < 4 carries quantity c
+        if (lane < 4) {
+            const uint32_t agg = s_w[lane][kScanT / 32 - 1];
+            unsigned long long* my = stat + 4 * (size_t)chunk + lane;
+            uint32_t pre = 0;
+            if (chunk == 0) {
+                st_status(my, kStatInc | agg);
+            } else {
+                st_status(my, kStatAgg | agg);
+                for (int64_t p = (int64_t)chunk - 1; p >= 0; p--) {
+                    unsigned long long w;
+                    do {
+                        w = ld_status(stat + 4 * (size_t)p + lane);
+                    } while ((w >> 62) == 0ull);
+                    pre += (uint32_t)w;
+                    if ((w >> 62) == 2ull) break;
                 }
+                st_status(my, kStatInc | (pre + agg));
             }
-            s_w[lane] = w;
-            s_wo[lane] = wo;
+            s_pre[lane] = pre;
+            if (chunk == n_chunks - 1) {  // the last chunk knows the totals
+                if (lane == 0) *total = pre + agg;
+                if (lane == 2) list_n[0] = pre + agg;
+                if (lane == 3) list_n[1] = pre + agg;
+                if (lane == 1) list_n[2] = 0u;  // k_tile_sort's small-tile work counter
+            }
         }
-        __syncthreads();
-        uint32_t excl = carry + (warp ? s_w[warp - 1] : 0u) + inc - sum;
-        uint32_t oexcl = ocarry + (warp ? s_wo[warp - 1] : 0u) + oinc - osum;
-#pragma unroll
-        for (int k = 0; k < kScanPer; k++) {  // starts replace the counts (all were read above)
-            const int idx = tid * kScanPer + k;
-            if (idx < m) {
-                s_c[idx] = excl;
-                s_o[idx] = oexcl;
-            }
-            excl += v[k];
-            oexcl += v[k] > kTileCap ? v[k] - kTileCap : 0u;
-        }
-        const uint32_t carry_next = carry + s_w[kScanT / 32 - 1];
-        const uint32_t ocarry_next = ocarry + s_wo[kScanT / 32 - 1];
-        __syncthreads();
-        const unsigned lt = (1u << lane) - 1u;
-        for (int i0 = 0; i0 < m; i0 += kScanT) {  // coalesced stores + list appends
-            const int i = i0 + tid;
-            uint32_t c = 0;
-            if (i < m) {
-                const uint32_t st = s_c[i];
-                c = (i + 1 < m ? s_c[i + 1] : carry_next) - st;
-                // clamped to the pair capacity (only after an overflow, which the stats report)
-                const uint32_t a = min(st, cap), b = min(st + c, cap);
-                reinterpret_cast<uint2*>(ranges)[r0 + i] = c ? make_uint2(a, b) : make_uint2(0u, 0u);
-                ovf_off[r0 + i] = s_o[i];
-                c = b - a;
-            }
-            const uint32_t t = (uint32_t)(r0 + i);
-            const unsigned mb = __ballot_sync(0xffffffffu, c > small_max);
-            const unsigned ms = __ballot_sync(0xffffffffu, c != 0u && c <= small_max);
-            uint32_t bb = 0, bs = 0;
-            if (lane == 0) {  // one shared atomic per warp and class (list order is irrelevant)
-                if (mb) bb = atomicAdd(&s_nb, (uint32_t)__popc(mb));
-                if (ms) bs = atomicAdd(&s_ns, (uint32_t)__popc(ms));
-            }
-            bb = __shfl_sync(0xffffffffu, bb, 0);
-            bs = __shfl_sync(0xffffffffu, bs, 0);
-            if ((mb >> lane) & 1u) list[bb + __popc(mb & lt)] = t;                     // big tiles from the front
-            if ((ms >> lane) & 1u) list[list_cap - 1 - (bs + __popc(ms & lt))] = t;  // small ones from the back
-        }
-        carry = carry_next;
-        ocarry = ocarry_next;
-        __syncthreads();
     }
+    __syncthreads();
+    uint32_t e[4];
+#pragma unroll
+    for (int c = 0; c < 4; c++) e[c] = s_pre[c] + (warp ? s_w[c][warp - 1] : 0u) + inc[c] - q[c];
+#pragma unroll
+    for (int k = 0; k < kScanPer; k++) {
+        const int64_t t = t0 + k;
+        if (t < n_tiles) {
+            // clamped to the pair capacity (only after an overflow, which the stats report)
+            const uint32_t a = min(e[0], cap), b = min(e[0] + v[k], cap);
+            reinterpret_cast<uint2*>(ranges)[t] = v[k] ? make_uint2(a, b) : make_uint2(0u, 0u);
+            ovf_off[t] = e[1];
+            if (v[k] > small_max) list[e[2]++] = (uint32_t)t;                                  // big tiles from the front
+            else if (v[k] != 0u) list[list_cap - 1 - e[3]++] = (uint32_t)t;                     // small ones from the back
+        }
+        e[0] += v[k];
+        e[1] += v[k] > kTileCap ? v[k] - kTileCap : 0u;
+    }
+    // the last block to finish re-arms the ticket and the status words
+    __syncthreads();
     if (tid == 0) {
-        list_n[0] = s_nb;
-        list_n[1] = s_ns;
-        list_n[2] = 0u;  // k_tile_sort's small-tile work counter
-        *total = carry;
+        __threadfence();
+        s_chunk = atomicAdd(&ctr[1], 1u) == n_chunks - 1 ? 1u : 0u;
+    }
+    __syncthreads();
+    if (s_chunk) {
+        for (uint32_t i = tid; i < 4 * n_chunks; i += kScanT) stat[i] = 0ull;
+        if (tid == 0) {
+            ctr[0] = 0u;
+            ctr[1] = 0u;
+        }
     }
 }
 
@@ -409,7 +442,7 @@ __global__ void __launch_bounds__(kBinT, 4) k_tile_sort(const uint32_t* __restri
     // small tiles: one warp each, taken dynamically (warp-private slice of s_k)
     const int lane = (int)(tid & 31u);
     __syncthreads();  // the block path is done with s_k
-    uint64_t* sw = s_k + (tid >> 5) * (32 * 9);
+    uint64_t* sw = s_k + (tid >> 5) * (32 * 17);  // 8 x 4.25 KB scratch inside s_k
     while (true) {
         uint32_t w = 0;
         if (lane == 0) w = atomicAdd(work, 1u);
@@ -418,10 +451,11 @@ __global__ void __launch_bounds__(kBinT, 4) k_tile_sort(const uint32_t* __restri
         const uint32_t t = list[list_cap - 1 - w];
         const uint32_t off = ranges[2 * (size_t)t], n = ranges[2 * (size_t)t + 1] - off;
         const uint64_t tk = (uint64_t)t << 32;
-        const uint64_t* tb = tbucket + (size_t)t * kTileCap;  // n <= 256 <= kTileCap: all direct slots
+        const uint64_t* tb = tbucket + (size_t)t * kTileCap;  // n <= kWarpSortMax <= kTileCap: all direct slots
         if (n <= 64) warp_sort_tile<2>(tb, n, tk, keys + off, vals + off, sw, lane);
         else if (n <= 128) warp_sort_tile<4>(tb, n, tk, keys + off, vals + off, sw, lane);
-        else warp_sort_tile<8>(tb, n, tk, keys + off, vals + off, sw, lane);
+        else if (n <= 256) warp_sort_tile<8>(tb, n, tk, keys + off, vals + off, sw, lane);
+        else warp_sort_tile<16>(tb, n, tk, keys + off, vals + off, sw, lane);
     }
 }
 
@@ -435,11 +469,14 @@ void launch_binsort(FrameBufs fb, int64_t cap, int64_t n_tiles, BinScratch b, cu
         return;
     }
     const int sort_smem = (int)(kBinCap * 8 + (kBinT / 32) * 32 * 9 * 8);
+    static_assert((kBinT / 32) * 32 * 17 <= kBinCap + (kBinT / 32) * 32 * 9, "small-tile scratch inside s_k");
     ensure_smem_attr((const void*)k_tile_sort, sort_smem);
     const int sms = sms_now();
-    ensure_smem_attr((const void*)k_tile_scan, (int)(2 * kScanRound * 4));
-    k_tile_scan<<<1, kScanT, 2 * kScanRound * 4, st>>>(b.tile_cnt, n_tiles, fb.ranges, b.ovf_off, fb.total, (uint32_t)cap, b.list,
-                                      b.list_n, b.max_tiles, min(b.cap_smem, (uint32_t)kWarpSortMax));
+    const uint32_t small_max = n_tiles >= (int64_t)kWarpSortTilesPerSm * sms ? (uint32_t)kWarpSortMax : 256u;
+    const unsigned n_chunks = (unsigned)((n_tiles + kScanChunk - 1) / kScanChunk);
+    k_tile_scan<<<n_chunks, kScanT, 0, st>>>(b.tile_cnt, n_tiles, fb.ranges, b.ovf_off, fb.total, (uint32_t)cap, b.list,
+                                             b.list_n, b.max_tiles, min(b.cap_smem, small_max), b.scan_stat,
+                                             b.scan_ctr);
     k_ovf_bucket<<<sms * 2, 256, 0, st>>>(fb.keys_alt, fb.vals_alt, b.rank, b.ovf_count, (uint32_t)cap, b.ovf_off,
                                           b.obucket);
     k_tile_sort<<<sms * VRS_TS_GRID, kBinT, sort_smem, st>>>(b.list, b.list_n, b.max_tiles, fb.ranges, b.tbucket, b.ovf_off,

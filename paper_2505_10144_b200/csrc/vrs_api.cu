@@ -142,7 +142,7 @@ static void free_all(vrs_context* c) {
                     c->d_sidk,
                     c->d_keys, c->d_keys_alt, c->d_vals, c->d_vals_alt, c->d_ranges, c->d_low_rgba, c->d_low_depth,
                     c->d_stats, c->d_scan_scratch, c->sort.hist, c->sort.status, c->sort.counters, c->d_vis,
-                    c->bin.tile_cnt, c->bin.rank, c->bin.list, c->bin.list_n, c->bin.tbucket, c->bin.ovf_off, c->bin.obucket,
+                    c->bin.tile_cnt, c->bin.rank, c->bin.list, c->bin.list_n, c->bin.scan_stat, c->bin.scan_ctr, c->bin.tbucket, c->bin.ovf_off, c->bin.obucket,
                     c->d_sat, c->d_cls, c->d_items, c->d_nitems, c->d_inv, c->d_lowcnt, c->d_lowcnt0, c->d_rays,
                     c->d_out_rgba, c->d_out_depth};
     for (void* p : ptrs)
@@ -221,6 +221,8 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     A(dalloc(&ctx->bin.obucket, (size_t)P));
     A(dalloc(&ctx->bin.list, (size_t)ctx->bin.max_tiles));
     A(dalloc(&ctx->bin.list_n, 4));
+    A(dalloc(&ctx->bin.scan_stat, (size_t)4 * ((ctx->bin.max_tiles + 1023) / 1024)));
+    A(dalloc(&ctx->bin.scan_ctr, 2));
     A(dalloc(&ctx->d_vis, (size_t)V * ctx->max_tiles_view));
     A(dalloc(&ctx->d_cls, (size_t)V * ctx->max_tiles_view));
     A(dalloc(&ctx->d_sat, (size_t)V * ctx->max_sat_view));
@@ -245,6 +247,8 @@ vrs_status vrs_create(const vrs_config* cfg, vrs_context** out) {
     cudaMemset(ctx->d_rec, 0, sizeof(float4) * (size_t)V * N * kRecF4);
     ctx->bin.ovf_count = ctx->d_misc + 5;
     cudaMemset(ctx->bin.tile_cnt, 0, sizeof(uint32_t) * ctx->bin.max_tiles);  // k_tile_scan re-zeroes per frame
+    cudaMemset(ctx->bin.scan_stat, 0, sizeof(unsigned long long) * 4 * ((ctx->bin.max_tiles + 1023) / 1024));
+    cudaMemset(ctx->bin.scan_ctr, 0, sizeof(uint32_t) * 2);  // (both re-armed by k_tile_scan's last block)
     *out = ctx;
     return VRS_OK;
 }

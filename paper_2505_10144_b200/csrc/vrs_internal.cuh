@@ -166,7 +166,7 @@ void launch_scan(const uint32_t* in, uint32_t* out, uint32_t* total, const uint3
                  int64_t expand_cap = 0);
 size_t scan_scratch_words(int64_t n);
 // Binned per-tile sort (k_binsort.cu): tile test -> per-tile buckets (direct
-// slots up to kTileCap, overflow list beyond), one-block tile-count scan ->
+// slots up to kTileCap, overflow list beyond), look-back tile-count scan ->
 // ranges (+ overflow offsets, pair total), overflow placement, per-tile sort
 // of (depth bits, g) -> sorted (keys, vals).  cap_smem: largest tile sorted in
 // shared memory (power of two <= kBinCap); bigger tiles merge in global memory.
@@ -181,6 +181,8 @@ struct BinScratch {
     uint32_t* rank;          // [cap] overflow entry's rank inside its tile
     uint32_t* list;          // [max tiles] non-empty tiles: big ones from the front, small from the back
     uint32_t* list_n;        // [3] (big, small, small-tile work counter)
+    unsigned long long* scan_stat;  // [4 * ceil(max tiles / 1024)] k_tile_scan look-back words (zero between frames)
+    uint32_t* scan_ctr;      // [2] k_tile_scan chunk ticket, finished blocks (zero between frames)
     int64_t max_tiles;
     uint32_t cap_smem;
 };
