@@ -86,8 +86,7 @@ __global__ void __launch_bounds__(256) k_blend_bwd(FrameParams fp, FrameBufs fb,
     const float Tfin = 1.0f - fo.w;
     if (tid < 8) {  // per-warp sample extent (the forward's conservative footprint skip)
         const int wwx = (tid & 1) * 8, wwy = (tid >> 1) * 4;
-        S.wblock[tid] = make_float4((float)(ox + wwx) + 0.5f, (float)(ox + wwx + 7) + 0.5f, (float)(oy + wwy) + 0.5f,
-                                    (float)(oy + wwy + 3) + 0.5f);
+        S.wblock[tid] = make_float4((float)(ox + wwx + 4), (float)(oy + wwy + 2), 3.5f, 1.5f);  // centre, half-extent
     }
     char* const wkb = reinterpret_cast<char*>(&S.w_key[0][tid]);
     char* const wab = reinterpret_cast<char*>(&S.w_a[0][tid]);
@@ -236,13 +235,7 @@ __global__ void __launch_bounds__(256) k_blend_bwd(FrameParams fp, FrameBufs fb,
             S.r4[tid] = __ldg(rp + 4);
             const float4 a5 = __ldg(rp + 5), a7 = __ldg(rp + 7);
             S.r5[tid] = make_float4(a5.x, a5.y, __uint_as_float(g), 0.0f);
-            uint32_t m = 0;
-#pragma unroll
-            for (int w = 0; w < 8; w++) {
-                const float4 b = S.wblock[w];
-                m |= !(a7.y < b.x || a7.x > b.y || a7.w < b.z || a7.z > b.w) ? (1u << w) : 0u;
-            }
-            S.mask[tid] = m;
+            S.mask[tid] = footprint_mask<8>(a7, S.wblock);
         }
         if (__syncthreads_count(!done) == 0) break;
         const int nb = min((int)(re - base), kGB);

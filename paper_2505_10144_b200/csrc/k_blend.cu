@@ -14,7 +14,7 @@
 // stages in flight.  The warps of a block consume the stages independently
 // (no block barrier in the loop): a warp waits on the stage's mbarrier,
 // culls the stage's entries against its own 8x4 sample block with their
-// conservative pixel footprints (the hierarchical culling of P:431 -- never
+// conservative pixel footprints (bounding box + minor-axis extent) (the hierarchical culling of P:431 -- never
 // changes results, only work), evaluates two entries' memberships per
 // iteration and runs their contributions in stream order; the last warp to
 // finish a stage re-arms the slot with the stage two ahead.
@@ -182,7 +182,7 @@ struct BlendSmem {
     float4 rec[kBatch][6];
     uint32_t mask[kBatch];    // g << 8 | the warps whose samples the entry's pixel footprint meets
     unsigned long long full;  // mbarrier: the batch landed (TMA staging)
-    float4 wblock[kWarps];    // per-warp sample extent xmin, xmax, ymin, ymax (pixel coords)
+    float4 wblock[kWarps];    // per-warp sample block: centre x, y, half-extent x, y (pixel coords)
     // per-thread resort window: ring of K slots, (tau, g) packed into one
     // order-preserving 64-bit key, alpha alongside; [slot][thread] layout is
     // bank-conflict free for any per-thread slot index
@@ -320,12 +320,10 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         if (tid < kWarps) {
             const int wwx = (tid & 1) * 8, wwy = (tid >> 1) * 4 + half * 8;
             float4 b;
-            if (g.kind == kItemLow)
-                b = make_float4((float)(g.x0 + 2 * wwx + 1), (float)(g.x0 + 2 * (wwx + 7) + 1),
-                                (float)(g.y0 + 2 * wwy + 1), (float)(g.y0 + 2 * (wwy + 3) + 1));
-            else
-                b = make_float4((float)(g.ox + wwx) + 0.5f, (float)(g.ox + wwx + 7) + 0.5f,
-                                (float)(g.oy + wwy) + 0.5f, (float)(g.oy + wwy + 3) + 0.5f);
+            if (g.kind == kItemLow)  // samples at x0 + 2 sx + 1, sx = wwx .. wwx + 7 (rows likewise)
+                b = make_float4((float)(g.x0 + 2 * wwx + 8), (float)(g.y0 + 2 * wwy + 4), 7.0f, 3.0f);
+            else  // samples at pixel centres ox + sx + 0.5
+                b = make_float4((float)(g.ox + wwx + 4), (float)(g.oy + wwy + 2), 3.5f, 1.5f);
             S.wblock[tid] = b;
         }
         xs = g.xs;
@@ -478,14 +476,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
             if (mine) {
                 g = __ldg(fb.vals + base + i);
                 g = (g < (uint32_t)fp.N) ? g : 0u;  // memory safety after a capacity overflow only
-                const float4 a7 = __ldg(recv + (size_t)g * kRecF4 + 7);
-                uint32_t m = 0;
-#pragma unroll
-                for (int w = 0; w < kWarps; w++) {
-                    const float4 b = S.wblock[w];
-                    const bool hit = !(a7.y < b.x || a7.x > b.y || a7.w < b.z || a7.z > b.w);
-                    m |= hit ? (1u << w) : 0u;
-                }
+                const uint32_t m = footprint_mask<kWarps>(__ldg(recv + (size_t)g * kRecF4 + 7), S.wblock);
                 S.mask[i] = (g << 8) | (fp.no_cull ? 0xffu : m);
             }
             // the previous batch was read through the generic proxy (ordered before
@@ -512,13 +503,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
                              a4 = __ldg(rp + 4), a5 = __ldg(rp + 5), a7 = __ldg(rp + 7);
                 S.rec[tid][0] = a0; S.rec[tid][1] = a1; S.rec[tid][2] = a2;
                 S.rec[tid][3] = a3; S.rec[tid][4] = a4; S.rec[tid][5] = a5;
-                uint32_t m = 0;
-#pragma unroll
-                for (int w = 0; w < kWarps; w++) {
-                    const float4 b = S.wblock[w];
-                    const bool hit = !(a7.y < b.x || a7.x > b.y || a7.w < b.z || a7.z > b.w);
-                    m |= hit ? (1u << w) : 0u;
-                }
+                const uint32_t m = footprint_mask<kWarps>(a7, S.wblock);
                 S.mask[tid] = (g << 8) | (fp.no_cull ? 0xffu : m);
             }
         }

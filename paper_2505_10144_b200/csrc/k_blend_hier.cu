@@ -113,12 +113,10 @@ __global__ void __launch_bounds__(kHT, VRS_HIER_MINB) k_blend_hier(FrameParams f
     if (tid < kHW) {
         const int wwx = (tid & 1) * 8, wwy = (tid >> 1) * 4;
         float4 b;
-        if (low)
-            b = make_float4((float)(x0 + 2 * wwx + 1), (float)(x0 + 2 * (wwx + 7) + 1), (float)(y0 + 2 * wwy + 1),
-                            (float)(y0 + 2 * (wwy + 3) + 1));
+        if (low)  // centre, half-extent of the warp's samples (k_blend layout)
+            b = make_float4((float)(x0 + 2 * wwx + 8), (float)(y0 + 2 * wwy + 4), 7.0f, 3.0f);
         else
-            b = make_float4((float)(ox + wwx) + 0.5f, (float)(ox + wwx + 7) + 0.5f, (float)(oy + wwy) + 0.5f,
-                            (float)(oy + wwy + 3) + 0.5f);
+            b = make_float4((float)(ox + wwx + 4), (float)(oy + wwy + 2), 3.5f, 1.5f);
         S.wblock[tid] = b;
     }
     if (kCounters && tid < 4) S.cnt[tid] = 0ull;
@@ -319,13 +317,7 @@ __global__ void __launch_bounds__(kHT, VRS_HIER_MINB) k_blend_hier(FrameParams f
             S.r[3][tid] = __ldg(rp + 3);
             S.r[4][tid] = __ldg(rp + 4);
             S.r[5][tid] = make_float4(a5.x, a5.y, __uint_as_float(g), 0.0f);
-            uint32_t m = 0;
-#pragma unroll
-            for (int w = 0; w < kHW; w++) {
-                const float4 b = S.wblock[w];
-                const bool hit = !(a7.y < b.x || a7.x > b.y || a7.w < b.z || a7.z > b.w);
-                m |= hit ? (1u << w) : 0u;
-            }
+            const uint32_t m = footprint_mask<kHW>(a7, S.wblock);
             S.mask[tid] = fp.no_cull ? 0xffu : m;
         }
         if (__syncthreads_count(!done) == 0) break;

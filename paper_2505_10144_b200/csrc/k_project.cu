@@ -26,7 +26,44 @@ struct Proj {
     int rect[4];
     float bbox[4];
     float m2[2], Cp[3];  // EWA baseline: pixel mean and conic
+    uint32_t foot[4];    // record slot 7: packed conservative footprint (vrs_internal.cuh Footprint)
 };
+
+// Record slot 7 (vrs_internal.cuh footprint_of): the bounding box rounded
+// outward to int16, and -- for an ellipse, ax = {minor-axis unit vector (2),
+// centre z0 (2), r^2, Q00, Q01, Q11, det} of the pixel-space conic
+// (z - z0)^T M (z - z0) <= r^2, M = [[Q00, Q01], [Q01, Q11]] -- a separating
+// axis: n rounded to binary16, the centre's offset d from the box centre
+// along n and the half-width r sqrt(n^T M^-1 n) + |d rounding| + 1 px,
+// rounded up; else (have_ax false) n = 0 and an infinite half-width: box only.
+__device__ __forceinline__ void pack_footprint(Proj& p, const bool have_ax, const double ax0 = 0.0, const double ax1 = 0.0,
+                                               const double ax2 = 0.0, const double ax3 = 0.0, const double ax4 = 0.0,
+                                               const double ax5 = 0.0, const double ax6 = 0.0, const double ax7 = 0.0,
+                                               const double ax8 = 0.0) {
+    const double ax[9] = {ax0, ax1, ax2, ax3, ax4, ax5, ax6, ax7, ax8};
+    auto i16 = [](double v) { return (uint32_t)(uint16_t)(int16_t)fmin(fmax(v, -32768.0), 32767.0); };
+    const double bx0 = floor((double)p.bbox[0]), bx1 = ceil((double)p.bbox[1]);
+    const double by0 = floor((double)p.bbox[2]), by1 = ceil((double)p.bbox[3]);
+    p.foot[0] = i16(bx0) | (i16(bx1) << 16);
+    p.foot[1] = i16(by0) | (i16(by1) << 16);
+    __half2 n = __floats2half2_rn(0.0f, 0.0f);
+    __half2 dh = __halves2half2(__float2half_rn(0.0f), __ushort_as_half((unsigned short)0x7c00u));  // (0, +inf)
+    if (have_ax && bx0 > -32768.0 && bx1 < 32767.0 && by0 > -32768.0 && by1 < 32767.0) {
+        const __half hx = __double2half(ax[0]), hy = __double2half(ax[1]);
+        const double nx = (double)__half2float(hx), ny = (double)__half2float(hy);
+        const double q = nx * nx * ax[7] - 2.0 * nx * ny * ax[6] + ny * ny * ax[5];  // det * n^T M^-1 n
+        const double ext = sqrt(ax[4] * q / ax[8]);
+        const double d = nx * (ax[2] - 0.5 * (bx0 + bx1)) + ny * (ax[3] - 0.5 * (by0 + by1));
+        const __half d16 = __double2half(d);
+        const double hw = ext + fabs(d - (double)__half2float(d16)) + 1.0;
+        if (isfinite(hw) && q >= 0.0) {
+            n = __halves2half2(hx, hy);
+            dh = __halves2half2(d16, __float2half_ru(__double2float_ru(hw)));
+        }
+    }
+    p.foot[2] = *reinterpret_cast<const uint32_t*>(&n);
+    p.foot[3] = *reinterpret_cast<const uint32_t*>(&dh);
+}
 
 __device__ __forceinline__ void set_rect(const ViewParams& v, int T, double xmin, double xmax, double ymin,
                                          double ymax, Proj& p) {
@@ -101,6 +138,7 @@ __device__ void project_splat_ewa(const ViewParams& v, float4 m4, float4 c0, flo
     p.valid = 1;
     const double rx = sqrt((double)p.qcut * c00), ry = sqrt((double)p.qcut * c11);
     set_rect(v, T, p.m2[0] - rx - 1.0, p.m2[0] + rx + 1.0, p.m2[1] - ry - 1.0, p.m2[1] + ry + 1.0, p);
+    pack_footprint(p, false);
 }
 
 // O1-O6 (DESIGN "Numerics contract"): view transform and near cull,
@@ -197,9 +235,7 @@ __device__ void project_splat(const ViewParams& v, float4 m4, float4 c0, float4 
     p.valid = 1;
     // O6(b,c) conic bounding box on the image plane (double), whole-screen fallback
     const double W = v.W, H = v.H;
-    double xmin, xmax, ymin, ymax;
-    bool whole = !(ud2 > sinb + 1e-3);
-    if (!whole) {
+    if (ud2 > sinb + 1e-3) {
         const double e1d[3] = {p.e1[0], p.e1[1], p.e1[2]}, e2d[3] = {p.e2[0], p.e2[1], p.e2[2]};
         const double ud[3] = {ud0, ud1, ud2};
         double G[3][3];
@@ -241,14 +277,31 @@ __device__ void project_splat(const ViewParams& v, float4 m4, float4 c0, float4 
             const double sx = sqrt(dx), sy = sqrt(dy), ia = 1.0 / a22;
             const double xa = (a02 - sx) * ia, xb = (a02 + sx) * ia;
             const double ya = (a12 - sy) * ia, yb = (a12 + sy) * ia;
-            xmin = fmin(xa, xb); xmax = fmax(xa, xb);
-            ymin = fmin(ya, yb); ymax = fmax(ya, yb);
-        } else {
-            whole = true;
+            set_rect(v, T, fmin(xa, xb) - 1.0, fmax(xa, xb) + 1.0, fmin(ya, yb) - 1.0, fmax(ya, yb) + 1.0, p);
+            // separating axis for the blend's per-warp footprint skip: the minor axis
+            // of the ellipse (M positive definite), r^2 = -det Q / det M
+            const double detQ = Q[0][0] * a00 + Q[0][1] * (Q[0][2] * Q[1][2] - Q[0][1] * Q[2][2]) + Q[0][2] * a02;
+            const double r2 = -detQ * ia;
+            if (a22 > 0.0 && Q[0][0] > 0.0 && r2 >= 0.0 && isfinite(r2)) {
+                const double hm = 0.5 * (Q[0][0] + Q[1][1]), dm = 0.5 * (Q[0][0] - Q[1][1]);
+                const double lmax = hm + sqrt(dm * dm + Q[0][1] * Q[0][1]);
+                // eigenvector of lmax: the longer of (Q01, lmax - Q00) and (lmax - Q11, Q01)
+                double nx = Q[0][1], ny = lmax - Q[0][0];
+                const double mx = lmax - Q[1][1], my = Q[0][1];
+                if (mx * mx + my * my > nx * nx + ny * ny) { nx = mx; ny = my; }
+                const double nn = sqrt(nx * nx + ny * ny);
+                if (nn > 0.0) {
+                    pack_footprint(p, true, nx / nn, ny / nn, a02 * ia, a12 * ia, r2, Q[0][0], Q[0][1], Q[1][1], a22);
+                    return;
+                }
+            }
+            pack_footprint(p, false);
+            return;
         }
     }
-    if (whole) { xmin = -1.0; xmax = W + 1.0; ymin = -1.0; ymax = H + 1.0; }
-    set_rect(v, T, xmin - 1.0, xmax + 1.0, ymin - 1.0, ymax + 1.0, p);
+    // whole-screen fallback
+    set_rect(v, T, -2.0, W + 2.0, -2.0, H + 2.0, p);
+    pack_footprint(p, false);
 }
 
 // Splat fields needed by the tile test and the key.
@@ -631,7 +684,8 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
                                                      : sqrtf(dot3(p.muc[0], p.muc[1], p.muc[2], p.muc[0], p.muc[1],
                                                                   p.muc[2]));
                 r6[3] = __uint_as_float(r23);
-                rec[7] = make_float4(p.bbox[0], p.bbox[1], p.bbox[2], p.bbox[3]);
+                rec[7] = make_float4(__uint_as_float(p.foot[0]), __uint_as_float(p.foot[1]),
+                                     __uint_as_float(p.foot[2]), __uint_as_float(p.foot[3]));
             }
         }
         // warp inclusive scan of the counts; visible splats (cnt > 0) listed alongside

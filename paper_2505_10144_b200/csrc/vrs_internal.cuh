@@ -248,6 +248,50 @@ __device__ __forceinline__ float quad3(float a, float b, float c, float p, float
     return fmaf(fmaf(a, x, fmaf(b, y, p * z)), x, fmaf(fmaf(c, y, e * z), y, (f * z) * z));
 }
 // z = 1 specialisation (bit-identical: p*1, e*1, f*1*1 are exact)
+// Conservative pixel footprint of a projected splat (record slot 7, written by
+// k_preprocess): x = its bounding box's columns as int16 (min | max << 16,
+// rounded outward), y = rows likewise, z = a separating axis n across the
+// ellipse (binary16 pair: its minor axis), w = binary16 pair (d, hw): the
+// offset of the ellipse centre from the box centre along n and the ellipse's
+// half-width along n, rounded up, with a 1 px margin (the margin of the box).
+// A block of samples whose box or whose extent along n misses it holds no
+// member sample (the hierarchical culling of P:431: never changes results).
+struct Footprint {
+    float bcx, bcy, ex, ey, nx, ny, k, e;
+};
+// hx, hy: half-extent of the sample blocks it will be tested against
+__device__ __forceinline__ Footprint footprint_of(const float4 a7, const float hx, const float hy) {
+    const uint32_t bx = __float_as_uint(a7.x), by = __float_as_uint(a7.y);
+    const float x0 = (float)(int)(short)(bx & 0xffffu), x1 = (float)(int)(short)(bx >> 16);
+    const float y0 = (float)(int)(short)(by & 0xffffu), y1 = (float)(int)(short)(by >> 16);
+    const __half2 n = *reinterpret_cast<const __half2*>(&a7.z), dh = *reinterpret_cast<const __half2*>(&a7.w);
+    Footprint f;
+    f.bcx = 0.5f * (x0 + x1);
+    f.bcy = 0.5f * (y0 + y1);
+    f.ex = fmaf(0.5f, x1 - x0, hx);
+    f.ey = fmaf(0.5f, y1 - y0, hy);
+    f.nx = __low2float(n);
+    f.ny = __high2float(n);
+    f.k = fmaf(f.nx, f.bcx, fmaf(f.ny, f.bcy, __low2float(dh)));
+    f.e = __high2float(dh) + fmaf(hx, fabsf(f.nx), hy * fabsf(f.ny));
+    return f;
+}
+// wb = (centre x, centre y, half-extent x, half-extent y) of a sample block
+__device__ __forceinline__ bool footprint_hits(const Footprint& f, const float4 wb) {
+    return fabsf(f.bcx - wb.x) <= f.ex && fabsf(f.bcy - wb.y) <= f.ey &&
+           fabsf(fmaf(f.nx, wb.x, fmaf(f.ny, wb.y, -f.k))) <= f.e;
+}
+// bit w set iff the footprint meets sample block wblock[w] (all of one size)
+template <int kBlocks>
+__device__ __forceinline__ uint32_t footprint_mask(const float4 a7, const float4* wblock) {
+    const float4 w0 = wblock[0];
+    const Footprint f = footprint_of(a7, w0.z, w0.w);
+    uint32_t m = 0;
+#pragma unroll
+    for (int w = 0; w < kBlocks; w++) m |= footprint_hits(f, wblock[w]) ? (1u << w) : 0u;
+    return m;
+}
+
 __device__ __forceinline__ float quad3z1(float a, float b, float c, float p, float e, float f, float x, float y) {
     return fmaf(fmaf(a, x, fmaf(b, y, p)), x, fmaf(fmaf(c, y, e), y, f));
 }
