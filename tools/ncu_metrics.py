@@ -12,7 +12,8 @@ KEEP = re.compile(r"^(gpu__time_duration\.sum|dram__bytes_(read|write)\.sum|smsp
                   r"launch__occupancy_limit_.*|smsp__thread_inst_executed_per_inst_executed\.ratio|"
                   r"lts__t_sector_hit_rate\.pct|l1tex__data_bank_conflicts_pipe_lsu_mem_shared\.sum|"
                   r"smsp__pcsamp_warps_issue_stalled_[a-z_]+$|launch__grid_size|launch__block_size|"
-                  r"dram__throughput\.avg\.pct_of_peak_sustained_elapsed)$")
+                  r"dram__throughput\.avg\.pct_of_peak_sustained_elapsed|l1tex__throughput\.avg\.pct_of_peak_sustained_active|"
+                  r"l1tex__data_pipe_lsu_wavefronts_mem_shared\.sum|sm__inst_executed_pipe_lsu\.avg\.pct_of_peak_sustained_active)$")
 
 rep = sys.argv[1]
 kre = re.compile(sys.argv[2]) if len(sys.argv) > 2 else None
