@@ -30,6 +30,13 @@ namespace vrs {
 namespace {
 
 constexpr int kGB = 80;  // staged records per batch (as k_blend)
+// at most 2^VRS_BWD_STEPS lanes of a group are summed by shuffles before one of them adds
+// (C9 backward: 15.9 ms with pairs (1), 16.4 with quads (2), 18.3 with octets (3), 20.7 with
+// whole groups (5), 22.4 with every lane adding its own record: the shuffles, not the L2
+// atomics, are the limit)
+#ifndef VRS_BWD_STEPS
+#define VRS_BWD_STEPS 1
+#endif
 
 // gradient record layout per (view, Gaussian)
 enum : int { kGRgb = 0, kGSigma = 3, kGU = 4, kGE1x = 7, kGE1z = 8, kGE2 = 9, kGC = 12, kGA = 15, kGB3 = 21 };
@@ -168,24 +175,27 @@ __global__ void __launch_bounds__(256) k_blend_bwd(FrameParams fp, FrameBufs fb,
             }
             float* gr = gview + (size_t)g * 24;
 #ifndef VRS_BWD_NO_AGG
-            // lanes blending the same Gaussian at this instant sum their records first
-            // (tree over the group's ranks by shuffles); one lane per group adds it
+            // lanes blending the same Gaussian at this instant sum their records first:
+            // suffix sums along the group's lanes by pointer jumping (each lane links to
+            // the next lane of its group; every step doubles the links): after s steps
+            // the lane of group rank r holds ranks r .. r + 2^s - 1, and the lanes of rank
+            // 0 mod 2^s add them
             const unsigned act = __activemask();
             const unsigned peers = __match_any_sync(act, g);
-            const int n = __popc(peers);
-            const int nmax = (int)__reduce_max_sync(act, (unsigned)n);
-            const int rk = __popc(peers & ((1u << lane) - 1u));
+            const int nmax = min((int)__reduce_max_sync(act, (unsigned)__popc(peers)), 1 << VRS_BWD_STEPS);
+            const unsigned above = peers & ~((2u << lane) - 1u);  // (lane 31: 2u << 31 = 0 -> none)
+            int nxt = above ? __ffs(above) - 1 : -1;
             for (int st = 1; st < nmax; st <<= 1) {
-                const int sr = rk + st;
-                const int src = (sr < n) ? (int)__fns(peers, 0, sr + 1) : lane;
-                const bool take = ((rk & (2 * st - 1)) == 0) && sr < n;
+                const int src = nxt >= 0 ? nxt : lane;
 #pragma unroll
                 for (int k = 0; k < 24; k++) {
                     const float o = __shfl_sync(act, gv[k], src);
-                    gv[k] += take ? o : 0.0f;
+                    gv[k] += nxt >= 0 ? o : 0.0f;
                 }
+                const int nn = __shfl_sync(act, nxt, src);
+                nxt = nxt >= 0 ? nn : -1;
             }
-            if (rk == 0)
+            if ((__popc(peers & ((1u << lane) - 1u)) & ((1 << VRS_BWD_STEPS) - 1)) == 0)
 #endif
 #pragma unroll
             for (int k = 0; k < 24; k += 4)
