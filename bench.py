@@ -533,6 +533,18 @@ def main():
         render(cams, fov, rgba, depth, stream=stream)
     counters = r.stats()
     r.vrs_set_instrumentation(counters=0, timing=0)  # the timed frames run the bare product path
+    # per-tile list-length histogram of that frame (SURVEY §8d reporting)
+    try:
+        rng = r.vrs_debug_ranges()
+        lens = (rng[:, 1].astype(np.int64) - rng[:, 0].astype(np.int64))
+        lens = lens[lens > 0]
+        edges = [1, 65, 129, 257, 513, 1025, 2049, 4097]
+        tile_hist = {f"{lo}-{hi - 1}" if hi else f">={lo}": int(((lens >= lo) & ((lens < hi) if hi else True)).sum())
+                     for lo, hi in zip(edges, edges[1:] + [0])}
+        tile_hist["max"] = int(lens.max()) if lens.size else 0
+        tile_hist["mean"] = float(lens.mean()) if lens.size else 0.0
+    except Exception as ex:  # (vrs_debug_ranges covers up to 1 M tiles)
+        tile_hist = {"unavailable": str(ex)[:80]}
 
     for w in range(args.warmup):
         with torch.cuda.stream(stream):
@@ -698,6 +710,7 @@ def main():
                                                            "overflow_samples", "terminated_samples", "work_items",
                                                            "visible_splats")},
             "tiles_by_class": dict(zip(["high", "low", "hybrid", "invisible"], counters["tiles_by_class"])),
+            "tile_list_hist": tile_hist,
             "roofline": {"kernel": "k_blend", "bound": "alu", "achieved": achieved / 1e12, "peak": peak_ops / 1e12,
                          "unit": "T lane-instr/s", "frac": achieved / peak_ops, "traffic": traffic,
                          "peak_source": f"148 SM x 4 schedulers x 32 lanes x sm_max_mhz ({src} MEASURED_PEAKS)",

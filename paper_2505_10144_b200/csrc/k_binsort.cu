@@ -281,6 +281,7 @@ __global__ void __launch_bounds__(kScanT) k_tile_scan(uint32_t* __restrict__ cnt
             }
             if (lane < kScanT / 32) s_w[c][lane] = w;  // inclusive over warps
         }
+        __syncwarp();  // (lanes 0-3 read lane 7's totals)
         // look-back: lane c < 4 carries quantity c
         if (lane < 4) {
             const uint32_t agg = s_w[lane][kScanT / 32 - 1];

@@ -1,7 +1,8 @@
 """Small renders through every kernel family for compute-sanitizer runs:
 flat foveated stereo (T=32, masks; thread and TMA staging; the in-launch
 compose), non-foveated T=16 + backward, hierarchical mode, EWA, two-pass,
-packed output, the global-sort baselines."""
+packed output, the global-sort baselines, and a 640x480 stereo frame
+(2400 tiles: the multi-chunk look-back of k_tile_scan)."""
 import os
 import sys
 
@@ -48,4 +49,13 @@ nofov = [sg.look_camera((x, 0, 0), 0.2, 0.1, 0.0, f=f, width=W, height=H) for x 
 rgba, depth = r.render(nofov)
 out = r.vrs_backward(rgba, depth, torch.ones_like(rgba), torch.ones_like(depth))
 torch.cuda.synchronize()
+r.close()
+# > 1024 tiles: k_tile_scan's multi-chunk look-back; > 256-pair tiles: the block sort path
+W2, H2 = 640, 480
+r = Renderer(max_gaussians=scene.n, max_views=2, max_pairs=1 << 21, max_width=W2, max_height=H2, assign_tile=16)
+r.upload(scene)
+f2 = sg.focal_for_hfov(W2, 110.0)
+r.render([sg.look_camera((x, 0, 0), 0.2, 0.1, 0.0, f=f2, width=W2, height=H2) for x in (-0.0315, 0.0315)])
+torch.cuda.synchronize()
+r.close()
 print("sanitize run done", float(out["means"].abs().max()))
