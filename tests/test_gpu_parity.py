@@ -205,6 +205,58 @@ def test_warp_culling_never_changes_results(vrs, oracle_mod):
     assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
 
 
+def _needle_scene(seed, n):
+    """Thin needles (one long axis, two ~100x shorter) and sheets at random
+    orientations, some close to the camera: the ellipses whose bounding boxes
+    are loose, where the footprint's separating axis culls most."""
+    base = sg.random_scene(seed, n=n, sh_degree=1, z_range=(0.6, 6.0), xy_frac=1.4)
+    rs = np.random.default_rng(seed)
+    ls = np.log(rs.uniform(0.001, 0.006, (n, 3)))
+    ls[:, 0] = np.log(rs.uniform(0.05, 0.6, n))
+    sheet = rs.random(n) < 0.3
+    ls[sheet, 1] = np.log(rs.uniform(0.05, 0.4, int(sheet.sum())))
+    return sg.RawScene(base.means, base.quats, ls.astype(np.float32), base.logits, base.sh, base.sh_degree)
+
+
+@pytest.mark.parametrize("case", ["foveated_t32", "full_t16_wide", "tma", "hier"])
+def test_footprint_axis_never_changes_results(vrs, oracle_mod, case):
+    """P12 for the footprint's separating axis (record slot 7): needle and
+    sheet splats at random orientations, 110-150 deg stereo; every warp-skip
+    variant (thread / TMA staging, flat / hierarchical resort) renders the same
+    bytes and the same counters with and without the skip, and the oracle's
+    counters."""
+    scene = _needle_scene(11, 6000)
+    W, H = 320, 256
+    hfov = 150.0 if case == "full_t16_wide" else 110.0
+    T = 16 if case == "full_t16_wide" else 32
+    cams = sg.stereo_pair(width=W, height=H, hfov_deg=hfov, masks=False)
+    fov = None if case == "full_t16_wide" else [sg.Fovea((W / 2, H / 2), (W / 4, H / 4), 0.1)] * 2
+    outs = []
+    for nc in (False, True):
+        r = vrs.Renderer(max_gaussians=scene.n, max_views=2, max_pairs=1 << 22, max_width=W, max_height=H,
+                         assign_tile=T)
+        r.upload(scene)
+        r.vrs_set_instrumentation(counters=1, no_cull=nc)
+        if case == "tma":
+            r.vrs_set_staging_mode(1)
+        if case == "hier":
+            r.vrs_set_resort_mode(1)
+        rgba, depth = r.render(cams, fov)
+        torch.cuda.synchronize()
+        outs.append((rgba.cpu().numpy(), depth.cpu().numpy(), r.stats()))
+        r.close()
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    for k in ("contributions", "overflow_samples", "terminated_samples"):
+        assert outs[0][2][k] == outs[1][2][k], k
+    if case in ("foveated_t32", "full_t16_wide"):
+        o = oracle_mod.Oracle(scene)
+        o.prepare(cams, fov, assign_tile=T)
+        o.render()
+        ost = o.stats()
+        for k in ("pairs", "contributions", "overflow_samples", "terminated_samples"):
+            assert outs[0][2][k] == ost[k], (k, outs[0][2][k], ost[k])
+
+
 @pytest.mark.parametrize("cap", [64, 128])
 def test_binned_sort_merge_path_parity(vrs, oracle_mod, cap):
     """Binned sort: tiles larger than the shared-memory capacity are sorted in
