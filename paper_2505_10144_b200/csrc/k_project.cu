@@ -36,6 +36,9 @@ struct Proj {
 // axis: n rounded to binary16, the centre's offset d from the box centre
 // along n and the half-width r sqrt(n^T M^-1 n) + |d rounding| + 1 px,
 // rounded up; else (have_ax false) n = 0 and an infinite half-width: box only.
+#ifndef VRS_FOOT_MARGIN
+#define VRS_FOOT_MARGIN 1.0
+#endif
 __device__ __forceinline__ void pack_footprint(Proj& p, const bool have_ax, const double ax0 = 0.0, const double ax1 = 0.0,
                                                const double ax2 = 0.0, const double ax3 = 0.0, const double ax4 = 0.0,
                                                const double ax5 = 0.0, const double ax6 = 0.0, const double ax7 = 0.0,
@@ -55,7 +58,7 @@ __device__ __forceinline__ void pack_footprint(Proj& p, const bool have_ax, cons
         const double ext = sqrt(ax[4] * q / ax[8]);
         const double d = nx * (ax[2] - 0.5 * (bx0 + bx1)) + ny * (ax[3] - 0.5 * (by0 + by1));
         const __half d16 = __double2half(d);
-        const double hw = ext + fabs(d - (double)__half2float(d16)) + 1.0;
+        const double hw = ext + fabs(d - (double)__half2float(d16)) + VRS_FOOT_MARGIN;
         if (isfinite(hw) && q >= 0.0) {
             n = __halves2half2(hx, hy);
             dh = __halves2half2(d16, __float2half_ru(__double2float_ru(hw)));
