@@ -163,6 +163,33 @@ def test_empty_and_fully_culled_scenes(vrs, oracle_mod):
     assert_images_close(g, oi)
 
 
+def test_max_gaussian_index_parity(vrs, oracle_mod):
+    """The largest scene the context accepts (max_gaussians = 2^24 - 1: the
+    blend stages a Gaussian index in 24 bits beside its 8-warp mask): all but
+    1500 Gaussians sit behind the camera, the visible ones carry the highest
+    indices (and one has index 0); pairs bit-exact, images within tolerance."""
+    n = (1 << 24) - 1
+    vis = sg.random_scene(7, n=1500, sh_degree=0)
+    means = np.zeros((n, 3), np.float32)
+    means[:, 2] = -5.0
+    quats = np.zeros((n, 4), np.float32)
+    quats[:, 0] = 1.0
+    log_scales = np.full((n, 3), np.log(0.05), np.float32)
+    logits = np.zeros(n, np.float32)
+    sh = np.zeros((n, 1, 3), np.float32)
+    idx = np.concatenate([[0], np.arange(n - 1499, n)])
+    means[idx], quats[idx], log_scales[idx] = vis.means, vis.quats, vis.log_scales
+    logits[idx], sh[idx] = vis.logits, vis.sh
+    scene = sg.RawScene(means, quats, log_scales, logits, sh, 0)
+    cam = identity_camera(128, 96, 64.0)
+    r, o, g, oi = render_both(vrs, oracle_mod, scene, [cam])
+    assert r.stats()["visible_splats"] > 1000
+    assert_lists_equal(r, o)
+    assert_images_close(g, oi)
+    k, v = r.vrs_debug_pairs(True)
+    assert v.max() >= n - 1499 and v.min() == 0
+
+
 @pytest.mark.parametrize("seed", list(range(100, 110)))
 def test_tiny_scenes_parity(vrs, oracle_mod, seed):
     sc, cam = tiny_set(seed)
