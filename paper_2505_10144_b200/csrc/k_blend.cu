@@ -167,9 +167,6 @@ constexpr int kWarps = kBT / 32;
 #ifndef VRS_BLEND_BATCH
 #define VRS_BLEND_BATCH 80
 #endif
-#ifndef VRS_SELMASK
-#define VRS_SELMASK 1
-#endif
 constexpr int kBatch = VRS_BLEND_BATCH;  // list entries staged per shared-memory batch
 constexpr uint32_t kStageBytes = 96;     // r0..r5 of a splat record
 static_assert(kBatch <= kBT && kBatch >= 10, "one staging thread per entry; the compose triggers reuse mask[]");
@@ -378,7 +375,6 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         }
         const unsigned long long kh = WK(hk);
         const float ah = WA(hk);
-#if VRS_SELMASK
         // one 64-bit compare, then bitwise selects (the compiler otherwise re-derives the
         // comparison for every use)
         uint32_t dm;  // all ones iff the new entry is the minimum
@@ -396,12 +392,6 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         blend_one(((unsigned long long)khi << 32) | klo, asel);
         if (kCounters && done) stop_pos = pos;
         if ((dm | (uint32_t)done) != 0u) return;
-#else
-        const bool direct = key < kh;  // the new entry is the minimum
-        blend_one(direct ? key : kh, direct ? alpha : ah);
-        if (kCounters && done) stop_pos = pos;
-        if (direct || done) return;
-#endif
         hk = (hk + kSlotBytes) & kRingMask;
         // insertion from the tail (entries arrive nearly sorted); dst
         // is the hole, starting at the popped head's slot

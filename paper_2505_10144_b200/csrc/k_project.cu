@@ -613,9 +613,6 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
 #ifndef VRS_TT_GRID
 #define VRS_TT_GRID 8
 #endif
-#ifndef VRS_TT_HOIST
-#define VRS_TT_HOIST 0
-#endif
 #ifndef VRS_TT_MINB
 #define VRS_TT_MINB 4
 #endif
@@ -754,9 +751,6 @@ __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const Fram
     const float4 r0 = __ldg(rec + 0), r1 = __ldg(rec + 1), r2 = __ldg(rec + 2), r5 = __ldg(rec + 5);
     // rect23 only: k_color writes the colour into rec[6].xyz concurrently (side stream)
     const float r6w = __ldg(reinterpret_cast<const float*>(rec + 6) + 3);
-#if VRS_TT_HOIST
-    const float4 r3 = __ldg(rec + 3), r4 = __ldg(rec + 4);  // issued with the others: one latency level less
-#endif
     const uint32_t r01 = __float_as_uint(r5.w), r23 = __float_as_uint(r6w);
     const int tx0 = r01 & 0xffff, ty0 = r01 >> 16, tx1 = r23 & 0xffff;
     const int rw = tx1 - tx0 + 1;
@@ -776,9 +770,7 @@ __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const Fram
         if (!tile_test(s, __ldg(v.xr + tx), __ldg(v.xr + tx + 1), __ldg(v.yr + ty), __ldg(v.yr + ty + 1), hx, hy, hz))
             return false;
     }
-#if !VRS_TT_HOIST
-    const float4 r3 = __ldg(rec + 3), r4 = __ldg(rec + 4);
-#endif
+    const float4 r3 = __ldg(rec + 3), r4 = __ldg(rec + 4);  // only for kept pairs
     s.A[0] = r3.x; s.A[1] = r3.y; s.A[2] = r3.z; s.A[3] = r3.w;
     s.A[4] = r4.x; s.A[5] = r4.y; s.bx = r4.z; s.by = r4.w; s.bz = r5.x;
     // StopThePop per-tile depth at x_hat (O8), or the global-sort baselines' per-Gaussian depth (N3)
