@@ -8,22 +8,25 @@
 // centre, or invisible tiles (background fill).  Every
 // item streams its coarse tile's sorted list in key order.
 //
-// Staging: the list is cut into stages of kStageN entries; each entry's
-// 128-B splat record is copied global -> shared by the TMA bulk-copy engine
-// (cp.async.bulk, one per record, completing on the stage's mbarrier), two
-// stages in flight.  The warps of a block consume the stages independently
-// (no block barrier in the loop): a warp waits on the stage's mbarrier,
-// culls the stage's entries against its own 8x4 sample block with their
-// conservative pixel footprints (bounding box + minor-axis extent) (the hierarchical culling of P:431 -- never
-// changes results, only work), evaluates two entries' memberships per
-// iteration and runs their contributions in stream order; the last warp to
-// finish a stage re-arms the slot with the stage two ahead.
+// Staging (default): the list is cut into batches of 32 entries held in a
+// two-stage ring in shared memory (the first 96 B of each entry's 128-B splat
+// record, its id g, and a mask of the warps whose 8x4 sample block the
+// entry's conservative pixel footprint -- bounding box + separating axis --
+// meets: the hierarchical culling of P:431, which never changes results,
+// only work).  The block stages batches 0 and 1; afterwards the warps consume
+// the stages independently, with no block barrier: the last warp to finish a
+// batch refills its stage with the batch two ahead (one entry per lane) and
+// arrives on the stage's mbarrier, a warp that needs a batch not staged yet
+// waits on that mbarrier.  A warp evaluates two relevant entries' memberships
+// per iteration and runs their contributions in stream order.  Alternative
+// staging (vrs_set_staging_mode): block-synchronous batches whose records are
+// copied by the TMA bulk-copy engine (cp.async.bulk, mbarrier completion).
 //
 // Each sample runs the StopThePop per-pixel resort: a
 // K = 16 window ordered by (tau, g) -- a per-thread ring in shared memory
-// ([slot][thread], bank-conflict free) whose head (the minimum) is mirrored
-// in registers together with its colour (fetched when the entry becomes the
-// head, off the critical path) -- popping the nearest entry on overflow and
+// ([slot][thread], bank-conflict free), started full of no-op sentinels so
+// every contribution is "compare with the head, blend the smaller, insert
+// the other from the tail" -- popping the nearest entry on overflow and
 // blending front to back (Eq.2 with product transmittance), terminating once
 // T < 1e-4 (checked after blending).  Hybrid pixels blend their value with
 // the 2x2 group average via warp shuffles.
@@ -164,8 +167,11 @@ namespace {
 
 constexpr int kBT = 256;                 // threads per block: one 16x16 item / one 32x32 LowRes item
 constexpr int kWarps = kBT / 32;
+#ifndef VRS_BLEND_ASYNC
+#define VRS_BLEND_ASYNC 1
+#endif
 #ifndef VRS_BLEND_BATCH
-#define VRS_BLEND_BATCH 80
+#define VRS_BLEND_BATCH (VRS_BLEND_ASYNC ? 64 : 80)
 #endif
 constexpr int kBatch = VRS_BLEND_BATCH;  // list entries staged per shared-memory batch
 constexpr uint32_t kStageBytes = 96;     // r0..r5 of a splat record
@@ -186,11 +192,23 @@ struct BlendSmem {
     unsigned long long w_key[kWindow][kBT];
     float w_a[kWindow][kBT];
     unsigned long long cnt[4];
+    // warp-asynchronous staging (VRS_BLEND_ASYNC): two stages of kSE entries in
+    // rec[] / mask[] rows s * kSE ..; fullb[s] completes when a refill of stage s
+    // landed, consumed[s] counts the warps done with its current batch, alive the
+    // warps with a sample still blending
+#if VRS_BLEND_ASYNC
+    unsigned long long fullb[2];
+    uint32_t consumed[2];
+    uint32_t alive;
+#endif
 };
 // 4 blocks of 256 threads per SM (the 64-register budget) need <= 57344 B each
 // (228 KB per SM, 1 KB reserved per block); after the blend loop the staging
 // mask holds the in-launch compose triggers
 static_assert(sizeof(BlendSmem) + 1024 <= 233472 / 4, "blend shared memory exceeds the 4-blocks/SM budget");
+
+constexpr int kSE = 32;  // entries per stage of the asynchronous staging ring (one per lane)
+static_assert(2 * kSE <= kBatch, "two async stages live in the batch buffer");
 
 constexpr uint32_t kSlotBytes = kBT * 8;                   // one ring slot of keys
 constexpr uint32_t kRingMask = (kWindow - 1) * kSlotBytes;    // byte-offset ring mask
@@ -238,6 +256,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(unsigned long long* bar, u
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
                  : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 __device__ __forceinline__ bool mbar_try_wait(unsigned long long* bar, uint32_t parity) {
     uint32_t ok;
     asm volatile(
@@ -274,7 +295,13 @@ __device__ __forceinline__ int block_id_opaque() {
 #define REC3(j) S.rec[j][3]
 #define REC4(j) S.rec[j][4]
 #define REC5(j) S.rec[j][5]
-#define GID(j) (S.mask[j] >> 8)
+// Thread staging overwrites the staged r5.w (the record's rect01, unused by the
+// blend) with g, so a contribution takes g from the r5 load it makes anyway;
+// TMA staging copies the record verbatim and keeps g in the mask word.
+#ifndef VRS_GID_IN_REC
+#define VRS_GID_IN_REC 1
+#endif
+#define GID(j) ((VRS_GID_IN_REC && !kTma) ? __float_as_uint(S.rec[j][5].w) : (S.mask[j] >> 8))
 #define MASKJ(j) S.mask[j]
 
 template <bool kCounters, bool kEwa, bool kTma, bool kGlobal>
@@ -446,6 +473,142 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         contribute(order_key(tau, g, fp.near_plane), alpha, pos);
     };
 
+    // one 32-entry chunk of staged rows r0 .. r0 + cnt - 1 (list positions pos0 ..):
+    // the warp's relevant entries (footprint mask) in stream order
+    auto chunk = [&](const int r0, const int cnt, const uint32_t pos0) {
+#define POS_OF(j) (pos0 + (uint32_t)((j) - r0))
+        const bool rel = (lane < cnt) && ((MASKJ(r0 + lane) >> warp) & 1u);
+        unsigned bits = __ballot_sync(0xffffffffu, rel);
+        if (!kEwa) {
+            // two list entries per iteration: both memberships first (independent
+            // chains), then the contributions in stream order
+            auto member = [&](const int j, float& num, float& ss) {
+                const float4 a0 = REC0(j), a1 = REC1(j), a2 = REC2(j);
+                const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
+                const float ex = fmaf(a1.x, x, a1.y);
+                const float ey = fmaf(a1.z, x, fmaf(a1.w, y, a2.x));
+                const float cx = fmaf(a2.y, ex, a2.z * ey), cy = fmaf(a2.z, ex, a2.w * ey);
+                num = fmaf(ex, cx, ey * cy);
+                ss = s * s;
+                return (s > 0.0f) && (num <= a0.w * ss);
+            };
+            auto contrib = [&](const int j, const float num, const float ss) {
+                const float4 a3 = REC3(j), a4 = REC4(j), t = REC5(j);
+                const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
+                const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, t.x));
+                float tau;
+                const float alpha = alpha_tau(num, ss, den, dtb, t.y, tau);
+                const uint32_t gj = (VRS_GID_IN_REC && !kTma) ? __float_as_uint(t.w) : GID(j);
+                contribute(order_key(tau, gj, fp.near_plane), alpha, POS_OF(j));
+            };
+            while (bits) {
+                const int j = r0 + __ffs(bits) - 1;
+                bits &= bits - 1;
+                float n1, s1;
+                const bool m1 = member(j, n1, s1) && !done;
+                if (bits) {
+                    const int j2 = r0 + __ffs(bits) - 1;
+                    bits &= bits - 1;
+                    float n2, s2;
+                    const bool m2 = member(j2, n2, s2);
+                    if (m1) contrib(j, n1, s1);
+                    if (m2 && !done) contrib(j2, n2, s2);
+                } else if (m1) {
+                    contrib(j, n1, s1);
+                }
+            }
+            return;
+        }
+        while (bits) {
+            const int j = r0 + __ffs(bits) - 1;
+            bits &= bits - 1;
+            evaluate(POS_OF(j), GID(j), REC0(j), REC1(j), kEwa ? REC1(j) : REC2(j),
+                     [&](float4& a3, float4& a4, float2& a5) {
+                         a3 = REC3(j);
+                         a4 = REC4(j);
+                         const float4 t = REC5(j);
+                         a5 = make_float2(t.x, t.y);
+                     });
+        }
+#undef POS_OF
+    };
+    // thread staging of list position pos into row `row`: seven independent LDG.128,
+    // the footprint mask against every warp's sample block
+    auto fill_row = [&](const uint32_t pos, const int row) {
+        uint32_t g = __ldg(fb.vals + pos);
+        g = (g < (uint32_t)fp.N) ? g : 0u;  // memory safety after a capacity overflow only
+        const float4* rp = recv + (size_t)g * kRecF4;
+        const float4 a0 = __ldg(rp + 0), a1 = __ldg(rp + 1), a2 = __ldg(rp + 2), a3 = __ldg(rp + 3),
+                     a4 = __ldg(rp + 4), a5 = __ldg(rp + 5), a7 = __ldg(rp + 7);
+        S.rec[row][0] = a0; S.rec[row][1] = a1; S.rec[row][2] = a2;
+        S.rec[row][3] = a3; S.rec[row][4] = a4;
+        S.rec[row][5] = make_float4(a5.x, a5.y, a5.z, VRS_GID_IN_REC ? __uint_as_float(g) : a5.w);
+        const uint32_t m = footprint_mask<kWarps>(a7, S.wblock);
+        S.mask[row] = (g << 8) | (fp.no_cull ? 0xffu : m);
+    };
+
+#if VRS_BLEND_ASYNC
+    if constexpr (!kTma) {
+        // Warp-asynchronous staging ring: stage s = b & 1 holds batch b (kSE list
+        // entries).  The block fills batches 0 and 1; afterwards the last warp to
+        // finish a stage's batch refills it with the batch two ahead and arrives on
+        // its mbarrier, so a warp never waits for the others at a block barrier --
+        // only for a batch that is not staged yet.
+        const uint32_t nbat = (re - rb + kSE - 1) / kSE;
+        if (tid == 0) {
+            mbar_init(&S.fullb[0], 1);
+            mbar_init(&S.fullb[1], 1);
+            S.consumed[0] = 0;
+            S.consumed[1] = 0;
+            S.alive = kWarps;
+        }
+        __syncthreads();  // wblock written
+        if (tid < 2 * kSE && rb + (uint32_t)tid < re) fill_row(rb + (uint32_t)tid, tid);
+        __syncthreads();  // batches 0 and 1 staged, mbarriers initialised
+        bool wdone = false;
+        volatile uint32_t* const alive = &S.alive;
+        for (uint32_t b = 0; b < nbat; b++) {
+            const int st = (int)(b & 1u);
+            if (b >= 2) {
+                const uint32_t par = ((b >> 1) - 1u) & 1u;
+                bool quit = false;
+                while (!mbar_try_wait(&S.fullb[st], par)) {
+                    if (*alive == 0u) { quit = true; break; }
+                }
+                if (quit) break;
+            }
+            const uint32_t base = rb + b * (uint32_t)kSE;
+            if (!wdone) chunk(st * kSE, (int)min(re - base, (uint32_t)kSE), base);
+            // release the stage; the last warp out refills it with batch b + 2
+            if (!wdone && __all_sync(0xffffffffu, done)) {
+                wdone = true;
+                if (lane == 0) atomicSub(&S.alive, 1u);
+            }
+            __syncwarp();
+            uint32_t last = 0;
+            if (lane == 0) {
+                __threadfence_block();
+                last = (atomicAdd(&S.consumed[st], 1u) == (uint32_t)kWarps - 1u) ? 1u : 0u;
+            }
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {
+                const uint32_t bn = b + 2;
+                if (lane == 0) S.consumed[st] = 0;
+                if (bn < nbat && *alive != 0u) {
+                    const uint32_t pos = rb + bn * (uint32_t)kSE + (uint32_t)lane;
+                    if (pos < re) fill_row(pos, st * kSE + lane);
+                    __syncwarp();
+                    if (lane == 0) {
+                        __threadfence_block();
+                        mbar_arrive(&S.fullb[st]);
+                    }
+                }
+            }
+        }
+        __syncthreads();  // every warp is out of the ring (the compose reuses mask[])
+    } else
+#endif
+    {
     uint32_t phase = 0;
     if (kTma && tid == 0) {
         mbar_init(&S.full, kWarps);
@@ -485,78 +648,16 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
             phase ^= 1u;
         } else {
             // the block's first n threads load one record each (seven independent LDG.128)
-            if ((uint32_t)tid < n) {
-                uint32_t g = __ldg(fb.vals + base + tid);
-                g = (g < (uint32_t)fp.N) ? g : 0u;  // memory safety after a capacity overflow only
-                const float4* rp = recv + (size_t)g * kRecF4;
-                const float4 a0 = __ldg(rp + 0), a1 = __ldg(rp + 1), a2 = __ldg(rp + 2), a3 = __ldg(rp + 3),
-                             a4 = __ldg(rp + 4), a5 = __ldg(rp + 5), a7 = __ldg(rp + 7);
-                S.rec[tid][0] = a0; S.rec[tid][1] = a1; S.rec[tid][2] = a2;
-                S.rec[tid][3] = a3; S.rec[tid][4] = a4; S.rec[tid][5] = a5;
-                const uint32_t m = footprint_mask<kWarps>(a7, S.wblock);
-                S.mask[tid] = (g << 8) | (fp.no_cull ? 0xffu : m);
-            }
+            if ((uint32_t)tid < n) fill_row(base + (uint32_t)tid, tid);
         }
         if (__syncthreads_count(!done) == 0) break;
         const int nb = min((int)(re - base), kBatch);
-#define POS_OF(j) (base + (uint32_t)(j))
         for (int c = 0; c < nb; c += 32) {
             if (__all_sync(0xffffffffu, done)) break;
-            const bool rel = (c + lane < nb) && ((MASKJ(c + lane) >> warp) & 1u);
-            unsigned bits = __ballot_sync(0xffffffffu, rel);
-            if (!kEwa) {
-                // two list entries per iteration: both memberships first (independent
-                // chains), then the contributions in stream order
-                auto member = [&](const int j, float& num, float& ss) {
-                    const float4 a0 = REC0(j), a1 = REC1(j), a2 = REC2(j);
-                    const float s = fmaf(a0.x, x, fmaf(a0.y, y, a0.z));
-                    const float ex = fmaf(a1.x, x, a1.y);
-                    const float ey = fmaf(a1.z, x, fmaf(a1.w, y, a2.x));
-                    const float cx = fmaf(a2.y, ex, a2.z * ey), cy = fmaf(a2.z, ex, a2.w * ey);
-                    num = fmaf(ex, cx, ey * cy);
-                    ss = s * s;
-                    return (s > 0.0f) && (num <= a0.w * ss);
-                };
-                auto contrib = [&](const int j, const float num, const float ss) {
-                    const float4 a3 = REC3(j), a4 = REC4(j), t = REC5(j);
-                    const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
-                    const float dtb = fmaf(a4.z, x, fmaf(a4.w, y, t.x));
-                    float tau;
-                    const float alpha = alpha_tau(num, ss, den, dtb, t.y, tau);
-                    contribute(order_key(tau, GID(j), fp.near_plane), alpha, POS_OF(j));
-                };
-                while (bits) {
-                    const int j = c + __ffs(bits) - 1;
-                    bits &= bits - 1;
-                    float n1, s1;
-                    const bool m1 = member(j, n1, s1) && !done;
-                    if (bits) {
-                        const int j2 = c + __ffs(bits) - 1;
-                        bits &= bits - 1;
-                        float n2, s2;
-                        const bool m2 = member(j2, n2, s2);
-                        if (m1) contrib(j, n1, s1);
-                        if (m2 && !done) contrib(j2, n2, s2);
-                    } else if (m1) {
-                        contrib(j, n1, s1);
-                    }
-                }
-                continue;
-            }
-            while (bits) {
-                const int j = c + __ffs(bits) - 1;
-                bits &= bits - 1;
-                evaluate(POS_OF(j), GID(j), REC0(j), REC1(j), kEwa ? REC1(j) : REC2(j),
-                         [&](float4& a3, float4& a4, float2& a5) {
-                             a3 = REC3(j);
-                             a4 = REC4(j);
-                             const float4 t = REC5(j);
-                             a5 = make_float2(t.x, t.y);
-                         });
-            }
+            chunk(c, min(nb - c, 32), base + (uint32_t)c);
         }
     }
-#undef POS_OF
+    }
     // drain the window in order (sentinels pop as no-ops)
 #pragma unroll 1
     for (int k = 0; k < kWindow && !done && !kGlobal; k++) {

@@ -449,7 +449,10 @@ __device__ __forceinline__ float tile_depth(const TileSplat& s, float x, float y
 }
 
 __device__ __forceinline__ uint32_t sat_count(const uint32_t* sat, int S, int x0, int y0, int x1, int y1) {
-    return sat[(y1 + 1) * S + x1 + 1] - sat[y0 * S + x1 + 1] - sat[(y1 + 1) * S + x0] + sat[y0 * S + x0];
+    // read-only for the whole frame (k_setup wrote it before): through the
+    // non-coherent path, so the per-view table stays in L1
+    return __ldg(sat + (y1 + 1) * S + x1 + 1) - __ldg(sat + y0 * S + x1 + 1) - __ldg(sat + (y1 + 1) * S + x0) +
+           __ldg(sat + y0 * S + x0);
 }
 
 __device__ __forceinline__ void proj_to_tilesplat(const Proj& p, TileSplat& s) {
@@ -604,11 +607,14 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
 // slot finding its owner by binary search over the block prefix (balanced
 // and coalesced whatever the rect sizes).  The list order across blocks is
 // arbitrary: the binned sort makes the final pair order independent of it.
+#ifndef VRS_PP_STAGE
+#define VRS_PP_STAGE 1
+#endif
 #ifndef VRS_PP_MINB
-#define VRS_PP_MINB 3
+#define VRS_PP_MINB (VRS_PP_STAGE ? 2 : 3)
 #endif
 #ifndef VRS_PP_GRID
-#define VRS_PP_GRID 6
+#define VRS_PP_GRID (VRS_PP_STAGE ? 2 : 6)
 #endif
 #ifndef VRS_TT_GRID
 #define VRS_TT_GRID 8
@@ -623,36 +629,98 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
 // binary search over the warp's prefix sums, by shuffles) -- no block barrier,
 // so warps do not wait for each other.  The next iteration's Gaussian data is
 // prefetched into L2 while this one is projected.
+// Input staging (VRS_PP_STAGE = 1, default): every lane copies its next
+// candidate's 80 input bytes (mu and the 64-B geometry record) into the
+// warp's shared-memory double buffer with cp.async while it projects the
+// current one, so the loads' latency hides behind the projection instead of
+// stalling it (the kernel runs at 3 blocks/SM: too few warps to hide it by
+// occupancy).  The candidate index itself is read two iterations ahead.
+namespace {
+constexpr int kPPWarps = 8;
+struct PPStage {
+    float4 in[2][5][32];  // [buffer][mu, geo0..geo3][lane]: conflict-free LDS.128 / cp.async
+};
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+}  // namespace
+
 __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, FrameParams fp, FrameBufs fb, int64_t test_cap) {
     const int lane = threadIdx.x & 31;
     const int64_t N = fp.N;
     const uint32_t nc = *fb.cand_count;
     const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
     const unsigned lt = (1u << lane) - 1u;
+    auto view_of = [&](uint32_t s) {  // view = number of view blocks of N below s (no 64-bit division)
+        int vi = 0;
+        while (vi + 1 < fp.n_views && (int64_t)s >= (int64_t)(vi + 1) * N) vi++;
+        return vi;
+    };
+#if VRS_PP_STAGE
+    __shared__ PPStage s_pp[kPPWarps];
+    PPStage& stg = s_pp[threadIdx.x >> 5];
+    // issue the copies of candidate s into buffer b (nothing if out of range); always one group
+    auto stage_in = [&](uint32_t ci, uint32_t s, int b) {
+        if (ci < nc) {
+            const int64_t g = (int64_t)s - (int64_t)view_of(s) * N;
+            cp_async16(&stg.in[b][0][lane], sc.mu + g);
+#pragma unroll
+            for (int k = 0; k < 4; k++) cp_async16(&stg.in[b][1 + k][lane], sc.geo + 4 * g + k);
+        }
+        cp_async_commit();
+    };
+    const uint32_t first = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u + (uint32_t)lane;
+    uint32_t s_cur = first < nc ? __ldg(fb.cand + first) : 0u;
+    uint32_t s_nxt = first + nw * 32u < nc ? __ldg(fb.cand + first + nw * 32u) : 0u;
+    stage_in(first, s_cur, 0);
+    int buf = 0;
+#else
     auto prefetch_l2 = [](const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); };
+#endif
     for (uint32_t b0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u; b0 < nc; b0 += nw * 32u) {
         const uint32_t i = b0 + lane;
+#if VRS_PP_STAGE
+        const uint32_t sidx_in = s_cur;
+        {
+            const uint32_t inext = i + nw * 32u, inn = inext + nw * 32u;
+            stage_in(inext, s_nxt, buf ^ 1);
+            s_cur = s_nxt;
+            s_nxt = inn < nc ? __ldg(fb.cand + inn) : 0u;
+            cp_async_wait1();  // this lane's copies of candidate i have landed
+        }
+#else
         {
             const uint32_t inext = i + nw * 32u;
             if (inext < nc) {
                 const uint32_t sn = __ldg(fb.cand + inext);
-                int vn = 0;
-                while (vn + 1 < fp.n_views && (int64_t)sn >= (int64_t)(vn + 1) * N) vn++;
-                const int64_t gn = (int64_t)sn - (int64_t)vn * N;
+                const int64_t gn = (int64_t)sn - (int64_t)view_of(sn) * N;
                 prefetch_l2(sc.mu + gn);
                 prefetch_l2(sc.geo + 4 * gn);  // 64 B: one line (the array is 64-B aligned)
             }
         }
+#endif
         uint32_t cnt = 0, sidx = 0;
         if (i < nc) {
+#if VRS_PP_STAGE
+            sidx = sidx_in;
+            const int vi = view_of(sidx);
+            const ViewParams& v = fp.v[vi];
+            const float4 m4 = stg.in[buf][0][lane];
+            const float4 c0 = stg.in[buf][1][lane], c1 = stg.in[buf][2][lane];
+            const float4 i0 = stg.in[buf][3][lane], i1 = stg.in[buf][4][lane];
+#else
             sidx = fb.cand[i];
-            int vi = 0;  // view = number of view blocks of N below sidx (no 64-bit division)
-            while (vi + 1 < fp.n_views && (int64_t)sidx >= (int64_t)(vi + 1) * N) vi++;
+            const int vi = view_of(sidx);
             const int64_t g = (int64_t)sidx - (int64_t)vi * N;
             const ViewParams& v = fp.v[vi];
             const float4 m4 = __ldg(&sc.mu[g]);
             const float4 c0 = __ldg(&sc.geo[4 * g + 0]), c1 = __ldg(&sc.geo[4 * g + 1]);
             const float4 i0 = __ldg(&sc.geo[4 * g + 2]), i1 = __ldg(&sc.geo[4 * g + 3]);
+#endif
             Proj p;
             if (fp.ewa) project_splat_ewa(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
             else project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
@@ -719,7 +787,13 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
             if (o < tot && pos < test_cap)
                 fb.sidk[pos] = (unsigned long long)e_sidx | ((unsigned long long)(o - (e_inc - e_cnt)) << 32);
         }
+#if VRS_PP_STAGE
+        buf ^= 1;
+#endif
     }
+#if VRS_PP_STAGE
+    asm volatile("cp.async.wait_all;" ::: "memory");
+#endif
 }
 
 
@@ -737,6 +811,7 @@ constexpr int kTT = 256;           // threads per block
 #define VRS_TT_ITEMS 2
 #endif
 constexpr int kTTItems = VRS_TT_ITEMS;  // candidates per thread (independent: ILP)
+
 constexpr int kTTTile = kTT * kTTItems;
 static_assert(kTT / 32 * kTTItems <= 32, "k_tiletest's single-warp scan covers at most 32 warp-slots");
 }  // namespace
