@@ -418,7 +418,9 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         const float asel = __uint_as_float(bsel(__float_as_uint(alpha), __float_as_uint(ah), dm));
         blend_one(((unsigned long long)khi << 32) | klo, asel);
         if (kCounters && done) stop_pos = pos;
-        if ((dm | (uint32_t)done) != 0u) return;
+        // (a sample that just terminated never reads its window again, so the
+        // insertion does not wait for the transmittance test)
+        if (dm != 0u) return;
         hk = (hk + kSlotBytes) & kRingMask;
         // insertion from the tail (entries arrive nearly sorted); dst
         // is the hole, starting at the popped head's slot
