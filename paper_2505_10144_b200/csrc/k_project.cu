@@ -600,21 +600,26 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
 }
 
 // Step 1b: exact per-(view, Gaussian) preprocess of the compacted candidates:
-// projection, footprint, candidate tile count, splat record and SH colour.
-// Step 2 (fused): each block scans its 256 candidate-tile counts, reserves
-// their total in the test list with one atomic and writes the expansion
-// (splat view*N+g | rect-local tile index << 32) cooperatively, every output
-// slot finding its owner by binary search over the block prefix (balanced
-// and coalesced whatever the rect sizes).  The list order across blocks is
-// arbitrary: the binned sort makes the final pair order independent of it.
-#ifndef VRS_PP_STAGE
-#define VRS_PP_STAGE 1
-#endif
+// projection, footprint, candidate tile count and splat record (the SH colour
+// runs in k_color on the side stream).
+// Step 2 (fused): each warp takes 32 consecutive candidates per iteration,
+// scans their tile counts with shuffles and writes the expansion (splat
+// view*N+g | rect-local tile index << 32) itself, every output slot finding
+// its owner lane by a binary search over the warp's prefix sums -- no block
+// barrier, so warps do not wait for each other.  The slices of the test list
+// and of the visible-splat list are reserved with one 64-bit atomic per warp
+// iteration (reserving for several iterations at once measured no faster).
+// The list order is arbitrary: the binned sort makes the final pair order
+// independent of it.
+// Input staging: every lane copies its next candidate's 80 input bytes (mu
+// and the 64-B geometry record) into the warp's shared-memory double buffer
+// with cp.async while it projects the current one; the candidate index itself
+// is read two iterations ahead.
 #ifndef VRS_PP_MINB
-#define VRS_PP_MINB (VRS_PP_STAGE ? 2 : 3)
+#define VRS_PP_MINB 2
 #endif
 #ifndef VRS_PP_GRID
-#define VRS_PP_GRID (VRS_PP_STAGE ? 2 : 6)
+#define VRS_PP_GRID 2
 #endif
 #ifndef VRS_TT_GRID
 #define VRS_TT_GRID 8
@@ -622,19 +627,6 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
 #ifndef VRS_TT_MINB
 #define VRS_TT_MINB 4
 #endif
-// Warp-independent form: each warp takes 32 consecutive candidates per
-// iteration, scans their tile counts with shuffles, reserves its slice of the
-// test list (and of the visible-splat list) with one atomic per warp, and
-// writes the expansion itself (each output slot finds its owner lane by a
-// binary search over the warp's prefix sums, by shuffles) -- no block barrier,
-// so warps do not wait for each other.  The next iteration's Gaussian data is
-// prefetched into L2 while this one is projected.
-// Input staging (VRS_PP_STAGE = 1, default): every lane copies its next
-// candidate's 80 input bytes (mu and the 64-B geometry record) into the
-// warp's shared-memory double buffer with cp.async while it projects the
-// current one, so the loads' latency hides behind the projection instead of
-// stalling it (the kernel runs at 3 blocks/SM: too few warps to hide it by
-// occupancy).  The candidate index itself is read two iterations ahead.
 namespace {
 constexpr int kPPWarps = 8;
 struct PPStage {
@@ -660,7 +652,6 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
         while (vi + 1 < fp.n_views && (int64_t)s >= (int64_t)(vi + 1) * N) vi++;
         return vi;
     };
-#if VRS_PP_STAGE
     __shared__ PPStage s_pp[kPPWarps];
     PPStage& stg = s_pp[threadIdx.x >> 5];
     // issue the copies of candidate s into buffer b (nothing if out of range); always one group
@@ -678,12 +669,8 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
     uint32_t s_nxt = first + nw * 32u < nc ? __ldg(fb.cand + first + nw * 32u) : 0u;
     stage_in(first, s_cur, 0);
     int buf = 0;
-#else
-    auto prefetch_l2 = [](const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); };
-#endif
     for (uint32_t b0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32u; b0 < nc; b0 += nw * 32u) {
         const uint32_t i = b0 + lane;
-#if VRS_PP_STAGE
         const uint32_t sidx_in = s_cur;
         {
             const uint32_t inext = i + nw * 32u, inn = inext + nw * 32u;
@@ -692,42 +679,22 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
             s_nxt = inn < nc ? __ldg(fb.cand + inn) : 0u;
             cp_async_wait1();  // this lane's copies of candidate i have landed
         }
-#else
-        {
-            const uint32_t inext = i + nw * 32u;
-            if (inext < nc) {
-                const uint32_t sn = __ldg(fb.cand + inext);
-                const int64_t gn = (int64_t)sn - (int64_t)view_of(sn) * N;
-                prefetch_l2(sc.mu + gn);
-                prefetch_l2(sc.geo + 4 * gn);  // 64 B: one line (the array is 64-B aligned)
-            }
-        }
-#endif
         uint32_t cnt = 0, sidx = 0;
         if (i < nc) {
-#if VRS_PP_STAGE
             sidx = sidx_in;
             const int vi = view_of(sidx);
             const ViewParams& v = fp.v[vi];
             const float4 m4 = stg.in[buf][0][lane];
             const float4 c0 = stg.in[buf][1][lane], c1 = stg.in[buf][2][lane];
             const float4 i0 = stg.in[buf][3][lane], i1 = stg.in[buf][4][lane];
-#else
-            sidx = fb.cand[i];
-            const int vi = view_of(sidx);
-            const int64_t g = (int64_t)sidx - (int64_t)vi * N;
-            const ViewParams& v = fp.v[vi];
-            const float4 m4 = __ldg(&sc.mu[g]);
-            const float4 c0 = __ldg(&sc.geo[4 * g + 0]), c1 = __ldg(&sc.geo[4 * g + 1]);
-            const float4 i0 = __ldg(&sc.geo[4 * g + 2]), i1 = __ldg(&sc.geo[4 * g + 3]);
-#endif
             Proj p;
             if (fp.ewa) project_splat_ewa(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
             else project_splat(v, m4, c0, c1, i0, i1, fp.T, fp.near_plane, p);
             // number of (Gaussian, tile) candidates = rect area, 0 if the rect holds no
             // visible tile (SAT); the exact Eq.4 tests run load-balanced in k_tiletest
+            // (a view without invisible tiles skips the table: every tile counts)
             if (p.valid && p.rect[0] <= p.rect[2] && p.rect[1] <= p.rect[3] &&
-                sat_count(v.sat, v.tw + 1, p.rect[0], p.rect[1], p.rect[2], p.rect[3]) > 0)
+                (v.n_inv == 0 || sat_count(v.sat, v.tw + 1, p.rect[0], p.rect[1], p.rect[2], p.rect[3]) > 0))
                 cnt = (uint32_t)((p.rect[2] - p.rect[0] + 1) * (p.rect[3] - p.rect[1] + 1));
             if (cnt) {
                 float4* rec = fb.rec + (size_t)sidx * kRecF4;
@@ -787,13 +754,9 @@ __global__ void __launch_bounds__(256, VRS_PP_MINB) k_preprocess(SceneDev sc, Fr
             if (o < tot && pos < test_cap)
                 fb.sidk[pos] = (unsigned long long)e_sidx | ((unsigned long long)(o - (e_inc - e_cnt)) << 32);
         }
-#if VRS_PP_STAGE
         buf ^= 1;
-#endif
     }
-#if VRS_PP_STAGE
     asm volatile("cp.async.wait_all;" ::: "memory");
-#endif
 }
 
 
@@ -830,7 +793,7 @@ __device__ __forceinline__ bool test_candidate(const FrameParams& fp, const Fram
     const int tx0 = r01 & 0xffff, ty0 = r01 >> 16, tx1 = r23 & 0xffff;
     const int rw = tx1 - tx0 + 1;
     const int tx = tx0 + (int)(l % (uint32_t)rw), ty = ty0 + (int)(l / (uint32_t)rw);
-    if (!v.vis[ty * v.tw + tx]) return false;
+    if (v.n_inv != 0 && !v.vis[ty * v.tw + tx]) return false;  // (no table read when every tile is visible)
     TileSplat s;
     const int T = fp.T, x0 = tx * T, y0 = ty * T;
     float hx, hy, hz;
@@ -1085,10 +1048,11 @@ __global__ void __launch_bounds__(256) k_color(SceneDev sc, FrameParams fp, Fram
 void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {
     cudaMemsetAsync(fb.tv, 0, 8, st);
     if (fp.N == 0) return;
-    const int B = 256;
+    constexpr int B = 256;
     cudaMemsetAsync(fb.cand_count, 0, 4, st);
     k_cull<<<(unsigned)((fp.N + B - 1) / B), B, 0, st>>>(sc, fp, fb);
     const int sms = device_sms();
+    static_assert(B == 32 * kPPWarps, "one staging buffer per warp");
     k_preprocess<<<sms * VRS_PP_GRID, B, 0, st>>>(sc, fp, fb, test_cap);
 }
 
