@@ -181,6 +181,37 @@ def cpu_model():
     return None
 
 
+def stage_roofline(counters, stage_ms, n, n_views, peaks):
+    """HBM roofline of the memory-side stages (SURVEY §8d "Roofline per stage"):
+    algorithmic bytes per unit x the frame's units, over the stage's event time,
+    against the measured copy bandwidth and the nominal 8 TB/s.  Units: N
+    Gaussians, G1 Gaussians in >= 1 view's frustum cone, V visible (view,
+    Gaussian), P pairs.  preprocess = 16 B/Gaussian (mu + q_cut) + 244 B per G1
+    (Sigma_w, Sigma_w^-1, sigma, SH3) + 112 B record per V + 4 B count per
+    (view, Gaussian); duplicate = 64 B read per V + 12 B written per pair; sort
+    (+ ranges) = 24 B per pair (one read + one write of key and value) + 8 B per
+    pair and per tile for the ranges."""
+    hbm = float(peaks.get("hbm_gbs", 6549.0))
+    N, G1 = float(n), float(counters.get("frustum_gaussians", 0))
+    V, P = float(counters.get("visible_splats", 0)), float(counters.get("pairs", 0))
+    tiles = float(sum(counters.get("tiles_by_class", [0, 0, 0, 0])))
+    rows = {
+        "preprocess": (16 * N + 244 * G1 + 112 * V + 4 * N * n_views, stage_ms[0] + stage_ms[1],
+                       "k_cull + k_preprocess (k_color on the side stream)"),
+        "duplicate": (64 * V + 12 * P, stage_ms[2], "k_tiletest_direct"),
+        "sort": (24 * P + 8 * P + 8 * tiles, stage_ms[3] + stage_ms[4], "k_tile_scan + k_ovf_bucket + k_tile_sort"),
+    }
+    out = {}
+    for k, (b, ms, kern) in rows.items():
+        gbs = b / (ms * 1e-3) / 1e9 if ms > 0 else 0.0
+        out[k] = {"kernels": kern, "bound": "hbm", "algorithmic_bytes": b, "ms": ms, "achieved_gbs": gbs,
+                  "frac": gbs / hbm, "frac_8tbs": gbs / 8000.0}
+    out["units"] = {"N": N, "G1": G1, "V": V, "P": P, "candidates": counters.get("candidates"),
+                    "tile_tests": counters.get("tile_tests")}
+    out["peak_gbs"] = hbm
+    return out
+
+
 def cpu_baseline(scene, cams, fov, masks, T, budget_s=15.0, threads=0):
     """The oracle as it stands on the host cores, on a bounded sample:
     full per-Gaussian stage + instantiation + sort + ranges for both eyes, then
@@ -719,6 +750,7 @@ def main():
                          # against the issue peak (148 SM x 4 schedulers x clock): how full the issue slots are
                          "issue_frac": (winst / (blend_ms * 1e-3 * 148 * 4 * float(peaks.get("sm_max_mhz", 1965.0))
                                                  * 1e6)) if winst and blend_ms > 0 else None},
+            "stage_roofline": stage_roofline(counters, stage_ms, r.n, n_views, peaks),
             "clocks": clocks,
             "gpu_launches": launches_per_step * args.steps,
             "e2e": e2e,

@@ -114,6 +114,9 @@ typedef struct {
     int64_t visible_splats;      /* (view, Gaussian) with >= 1 pair */
     float stage_ms[8];           /* preprocess, scan, duplicate, sort, ranges, blend, compose, total
                                     (filled only when timing is enabled) */
+    int64_t candidates;          /* (view, Gaussian) passing the conservative frustum-cone cull (step 1a) */
+    int64_t frustum_gaussians;   /* Gaussians passing it for >= 1 view (read by step 1b) */
+    int64_t tile_tests;          /* (Gaussian, tile) candidates of the Eq.4 test (step 3) */
 } vrs_frame_stats;
 
 /* Create a context on cfg->device; allocates all device memory.

@@ -556,6 +556,7 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     __shared__ uint32_t s_wcnt[32];
     __shared__ uint32_t s_base;
+    bool any = false;
     for (int vi = 0; vi < fp.n_views; vi++) {
         const ViewParams& v = fp.v[vi];
         bool pass = false;
@@ -595,8 +596,11 @@ __global__ void __launch_bounds__(256) k_cull(SceneDev sc, FrameParams fp, Frame
         __syncthreads();
         if (pass)
             fb.cand[s_base + s_wcnt[warp] + __popc(m & ((1u << lane) - 1u))] = (uint32_t)((int64_t)vi * N + g);
+        any = any || pass;
         __syncthreads();
     }
+    const int nany = __syncthreads_count(any);  // Gaussians read by step 1b (statistic, one atomic per block)
+    if (threadIdx.x == 0 && nany) atomicAdd(fb.frustum_count, (uint32_t)nany);
 }
 
 // Step 1b: exact per-(view, Gaussian) preprocess of the compacted candidates:
@@ -1047,9 +1051,10 @@ __global__ void __launch_bounds__(256) k_color(SceneDev sc, FrameParams fp, Fram
 
 void launch_preprocess(const SceneDev& sc, const FrameParams& fp, FrameBufs fb, int64_t test_cap, cudaStream_t st) {
     cudaMemsetAsync(fb.tv, 0, 8, st);
+    cudaMemsetAsync(fb.cand_count, 0, 4, st);
+    cudaMemsetAsync(fb.frustum_count, 0, 4, st);
     if (fp.N == 0) return;
     constexpr int B = 256;
-    cudaMemsetAsync(fb.cand_count, 0, 4, st);
     k_cull<<<(unsigned)((fp.N + B - 1) / B), B, 0, st>>>(sc, fp, fb);
     const int sms = device_sms();
     static_assert(B == 32 * kPPWarps, "one staging buffer per warp");

@@ -53,7 +53,7 @@ struct vrs_context {
     float4* d_rec = nullptr;
     float4* d_col = nullptr;
     uint32_t* d_cand = nullptr;
-    uint32_t *d_counts = nullptr, *d_misc = nullptr;  // misc: pairs, overflow, -, candidates, -
+    uint32_t *d_counts = nullptr, *d_misc = nullptr;  // misc: pairs, overflow, -, candidates, -, ovf, frustum, -
     unsigned long long* d_tv = nullptr;               // tile tests | visible splats << 36
     uint32_t* d_vis_list = nullptr;
     unsigned long long* d_sidk = nullptr;    // [test_cap] candidate map
@@ -646,6 +646,7 @@ static FrameBufs frame_bufs(vrs_context* ctx) {
     fb.col = ctx->d_col;
     fb.cand = ctx->d_cand;
     fb.cand_count = ctx->d_misc + 3;
+    fb.frustum_count = ctx->d_misc + 6;
     fb.vis_list = ctx->d_vis_list;
     fb.tv = ctx->d_tv;
     fb.sidk = ctx->d_sidk;
@@ -894,11 +895,14 @@ vrs_status vrs_get_frame_stats(vrs_context* ctx, vrs_frame_stats* out) {
     CK(cudaSetDevice(ctx->cfg.device));
     CK(cudaStreamSynchronize(ctx->last_stream));
     std::memset(out, 0, sizeof(*out));
-    uint32_t misc[3] = {0, 0, 0};
+    uint32_t misc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     unsigned long long tv = 0;
-    CK(cudaMemcpy(misc, ctx->d_misc, 12, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(misc, ctx->d_misc, 32, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(&tv, ctx->d_tv, 8, cudaMemcpyDeviceToHost));
     out->pairs = misc[0];
+    out->candidates = misc[3];
+    out->frustum_gaussians = misc[6];
+    out->tile_tests = (int64_t)(tv & ((1ull << 36) - 1ull));
     unsigned long long st[8] = {0};
     if (ctx->counters) CK(cudaMemcpy(st, ctx->d_stats, sizeof(st), cudaMemcpyDeviceToHost));
     out->evaluations = (int64_t)st[0];

@@ -98,6 +98,7 @@ struct FrameBufs {
     float4* rec;             // [V][N][8]
     uint32_t* cand;          // [V*N] (view*N + g) passing the conservative cull
     uint32_t* cand_count;    // [1]
+    uint32_t* frustum_count; // [1] Gaussians with >= 1 candidate (step 1a statistic)
     unsigned long long* tv;  // [1] expanded tile tests (bits 0-35) | visible splats (bits 36-63), device
     unsigned long long* sidk;  // [test_cap] candidate -> (splat view*N+g) | (rect-local tile index << 32)
     uint32_t* vis_list;      // [V*N] (view*N + g) with >= 1 candidate tile (colour work list)

@@ -54,7 +54,8 @@ class vrs_frame_stats(C.Structure):
     _fields_ = [("pairs", C.c_int64), ("samples", C.c_int64), ("evaluations", C.c_int64),
                 ("contributions", C.c_int64), ("overflow_samples", C.c_int64), ("terminated_samples", C.c_int64),
                 ("tiles_by_class", C.c_int32 * 4), ("work_items", C.c_int64), ("visible_splats", C.c_int64),
-                ("stage_ms", C.c_float * 8)]
+                ("stage_ms", C.c_float * 8), ("candidates", C.c_int64), ("frustum_gaussians", C.c_int64),
+                ("tile_tests", C.c_int64)]
 
     def as_dict(self):
         d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("tiles_by_class", "stage_ms")}
