@@ -587,13 +587,18 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
                 if (lane == 0) atomicSub(&S.alive, 1u);
             }
             __syncwarp();
+            // (fence-fence synchronisation through the counter: every warp's reads of
+            // the stage are ordered before its increment, the last warp's refill writes
+            // after its observation of the full count)
             uint32_t last = 0;
             if (lane == 0) {
                 __threadfence_block();
                 last = (atomicAdd(&S.consumed[st], 1u) == (uint32_t)kWarps - 1u) ? 1u : 0u;
+                if (last) __threadfence_block();
             }
             last = __shfl_sync(0xffffffffu, last, 0);
             if (last) {
+                __syncwarp();
                 const uint32_t bn = b + 2;
                 if (lane == 0) S.consumed[st] = 0;
                 if (bn < nbat && *alive != 0u) {
