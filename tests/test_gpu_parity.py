@@ -140,6 +140,31 @@ def test_foveated_masked_stereo_parity(vrs, oracle_mod):
     assert st["samples"] == ost["samples"] and st["work_items"] == ost["work_items"]
 
 
+def test_front_end_statistics(vrs, oracle_mod):
+    """vrs_frame_stats' front-end counters (the units of bench.py's per-stage
+    HBM roofline) obey their definitions: every Gaussian with a pair passed the
+    conservative cone cull for some view, candidates are (view, Gaussian) with
+    1 <= views per Gaussian <= n_views, every visible (view, Gaussian) was a
+    candidate, every pair was a tested tile; masked and unmasked views alike."""
+    scene = sg.vr_room(7, 20000, sh_degree=1)
+    W, H = 320, 256
+    f = sg.focal_for_hfov(W, 110.0)
+    for masked in (True, False):
+        cams = [sg.look_camera((x, 0, 0), 0.3, 0.1, 0.0, f=f, width=W, height=H, mask_slot=e if masked else -1)
+                for e, x in enumerate((-0.0315, 0.0315))]
+        masks = {0: sg.ellipse_mask(W, H), 1: sg.ellipse_mask(W, H, 1.0)} if masked else None
+        r, o, g, oi = render_both(vrs, oracle_mod, scene, cams, None, T=16, masks=masks)
+        assert_lists_equal(r, o)
+        st = r.stats()
+        k, v = r.vrs_debug_pairs(True)
+        assert 0 < st["frustum_gaussians"] <= scene.n
+        assert st["frustum_gaussians"] <= st["candidates"] <= 2 * st["frustum_gaussians"]
+        assert len(np.unique(v)) <= st["frustum_gaussians"]
+        assert st["visible_splats"] <= st["candidates"]
+        assert st["pairs"] <= st["tile_tests"]
+        assert st["pairs"] == len(k) == o.stats()["pairs"]
+
+
 @pytest.mark.parametrize("W,H,T", [(37, 29, 16), (65, 33, 32), (16, 16, 16), (1, 1, 16), (300, 17, 32)])
 def test_odd_sizes_and_edges(vrs, oracle_mod, W, H, T):
     """Ragged image borders (partial tiles, odd widths, 1x1)."""
