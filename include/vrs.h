@@ -242,16 +242,6 @@ VRS_API vrs_status vrs_render_views_two_pass(vrs_context* ctx, int32_t n_views, 
  * mode 1 with the EWA projection). */
 VRS_API vrs_status vrs_set_resort_mode(vrs_context* ctx, int32_t mode, int32_t block_queue, int32_t pixel_window);
 
-/* How the blend stages each batch of splat records (the tile list's entries,
- * north_star "Gaussian batches staged into shared memory") -- results are
- * identical, only the copy engine differs:
- *   VRS_STAGING_THREADS (default): the block's threads load the records
- *     (seven 16-B loads each) and store them to shared memory;
- *   VRS_STAGING_TMA: the Tensor Memory Accelerator copies them
- *     (cp.async.bulk global -> shared, one 96-B copy per entry issued by the
- *     block's warps, completion on an mbarrier).
- * Applies to the flat (mode 0) blend from the next render.  Errors:
- * VRS_E_INVALID_ARG (unknown mode). */
 /* Sort order: VRS_SORT_STOPTHEPOP (default)
  * = the method -- per-tile key depth at the tile's maximum point and
  * the per-sample K = 16 resort window; VRS_SORT_Z = Mini-Splatting (z): one
@@ -267,6 +257,20 @@ VRS_API vrs_status vrs_set_resort_mode(vrs_context* ctx, int32_t mode, int32_t b
 #define VRS_SORT_DIST 2
 VRS_API vrs_status vrs_set_sort_mode(vrs_context* ctx, int32_t mode);
 
+/* How the blend stages each batch of splat records (the tile list's entries,
+ * north_star "Gaussian batches staged into shared memory") -- results are
+ * identical, only the staging differs:
+ *   VRS_STAGING_THREADS (default): 32-entry batches in a two-stage shared-
+ *     memory ring; the block's threads stage the first two, then the warps
+ *     consume the stages at their own pace and the last warp done with a
+ *     batch refills its stage with the batch two ahead (seven 16-B loads per
+ *     entry, one entry per lane), completion on the stage's mbarrier -- no
+ *     block barrier inside the blend loop;
+ *   VRS_STAGING_TMA: block-synchronous batches of 64 whose records the Tensor
+ *     Memory Accelerator copies (cp.async.bulk global -> shared, one 96-B copy
+ *     per entry issued by the block's warps, completion on an mbarrier).
+ * Applies to the flat (mode 0) blend from the next render.  Errors:
+ * VRS_E_INVALID_ARG (unknown mode). */
 #define VRS_STAGING_THREADS 0
 #define VRS_STAGING_TMA 1
 VRS_API vrs_status vrs_set_staging_mode(vrs_context* ctx, int32_t mode);
