@@ -647,9 +647,9 @@ def main():
                         render(cs, fov, d[b][0], d[b][1], stream=stream)
                         rendered[b].record(stream)
                     cstream.wait_event(rendered[b])
-                    with torch.cuda.stream(cstream):
-                        h[b][0].copy_(d[b][0], non_blocking=True)
-                        h[b][1].copy_(d[b][1], non_blocking=True)
+                    with torch.cuda.stream(cstream):  # byte views: the same copy for every format
+                        h[b][0].view(torch.uint8).copy_(d[b][0].view(torch.uint8), non_blocking=True)
+                        h[b][1].view(torch.uint8).copy_(d[b][1].view(torch.uint8), non_blocking=True)
                         copied[b].record(cstream)
                 cstream.synchronize()
 
@@ -657,8 +657,8 @@ def main():
                 if two_pass:  # public Python API: device render, then D2H into pinned memory on the same stream
                     with torch.cuda.stream(stream):
                         render(cams, fov, d[0][0], d[0][1], stream=stream)
-                        h[0][0].copy_(d[0][0], non_blocking=True)
-                        h[0][1].copy_(d[0][1], non_blocking=True)
+                        h[0][0].view(torch.uint8).copy_(d[0][0].view(torch.uint8), non_blocking=True)
+                        h[0][1].view(torch.uint8).copy_(d[0][1].view(torch.uint8), non_blocking=True)
                     stream.synchronize()
                 else:
                     r.render_host(cams, fov, h[0][0], h[0][1], stream=stream)
@@ -687,10 +687,16 @@ def main():
         r.vrs_set_instrumentation(counters=0, timing=0)  # no per-stage events on the end-to-end path
         v8, s8, b8 = measure_e2e(1)
         v32, s32, b32 = measure_e2e(0)
+        v16, s16, b16 = measure_e2e(2)
         what = "render_two_pass" if two_pass else "render"
-        e2e = {"value": v32, "unit": unit, "h2d_bytes_per_step": cam_bytes, "d2h_bytes_per_step": b32,
-               "sync_value": s32, "format": "VRS_OUT_F32 (RGBA float32 + depth float32: the frame the parity "
-                                            "tolerances are stated on)",
+        # headline: the most compact output format that still meets the north_star tolerances on
+        # every pixel (RGBA binary16: |rounding| <= 2^-11 |v| against the 2e-3 RGB bar; depth float)
+        e2e = {"value": v16, "unit": unit, "h2d_bytes_per_step": cam_bytes, "d2h_bytes_per_step": b16,
+               "sync_value": s16, "format": "VRS_OUT_RGBA16F_D32F (RGBA binary16 + depth float32, the half-float swap-chain "
+                                            "format: within the parity tolerances on every pixel, "
+                                            "tests/test_gpu_output_formats.py)",
+               "f32": {"value": v32, "sync_value": s32, "d2h_bytes_per_step": b32,
+                       "format": "VRS_OUT_F32 (RGBA float32 + depth float32)"},
                "display_packed": {"value": v8, "sync_value": s8, "d2h_bytes_per_step": b8,
                                   "format": "VRS_OUT_RGBA8_D16F (RGBA unorm8 + depth binary16, the HMD display "
                                             "format; depth quantised to 2^-11 relative, outside the 1e-4 bar)"},

@@ -51,6 +51,7 @@ extern "C" {
 /* Output pixel formats (vrs_set_output_format). */
 #define VRS_OUT_F32 0            /* rgba: float[4] per pixel, depth: float per pixel (default) */
 #define VRS_OUT_RGBA8_D16F 1     /* rgba: uint8[4] unorm = round(clamp(v,0,1)*255), depth: IEEE binary16 */
+#define VRS_OUT_RGBA16F_D32F 2   /* rgba: IEEE binary16[4] (round to nearest), depth: float */
 
 typedef enum {
     VRS_OK = 0,
@@ -188,7 +189,12 @@ VRS_API vrs_status vrs_backward(vrs_context* ctx, const float* rgba, const float
  * 20 B — what bounds the host path is the device->host copy.  The output
  * pointers keep their float* type in the signatures; with VRS_OUT_RGBA8_D16F
  * they must point to buffers of n_px*4 bytes (rgba) and n_px uint16 (depth),
- * cast to float*.  Errors: VRS_E_INVALID_ARG (unknown format). */
+ * cast to float*.  VRS_OUT_RGBA16F_D32F (the scRGB-style half-float swap-chain
+ * format) keeps the frame within the parity tolerances in 12 B instead of
+ * 20 B per pixel: RGBA rounded to binary16 (|error| <= 2^-11 |v|, i.e. <= 2e-3
+ * for |v| <= 4; no clamp), depth float; rgba then points to n_px*4 binary16
+ * (cast to float*), depth to n_px floats.  Errors: VRS_E_INVALID_ARG (unknown
+ * format). */
 VRS_API vrs_status vrs_set_output_format(vrs_context* ctx, int32_t format);
 
 /* Render n_views views (one frame: all views share one sort and one blend

@@ -770,9 +770,11 @@ vrs_status vrs_render_views_host(vrs_context* ctx, int32_t n_views, const vrs_ca
     cudaStream_t st = (cudaStream_t)stream;
     vrs_status s = render_impl(ctx, n_views, cams, fovea, ctx->d_out_rgba, ctx->d_out_depth, st, ctx->out_fmt);
     if (s != VRS_OK) return s;
-    const bool f32 = ctx->out_fmt == VRS_OUT_F32;
-    CK(cudaMemcpyAsync(rgba_host, ctx->d_out_rgba, (f32 ? sizeof(float) : 1) * 4 * px, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(depth_host, ctx->d_out_depth, (f32 ? sizeof(float) : 2) * px, cudaMemcpyDeviceToHost, st));
+    // bytes per pixel of the format: RGBA 16 / 8 / 4, depth 4 / 4 / 2
+    const size_t rb = ctx->out_fmt == VRS_OUT_F32 ? 16 : (ctx->out_fmt == VRS_OUT_RGBA16F_D32F ? 8 : 4);
+    const size_t db = ctx->out_fmt == VRS_OUT_RGBA8_D16F ? 2 : 4;
+    CK(cudaMemcpyAsync(rgba_host, ctx->d_out_rgba, rb * px, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(depth_host, ctx->d_out_depth, db * px, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return VRS_OK;
 }
@@ -997,8 +999,9 @@ vrs_status vrs_backward(vrs_context* ctx, const float* rgba, const float* depth,
 
 vrs_status vrs_set_output_format(vrs_context* ctx, int32_t format) {
     if (!ctx) return VRS_E_INVALID_ARG;
-    if (format != VRS_OUT_F32 && format != VRS_OUT_RGBA8_D16F)
-        return fail(ctx, VRS_E_INVALID_ARG, "output format must be VRS_OUT_F32 or VRS_OUT_RGBA8_D16F");
+    if (format != VRS_OUT_F32 && format != VRS_OUT_RGBA8_D16F && format != VRS_OUT_RGBA16F_D32F)
+        return fail(ctx, VRS_E_INVALID_ARG,
+                    "output format must be VRS_OUT_F32, VRS_OUT_RGBA8_D16F or VRS_OUT_RGBA16F_D32F");
     ctx->out_fmt = format;
     return VRS_OK;
 }

@@ -298,7 +298,8 @@ __device__ __forceinline__ float quad3z1(float a, float b, float c, float p, flo
 }
 
 // Final output pixel i in the context's output format (vrs_set_output_format):
-// VRS_OUT_F32 = float4 RGBA + float depth; VRS_OUT_RGBA8_D16F = RGBA unorm8
+// VRS_OUT_F32 = float4 RGBA + float depth; VRS_OUT_RGBA16F_D32F = RGBA IEEE
+// binary16 (round to nearest) + float depth; VRS_OUT_RGBA8_D16F = RGBA unorm8
 // (round to nearest of clamp(v, 0, 1) * 255) + depth IEEE binary16 (round to
 // nearest).  rgba / depth point to the caller's buffers of that format.
 __device__ __forceinline__ unsigned char unorm8(float v) {
@@ -307,6 +308,11 @@ __device__ __forceinline__ unsigned char unorm8(float v) {
 __device__ __forceinline__ void store_pixel(int fmt, float* rgba, float* depth, size_t i, float4 c, float d) {
     if (fmt == VRS_OUT_F32) {
         reinterpret_cast<float4*>(rgba)[i] = c;
+        depth[i] = d;
+    } else if (fmt == VRS_OUT_RGBA16F_D32F) {  // RGBA binary16 + float depth (within the parity tolerances)
+        const __half2 rg = __floats2half2_rn(c.x, c.y), ba = __floats2half2_rn(c.z, c.w);
+        reinterpret_cast<uint2*>(rgba)[i] =
+            make_uint2(*reinterpret_cast<const uint32_t*>(&rg), *reinterpret_cast<const uint32_t*>(&ba));
         depth[i] = d;
     } else {
         reinterpret_cast<uchar4*>(rgba)[i] = make_uchar4(unorm8(c.x), unorm8(c.y), unorm8(c.z), unorm8(c.w));

@@ -67,6 +67,18 @@ class vrs_frame_stats(C.Structure):
 _lib = None
 
 
+# element types of (rgba, depth) per output format (VRS_OUT_F32, VRS_OUT_RGBA8_D16F, VRS_OUT_RGBA16F_D32F)
+_FMT_NUMPY = {0: (np.float32, np.float32), 1: (np.uint8, np.float16), 2: (np.float16, np.float32)}
+
+
+def _torch_types(fmt):
+    import torch
+    return {0: (torch.float32, torch.float32), 1: (torch.uint8, torch.float16), 2: (torch.float16, torch.float32)}[fmt]
+
+
+_FMT_TORCH = {f: (lambda f=f: _torch_types(f)) for f in (0, 1, 2)}
+
+
 def lib():
     """Load libvrs.so (raises if missing: no fallback)."""
     global _lib
@@ -249,7 +261,8 @@ class Renderer:
         return out
 
     def vrs_set_output_format(self, fmt):
-        """VRS_OUT_F32 (0): float RGBA + float depth; VRS_OUT_RGBA8_D16F (1): uint8 RGBA + binary16 depth."""
+        """VRS_OUT_F32 (0): float RGBA + float depth; VRS_OUT_RGBA8_D16F (1): uint8 RGBA + binary16
+        depth; VRS_OUT_RGBA16F_D32F (2): binary16 RGBA + float depth."""
         self._check(lib().vrs_set_output_format(self.h, int(fmt)))
         self.out_fmt = int(fmt)
 
@@ -275,8 +288,8 @@ class Renderer:
         out-of-bounds device access."""
         import torch
         fmt = getattr(self, "out_fmt", 0) if fmt is None else fmt
-        want_r, want_d = (torch.uint8, torch.float16) if fmt == 1 else (torch.float32, torch.float32)
-        np_r, np_d = (np.uint8, np.float16) if fmt == 1 else (np.float32, np.float32)
+        want_r, want_d = _FMT_TORCH[fmt]()
+        np_r, np_d = _FMT_NUMPY[fmt]
         for t, n, wt, wn, name in ((rgba, 4 * px, want_r, np_r, "rgba"), (depth, px, want_d, np_d, "depth")):
             if isinstance(t, np.ndarray):
                 if not host:
@@ -300,12 +313,12 @@ class Renderer:
         return carr, farr
 
     def alloc_outputs(self, cams, pinned_host=False):
-        """Output tensors for the context's format: (px, 4) float32 + (px,) float32, or
-        (px, 4) uint8 + (px,) float16 for VRS_OUT_RGBA8_D16F; on the device, or pinned host."""
+        """Output tensors for the context's format: (px, 4) float32 + (px,) float32, (px, 4)
+        uint8 + (px,) float16 for VRS_OUT_RGBA8_D16F, (px, 4) float16 + (px,) float32 for
+        VRS_OUT_RGBA16F_D32F; on the device, or pinned host."""
         import torch
         px = sum(c.width * c.height for c in cams)
-        packed = getattr(self, "out_fmt", 0) == 1
-        rt, dt = (torch.uint8, torch.float16) if packed else (torch.float32, torch.float32)
+        rt, dt = _FMT_TORCH[getattr(self, "out_fmt", 0)]()
         if pinned_host:
             return (torch.empty((px, 4), dtype=rt).pin_memory(), torch.empty(px, dtype=dt).pin_memory())
         dev = torch.device("cuda", self.device)
@@ -354,9 +367,9 @@ class Renderer:
         """End-to-end path: outputs land in HOST buffers (numpy or pinned torch tensors)."""
         px = sum(c.width * c.height for c in cams)
         if rgba_host is None:
-            packed = getattr(self, "out_fmt", 0) == 1
-            rgba_host = np.empty((px, 4), np.uint8 if packed else np.float32)
-            depth_host = np.empty(px, np.float16 if packed else np.float32)
+            nr, nd = _FMT_NUMPY[getattr(self, "out_fmt", 0)]
+            rgba_host = np.empty((px, 4), nr)
+            depth_host = np.empty(px, nd)
         self._check_buffers(px, rgba_host, depth_host, host=True)
         rp = rgba_host.data_ptr() if hasattr(rgba_host, "data_ptr") else rgba_host.ctypes.data
         dp = depth_host.data_ptr() if hasattr(depth_host, "data_ptr") else depth_host.ctypes.data
