@@ -779,20 +779,23 @@ def main():
 def measure_gather(args, r, render, cams, fov, stream, rank, world, local, one_gpu):
     """Render + gather per step: each rank renders its step's frame into one of two
     device buffers; a side stream waits for it and runs the grouped send/recv of
-    the frame (RGBA f32 + depth f32) to rank 0, which receives every rank's frame
+    the frame to rank 0 in the half-float format that meets the parity
+    tolerances (VRS_OUT_RGBA16F_D32F: RGBA binary16 + depth f32, 12 B/px),
+    which receives every rank's frame
     into its own double buffer; a buffer is re-rendered only after its send
     finished.  Host wall clock over the steps, max over ranks."""
     import torch
     import torch.distributed as dist
     n = min(args.steps, 20)
     cstream = torch.cuda.Stream(device=local)
+    r.vrs_set_output_format(2)
     d = [r.alloc_outputs(cams) for _ in range(2)]
     sent = [torch.cuda.Event() for _ in range(2)]
     rendered = [torch.cuda.Event() for _ in range(2)]
     recv = None
     if rank == 0:
         recv = [[r.alloc_outputs(cams) for _ in range(world)] for _ in range(2)]
-    bytes_per_rank = int(d[0][0].numel() * 4 + d[0][1].numel() * 4)
+    bytes_per_rank = int(d[0][0].numel() * d[0][0].element_size() + d[0][1].numel() * d[0][1].element_size())
 
     def step(s):
         b = s & 1
@@ -835,11 +838,13 @@ def measure_gather(args, r, render, cams, fov, stream, rank, world, local, one_g
     tt = torch.tensor([t], dtype=torch.float64, device="cuda")
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t = float(tt.item())
+    r.vrs_set_output_format(0)
     unit = "stereo frames/s" if len(cams) == 2 else "frames/s"
     return {"value": world * n / t, "unit": unit, "steps": n, "ms_per_step": 1000.0 * t / n,
             "gathered_bytes_per_step": bytes_per_rank * (world - 1),
-            "note": "render + grouped send/recv of every rank's RGBA f32 + depth f32 frame to rank 0 on a side "
-                    "stream (double-buffered), host wall clock, max over ranks; `value` above is render-only"}
+            "note": "render + grouped send/recv of every rank's frame (RGBA binary16 + depth f32, within the "
+                    "parity tolerances) to rank 0 on a side stream (double-buffered), host wall clock, max over "
+                    "ranks; `value` above is render-only"}
 
 
 def compare_flat(r, render, cams, fov, rgba, depth, stream, counters):
