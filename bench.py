@@ -34,6 +34,8 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
+# frames in flight on the end-to-end path (device/pinned output buffers rotating between render and D2H)
+E2E_DEPTH = int(os.environ.get("VRS_E2E_DEPTH", "2"))
 sys.path.insert(0, ROOT)
 
 import scenegen as sg  # noqa: E402
@@ -630,18 +632,18 @@ def main():
 
         def measure_e2e(fmt):
             r.vrs_set_output_format(fmt)
-            h = [r.alloc_outputs(cams, pinned_host=True) for _ in range(2)]
-            d = [r.alloc_outputs(cams) for _ in range(2)]
+            h = [r.alloc_outputs(cams, pinned_host=True) for _ in range(E2E_DEPTH)]
+            d = [r.alloc_outputs(cams) for _ in range(E2E_DEPTH)]
             cstream = torch.cuda.Stream(device=local)
-            rendered = [torch.cuda.Event() for _ in range(2)]
-            copied = [torch.cuda.Event() for _ in range(2)]
+            rendered = [torch.cuda.Event() for _ in range(E2E_DEPTH)]
+            copied = [torch.cuda.Event() for _ in range(E2E_DEPTH)]
             n_e2e = min(args.steps, 20)
 
             def pipelined(n):
                 for s in range(n):
-                    b = s & 1
+                    b = s % E2E_DEPTH
                     cs = step_cams(args.config, cams, s, rank, world)
-                    if s >= 2:
+                    if s >= E2E_DEPTH:
                         stream.wait_event(copied[b])
                     with torch.cuda.stream(stream):
                         render(cs, fov, d[b][0], d[b][1], stream=stream)
@@ -701,7 +703,7 @@ def main():
                                   "format": "VRS_OUT_RGBA8_D16F (RGBA unorm8 + depth binary16, the HMD display "
                                             "format; depth quantised to 2^-11 relative, outside the 1e-4 bar)"},
                "note": what + " into device buffers with the D2H of the frame into pinned host memory on a copy "
-                       "stream, two frames in flight (value); sync_value = " +
+                       "stream, " + str(E2E_DEPTH) + " frames in flight (value); sync_value = " +
                        ("render_two_pass + D2H + sync" if two_pass else "vrs_render_views_host") +
                        " per frame; host wall clock; camera/fovea structs travel as kernel parameters"}
 
