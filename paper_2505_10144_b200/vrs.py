@@ -76,9 +76,6 @@ def _torch_types(fmt):
     return {0: (torch.float32, torch.float32), 1: (torch.uint8, torch.float16), 2: (torch.float16, torch.float32)}[fmt]
 
 
-_FMT_TORCH = {f: (lambda f=f: _torch_types(f)) for f in (0, 1, 2)}
-
-
 def lib():
     """Load libvrs.so (raises if missing: no fallback)."""
     global _lib
@@ -288,7 +285,7 @@ class Renderer:
         out-of-bounds device access."""
         import torch
         fmt = getattr(self, "out_fmt", 0) if fmt is None else fmt
-        want_r, want_d = _FMT_TORCH[fmt]()
+        want_r, want_d = _torch_types(fmt)
         np_r, np_d = _FMT_NUMPY[fmt]
         for t, n, wt, wn, name in ((rgba, 4 * px, want_r, np_r, "rgba"), (depth, px, want_d, np_d, "depth")):
             if isinstance(t, np.ndarray):
@@ -318,7 +315,7 @@ class Renderer:
         VRS_OUT_RGBA16F_D32F; on the device, or pinned host."""
         import torch
         px = sum(c.width * c.height for c in cams)
-        rt, dt = _FMT_TORCH[getattr(self, "out_fmt", 0)]()
+        rt, dt = _torch_types(getattr(self, "out_fmt", 0))
         if pinned_host:
             return (torch.empty((px, 4), dtype=rt).pin_memory(), torch.empty(px, dtype=dt).pin_memory())
         dev = torch.device("cuda", self.device)
