@@ -826,21 +826,23 @@ def measure_gather(args, r, render, cams, fov, stream, rank, world, local, one_g
                 req.wait()
             sent[b].record(cstream)
 
-    for s in range(2):
-        step(s)
-    torch.cuda.synchronize()
-    dist.barrier()
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    for s in range(n):
-        step(s)
-    cstream.synchronize()
-    torch.cuda.synchronize()
-    t = time.perf_counter() - t0
+    try:
+        for s in range(2):
+            step(s)
+        torch.cuda.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for s in range(n):
+            step(s)
+        cstream.synchronize()
+        torch.cuda.synchronize()
+        t = time.perf_counter() - t0
+    finally:
+        r.vrs_set_output_format(0)
     tt = torch.tensor([t], dtype=torch.float64, device="cuda")
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     t = float(tt.item())
-    r.vrs_set_output_format(0)
     unit = "stereo frames/s" if len(cams) == 2 else "frames/s"
     return {"value": world * n / t, "unit": unit, "steps": n, "ms_per_step": 1000.0 * t / n,
             "gathered_bytes_per_step": bytes_per_rank * (world - 1),
