@@ -462,23 +462,19 @@ def test_c2_full_size_parity(vrs, oracle_mod):
         assert st[k] == ost[k], (k, st[k], ost[k])
 
 
-def test_c3_full_size_sampled_parity(vrs, oracle_mod):
-    """Config C3 at full size (3M Gaussians, stereo, no foveation, T_a = 16):
-    pair list bit-exact, 20k sampled output pixels within tolerance."""
+def test_c3_full_size_parity(vrs, oracle_mod):
+    """Config C3 at full size, in bench.py's launch configuration (3M
+    Gaussians, stereo 2x2064x2208, no foveation, T_a = 16): pair list, ranges
+    and per-splat counts bit-exact; EVERY output pixel of both eyes within the
+    tolerances; workload counters equal."""
     scene, cams, fov, mk = _quest_workload(3, 3_000_000, (1 / 6) ** 0.5, False, 16, False)
-    r, o, g, _ = render_both(vrs, oracle_mod, scene, cams, None, T=16, max_pairs=16 << 20, oracle_render=False)
-    k, v = r.vrs_debug_pairs(True)
-    ok, ov = o.pairs(True)
-    assert np.array_equal(k, ok) and np.array_equal(v, ov)
-    assert np.array_equal(r.vrs_debug_ranges(), o.ranges())
-    rs = np.random.default_rng(0)
-    n = 20000
-    vxy = np.stack([rs.integers(0, 2, n), rs.integers(0, sg.QUEST_W, n), rs.integers(0, sg.QUEST_H, n)], 1)
-    orgba, odep = o.render_pixels(vxy)
-    grgba = np.stack([g[vv][0][yy, xx] for vv, xx, yy in vxy])
-    gdep = np.array([g[vv][1][yy, xx] for vv, xx, yy in vxy])
-    assert np.abs(grgba - orgba).max() <= RGB_TOL
-    assert (np.abs(gdep - odep) - DEPTH_REL * np.abs(odep)).max() <= 1e-6
+    r, o, g, oi = render_both(vrs, oracle_mod, scene, cams, None, T=16, max_pairs=16 << 20)
+    assert_lists_equal(r, o)
+    assert_images_close(g, oi)
+    st, ost = r.stats(), o.stats()
+    for k in ("pairs", "samples", "evaluations", "contributions", "overflow_samples", "terminated_samples",
+              "work_items", "visible_splats"):
+        assert st[k] == ost[k], (k, st[k], ost[k])
 
 
 # --------------------------------------------------------------------- EWA baseline (config C5)
@@ -618,48 +614,33 @@ def test_packed_output_is_the_quantised_f32_frame(vrs, mode):
 
 # --------------------------------------------------------------------- more full-size and maximum-size cases
 
-def _sampled_pixels_close(o, g, cams, n=20000, seed=0):
-    rs = np.random.default_rng(seed)
-    vxy = np.stack([rs.integers(0, len(cams), n), rs.integers(0, cams[0].width, n),
-                    rs.integers(0, cams[0].height, n)], 1)
-    orgba, odep = o.render_pixels(vxy)
-    grgba = np.stack([g[vv][0][yy, xx] for vv, xx, yy in vxy])
-    gdep = np.array([g[vv][1][yy, xx] for vv, xx, yy in vxy])
-    assert np.abs(grgba - orgba).max() <= RGB_TOL
-    assert (np.abs(gdep - odep) - DEPTH_REL * np.abs(odep)).max() <= 1e-6
-
-
 @pytest.mark.parametrize("t", [45, 300])
 def test_c4_trajectory_pose_full_size_parity(vrs, oracle_mod, t):
     """Config C4 at full size at two trajectory poses (1M Gaussians, scales x0.707,
-    foveated, masks, T_a = 32): sorted pair list and ranges bit-exact, 20k
-    sampled output pixels within tolerance."""
+    foveated, masks, T_a = 32): sorted pair list and ranges bit-exact, EVERY
+    output pixel of both eyes within tolerance, workload counters equal."""
     scene = sg.vr_room(4, 1_000_000, scale_mul=0.707, sh_degree=3)
     head, yaw, pitch, roll = sg.trajectory_pose(t)
     cams = sg.stereo_pair(head, yaw, pitch, roll, masks=True)
     fov = [sg.quest_fovea()] * 2
     mk = {0: sg.ellipse_mask(sg.QUEST_W, sg.QUEST_H), 1: sg.ellipse_mask(sg.QUEST_W, sg.QUEST_H)}
-    r, o, g, _ = render_both(vrs, oracle_mod, scene, cams, fov, T=32, masks=mk, max_pairs=8 << 20,
-                             oracle_render=False)
-    k, v = r.vrs_debug_pairs(True)
-    ok, ov = o.pairs(True)
-    assert np.array_equal(k, ok) and np.array_equal(v, ov)
-    assert np.array_equal(r.vrs_debug_ranges(), o.ranges())
-    _sampled_pixels_close(o, g, cams, seed=t)
+    r, o, g, oi = render_both(vrs, oracle_mod, scene, cams, fov, T=32, masks=mk, max_pairs=8 << 20)
+    assert_lists_equal(r, o)
+    assert_images_close(g, oi)
+    st, ost = r.stats(), o.stats()
+    for k in ("pairs", "samples", "evaluations", "contributions", "terminated_samples"):
+        assert st[k] == ost[k], (k, st[k], ost[k])
 
 
 def test_c5_ewa_160_full_size_parity(vrs, oracle_mod):
     """Config C5's widest point at full size: C2 scene, 160 deg, EWA baseline
-    (footprints blow up): lists bit-exact, sampled pixels in tolerance."""
+    (footprints blow up): lists bit-exact, EVERY pixel in tolerance."""
     scene = sg.vr_room(2, 500_000, scale_mul=1.0, sh_degree=3)
     cams = sg.stereo_pair(hfov_deg=160.0, masks=False)
     fov = [sg.quest_fovea()] * 2
-    r, o, g, _ = render_both(vrs, oracle_mod, scene, cams, fov, T=32, max_pairs=8 << 20, oracle_render=False,
-                             projection=1)
-    k, v = r.vrs_debug_pairs(True)
-    ok, ov = o.pairs(True)
-    assert np.array_equal(k, ok) and np.array_equal(v, ov)
-    _sampled_pixels_close(o, g, cams, seed=5)
+    r, o, g, oi = render_both(vrs, oracle_mod, scene, cams, fov, T=32, max_pairs=8 << 20, projection=1)
+    assert_lists_equal(r, o)
+    assert_images_close(g, oi)
 
 
 def test_maximum_views_in_one_call(vrs, oracle_mod):
