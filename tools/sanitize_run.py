@@ -40,6 +40,9 @@ for proj in (0, 1):
         r.vrs_set_resort_mode(0)
         r.vrs_set_output_format(1)
         r.render(cams, fov)
+        r.vrs_set_output_format(2)  # half-float RGBA + float depth
+        r.render(cams, fov)
+        r.render_two_pass(cams, fov)
         r.vrs_set_output_format(0)
     torch.cuda.synchronize()
     r.close()
