@@ -30,6 +30,18 @@ namespace vrs {
 namespace {
 
 constexpr int kGB = 80;  // staged records per batch (as k_blend)
+// Gradient arithmetic needs no bit-exactness (the replayed forward decisions
+// do, and keep the R9 forms): its divisions use the fast MUFU reciprocal
+// (relative error ~1e-7 against the 2e-3 gradient tolerance) instead of the
+// IEEE division sequence.
+#ifndef VRS_BWD_FASTDIV
+#define VRS_BWD_FASTDIV 1
+#endif
+#if VRS_BWD_FASTDIV
+#define GDIV(a, b) __fdividef((a), (b))
+#else
+#define GDIV(a, b) ((a) / (b))
+#endif
 // at most 2^VRS_BWD_STEPS lanes of a group are summed by shuffles before one of them adds
 // (C9 backward: 15.9 ms with pairs (1), 16.4 with quads (2), 18.3 with octets (3), 20.7 with
 // whole groups (5), 22.4 with every lane adding its own record: the shuffles, not the L2
@@ -120,7 +132,7 @@ __global__ void __launch_bounds__(256) k_blend_bwd(FrameParams fp, FrameBufs fb,
             Cg = fmaf(col.y, wgt, Cg);
             Cb = fmaf(col.z, wgt, Cb);
             Dd = fmaf(tau, wgt, Dd);
-            const float inv1a = 1.0f / (1.0f - a);
+            const float inv1a = GDIV(1.0f, 1.0f - a);
             float ga = go.x * (col.x * Tk - (fo.x - Cr) * inv1a) + go.y * (col.y * Tk - (fo.y - Cg) * inv1a) +
                        go.z * (col.z * Tk - (fo.z - Cb) * inv1a) + go.w * Tfin * inv1a +
                        gd * (tau * dn * Tk - (fd - Dd * dn) * inv1a);
@@ -139,10 +151,10 @@ __global__ void __launch_bounds__(256) k_blend_bwd(FrameParams fp, FrameBufs fb,
                 const float ex = fmaf(a1.x, x, a1.y);
                 const float ey = fmaf(a1.z, x, fmaf(a1.w, y, a2.x));
                 const float num = fmaf(ex, fmaf(a2.y, ex, a2.z * ey), ey * fmaf(a2.z, ex, a2.w * ey));
-                const float is = 1.0f / s;
+                const float is = GDIV(1.0f, s);
                 const float q = num * is * is;
                 const float sigma = a5.y;
-                gv[kGSigma] = ga * (a / sigma);
+                gv[kGSigma] = ga * GDIV(a, sigma);
                 const float gq = -0.5f * ga * a;
                 const float gnum = gq * is * is, gs = -2.0f * gq * q * is;
                 gv[kGC + 0] = gnum * ex * ex;
@@ -162,7 +174,8 @@ __global__ void __launch_bounds__(256) k_blend_bwd(FrameParams fp, FrameBufs fb,
             if (tau > fp.near_plane) {  // tau = dtb / den unclamped
                 const float den = quad3z1(a3.x, a3.y, a3.z, a3.w, a4.x, a4.y, x, y);
                 const float gt = gd * dn * wgt;
-                const float gdtb = gt / den, gden = -gt * tau / den;
+                const float rden = GDIV(1.0f, den);
+                const float gdtb = gt * rden, gden = -gt * tau * rden;
                 gv[kGB3 + 0] = gdtb * x;
                 gv[kGB3 + 1] = gdtb * y;
                 gv[kGB3 + 2] = gdtb;
