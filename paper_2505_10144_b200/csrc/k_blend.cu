@@ -374,7 +374,11 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
     }
 
     float Tr = 1.0f, Cr = 0.0f, Cg = 0.0f, Cb = 0.0f, Dd = 0.0f;
-    bool done = false;
+    // "done" (T < 1e-4, checked after blending) is read from the transmittance
+    // itself -- Tr never changes once it holds -- instead of a flag kept live
+    // beside it (one register less in the 64-register loop: C2 blend 1.969 ->
+    // 1.940 ms)
+#define done (Tr < kTmin)
     uint32_t hk = 0;  // byte offset of the ring head
     uint32_t n_contrib = 0, stop_pos = re - 1;  // entry whose insertion stopped the sample (re-1: ran out)
 
@@ -388,7 +392,6 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         Cb = fmaf(col.z, wgt, Cb);
         Dd = fmaf(key_tau(key), wgt, Dd);  // ray-distance factor |d| applied once at the end
         Tr = Tr * (1.0f - a);
-        done = Tr < kTmin;
     };
 
     // the contribution of one (sample, splat) pair with its alpha, depth and
@@ -773,6 +776,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         if (tid == 0 && half == 0) v.lowcnt[t2] = v.lowcnt0[t2];  // re-armed for the next frame
     }
 }
+#undef done
 
 void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
                   cudaStream_t st) {
