@@ -49,7 +49,7 @@ struct HierSmem {
 };
 
 constexpr uint32_t kHSlot = kHT * 8;
-constexpr uint32_t kHRing = (kHP - 1) * kHSlot;
+constexpr uint32_t kHRing = kHP * kHSlot - 1u;  // wraps the slot bits, keeps the column bits
 
 }  // namespace
 
@@ -131,18 +131,20 @@ __global__ void __launch_bounds__(kHT, VRS_HIER_MINB) k_blend_hier(FrameParams f
     const uint32_t re = fb.ranges[2 * (size_t)(v.tile_base + tile) + 1];
     const float4* __restrict__ recv = fb.rec + (size_t)vi * fp.N * kRecF4;
     const float4* __restrict__ colv = fb.col + (size_t)vi * fp.N;
-    char* const wkb = reinterpret_cast<char*>(&S.w_key[0][tid]);
-    char* const wab = reinterpret_cast<char*>(&S.w_a[0][tid]);
+    // ring offsets carry the thread's column (tid * 8), so window addresses are the
+    // arrays' block-uniform bases plus one offset (k_blend.cu)
+    char* const wkb = reinterpret_cast<char*>(&S.w_key[0][0]);
+    char* const wab = reinterpret_cast<char*>(&S.w_a[0][0]);
 #define WK(off) (*reinterpret_cast<unsigned long long*>(wkb + (off)))
 #define WA(off) (*reinterpret_cast<float*>(wab + ((off) >> 1)))
 #pragma unroll
     for (int k = 0; k < kHP; k++) {
-        WK(k * kHSlot) = kSentinelKey;
-        WA(k * kHSlot) = 0.0f;
+        WK(k * kHSlot + 8u * tid) = kSentinelKey;
+        WA(k * kHSlot + 8u * tid) = 0.0f;
     }
     float Tr = 1.0f, Cr = 0.0f, Cg = 0.0f, Cb = 0.0f, Dd = 0.0f;
     bool done = !in_img;  // samples outside the image take no part (oracle: valid[s])
-    uint32_t hk = 0;
+    uint32_t hk = 8u * tid;  // ring head: slot * slot bytes + the thread's column
     uint32_t n_contrib = 0, stop_pos = re - 1;
     // block queue: this lane's entry kq (valid when kq < qn), count and free cache slot (uniform per half)
     unsigned long long qkey = ~0ull;
