@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
     // itself -- Tr never changes once it holds -- instead of a flag kept live
     // beside it (one register less in the 64-register loop: C2 blend 1.969 ->
     // 1.940 ms)
-#define done (Tr < kTmin)
+#define DONE (Tr < kTmin)
     uint32_t hk = 8u * tid;  // byte offset of the ring head (slot * kSlotBytes + column)
     uint32_t n_contrib = 0, stop_pos = re - 1;  // entry whose insertion stopped the sample (re-1: ran out)
 
@@ -404,7 +404,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         if (kCounters) n_contrib++;
         if constexpr (kGlobal) {  // global-sort baselines (N3): no window, list order
             blend_one(key, alpha);
-            if (kCounters && done) stop_pos = pos;
+            if (kCounters && DONE) stop_pos = pos;
             return;
         }
         const unsigned long long kh = WK(hk);
@@ -424,7 +424,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         const uint32_t khi = bsel((uint32_t)(key >> 32), (uint32_t)(kh >> 32), dm);
         const float asel = __uint_as_float(bsel(__float_as_uint(alpha), __float_as_uint(ah), dm));
         blend_one(((unsigned long long)khi << 32) | klo, asel);
-        if (kCounters && done) stop_pos = pos;
+        if (kCounters && DONE) stop_pos = pos;
         // (a sample that just terminated never reads its window again, so the
         // insertion does not wait for the transmittance test)
         if (dm != 0u) return;
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
     // membership + alpha/tau of entry g for this sample; a3..a5 fetched only on contribution
     auto evaluate = [&](const uint32_t pos, const uint32_t g, const float4 a0, const float4 a1, const float4 a2,
                         auto&& load345) {
-        if (done) return;
+        if (DONE) return;
         float alpha, tau;
         if (kEwa) {  // EWA baseline: q from the projected mean in pixels
             const float dxp = xs - a0.x, dyp = ys - a0.y;
@@ -514,14 +514,14 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
                 const int j = r0 + __ffs(bits) - 1;
                 bits &= bits - 1;
                 float n1, s1;
-                const bool m1 = member(j, n1, s1) && !done;
+                const bool m1 = member(j, n1, s1) && !DONE;
                 if (bits) {
                     const int j2 = r0 + __ffs(bits) - 1;
                     bits &= bits - 1;
                     float n2, s2;
                     const bool m2 = member(j2, n2, s2);
                     if (m1) contrib(j, n1, s1);
-                    if (m2 && !done) contrib(j2, n2, s2);
+                    if (m2 && !DONE) contrib(j2, n2, s2);
                 } else if (m1) {
                     contrib(j, n1, s1);
                 }
@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
             const uint32_t base = rb + b * (uint32_t)kSE;
             if (!wdone) chunk(st * kSE, (int)min(re - base, (uint32_t)kSE), base);
             // release the stage; the last warp out refills it with batch b + 2
-            if (!wdone && __all_sync(0xffffffffu, done)) {
+            if (!wdone && __all_sync(0xffffffffu, DONE)) {
                 wdone = true;
                 if (lane == 0) atomicSub(&S.alive, 1u);
             }
@@ -664,17 +664,17 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
             // the block's first n threads load one record each (seven independent LDG.128)
             if ((uint32_t)tid < n) fill_row(base + (uint32_t)tid, tid);
         }
-        if (__syncthreads_count(!done) == 0) break;
+        if (__syncthreads_count(!DONE) == 0) break;
         const int nb = min((int)(re - base), kBatch);
         for (int c = 0; c < nb; c += 32) {
-            if (__all_sync(0xffffffffu, done)) break;
+            if (__all_sync(0xffffffffu, DONE)) break;
             chunk(c, min(nb - c, 32), base + (uint32_t)c);
         }
     }
     }
     // drain the window in order (sentinels pop as no-ops)
 #pragma unroll 1
-    for (int k = 0; k < kWindow && !done && !kGlobal; k++) {
+    for (int k = 0; k < kWindow && !DONE && !kGlobal; k++) {
         blend_one(WK(hk), WA(hk));
         hk = (hk + kSlotBytes) & kRM;
     }
@@ -720,11 +720,11 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
     }
     if (kCounters) {
         // evaluations: list entries visited before termination
-        const unsigned long long ev = done ? (unsigned long long)(stop_pos - rb + 1) : (unsigned long long)(re - rb);
+        const unsigned long long ev = DONE ? (unsigned long long)(stop_pos - rb + 1) : (unsigned long long)(re - rb);
         const bool in_img = (px < v.W && py < v.H);
         const bool overflowed = !kGlobal && n_contrib > (uint32_t)kWindow;
         unsigned long long c0 = in_img ? ev : 0ull, c1 = in_img ? n_contrib : 0u,
-                           c2 = (in_img && overflowed) ? 1u : 0u, c3 = (in_img && done) ? 1u : 0u;
+                           c2 = (in_img && overflowed) ? 1u : 0u, c3 = (in_img && DONE) ? 1u : 0u;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
             c0 += __shfl_xor_sync(0xffffffffu, c0, o);
@@ -780,7 +780,7 @@ __global__ void __launch_bounds__(kBT, VRS_BLEND_MINB) k_blend(FrameParams fp, F
         if (tid == 0 && half == 0) v.lowcnt[t2] = v.lowcnt0[t2];  // re-armed for the next frame
     }
 }
-#undef done
+#undef DONE
 
 void launch_blend(const FrameParams& fp, FrameBufs fb, int total_items, float* rgba, float* depth,
                   cudaStream_t st) {
